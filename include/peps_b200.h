@@ -1,0 +1,178 @@
+/*
+ * peps_b200.h — C ABI of the B200-native einsumsvd library.
+ *
+ * The reference (arxiv/paper_2006_15234, /root/reference/proj) has no FFI: its
+ * drop-in interface is the public C++ API in proj/include/peps/*.hpp, and
+ * proj/include/peps/backend.hpp:7-10 states that another engine "would slot in
+ * behind the same kernel signatures".  Each entry point below replaces one of
+ * those signatures (cited per function); a reference-side C++ shim that binds
+ * them is shown in INTEGRATION.md.
+ *
+ * Conventions
+ *  - Every tensor is complex128, row-major, last index fastest, exactly the
+ *    reference's Tensor layout (proj/include/peps/tensor.hpp:13-20); host
+ *    buffers are interleaved (re, im) doubles.
+ *  - Tensors, states and boundaries live in device memory behind opaque
+ *    handles so sweeps never round-trip through the host.
+ *  - Every function returns 0 on success or a PEPSB_E_* kind; the message is
+ *    in pepsb_last_error() (thread-local).  Kinds mirror the reference
+ *    exceptions (proj/include/peps/errors.hpp:10-34).
+ *  - There is no CPU fallback: without a usable sm_100a device every call
+ *    fails with PEPSB_E_CUDA.
+ */
+#ifndef PEPS_B200_H
+#define PEPS_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  PEPSB_OK = 0,
+  PEPSB_E_SHAPE = 1,      /* peps::ShapeError */
+  PEPSB_E_VALIDATION = 2, /* peps::ValidationError */
+  PEPSB_E_RESOURCE = 3,   /* peps::ResourceError */
+  PEPSB_E_NUMERICAL = 4,  /* peps::NumericalError */
+  PEPSB_E_CONFIG = 5,     /* peps::ConfigError */
+  PEPSB_E_CUDA = 6,       /* device / driver failure */
+  PEPSB_E_OTHER = 9
+};
+
+enum { PEPSB_EXACT = 0, PEPSB_IMPLICIT_RSVD = 1 };         /* peps::SvdStrategy (decomposition.hpp:34) */
+enum { PEPSB_SPLIT = 0, PEPSB_LEFT = 1, PEPSB_RIGHT = 2 };  /* peps::Absorb (decomposition.hpp:37) */
+
+typedef struct pepsb_ctx pepsb_ctx;
+typedef struct pepsb_tensor pepsb_tensor;
+typedef struct pepsb_state pepsb_state;
+typedef struct pepsb_boundary pepsb_boundary;
+typedef struct pepsb_row_cache pepsb_row_cache;
+typedef struct pepsb_band_env pepsb_band_env;
+
+/* peps::TruncationPolicy (decomposition.hpp:14-17) */
+typedef struct {
+  uint64_t max_rank; /* 0: unbounded */
+  double rel_cutoff; /* default 1e-14 */
+} pepsb_trunc;
+
+/* peps::RsvdConfig (decomposition.hpp:21-25) */
+typedef struct {
+  int32_t power_iters; /* default 2 */
+  int32_t oversample;  /* < 0: max(5, ceil(0.1 * target)) */
+  uint64_t seed;
+} pepsb_rsvd;
+
+/* peps::ContractOption, two-layer fields (contraction.hpp:18-32) */
+typedef struct {
+  pepsb_trunc trunc;
+  int32_t strategy; /* PEPSB_EXACT / PEPSB_IMPLICIT_RSVD */
+  pepsb_rsvd rsvd;
+  int32_t canonicalize;
+  uint64_t seed;
+} pepsb_contract_opt;
+
+/* ---------------------------------------------------------------- context */
+const char* pepsb_last_error(void);
+int pepsb_last_error_kind(void);
+int pepsb_ctx_create(int device, pepsb_ctx** out);
+int pepsb_ctx_destroy(pepsb_ctx* ctx);
+int pepsb_ctx_sync(pepsb_ctx* ctx);
+/* keys: "orth_mode" (0 reference Gram-eigh, 1 CholeskyQR2) */
+int pepsb_ctx_set_option(pepsb_ctx* ctx, const char* key, int64_t value);
+/* out[0..3] = flops (instr::flops convention, instrument.hpp:19-65),
+ * einsumsvd_flops, peak_elements, kernel launches issued by the library */
+int pepsb_ctx_counters(pepsb_ctx* ctx, uint64_t* out4);
+int pepsb_ctx_reset_counters(pepsb_ctx* ctx);
+/* CUDA stream the library enqueues on (cudaStream_t), for event timing */
+void* pepsb_ctx_stream(pepsb_ctx* ctx);
+
+/* ---------------------------------------------------------------- tensors (peps::Tensor, tensor.hpp:20-69) */
+int pepsb_tensor_from_host(pepsb_ctx* ctx, int ndim, const int64_t* shape, const double* data, pepsb_tensor** out);
+int pepsb_tensor_from_device(pepsb_ctx* ctx, int ndim, const int64_t* shape, const void* dptr, pepsb_tensor** out);
+int pepsb_tensor_ndim(const pepsb_tensor* t);
+int pepsb_tensor_shape(const pepsb_tensor* t, int64_t* shape);
+int pepsb_tensor_to_host(pepsb_ctx* ctx, const pepsb_tensor* t, double* out);
+int pepsb_tensor_to_device(pepsb_ctx* ctx, const pepsb_tensor* t, void* dptr);
+void pepsb_tensor_free(pepsb_tensor* t);
+
+/* random_tensor / random_tensor_real (tensor.hpp:74-80, tensor.cpp:192-208), bit-identical */
+int pepsb_random_tensor(pepsb_ctx* ctx, int ndim, const int64_t* shape, uint64_t seed, int real, pepsb_tensor** out);
+
+/* contract(spec, tensors) (einsum.hpp:27) */
+int pepsb_contract(pepsb_ctx* ctx, const char* spec, int n, pepsb_tensor* const* ts, pepsb_tensor** out);
+
+/* ImplicitOperator::apply / adjoint_apply / materialize (implicit.hpp:26-30).
+ * labels_csv: comma-separated label strings, one per tensor.
+ * mode 0: apply(probe), 1: adjoint_apply(probe), 2: materialize() (probe ignored) */
+int pepsb_implicit(pepsb_ctx* ctx, int n, pepsb_tensor* const* ts, const char* labels_csv, const char* rows,
+                   const char* cols, const pepsb_tensor* probe, int mode, pepsb_tensor** out);
+
+/* gram_orthogonalize(Tensor, split) (decomposition.hpp:52) */
+int pepsb_gram_orthogonalize(pepsb_ctx* ctx, const pepsb_tensor* a, int split, pepsb_tensor** q, pepsb_tensor** r);
+
+/* svd(Tensor, split) (linalg.hpp:21-22); s has capacity s_cap, *k = min extent */
+int pepsb_svd(pepsb_ctx* ctx, const pepsb_tensor* a, int split, pepsb_tensor** u, double* s, int64_t s_cap,
+              int64_t* k, pepsb_tensor** v);
+
+/* randomized_svd (decomposition.hpp:43-44) */
+int pepsb_randomized_svd(pepsb_ctx* ctx, int n, pepsb_tensor* const* ts, const char* labels_csv, const char* rows,
+                         const char* cols, const pepsb_trunc* policy, const pepsb_rsvd* cfg, pepsb_tensor** u,
+                         double* s, int64_t s_cap, int64_t* rank, pepsb_tensor** v, int* rank_clamped);
+
+/* einsumsvd (decomposition.hpp:65-67) */
+int pepsb_einsumsvd(pepsb_ctx* ctx, int n, pepsb_tensor* const* ts, const char* labels_csv, const char* rows,
+                    const char* cols, const pepsb_trunc* policy, int strategy, int absorb, const pepsb_rsvd* cfg,
+                    pepsb_tensor** t1, pepsb_tensor** t2, double* s, int64_t s_cap, int64_t* rank,
+                    int* rank_clamped);
+
+/* ---------------------------------------------------------------- PEPS (state.hpp:33-61) */
+int pepsb_state_create(pepsb_ctx* ctx, int rows, int cols, int d, pepsb_tensor* const* sites, pepsb_state** out);
+int pepsb_state_site(const pepsb_state* s, int row, int col, pepsb_tensor** out);
+void pepsb_state_free(pepsb_state* s);
+
+/* TwoLayerBoundary (contraction.hpp:77-80) */
+int pepsb_boundary_create(pepsb_ctx* ctx, int n, pepsb_tensor* const* sites, const int64_t* phys_pairs,
+                          pepsb_boundary** out);
+int pepsb_boundary_length(const pepsb_boundary* b);
+int pepsb_boundary_site(const pepsb_boundary* b, int i, pepsb_tensor** out);
+int pepsb_boundary_phys(const pepsb_boundary* b, int64_t* pairs);
+void pepsb_boundary_free(pepsb_boundary* b);
+
+/* two_layer_first_row / two_layer_apply_row / contract_two_layer (contraction.hpp:82-90) */
+int pepsb_two_layer_first_row(pepsb_ctx* ctx, const pepsb_state* bra, const pepsb_state* ket, pepsb_boundary** out);
+int pepsb_two_layer_apply_row(pepsb_ctx* ctx, const pepsb_boundary* top, const pepsb_state* bra,
+                              const pepsb_state* ket, int row, const pepsb_contract_opt* opt, uint64_t seed_tag,
+                              pepsb_boundary** out);
+int pepsb_contract_two_layer(pepsb_ctx* ctx, const pepsb_state* bra, const pepsb_state* ket,
+                             const pepsb_contract_opt* opt, double* re, double* im);
+/* chain_scalar (mps.hpp:52) */
+int pepsb_chain_scalar(pepsb_ctx* ctx, const pepsb_boundary* b, double* re, double* im);
+
+/* build_row_cache (observables.hpp:61) */
+int pepsb_build_row_cache(pepsb_ctx* ctx, const pepsb_state* s, const pepsb_contract_opt* opt, pepsb_row_cache** out);
+/* which 0: tops[k], 1: bots[k] */
+int pepsb_row_cache_get(const pepsb_row_cache* c, int which, int k, pepsb_boundary** out);
+void pepsb_row_cache_free(pepsb_row_cache* c);
+
+/* band_environment / band_splice / band_value (contraction.hpp:101-125).
+ * Insertion pieces (contraction.hpp:95-99): piece i sits at (rc[2i], rc[2i+1]),
+ * operator ops[i] (d_out, d_in, bond...), nbonds[i] bond ids taken in order
+ * from bond_ids.  top / bottom may be NULL at the lattice edge. */
+int pepsb_band_environment(pepsb_ctx* ctx, const pepsb_boundary* top, const pepsb_state* bra, const pepsb_state* ket,
+                           int r0, int r1, const pepsb_boundary* bottom, pepsb_band_env** out);
+int pepsb_band_splice(pepsb_ctx* ctx, const pepsb_band_env* env, const pepsb_boundary* top, const pepsb_state* bra,
+                      const pepsb_state* ket, const pepsb_boundary* bottom, int npieces, const int* rc,
+                      pepsb_tensor* const* ops, const int* nbonds, const int* bond_ids, int c0, int c1, double* re,
+                      double* im);
+int pepsb_band_value(pepsb_ctx* ctx, const pepsb_boundary* top, const pepsb_state* bra, const pepsb_state* ket, int r0,
+                     int r1, const pepsb_boundary* bottom, int npieces, const int* rc, pepsb_tensor* const* ops,
+                     const int* nbonds, const int* bond_ids, double* re, double* im);
+void pepsb_band_env_free(pepsb_band_env* e);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PEPS_B200_H */

@@ -1,0 +1,479 @@
+"""Host API mirroring the reference's public C++ interface for the einsumsvd path.
+
+Names, argument meaning and error behaviour follow /root/reference/proj/include/peps:
+``ImplicitOperator`` (implicit.hpp:15-44), ``einsumsvd`` / ``randomized_svd`` /
+``gram_orthogonalize`` (decomposition.hpp:14-76), ``svd`` (linalg.hpp:15-22),
+``contract`` (einsum.hpp:27), ``two_layer_first_row`` / ``two_layer_apply_row`` /
+``contract_two_layer`` (contraction.hpp:77-90), ``chain_scalar`` (mps.hpp:52),
+``build_row_cache`` (observables.hpp:56-61), ``band_environment`` / ``band_splice`` /
+``band_value`` (contraction.hpp:95-125).  Every call goes through the C ABI of
+lib/libpeps_b200.so; tensors are device-resident ``DeviceTensor`` handles (numpy
+complex arrays are uploaded on the fly).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from enum import IntEnum
+from typing import List, Optional, Sequence, Tuple
+
+import numpy as np
+
+from . import _lib
+from ._lib import PepsError, check, lib
+
+_VP = C.c_void_p
+
+
+class SvdStrategy(IntEnum):
+    exact = 0
+    implicit_rsvd = 1
+
+
+class Absorb(IntEnum):
+    split = 0
+    left = 1
+    right = 2
+
+
+@dataclass
+class TruncationPolicy:
+    max_rank: int = 0
+    rel_cutoff: float = 1e-14
+
+    def c(self):
+        return _lib.Trunc(int(self.max_rank) & 0xFFFFFFFFFFFFFFFF, float(self.rel_cutoff))
+
+
+@dataclass
+class RsvdConfig:
+    power_iters: int = 2
+    oversample: int = -1
+    seed: int = 0
+
+    def c(self):
+        return _lib.Rsvd(int(self.power_iters), int(self.oversample), int(self.seed) & 0xFFFFFFFFFFFFFFFF)
+
+
+@dataclass
+class ContractOption:
+    trunc: TruncationPolicy = field(default_factory=lambda: TruncationPolicy(0, 1e-14))
+    strategy: SvdStrategy = SvdStrategy.implicit_rsvd
+    rsvd: RsvdConfig = field(default_factory=RsvdConfig)
+    canonicalize: bool = True
+    seed: int = 0
+
+    @staticmethod
+    def two_layer_opt(m: int, seed: int = 0, power_iters: int = 2, oversample: int = -1):
+        """contraction.cpp:54-62 (+ the oversample knob the configs set)."""
+        return ContractOption(TruncationPolicy(m, 1e-14), SvdStrategy.implicit_rsvd,
+                              RsvdConfig(power_iters, oversample, 0), True, seed)
+
+    def c(self):
+        return _lib.ContractOpt(self.trunc.c(), int(self.strategy), self.rsvd.c(), int(bool(self.canonicalize)),
+                                int(self.seed) & 0xFFFFFFFFFFFFFFFF)
+
+
+# ----------------------------------------------------------------------------- context
+
+class Context:
+    """One device context (stream + memory pool) of the library."""
+
+    def __init__(self, device: int = 0):
+        h = _VP()
+        check(lib().pepsb_ctx_create(int(device), C.byref(h)))
+        self.h = h
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().pepsb_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def sync(self):
+        check(lib().pepsb_ctx_sync(self.h))
+
+    def set_option(self, key: str, value: int):
+        check(lib().pepsb_ctx_set_option(self.h, key.encode(), int(value)))
+
+    def counters(self) -> dict:
+        a = (C.c_uint64 * 4)()
+        check(lib().pepsb_ctx_counters(self.h, a))
+        return dict(flops=int(a[0]), einsumsvd_flops=int(a[1]), peak_elements=int(a[2]), launches=int(a[3]))
+
+    def reset_counters(self):
+        check(lib().pepsb_ctx_reset_counters(self.h))
+
+    @property
+    def stream(self) -> int:
+        return int(lib().pepsb_ctx_stream(self.h) or 0)
+
+
+_default: Optional[Context] = None
+
+
+def default_context() -> Context:
+    global _default
+    if _default is None:
+        _default = Context(0)
+    return _default
+
+
+# ----------------------------------------------------------------------------- tensors
+
+class DeviceTensor:
+    """Device-resident complex128 tensor in the reference's row-major layout."""
+
+    def __init__(self, handle, ctx: Context):
+        self.h = handle
+        self.ctx = ctx
+
+    def __del__(self):
+        try:
+            if self.h:
+                lib().pepsb_tensor_free(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+    @property
+    def shape(self) -> Tuple[int, ...]:
+        nd = lib().pepsb_tensor_ndim(self.h)
+        s = (C.c_int64 * max(1, nd))()
+        check(lib().pepsb_tensor_shape(self.h, s))
+        return tuple(int(s[i]) for i in range(nd))
+
+    @property
+    def size(self) -> int:
+        return int(np.prod(self.shape)) if self.shape else 1
+
+    def numpy(self) -> np.ndarray:
+        out = np.empty(self.shape, dtype=np.complex128)
+        check(lib().pepsb_tensor_to_host(self.ctx.h, self.h, out.ctypes.data_as(_VP)))
+        return out
+
+    def __repr__(self):
+        return f"DeviceTensor{self.shape}"
+
+
+def to_device(a, ctx: Optional[Context] = None) -> DeviceTensor:
+    ctx = ctx or default_context()
+    if isinstance(a, DeviceTensor):
+        return a
+    a = np.ascontiguousarray(a, dtype=np.complex128)
+    shp = (C.c_int64 * max(1, a.ndim))(*a.shape)
+    h = _VP()
+    check(lib().pepsb_tensor_from_host(ctx.h, a.ndim, shp, a.ctypes.data_as(_VP), C.byref(h)))
+    return DeviceTensor(h, ctx)
+
+
+def _handles(ts, ctx):
+    dts = [to_device(t, ctx) for t in ts]
+    arr = (_VP * max(1, len(dts)))(*[d.h for d in dts])
+    return dts, arr
+
+
+def random_tensor(shape, seed: int, real: bool = False, ctx: Optional[Context] = None) -> DeviceTensor:
+    """random_tensor / random_tensor_real (tensor.cpp:192-208), generated on the device."""
+    ctx = ctx or default_context()
+    shp = (C.c_int64 * max(1, len(shape)))(*shape)
+    h = _VP()
+    check(lib().pepsb_random_tensor(ctx.h, len(shape), shp, C.c_uint64(seed & 0xFFFFFFFFFFFFFFFF), int(real),
+                                    C.byref(h)))
+    return DeviceTensor(h, ctx)
+
+
+def contract(spec: str, *tensors, ctx: Optional[Context] = None) -> DeviceTensor:
+    ctx = ctx or default_context()
+    dts, arr = _handles(tensors, ctx)
+    h = _VP()
+    check(lib().pepsb_contract(ctx.h, spec.encode(), len(dts), arr, C.byref(h)))
+    return DeviceTensor(h, ctx)
+
+
+class ImplicitOperator:
+    """implicit.hpp:15-44 — a linear map given as an uncontracted network."""
+
+    def __init__(self, tensors: Sequence, labels: Sequence[str], row_labels: str, col_labels: str,
+                 ctx: Optional[Context] = None):
+        self.ctx = ctx or default_context()
+        self.tensors = [to_device(t, self.ctx) for t in tensors]
+        self.labels = list(labels)
+        self.row_labels = row_labels
+        self.col_labels = col_labels
+
+    def _args(self):
+        arr = (_VP * max(1, len(self.tensors)))(*[t.h for t in self.tensors])
+        return (len(self.tensors), arr, ",".join(self.labels).encode(), self.row_labels.encode(),
+                self.col_labels.encode())
+
+    def _call(self, probe, mode):
+        h = _VP()
+        p = to_device(probe, self.ctx) if probe is not None else None
+        check(lib().pepsb_implicit(self.ctx.h, *self._args(), p.h if p is not None else None, mode, C.byref(h)))
+        return DeviceTensor(h, self.ctx)
+
+    def apply(self, q) -> DeviceTensor:
+        return self._call(q, 0)
+
+    def adjoint_apply(self, p) -> DeviceTensor:
+        return self._call(p, 1)
+
+    def materialize(self) -> DeviceTensor:
+        return self._call(None, 2)
+
+
+@dataclass
+class EinsumsvdResult:
+    t1: DeviceTensor
+    t2: DeviceTensor
+    s: np.ndarray
+    rank_clamped: bool
+
+
+@dataclass
+class SvdTriple:
+    u: DeviceTensor
+    s: np.ndarray
+    v: DeviceTensor
+    rank_clamped: bool
+
+
+def einsumsvd(network: ImplicitOperator, policy: TruncationPolicy, strategy: SvdStrategy,
+              absorb: Absorb = Absorb.split, cfg: RsvdConfig = RsvdConfig()) -> EinsumsvdResult:
+    """decomposition.cpp:308-352."""
+    ctx = network.ctx
+    t1, t2 = _VP(), _VP()
+    cap = 4096
+    s = np.zeros(cap)
+    rank = C.c_int64()
+    clamped = C.c_int()
+    pol, rc = policy.c(), cfg.c()
+    check(lib().pepsb_einsumsvd(ctx.h, *network._args(), C.byref(pol), int(strategy), int(absorb), C.byref(rc),
+                                C.byref(t1), C.byref(t2), s.ctypes.data_as(C.POINTER(C.c_double)), cap,
+                                C.byref(rank), C.byref(clamped)))
+    return EinsumsvdResult(DeviceTensor(t1, ctx), DeviceTensor(t2, ctx), s[:rank.value].copy(), bool(clamped.value))
+
+
+def randomized_svd(op: ImplicitOperator, policy: TruncationPolicy, cfg: RsvdConfig = RsvdConfig()) -> SvdTriple:
+    """decomposition.cpp:259-306."""
+    ctx = op.ctx
+    u, v = _VP(), _VP()
+    cap = 4096
+    s = np.zeros(cap)
+    rank = C.c_int64()
+    clamped = C.c_int()
+    pol, rc = policy.c(), cfg.c()
+    check(lib().pepsb_randomized_svd(ctx.h, *op._args(), C.byref(pol), C.byref(rc), C.byref(u),
+                                     s.ctypes.data_as(C.POINTER(C.c_double)), cap, C.byref(rank), C.byref(v),
+                                     C.byref(clamped)))
+    return SvdTriple(DeviceTensor(u, ctx), s[:rank.value].copy(), DeviceTensor(v, ctx), bool(clamped.value))
+
+
+def gram_orthogonalize(a, split: int, ctx: Optional[Context] = None):
+    """decomposition.cpp:160-193."""
+    ctx = ctx or default_context()
+    d = to_device(a, ctx)
+    q, r = _VP(), _VP()
+    check(lib().pepsb_gram_orthogonalize(ctx.h, d.h, int(split), C.byref(q), C.byref(r)))
+    return DeviceTensor(q, ctx), DeviceTensor(r, ctx)
+
+
+def svd(a, split: int, ctx: Optional[Context] = None):
+    """linalg.cpp:193-207 — returns (u, s, v) with phase-fixed u."""
+    ctx = ctx or default_context()
+    d = to_device(a, ctx)
+    u, v = _VP(), _VP()
+    cap = 4096
+    s = np.zeros(cap)
+    k = C.c_int64()
+    check(lib().pepsb_svd(ctx.h, d.h, int(split), C.byref(u), s.ctypes.data_as(C.POINTER(C.c_double)), cap,
+                          C.byref(k), C.byref(v)))
+    return DeviceTensor(u, ctx), s[:k.value].copy(), DeviceTensor(v, ctx)
+
+
+# ----------------------------------------------------------------------------- PEPS level
+
+class PepsState:
+    """state.hpp:33-61 — sites (phys, up, left, down, right), row-major list."""
+
+    def __init__(self, rows: int, cols: int, phys_dim: int, sites: Sequence, ctx: Optional[Context] = None):
+        self.ctx = ctx or default_context()
+        self.rows, self.cols, self.d = rows, cols, phys_dim
+        self.sites = [to_device(s, self.ctx) for s in sites]
+        arr = (_VP * len(self.sites))(*[s.h for s in self.sites])
+        h = _VP()
+        check(lib().pepsb_state_create(self.ctx.h, rows, cols, phys_dim, arr, C.byref(h)))
+        self.h = h
+
+    def __del__(self):
+        try:
+            if self.h:
+                lib().pepsb_state_free(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+    def site(self, r, c) -> DeviceTensor:
+        return self.sites[r * self.cols + c]
+
+
+class TwoLayerBoundary:
+    """contraction.hpp:77-80 — MPS sites (pb*pk, left, right) + phys pairs."""
+
+    def __init__(self, handle, ctx: Context):
+        self.h = handle
+        self.ctx = ctx
+
+    @staticmethod
+    def from_sites(sites: Sequence, phys: Sequence[Tuple[int, int]], ctx: Optional[Context] = None):
+        ctx = ctx or default_context()
+        dts, arr = _handles(sites, ctx)
+        pp = (C.c_int64 * (2 * len(phys)))(*[int(x) for p in phys for x in p])
+        h = _VP()
+        check(lib().pepsb_boundary_create(ctx.h, len(dts), arr, pp, C.byref(h)))
+        return TwoLayerBoundary(h, ctx)
+
+    def __del__(self):
+        try:
+            if self.h:
+                lib().pepsb_boundary_free(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+    def __len__(self):
+        return lib().pepsb_boundary_length(self.h)
+
+    def site(self, i) -> DeviceTensor:
+        h = _VP()
+        check(lib().pepsb_boundary_site(self.h, int(i), C.byref(h)))
+        return DeviceTensor(h, self.ctx)
+
+    @property
+    def sites(self) -> List[DeviceTensor]:
+        return [self.site(i) for i in range(len(self))]
+
+    @property
+    def phys(self) -> List[Tuple[int, int]]:
+        n = len(self)
+        a = (C.c_int64 * (2 * n))()
+        check(lib().pepsb_boundary_phys(self.h, a))
+        return [(int(a[2 * i]), int(a[2 * i + 1])) for i in range(n)]
+
+
+def two_layer_first_row(bra: PepsState, ket: PepsState) -> TwoLayerBoundary:
+    h = _VP()
+    check(lib().pepsb_two_layer_first_row(bra.ctx.h, bra.h, ket.h, C.byref(h)))
+    return TwoLayerBoundary(h, bra.ctx)
+
+
+def two_layer_apply_row(top: TwoLayerBoundary, bra: PepsState, ket: PepsState, row: int, opt: ContractOption,
+                        seed_tag: int = 0x20) -> TwoLayerBoundary:
+    h = _VP()
+    o = opt.c()
+    check(lib().pepsb_two_layer_apply_row(bra.ctx.h, top.h, bra.h, ket.h, int(row), C.byref(o), C.c_uint64(seed_tag),
+                                          C.byref(h)))
+    return TwoLayerBoundary(h, bra.ctx)
+
+
+def contract_two_layer(bra: PepsState, ket: PepsState, opt: ContractOption) -> complex:
+    re, im = C.c_double(), C.c_double()
+    o = opt.c()
+    check(lib().pepsb_contract_two_layer(bra.ctx.h, bra.h, ket.h, C.byref(o), C.byref(re), C.byref(im)))
+    return complex(re.value, im.value)
+
+
+def chain_scalar(b: TwoLayerBoundary) -> complex:
+    re, im = C.c_double(), C.c_double()
+    check(lib().pepsb_chain_scalar(b.ctx.h, b.h, C.byref(re), C.byref(im)))
+    return complex(re.value, im.value)
+
+
+@dataclass
+class RowCache:
+    tops: List[TwoLayerBoundary]
+    bots: List[TwoLayerBoundary]
+
+
+def build_row_cache(s: PepsState, opt: ContractOption) -> RowCache:
+    h = _VP()
+    o = opt.c()
+    check(lib().pepsb_build_row_cache(s.ctx.h, s.h, C.byref(o), C.byref(h)))
+    try:
+        tops, bots = [], []
+        for which, dst in ((0, tops), (1, bots)):
+            for k in range(s.rows):
+                b = _VP()
+                check(lib().pepsb_row_cache_get(h, which, k, C.byref(b)))
+                dst.append(TwoLayerBoundary(b, s.ctx))
+        return RowCache(tops, bots)
+    finally:
+        lib().pepsb_row_cache_free(h)
+
+
+@dataclass
+class InsertionPiece:
+    """contraction.hpp:95-99."""
+    site: Tuple[int, int]
+    op: object
+    bond_ids: List[int] = field(default_factory=list)
+
+
+class BandEnvironment:
+    def __init__(self, handle, ctx):
+        self.h = handle
+        self.ctx = ctx
+
+    def __del__(self):
+        try:
+            if self.h:
+                lib().pepsb_band_env_free(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+
+def _pieces(pieces: Sequence[InsertionPiece], ctx):
+    n = len(pieces)
+    rc = (C.c_int * max(1, 2 * n))(*[int(x) for p in pieces for x in p.site])
+    ops = [to_device(p.op, ctx) for p in pieces]
+    oa = (_VP * max(1, n))(*[o.h for o in ops])
+    nb = (C.c_int * max(1, n))(*[len(p.bond_ids) for p in pieces])
+    ids = [int(i) for p in pieces for i in p.bond_ids]
+    ia = (C.c_int * max(1, len(ids)))(*ids)
+    return n, rc, ops, oa, nb, ia
+
+
+def band_environment(top: Optional[TwoLayerBoundary], bra: PepsState, ket: PepsState, r0: int, r1: int,
+                     bottom: Optional[TwoLayerBoundary]) -> BandEnvironment:
+    h = _VP()
+    check(lib().pepsb_band_environment(bra.ctx.h, top.h if top else None, bra.h, ket.h, int(r0), int(r1),
+                                       bottom.h if bottom else None, C.byref(h)))
+    return BandEnvironment(h, bra.ctx)
+
+
+def band_splice(env: BandEnvironment, top, bra: PepsState, ket: PepsState, bottom, pieces, c0: int,
+                c1: int) -> complex:
+    n, rc, ops, oa, nb, ia = _pieces(pieces, bra.ctx)
+    re, im = C.c_double(), C.c_double()
+    check(lib().pepsb_band_splice(bra.ctx.h, env.h, top.h if top else None, bra.h, ket.h,
+                                  bottom.h if bottom else None, n, rc, oa, nb, ia, int(c0), int(c1), C.byref(re),
+                                  C.byref(im)))
+    return complex(re.value, im.value)
+
+
+def band_value(top, bra: PepsState, ket: PepsState, r0: int, r1: int, bottom, pieces) -> complex:
+    n, rc, ops, oa, nb, ia = _pieces(pieces, bra.ctx)
+    re, im = C.c_double(), C.c_double()
+    check(lib().pepsb_band_value(bra.ctx.h, top.h if top else None, bra.h, ket.h, int(r0), int(r1),
+                                 bottom.h if bottom else None, n, rc, oa, nb, ia, C.byref(re), C.byref(im)))
+    return complex(re.value, im.value)
+
+
+__all__ = [n for n in dir() if not n.startswith("_")] + ["PepsError"]

@@ -1,0 +1,522 @@
+// extern "C" boundary (include/peps_b200.h): POD in, handles out, status codes.
+#include <cstring>
+#include <exception>
+#include <string>
+
+#include "../../include/peps_b200.h"
+#include "peps.h"
+#include "tensor_ops.cuh"
+
+using namespace pepsb;
+
+struct pepsb_ctx {
+  Ctx* ctx;
+};
+struct pepsb_tensor {
+  DTensor t;
+};
+struct pepsb_state {
+  PepsStateD s;
+};
+struct pepsb_boundary {
+  BoundaryD b;
+};
+struct pepsb_row_cache {
+  RowCacheD c;
+};
+struct pepsb_band_env {
+  BandEnvD e;
+};
+
+namespace {
+
+thread_local std::string g_err;
+thread_local int g_kind = 0;
+
+template <class F>
+int guard(F&& f) {
+  try {
+    f();
+    return PEPSB_OK;
+  } catch (const Error& e) {
+    g_err = e.what();
+    g_kind = e.kind;
+  } catch (const std::bad_alloc& e) {
+    g_err = "host allocation failed";
+    g_kind = PEPSB_E_RESOURCE;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    g_kind = PEPSB_E_OTHER;
+  }
+  return g_kind;
+}
+
+void need(const void* p, const char* what) {
+  if (!p) throw Error(kValidationError, std::string("null ") + what);
+}
+
+std::vector<int64_t> shape_of(int ndim, const int64_t* shape) {
+  if (ndim < 0 || ndim > kMaxModes) throw Error(kShapeError, "tensor order out of range");
+  std::vector<int64_t> s(shape, shape + ndim);
+  for (auto e : s)
+    if (e < 1) throw Error(kShapeError, "tensor extent must be >= 1");
+  return s;
+}
+
+std::vector<std::string> split_csv(const char* s) {
+  std::vector<std::string> out;
+  std::string cur;
+  for (const char* p = s; *p; ++p) {
+    if (*p == ',') {
+      out.push_back(cur);
+      cur.clear();
+    } else {
+      cur += *p;
+    }
+  }
+  out.push_back(cur);
+  return out;
+}
+
+pepsb_tensor* wrap(const DTensor& t) { return new pepsb_tensor{t}; }
+
+Trunc trunc_of(const pepsb_trunc* p) {
+  Trunc t;
+  if (p) {
+    t.max_rank = p->max_rank;
+    t.rel_cutoff = p->rel_cutoff;
+  }
+  return t;
+}
+
+Rsvd rsvd_of(const pepsb_rsvd* p) {
+  Rsvd r;
+  if (p) {
+    r.power_iters = p->power_iters;
+    r.oversample = p->oversample;
+    r.seed = p->seed;
+  }
+  return r;
+}
+
+ContractOptD opt_of(const pepsb_contract_opt* p) {
+  ContractOptD o;
+  if (p) {
+    o.trunc = trunc_of(&p->trunc);
+    o.strategy = p->strategy;
+    o.rsvd = rsvd_of(&p->rsvd);
+    o.canonicalize = p->canonicalize != 0;
+    o.seed = p->seed;
+  }
+  return o;
+}
+
+ImplicitOp make_op(int n, pepsb_tensor* const* ts, const char* labels_csv, const char* rows, const char* cols) {
+  need(ts, "tensor list");
+  need(labels_csv, "labels");
+  std::vector<DTensor> v;
+  for (int i = 0; i < n; ++i) {
+    need(ts[i], "tensor");
+    v.push_back(ts[i]->t);
+  }
+  return ImplicitOp(v, split_csv(labels_csv), rows ? rows : "", cols ? cols : "");
+}
+
+std::vector<InsertionPieceD> pieces_of(int npieces, const int* rc, pepsb_tensor* const* ops, const int* nbonds,
+                                       const int* bond_ids) {
+  std::vector<InsertionPieceD> out;
+  int bi = 0;
+  for (int i = 0; i < npieces; ++i) {
+    InsertionPieceD p;
+    p.row = rc[2 * i];
+    p.col = rc[2 * i + 1];
+    need(ops[i], "piece operator");
+    p.op = ops[i]->t;
+    for (int j = 0; j < nbonds[i]; ++j) p.bond_ids.push_back(bond_ids[bi++]);
+    out.push_back(p);
+  }
+  return out;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* pepsb_last_error(void) { return g_err.c_str(); }
+int pepsb_last_error_kind(void) { return g_kind; }
+
+int pepsb_ctx_create(int device, pepsb_ctx** out) {
+  return guard([&] {
+    need(out, "out");
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess || n == 0) {
+      cudaGetLastError();
+      throw Error(kCudaError, "no CUDA device available (the B200 library has no CPU fallback)");
+    }
+    cudaDeviceProp prop;
+    PEPSB_CUDA(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10) throw Error(kCudaError, std::string("device is not sm_100 (found ") + prop.name + ")");
+    *out = new pepsb_ctx{new Ctx(device)};
+  });
+}
+
+int pepsb_ctx_destroy(pepsb_ctx* c) {
+  return guard([&] {
+    if (c) {
+      delete c->ctx;
+      delete c;
+    }
+  });
+}
+
+int pepsb_ctx_sync(pepsb_ctx* c) {
+  return guard([&] {
+    need(c, "ctx");
+    c->ctx->sync();
+  });
+}
+
+int pepsb_ctx_set_option(pepsb_ctx* c, const char* key, int64_t value) {
+  return guard([&] {
+    need(c, "ctx");
+    std::string k = key ? key : "";
+    if (k == "orth_mode") c->ctx->orth_mode = static_cast<int>(value);
+    else throw Error(kConfigError, "unknown option '" + k + "'");
+  });
+}
+
+int pepsb_ctx_counters(pepsb_ctx* c, uint64_t* out) {
+  return guard([&] {
+    need(c, "ctx");
+    out[0] = c->ctx->flops;
+    out[1] = c->ctx->einsumsvd_flops;
+    out[2] = c->ctx->peak_elements;
+    out[3] = static_cast<uint64_t>(c->ctx->launches);
+  });
+}
+
+int pepsb_ctx_reset_counters(pepsb_ctx* c) {
+  return guard([&] {
+    need(c, "ctx");
+    c->ctx->flops = c->ctx->einsumsvd_flops = c->ctx->peak_elements = 0;
+    c->ctx->launches = 0;
+  });
+}
+
+void* pepsb_ctx_stream(pepsb_ctx* c) { return c ? static_cast<void*>(c->ctx->stream) : nullptr; }
+
+int pepsb_tensor_from_host(pepsb_ctx* c, int ndim, const int64_t* shape, const double* data, pepsb_tensor** out) {
+  return guard([&] {
+    need(c, "ctx");
+    DTensor t = c->ctx->empty(shape_of(ndim, shape));
+    if (t.size())
+      PEPSB_CUDA(cudaMemcpyAsync(t.data(), data, t.size() * sizeof(double2), cudaMemcpyHostToDevice, c->ctx->stream));
+    *out = wrap(t);
+  });
+}
+
+int pepsb_tensor_from_device(pepsb_ctx* c, int ndim, const int64_t* shape, const void* dptr, pepsb_tensor** out) {
+  return guard([&] {
+    need(c, "ctx");
+    DTensor t = c->ctx->empty(shape_of(ndim, shape));
+    if (t.size())
+      PEPSB_CUDA(cudaMemcpyAsync(t.data(), dptr, t.size() * sizeof(double2), cudaMemcpyDeviceToDevice, c->ctx->stream));
+    *out = wrap(t);
+  });
+}
+
+int pepsb_tensor_ndim(const pepsb_tensor* t) { return t ? static_cast<int>(t->t.shape.size()) : -1; }
+
+int pepsb_tensor_shape(const pepsb_tensor* t, int64_t* shape) {
+  return guard([&] {
+    need(t, "tensor");
+    for (size_t a = 0; a < t->t.shape.size(); ++a) shape[a] = t->t.shape[a];
+  });
+}
+
+int pepsb_tensor_to_host(pepsb_ctx* c, const pepsb_tensor* t, double* out) {
+  return guard([&] {
+    need(c, "ctx");
+    need(t, "tensor");
+    if (t->t.size())
+      PEPSB_CUDA(cudaMemcpyAsync(out, t->t.data(), t->t.size() * sizeof(double2), cudaMemcpyDeviceToHost, c->ctx->stream));
+    c->ctx->sync();
+  });
+}
+
+int pepsb_tensor_to_device(pepsb_ctx* c, const pepsb_tensor* t, void* dptr) {
+  return guard([&] {
+    need(c, "ctx");
+    need(t, "tensor");
+    if (t->t.size())
+      PEPSB_CUDA(cudaMemcpyAsync(dptr, t->t.data(), t->t.size() * sizeof(double2), cudaMemcpyDeviceToDevice, c->ctx->stream));
+  });
+}
+
+void pepsb_tensor_free(pepsb_tensor* t) { delete t; }
+
+int pepsb_random_tensor(pepsb_ctx* c, int ndim, const int64_t* shape, uint64_t seed, int real, pepsb_tensor** out) {
+  return guard([&] {
+    need(c, "ctx");
+    DTensor t = c->ctx->empty(shape_of(ndim, shape));
+    std::vector<int64_t> lstr = row_major_strides(t.shape);
+    random_fill(t.data(), ndim, t.shape.data(), lstr.data(), seed, real, c->ctx->stream);
+    ++c->ctx->launches;
+    *out = wrap(t);
+  });
+}
+
+int pepsb_contract(pepsb_ctx* c, const char* spec, int n, pepsb_tensor* const* ts, pepsb_tensor** out) {
+  return guard([&] {
+    need(c, "ctx");
+    need(spec, "spec");
+    std::vector<std::string> ins;
+    std::string output;
+    parse_spec(spec, ins, output);
+    if (static_cast<int>(ins.size()) != n)
+      throw Error(kShapeError, "spec lists " + std::to_string(ins.size()) + " inputs, got " + std::to_string(n) +
+                                   " tensors");
+    std::vector<LTensor> leaves;
+    for (int i = 0; i < n; ++i) {
+      need(ts[i], "tensor");
+      leaves.push_back(as_labelled(ts[i]->t, ins[i]));
+    }
+    LTensor r = contract_network(*c->ctx, leaves, output);
+    *out = wrap(materialize(*c->ctx, r, r.labels));
+  });
+}
+
+int pepsb_implicit(pepsb_ctx* c, int n, pepsb_tensor* const* ts, const char* labels_csv, const char* rows,
+                   const char* cols, const pepsb_tensor* probe, int mode, pepsb_tensor** out) {
+  return guard([&] {
+    need(c, "ctx");
+    ImplicitOp op = make_op(n, ts, labels_csv, rows, cols);
+    if (mode == 2) {
+      *out = wrap(implicit_materialize(*c->ctx, op));
+    } else {
+      need(probe, "probe");
+      *out = wrap(implicit_apply(*c->ctx, op, probe->t, mode == 1));
+    }
+  });
+}
+
+int pepsb_gram_orthogonalize(pepsb_ctx* c, const pepsb_tensor* a, int split, pepsb_tensor** q, pepsb_tensor** r) {
+  return guard([&] {
+    need(c, "ctx");
+    need(a, "tensor");
+    auto [Q, R] = gram_orthogonalize(*c->ctx, a->t, split);
+    *q = wrap(Q);
+    *r = wrap(R);
+  });
+}
+
+int pepsb_svd(pepsb_ctx* c, const pepsb_tensor* a, int split, pepsb_tensor** u, double* s, int64_t s_cap, int64_t* k,
+              pepsb_tensor** v) {
+  return guard([&] {
+    need(c, "ctx");
+    need(a, "tensor");
+    SvdD r = svd(*c->ctx, a->t, split);
+    if (static_cast<int64_t>(r.s.size()) > s_cap) throw Error(kValidationError, "singular value buffer too small");
+    std::memcpy(s, r.s.data(), r.s.size() * sizeof(double));
+    *k = static_cast<int64_t>(r.s.size());
+    *u = wrap(r.u);
+    *v = wrap(r.v);
+  });
+}
+
+int pepsb_randomized_svd(pepsb_ctx* c, int n, pepsb_tensor* const* ts, const char* labels_csv, const char* rows,
+                         const char* cols, const pepsb_trunc* policy, const pepsb_rsvd* cfg, pepsb_tensor** u, double* s,
+                         int64_t s_cap, int64_t* rank, pepsb_tensor** v, int* clamped) {
+  return guard([&] {
+    need(c, "ctx");
+    ImplicitOp op = make_op(n, ts, labels_csv, rows, cols);
+    SvdTripleD r = randomized_svd(*c->ctx, op, trunc_of(policy), rsvd_of(cfg));
+    if (static_cast<int64_t>(r.s.size()) > s_cap) throw Error(kValidationError, "singular value buffer too small");
+    std::memcpy(s, r.s.data(), r.s.size() * sizeof(double));
+    *rank = static_cast<int64_t>(r.s.size());
+    *u = wrap(r.u);
+    *v = wrap(r.v);
+    *clamped = r.rank_clamped;
+  });
+}
+
+int pepsb_einsumsvd(pepsb_ctx* c, int n, pepsb_tensor* const* ts, const char* labels_csv, const char* rows,
+                    const char* cols, const pepsb_trunc* policy, int strategy, int absorb, const pepsb_rsvd* cfg,
+                    pepsb_tensor** t1, pepsb_tensor** t2, double* s, int64_t s_cap, int64_t* rank, int* clamped) {
+  return guard([&] {
+    need(c, "ctx");
+    ImplicitOp op = make_op(n, ts, labels_csv, rows, cols);
+    EinsumsvdResultD r = einsumsvd(*c->ctx, op, trunc_of(policy), strategy, absorb, rsvd_of(cfg));
+    if (static_cast<int64_t>(r.s.size()) > s_cap) throw Error(kValidationError, "singular value buffer too small");
+    std::memcpy(s, r.s.data(), r.s.size() * sizeof(double));
+    *rank = static_cast<int64_t>(r.s.size());
+    *t1 = wrap(r.t1);
+    *t2 = wrap(r.t2);
+    *clamped = r.rank_clamped;
+  });
+}
+
+int pepsb_state_create(pepsb_ctx* c, int rows, int cols, int d, pepsb_tensor* const* sites, pepsb_state** out) {
+  return guard([&] {
+    need(c, "ctx");
+    PepsStateD s;
+    s.rows = rows;
+    s.cols = cols;
+    s.d = d;
+    for (int i = 0; i < rows * cols; ++i) {
+      need(sites[i], "site");
+      s.sites.push_back(sites[i]->t);
+    }
+    s.validate();
+    *out = new pepsb_state{s};
+  });
+}
+
+int pepsb_state_site(const pepsb_state* s, int row, int col, pepsb_tensor** out) {
+  return guard([&] {
+    need(s, "state");
+    if (row < 0 || col < 0 || row >= s->s.rows || col >= s->s.cols) throw Error(kValidationError, "site outside the grid");
+    *out = wrap(s->s.site(row, col));
+  });
+}
+
+void pepsb_state_free(pepsb_state* s) { delete s; }
+
+int pepsb_boundary_create(pepsb_ctx* c, int n, pepsb_tensor* const* sites, const int64_t* phys, pepsb_boundary** out) {
+  return guard([&] {
+    need(c, "ctx");
+    BoundaryD b;
+    for (int i = 0; i < n; ++i) {
+      need(sites[i], "site");
+      if (sites[i]->t.shape.size() != 3) throw Error(kShapeError, "boundary sites must be order 3");
+      b.sites.push_back(sites[i]->t);
+      b.phys.emplace_back(phys[2 * i], phys[2 * i + 1]);
+      if (phys[2 * i] * phys[2 * i + 1] != sites[i]->t.shape[0])
+        throw Error(kShapeError, "boundary phys pair does not match site extent");
+    }
+    b.validate();
+    *out = new pepsb_boundary{b};
+  });
+}
+
+int pepsb_boundary_length(const pepsb_boundary* b) { return b ? static_cast<int>(b->b.sites.size()) : -1; }
+
+int pepsb_boundary_site(const pepsb_boundary* b, int i, pepsb_tensor** out) {
+  return guard([&] {
+    need(b, "boundary");
+    if (i < 0 || i >= static_cast<int>(b->b.sites.size())) throw Error(kValidationError, "site index out of range");
+    *out = wrap(b->b.sites[i]);
+  });
+}
+
+int pepsb_boundary_phys(const pepsb_boundary* b, int64_t* pairs) {
+  return guard([&] {
+    need(b, "boundary");
+    for (size_t i = 0; i < b->b.phys.size(); ++i) {
+      pairs[2 * i] = b->b.phys[i].first;
+      pairs[2 * i + 1] = b->b.phys[i].second;
+    }
+  });
+}
+
+void pepsb_boundary_free(pepsb_boundary* b) { delete b; }
+
+int pepsb_two_layer_first_row(pepsb_ctx* c, const pepsb_state* bra, const pepsb_state* ket, pepsb_boundary** out) {
+  return guard([&] {
+    need(c, "ctx");
+    need(bra, "bra");
+    need(ket, "ket");
+    *out = new pepsb_boundary{two_layer_first_row(*c->ctx, bra->s, ket->s)};
+  });
+}
+
+int pepsb_two_layer_apply_row(pepsb_ctx* c, const pepsb_boundary* top, const pepsb_state* bra, const pepsb_state* ket,
+                              int row, const pepsb_contract_opt* opt, uint64_t tag, pepsb_boundary** out) {
+  return guard([&] {
+    need(c, "ctx");
+    need(top, "top");
+    need(bra, "bra");
+    need(ket, "ket");
+    if (row < 0 || row >= bra->s.rows) throw Error(kValidationError, "row outside the grid");
+    *out = new pepsb_boundary{two_layer_apply_row(*c->ctx, top->b, bra->s, ket->s, row, opt_of(opt), tag)};
+  });
+}
+
+int pepsb_contract_two_layer(pepsb_ctx* c, const pepsb_state* bra, const pepsb_state* ket, const pepsb_contract_opt* opt,
+                             double* re, double* im) {
+  return guard([&] {
+    need(c, "ctx");
+    auto v = contract_two_layer(*c->ctx, bra->s, ket->s, opt_of(opt));
+    *re = v.first;
+    *im = v.second;
+  });
+}
+
+int pepsb_chain_scalar(pepsb_ctx* c, const pepsb_boundary* b, double* re, double* im) {
+  return guard([&] {
+    need(c, "ctx");
+    need(b, "boundary");
+    auto v = chain_scalar(*c->ctx, b->b);
+    *re = v.first;
+    *im = v.second;
+  });
+}
+
+int pepsb_build_row_cache(pepsb_ctx* c, const pepsb_state* s, const pepsb_contract_opt* opt, pepsb_row_cache** out) {
+  return guard([&] {
+    need(c, "ctx");
+    need(s, "state");
+    *out = new pepsb_row_cache{build_row_cache(*c->ctx, s->s, opt_of(opt))};
+  });
+}
+
+int pepsb_row_cache_get(const pepsb_row_cache* rc, int which, int k, pepsb_boundary** out) {
+  return guard([&] {
+    need(rc, "cache");
+    const auto& v = which == 0 ? rc->c.tops : rc->c.bots;
+    if (k < 0 || k >= static_cast<int>(v.size())) throw Error(kValidationError, "row out of range");
+    *out = new pepsb_boundary{v[k]};
+  });
+}
+
+void pepsb_row_cache_free(pepsb_row_cache* c) { delete c; }
+
+int pepsb_band_environment(pepsb_ctx* c, const pepsb_boundary* top, const pepsb_state* bra, const pepsb_state* ket,
+                           int r0, int r1, const pepsb_boundary* bottom, pepsb_band_env** out) {
+  return guard([&] {
+    need(c, "ctx");
+    *out = new pepsb_band_env{band_environment(*c->ctx, top ? &top->b : nullptr, bra->s, ket->s, r0, r1,
+                                               bottom ? &bottom->b : nullptr)};
+  });
+}
+
+int pepsb_band_splice(pepsb_ctx* c, const pepsb_band_env* env, const pepsb_boundary* top, const pepsb_state* bra,
+                      const pepsb_state* ket, const pepsb_boundary* bottom, int npieces, const int* rc,
+                      pepsb_tensor* const* ops, const int* nbonds, const int* bond_ids, int c0, int c1, double* re,
+                      double* im) {
+  return guard([&] {
+    need(c, "ctx");
+    need(env, "env");
+    auto v = band_splice(*c->ctx, env->e, top ? &top->b : nullptr, bra->s, ket->s, bottom ? &bottom->b : nullptr,
+                         pieces_of(npieces, rc, ops, nbonds, bond_ids), c0, c1);
+    *re = v.first;
+    *im = v.second;
+  });
+}
+
+int pepsb_band_value(pepsb_ctx* c, const pepsb_boundary* top, const pepsb_state* bra, const pepsb_state* ket, int r0,
+                     int r1, const pepsb_boundary* bottom, int npieces, const int* rc, pepsb_tensor* const* ops,
+                     const int* nbonds, const int* bond_ids, double* re, double* im) {
+  return guard([&] {
+    need(c, "ctx");
+    auto v = band_value(*c->ctx, top ? &top->b : nullptr, bra->s, ket->s, r0, r1, bottom ? &bottom->b : nullptr,
+                        pieces_of(npieces, rc, ops, nbonds, bond_ids));
+    *re = v.first;
+    *im = v.second;
+  });
+}
+
+void pepsb_band_env_free(pepsb_band_env* e) { delete e; }
+
+}  // extern "C"

@@ -1,0 +1,97 @@
+#include "context.h"
+
+#include <cstdint>
+
+#include "tensor_ops.cuh"
+
+namespace pepsb {
+
+Buf::~Buf() {
+  if (p && ctx) cudaFreeAsync(p, ctx->stream);
+}
+
+int64_t LTensor::extent_of(char c) const {
+  auto pos = labels.find(c);
+  if (pos == std::string::npos) throw Error(kShapeError, std::string("label '") + c + "' not found");
+  return ext[pos];
+}
+
+int64_t LTensor::stride_of(char c) const {
+  auto pos = labels.find(c);
+  if (pos == std::string::npos) throw Error(kShapeError, std::string("label '") + c + "' not found");
+  return str[pos];
+}
+
+std::vector<int64_t> row_major_strides(const std::vector<int64_t>& ext) {
+  std::vector<int64_t> s(ext.size(), 1);
+  for (size_t a = ext.size(); a-- > 1;) s[a - 1] = s[a] * ext[a];
+  return s;
+}
+
+LTensor as_labelled(const DTensor& t, const std::string& labels, bool conj) {
+  if (labels.size() != t.shape.size())
+    throw Error(kShapeError, "label string '" + labels + "' does not match tensor order " +
+                                 std::to_string(t.shape.size()));
+  LTensor l;
+  l.buf = t.buf;
+  l.ptr = t.data();
+  l.labels = labels;
+  l.ext = t.shape;
+  l.str = row_major_strides(t.shape);
+  l.conj = conj;
+  return l;
+}
+
+Ctx::Ctx(int dev) : device(dev) {
+  PEPSB_CUDA(cudaSetDevice(dev));
+  PEPSB_CUDA(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev));
+  PEPSB_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+  cudaMemPool_t pool;
+  PEPSB_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
+  uint64_t thr = UINT64_MAX;
+  PEPSB_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+  PEPSB_CUDA(cudaMalloc(&d_status, 64 * sizeof(int)));
+  PEPSB_CUDA(cudaMemset(d_status, 0, 64 * sizeof(int)));
+  PEPSB_CUDA(cudaMallocHost(&h_status, 64 * sizeof(int)));
+}
+
+Ctx::~Ctx() {
+  if (stream) cudaStreamSynchronize(stream);
+  if (d_status) cudaFree(d_status);
+  if (h_status) cudaFreeHost(h_status);
+  if (stream) cudaStreamDestroy(stream);
+}
+
+BufPtr Ctx::alloc(int64_t n) {
+  auto b = std::make_shared<Buf>();
+  b->n = n;
+  b->ctx = this;
+  if (n > 0) {
+    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&b->p), static_cast<size_t>(n) * sizeof(double2), stream);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      throw Error(kResourceError, "device allocation of " + std::to_string(n) + " complex elements failed: " +
+                                      cudaGetErrorString(e));
+    }
+  }
+  record_intermediate(static_cast<uint64_t>(n));
+  return b;
+}
+
+DTensor Ctx::empty(const std::vector<int64_t>& shape) {
+  DTensor t;
+  t.shape = shape;
+  t.buf = alloc(t.size());
+  return t;
+}
+
+DTensor Ctx::zeros(const std::vector<int64_t>& shape) {
+  DTensor t = empty(shape);
+  fill_zero(t.data(), t.size(), stream);
+  ++launches;
+  return t;
+}
+
+void Ctx::sync() { PEPSB_CUDA(cudaStreamSynchronize(stream)); }
+
+}  // namespace pepsb

@@ -1,0 +1,93 @@
+// Device context, stream-ordered buffers and labelled tensor views.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+
+namespace pepsb {
+
+class Ctx;
+
+// Stream-ordered device buffer (cudaMallocAsync from the device pool; freed
+// with cudaFreeAsync on the context stream when the last reference drops).
+struct Buf {
+  double2* p = nullptr;
+  int64_t n = 0;
+  Ctx* ctx = nullptr;
+  ~Buf();
+};
+using BufPtr = std::shared_ptr<Buf>;
+
+// Contiguous row-major device tensor in the reference's logical axis order.
+struct DTensor {
+  BufPtr buf;
+  std::vector<int64_t> shape;
+  int64_t size() const {
+    int64_t n = 1;
+    for (auto e : shape) n *= e;
+    return n;
+  }
+  double2* data() const { return buf ? buf->p : nullptr; }
+};
+
+// Labelled strided view used by the contraction engine.  Axis a carries
+// label labels[a], extent ext[a], element stride str[a]; conj is applied
+// lazily by the consumer.
+struct LTensor {
+  BufPtr buf;
+  const double2* ptr = nullptr;
+  std::string labels;
+  std::vector<int64_t> ext, str;
+  bool conj = false;
+  int64_t size() const {
+    int64_t n = 1;
+    for (auto e : ext) n *= e;
+    return n;
+  }
+  int64_t extent_of(char c) const;
+  int64_t stride_of(char c) const;
+};
+
+LTensor as_labelled(const DTensor& t, const std::string& labels, bool conj = false);
+std::vector<int64_t> row_major_strides(const std::vector<int64_t>& ext);
+
+class Ctx {
+ public:
+  explicit Ctx(int device);
+  ~Ctx();
+  Ctx(const Ctx&) = delete;
+  Ctx& operator=(const Ctx&) = delete;
+
+  BufPtr alloc(int64_t n);  // n complex elements (uninitialised)
+  DTensor empty(const std::vector<int64_t>& shape);
+  DTensor zeros(const std::vector<int64_t>& shape);
+  void sync();
+
+  int device = 0;
+  int num_sms = 148;
+  cudaStream_t stream = nullptr;
+  // Device status word shared by the small factorization kernels
+  // (SmallStatus bits); read back at the einsumsvd sync points.
+  int* d_status = nullptr;
+  int* h_status = nullptr;  // pinned
+  // Launch accounting (for the bench's gpu_launches claim).
+  int64_t launches = 0;
+  // Cost counters (reference instr::flops definition: 2 per complex MAC,
+  // proj/include/peps/instrument.hpp:19-65).
+  uint64_t flops = 0;
+  uint64_t einsumsvd_flops = 0;
+  uint64_t peak_elements = 0;
+  void record_intermediate(uint64_t n) {
+    if (n > peak_elements) peak_elements = n;
+  }
+  // Options
+  int orth_mode = 0;  // 0: reference-faithful Gram eigh; 1: CholeskyQR2
+};
+
+}  // namespace pepsb

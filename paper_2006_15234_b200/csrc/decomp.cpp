@@ -1,0 +1,574 @@
+// einsumsvd on the device (see decomp.h).
+//
+// randomized_svd (decomposition.cpp:259-306), re-planned for B200:
+//   * the sketch Omega is generated on the device by the counter-based
+//     SplitMix64 stream, bit-identical to random_tensor (tensor.cpp:192-201),
+//     directly in the layout the first contraction of A wants;
+//   * apply / adjoint_apply run as cached contraction plans whose outputs are
+//     written in each other's preferred probe layouts, so no probe is ever
+//     permuted;
+//   * orthogonalisation is the reference's Gram route (G = Y^H Y, eigh, clamp
+//     1e-12 lambda_max, completion; decomposition.cpp:86-193) with the k x k
+//     eigenproblem solved in one thread block, or CholeskyQR2 (orth_mode 1);
+//   * the projected SVD of B = P^H A (linalg.cpp:87-156 wide route) is
+//     CholeskyQR2 of Z = A^* P (shifted CholeskyQR3 when Z is numerically rank
+//     deficient) followed by a one-sided Jacobi SVD of the k x k R^H;
+//   * absorption weights and rank slicing are folded into the k x k factors,
+//     and t1 / t2 are scattered straight into the reference layouts
+//     (row axes..., rank) / (rank, col axes...).
+#include "decomp.h"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <set>
+
+#include "smalldense.cuh"
+#include "tensor_ops.cuh"
+#include "zgemm.cuh"
+
+namespace pepsb {
+
+namespace {
+
+bool has(const std::string& s, char c) { return s.find(c) != std::string::npos; }
+
+int64_t prod(const std::vector<int64_t>& v) {
+  int64_t n = 1;
+  for (auto e : v) n *= e;
+  return n;
+}
+
+// Row-major matrix product C (M x N) = op(A) op(B) with A given as M x K
+// (transA: K x M) and B as K x N (transB: N x K), optional conjugation.
+void mm(Ctx& ctx, double2* C, const double2* A, bool transA, bool conjA, const double2* B, bool transB,
+        bool conjB, int64_t M, int64_t N, int64_t K) {
+  ZgemmParams p;
+  p.A = A;
+  p.B = B;
+  p.C = C;
+  p.M = M;
+  p.N = N;
+  p.K = K;
+  p.sAi = transA ? 1 : K;
+  p.sAk = transA ? M : 1;
+  p.sBk = transB ? 1 : N;
+  p.sBj = transB ? K : 1;
+  p.conjA = conjA;
+  p.conjB = conjB;
+  p.nr = 1;
+  p.rext[0] = M;
+  p.rstr[0] = N;
+  p.nc = 1;
+  p.cext[0] = N;
+  p.cstr[0] = 1;
+  int64_t ws = zgemm_plan_splits(p, ctx.num_sms);
+  BufPtr work;
+  if (ws > 0) {
+    work = ctx.alloc(ws);
+    p.work = work->p;
+  }
+  zgemm_launch(p, ctx.stream);
+  ctx.launches += p.splits > 1 ? 2 : 1;
+  ctx.flops += 2ull * M * N * K;
+}
+
+LTensor wrap(const BufPtr& b, const std::string& labels, const std::vector<int64_t>& ext, bool conj = false) {
+  LTensor l;
+  l.buf = b;
+  l.ptr = b->p;
+  l.labels = labels;
+  l.ext = ext;
+  l.str = row_major_strides(ext);
+  l.conj = conj;
+  return l;
+}
+
+std::string unused_labels(const std::string& used, int n) {
+  std::string out;
+  const std::string pool = "ABCDEFGHIJKLMNOPQRSTUVWXYZabcdefghijklmnopqrstuvwxyz0123456789";
+  for (char c : pool) {
+    if ((int)out.size() == n) break;
+    if (!has(used, c)) out += c;
+  }
+  if ((int)out.size() < n) throw Error(kShapeError, "no free label available");
+  return out;
+}
+
+void read_status(Ctx& ctx) {
+  PEPSB_CUDA(cudaMemcpyAsync(ctx.h_status, ctx.d_status, sizeof(int), cudaMemcpyDeviceToHost, ctx.stream));
+}
+
+void clear_status(Ctx& ctx) { PEPSB_CUDA(cudaMemsetAsync(ctx.d_status, 0, sizeof(int), ctx.stream)); }
+
+void raise_status(int st, bool gram_stage) {
+  if (st & kSmallZeroGram) throw Error(kNumericalError, "gram orthogonalization of a zero operator");
+  if (st & kSmallNotHermitian) throw Error(kValidationError, "matrix is not Hermitian within tolerance");
+  if (st & kSmallCompletionExhausted) throw Error(kNumericalError, "orthonormal completion exhausted basis");
+  (void)gram_stage;
+}
+
+// Gram orthogonalisation of a contiguous rows x k matrix (in place layout):
+// returns Q with the same labels/layout.  decomposition.cpp:160-193.
+LTensor orth(Ctx& ctx, const LTensor& Y) {
+  const int64_t k = Y.ext.back();
+  const int64_t rows = Y.size() / k;
+  BufPtr G = ctx.alloc(k * k);
+  mm(ctx, G->p, Y.ptr, true, true, Y.ptr, false, false, k, k, rows);
+  BufPtr Q = ctx.alloc(rows * k);
+  if (ctx.orth_mode == 1) {
+    BufPtr R = ctx.alloc(k * k), Ri = ctx.alloc(k * k), G2 = ctx.alloc(k * k), Q1 = ctx.alloc(rows * k);
+    chol_factors(G->p, static_cast<int>(k), 0.0, R->p, Ri->p, ctx.d_status, ctx.stream);
+    mm(ctx, Q1->p, Y.ptr, false, false, Ri->p, false, false, rows, k, k);
+    mm(ctx, G2->p, Q1->p, true, true, Q1->p, false, false, k, k, rows);
+    chol_factors(G2->p, static_cast<int>(k), 0.0, R->p, Ri->p, ctx.d_status, ctx.stream);
+    mm(ctx, Q->p, Q1->p, false, false, Ri->p, false, false, rows, k, k);
+    ctx.launches += 2;
+  } else {
+    BufPtr P = ctx.alloc(k * k), R = ctx.alloc(k * k), def = ctx.alloc((k + 2 + 1) / 2 + 1);
+    int* d_def = reinterpret_cast<int*>(def->p);
+    int* d_any = d_def + k;
+    BufPtr work;
+    if (2 * k * k * 16 > 200 * 1024) work = ctx.alloc(2 * k * k);
+    gram_factors(G->p, static_cast<int>(k), P->p, R->p, d_def, d_any, ctx.d_status, work ? work->p : nullptr,
+                 ctx.stream);
+    mm(ctx, Q->p, Y.ptr, false, Y.conj, P->p, false, false, rows, k, k);
+    complete_columns(Q->p, rows, static_cast<int>(k), d_def, d_any, ctx.d_status, ctx.stream);
+    ctx.launches += 2;
+  }
+  LTensor out = Y;
+  out.buf = Q;
+  out.ptr = Q->p;
+  out.conj = false;
+  out.str = row_major_strides(out.ext);
+  return out;
+}
+
+struct Projected {
+  BufPtr Ut, Wh, Rinv;  // k x k each
+  std::vector<double> s;
+};
+
+// SVD of B = Z^H (Z: rows x k contiguous): CholeskyQR2 (+shift) then Jacobi on R^H.
+Projected projected_svd(Ctx& ctx, const LTensor& Z) {
+  const int64_t k = Z.ext.back();
+  const int64_t rows = Z.size() / k;
+  const int ki = static_cast<int>(k);
+  auto gram = [&](const double2* X) {
+    BufPtr G = ctx.alloc(k * k);
+    mm(ctx, G->p, X, true, true, X, false, false, k, k, rows);
+    return G;
+  };
+  BufPtr G1 = gram(Z.ptr);
+  BufPtr R1 = ctx.alloc(k * k), R1i = ctx.alloc(k * k);
+  chol_factors(G1->p, ki, 0.0, R1->p, R1i->p, ctx.d_status, ctx.stream);
+  ++ctx.launches;
+  read_status(ctx);
+  ctx.sync();
+  int st = *ctx.h_status;
+  raise_status(st, true);
+  bool shifted = false;
+  if (st & kSmallCholBreakdown) {
+    clear_status(ctx);
+    // shifted CholeskyQR3 (Fukaya et al.): s = 11 (m n + n (n + 1)) u ||Z||_2^2, ||Z||_2^2 <= trace(G)
+    const double u = 1.1102230246251565e-16;
+    const double shift_rel = 11.0 * (static_cast<double>(rows) * k + static_cast<double>(k) * (k + 1)) * u;
+    chol_factors(G1->p, ki, shift_rel, R1->p, R1i->p, ctx.d_status, ctx.stream);
+    ++ctx.launches;
+    shifted = true;
+  }
+  BufPtr Q1 = ctx.alloc(rows * k);
+  mm(ctx, Q1->p, Z.ptr, false, false, R1i->p, false, false, rows, k, k);
+  BufPtr G2 = gram(Q1->p);
+  BufPtr R2 = ctx.alloc(k * k), R2i = ctx.alloc(k * k);
+  chol_factors(G2->p, ki, 0.0, R2->p, R2i->p, ctx.d_status, ctx.stream);
+  ++ctx.launches;
+  BufPtr R = ctx.alloc(k * k), Ri = ctx.alloc(k * k);
+  if (!shifted) {
+    mm(ctx, R->p, R2->p, false, false, R1->p, false, false, k, k, k);
+    mm(ctx, Ri->p, R1i->p, false, false, R2i->p, false, false, k, k, k);
+  } else {
+    BufPtr Q2 = ctx.alloc(rows * k);
+    mm(ctx, Q2->p, Q1->p, false, false, R2i->p, false, false, rows, k, k);
+    BufPtr G3 = gram(Q2->p);
+    BufPtr R3 = ctx.alloc(k * k), R3i = ctx.alloc(k * k), T = ctx.alloc(k * k);
+    chol_factors(G3->p, ki, 0.0, R3->p, R3i->p, ctx.d_status, ctx.stream);
+    ++ctx.launches;
+    mm(ctx, T->p, R3->p, false, false, R2->p, false, false, k, k, k);
+    mm(ctx, R->p, T->p, false, false, R1->p, false, false, k, k, k);
+    mm(ctx, T->p, R1i->p, false, false, R2i->p, false, false, k, k, k);
+    mm(ctx, Ri->p, T->p, false, false, R3i->p, false, false, k, k, k);
+  }
+  // Rh = R^H
+  LTensor Rl = wrap(R, "ab", {k, k}, true);
+  LTensor Rh = reduce_to(ctx, Rl, "ba");
+  Projected out;
+  out.Ut = ctx.alloc(k * k);
+  out.Wh = ctx.alloc(k * k);
+  out.Rinv = Ri;
+  BufPtr sdev = ctx.alloc((k + 1) / 2);
+  double* d_s = reinterpret_cast<double*>(sdev->p);
+  BufPtr work;
+  int64_t ws = small_svd_workspace(ki, ki, 1);
+  if (ws) work = ctx.alloc(ws);
+  small_svd(Rh.ptr, 0, ki, ki, ki, out.Ut->p, 0, d_s, 0, out.Wh->p, 0, 1, ctx.d_status, work ? work->p : nullptr,
+            ctx.stream);
+  ++ctx.launches;
+  out.s.resize(k);
+  PEPSB_CUDA(cudaMemcpyAsync(out.s.data(), d_s, k * sizeof(double), cudaMemcpyDeviceToHost, ctx.stream));
+  read_status(ctx);
+  ctx.sync();
+  st = *ctx.h_status;
+  raise_status(st, false);
+  if (st & kSmallCholBreakdown) throw Error(kNumericalError, "SVD failed to converge (CholeskyQR breakdown)");
+  return out;
+}
+
+BufPtr upload_doubles(Ctx& ctx, const std::vector<double>& w) {
+  BufPtr b = ctx.alloc((static_cast<int64_t>(w.size()) + 1) / 2 + 1);
+  PEPSB_CUDA(cudaMemcpyAsync(b->p, w.data(), w.size() * sizeof(double), cudaMemcpyHostToDevice, ctx.stream));
+  return b;
+}
+
+void absorb_weights(const std::vector<double>& s, int absorb, std::vector<double>& wl, std::vector<double>& wr) {
+  wl.assign(s.size(), 1.0);
+  wr.assign(s.size(), 1.0);
+  for (size_t i = 0; i < s.size(); ++i) {
+    if (absorb == kSplit) wl[i] = wr[i] = std::sqrt(s[i]);
+    else if (absorb == kLeft) wl[i] = s[i];
+    else if (absorb == kRight) wr[i] = s[i];
+  }
+}
+
+// Core of randomized_svd / einsumsvd(implicit_rsvd).  Weights (absorb) are
+// applied when `absorb` >= 0, otherwise plain U, S, V are returned.
+EinsumsvdResultD rsvd_core(Ctx& ctx, const ImplicitOp& op, const Trunc& policy, const Rsvd& cfg, int absorb,
+                           const std::vector<int>& t1_perm) {
+  if (policy.max_rank < 1) throw Error(kValidationError, "randomized svd needs target rank >= 1");
+  const int64_t mindim = std::min(op.row_extent(), op.col_extent());
+  const int64_t target = static_cast<int64_t>(std::min<uint64_t>(policy.max_rank, static_cast<uint64_t>(mindim)));
+  const bool clamped = policy.max_rank > static_cast<uint64_t>(mindim);
+  const int64_t probe = std::min<int64_t>(target + static_cast<int64_t>(effective_oversample(cfg, target)), mindim);
+  const char X = op.fresh_label();
+  std::string used = op.rows + op.cols + X;
+  for (auto& l : op.labels) used += l;
+  const std::string extra = unused_labels(used, 2);
+  const char RK = extra[0], LL = extra[1];
+
+  const size_t nt = op.tensors.size();
+  std::vector<LeafMeta> meta_ap, meta_adj;
+  for (size_t i = 0; i < nt; ++i) {
+    meta_ap.push_back({op.labels[i], op.tensors[i].shape});
+    meta_adj.push_back({op.labels[i], op.tensors[i].shape});
+  }
+  std::vector<int64_t> qshape = op.col_shape(), pshape = op.row_shape();
+  qshape.push_back(probe);
+  pshape.push_back(probe);
+  meta_ap.push_back({op.cols + X, qshape});
+  meta_adj.push_back({op.rows + X, pshape});
+  ContractionPlan plan_ap(meta_ap, op.rows + X, static_cast<int>(nt), X);
+  ContractionPlan plan_adj(meta_adj, op.cols + X, static_cast<int>(nt), X);
+  plan_ap.finalize(plan_adj.flexible_order());
+  plan_adj.finalize(plan_ap.flexible_order());
+  plan_ap.cache_static = plan_adj.cache_static = true;
+
+  std::vector<LTensor> leaves_ap, leaves_adj;
+  for (size_t i = 0; i < nt; ++i) {
+    leaves_ap.push_back(as_labelled(op.tensors[i], op.labels[i], op.conj[i]));
+    leaves_adj.push_back(as_labelled(op.tensors[i], op.labels[i], !op.conj[i]));
+  }
+  leaves_ap.push_back(LTensor());
+  leaves_adj.push_back(LTensor());
+
+  // Omega = random_tensor(col_shape + [probe], seed) generated in the probe layout.
+  const std::string qord = plan_ap.flexible_order();
+  std::vector<int64_t> pext, lstr;
+  {
+    const std::string logical = op.cols + X;
+    std::vector<int64_t> lst = row_major_strides(qshape);
+    for (char c : qord) {
+      auto pos = logical.find(c);
+      pext.push_back(qshape[pos]);
+      lstr.push_back(lst[pos]);
+    }
+  }
+  BufPtr om = ctx.alloc(prod(qshape));
+  random_fill(om->p, static_cast<int>(qord.size()), pext.data(), lstr.data(), cfg.seed, 0, ctx.stream);
+  ++ctx.launches;
+  LTensor q = wrap(om, qord, pext);
+  clear_status(ctx);
+
+  auto apply = [&](const LTensor& qq) {
+    leaves_ap.back() = qq;
+    return plan_ap.execute(ctx, leaves_ap);
+  };
+  auto adjoint = [&](const LTensor& pp) {
+    leaves_adj.back() = pp;
+    return plan_adj.execute(ctx, leaves_adj);
+  };
+
+  LTensor p = orth(ctx, apply(q));
+  for (int i = 0; i < cfg.power_iters; ++i) {
+    q = orth(ctx, adjoint(p));
+    p = orth(ctx, apply(q));
+  }
+  LTensor z = adjoint(p);
+  q = LTensor();
+  Projected pr = projected_svd(ctx, z);
+
+  Trunc pol = policy;
+  int64_t rank = static_cast<int64_t>(retained_rank(pr.s, pol));
+  rank = std::min(rank, target);
+  std::vector<double> s(pr.s.begin(), pr.s.begin() + rank);
+  std::vector<double> wl, wr;
+  if (absorb >= 0) absorb_weights(s, absorb, wl, wr);
+  else {
+    wl.assign(rank, 1.0);
+    wr.assign(rank, 1.0);
+  }
+  BufPtr dwl = upload_doubles(ctx, wl), dwr = upload_doubles(ctx, wr);
+  const int64_t k = probe;
+  // Uw = Ut[:, :rank] diag(wl)   (k x rank)
+  BufPtr Uw = ctx.alloc(k * rank);
+  slice_scale_cols(Uw->p, pr.Ut->p, k, rank, k, reinterpret_cast<double*>(dwl->p), 0, ctx.stream);
+  // Whw = diag(wr) Wh[:rank, :]  (rank x k)
+  BufPtr Whw = ctx.alloc(rank * k);
+  slice_scale_cols(Whw->p, pr.Wh->p, rank, k, k, nullptr, 0, ctx.stream);
+  scale_axis(Whw->p, rank * k, k, rank, reinterpret_cast<double*>(dwr->p), ctx.stream);
+  ctx.launches += 3;
+  // Mc = conj(Rinv) Whw^T  (k x rank):  Mc[a][j] = sum_l conj(Rinv[a][l]) Whw[j][l]
+  LTensor Mc = pairwise_gemm(ctx, wrap(pr.Rinv, std::string(1, X) + LL, {k, k}, true),
+                             wrap(Whw, std::string(1, RK) + LL, {rank, k}), "", std::string(1, LL),
+                             std::string(1, X) + RK);
+  // t1 = P Uw -> (row axes..., rank);  t2 = conj(Z) Mc -> (rank, col axes...)
+  std::string t1_order = op.rows + RK;
+  if (!t1_perm.empty()) {
+    std::string o;
+    for (int a : t1_perm) o += t1_order[a];
+    t1_order = o;
+  }
+  LTensor t1 = pairwise_gemm(ctx, p, wrap(Uw, std::string(1, X) + RK, {k, rank}), "", std::string(1, X),
+                             t1_order);
+  LTensor t2 = pairwise_gemm(ctx, [&] { LTensor zc = z; zc.conj = true; return zc; }(), Mc, "",
+                             std::string(1, X), std::string(1, RK) + op.cols);
+  EinsumsvdResultD out;
+  out.t1.buf = t1.buf;
+  out.t1.shape = t1.ext;
+  out.t2.buf = t2.buf;
+  out.t2.shape = t2.ext;
+  out.s = s;
+  out.rank_clamped = clamped;
+  return out;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------- ImplicitOp
+
+ImplicitOp::ImplicitOp(std::vector<DTensor> t, std::vector<std::string> l, std::string r, std::string c,
+                       std::vector<bool> cj)
+    : tensors(std::move(t)), labels(std::move(l)), rows(std::move(r)), cols(std::move(c)), conj(std::move(cj)) {
+  if (conj.empty()) conj.assign(tensors.size(), false);
+  if (tensors.size() != labels.size() || conj.size() != tensors.size())
+    throw Error(kShapeError, "one label string per tensor required");
+  std::map<char, int64_t> ext;
+  std::map<char, int> count;
+  for (size_t i = 0; i < tensors.size(); ++i) {
+    if (labels[i].size() != tensors[i].shape.size())
+      throw Error(kShapeError, "label string '" + labels[i] + "' does not match tensor order");
+    for (size_t a = 0; a < labels[i].size(); ++a) {
+      char ch = labels[i][a];
+      auto [it, ins] = ext.emplace(ch, tensors[i].shape[a]);
+      if (!ins && it->second != tensors[i].shape[a])
+        throw Error(kShapeError, std::string("extent mismatch on label '") + ch + "'");
+      ++count[ch];
+    }
+  }
+  for (char ch : rows)
+    if (has(cols, ch)) throw Error(kShapeError, std::string("label '") + ch + "' in both row and column groups");
+  auto check_open = [&](const std::string& g) {
+    for (char ch : g) {
+      auto it = count.find(ch);
+      if (it == count.end() || it->second != 1)
+        throw Error(kShapeError, std::string("open label '") + ch + "' must appear exactly once");
+    }
+  };
+  check_open(rows);
+  check_open(cols);
+  for (char ch : rows) row_shape_.push_back(ext[ch]);
+  for (char ch : cols) col_shape_.push_back(ext[ch]);
+}
+
+int64_t ImplicitOp::row_extent() const { return prod(row_shape_); }
+int64_t ImplicitOp::col_extent() const { return prod(col_shape_); }
+
+char ImplicitOp::fresh_label() const {
+  std::string used = rows + cols;
+  for (auto& l : labels) used += l;
+  for (char ch = 'A'; ch <= 'Z'; ++ch)
+    if (!has(used, ch)) return ch;
+  for (char ch = 'a'; ch <= 'z'; ++ch)
+    if (!has(used, ch)) return ch;
+  throw Error(kShapeError, "no free label available");
+}
+
+DTensor implicit_apply(Ctx& ctx, const ImplicitOp& op, const DTensor& q, bool adjoint) {
+  const auto& shp = adjoint ? op.row_shape() : op.col_shape();
+  if (q.shape.size() != shp.size() + 1)
+    throw Error(kShapeError, adjoint ? "probe order must be row order + 1" : "probe order must be column order + 1");
+  for (size_t a = 0; a < shp.size(); ++a)
+    if (q.shape[a] != shp[a])
+      throw Error(kShapeError, std::string("probe shape mismatch on ") + (adjoint ? "row" : "column") + " axis " +
+                                   std::to_string(a));
+  const char f = op.fresh_label();
+  std::vector<LTensor> leaves;
+  for (size_t i = 0; i < op.tensors.size(); ++i)
+    leaves.push_back(as_labelled(op.tensors[i], op.labels[i], adjoint ? !op.conj[i] : op.conj[i]));
+  leaves.push_back(as_labelled(q, (adjoint ? op.rows : op.cols) + f));
+  LTensor r = contract_network(ctx, leaves, (adjoint ? op.cols : op.rows) + f);
+  return materialize(ctx, r, r.labels);
+}
+
+DTensor implicit_materialize(Ctx& ctx, const ImplicitOp& op) {
+  std::vector<LTensor> leaves;
+  for (size_t i = 0; i < op.tensors.size(); ++i) leaves.push_back(as_labelled(op.tensors[i], op.labels[i], op.conj[i]));
+  LTensor r = contract_network(ctx, leaves, op.rows + op.cols);
+  return materialize(ctx, r, r.labels);
+}
+
+// ---------------------------------------------------------------------------- public
+
+size_t effective_oversample(const Rsvd& cfg, size_t target) {
+  if (cfg.oversample >= 0) return static_cast<size_t>(cfg.oversample);
+  return std::max<size_t>(5, static_cast<size_t>(std::ceil(0.1 * static_cast<double>(target))));
+}
+
+size_t retained_rank(const std::vector<double>& s, const Trunc& policy) {
+  if (s.empty()) return 0;
+  const double floor = policy.rel_cutoff * s[0];
+  size_t above = 0;
+  for (double v : s)
+    if (v >= floor) ++above;
+  const size_t cap = policy.max_rank == 0 ? s.size() : static_cast<size_t>(std::min<uint64_t>(policy.max_rank, SIZE_MAX));
+  return std::max<size_t>(1, std::min(above, cap));
+}
+
+std::pair<DTensor, DTensor> gram_orthogonalize(Ctx& ctx, const DTensor& a, int split) {
+  const int order = static_cast<int>(a.shape.size());
+  if (split < 1 || split >= order) throw Error(kShapeError, "gram split must satisfy 1 <= split < order");
+  std::vector<int64_t> rs(a.shape.begin(), a.shape.begin() + split), cs(a.shape.begin() + split, a.shape.end());
+  const int64_t rows = prod(rs), cols = prod(cs);
+  if (rows < cols) throw Error(kShapeError, "gram orthogonalization needs row extent >= col extent");
+  if (cols > 256) throw Error(kShapeError, "gram orthogonalization: col extent > 256 not supported on device");
+  clear_status(ctx);
+  BufPtr G = ctx.alloc(cols * cols);
+  mm(ctx, G->p, a.data(), true, true, a.data(), false, false, cols, cols, rows);
+  BufPtr P = ctx.alloc(cols * cols), def = ctx.alloc(cols / 2 + 2);
+  int* d_def = reinterpret_cast<int*>(def->p);
+  int* d_any = d_def + cols;
+  BufPtr work;
+  if (2 * cols * cols * 16 > 200 * 1024) work = ctx.alloc(2 * cols * cols);
+  DTensor R;
+  std::vector<int64_t> rshape = cs;
+  rshape.insert(rshape.end(), cs.begin(), cs.end());
+  R.shape = rshape;
+  R.buf = ctx.alloc(cols * cols);
+  gram_factors(G->p, static_cast<int>(cols), P->p, R.data(), d_def, d_any, ctx.d_status, work ? work->p : nullptr,
+               ctx.stream);
+  DTensor Q;
+  std::vector<int64_t> qshape = rs;
+  qshape.insert(qshape.end(), cs.begin(), cs.end());
+  Q.shape = qshape;
+  Q.buf = ctx.alloc(rows * cols);
+  mm(ctx, Q.data(), a.data(), false, false, P->p, false, false, rows, cols, cols);
+  complete_columns(Q.data(), rows, static_cast<int>(cols), d_def, d_any, ctx.d_status, ctx.stream);
+  ctx.launches += 2;
+  read_status(ctx);
+  ctx.sync();
+  raise_status(*ctx.h_status, true);
+  return {Q, R};
+}
+
+SvdD svd(Ctx& ctx, const DTensor& t, int split) {
+  const int order = static_cast<int>(t.shape.size());
+  if (split < 1 || split >= order) throw Error(kShapeError, "svd split must satisfy 1 <= split < order");
+  std::vector<int64_t> rs(t.shape.begin(), t.shape.begin() + split), cs(t.shape.begin() + split, t.shape.end());
+  const int64_t m = prod(rs), n = prod(cs), k = std::min(m, n);
+  clear_status(ctx);
+  SvdD out;
+  std::vector<int64_t> us = rs, vs = {k};
+  us.push_back(k);
+  vs.insert(vs.end(), cs.begin(), cs.end());
+  out.u = ctx.empty(us);
+  out.v = ctx.empty(vs);
+  BufPtr sd = ctx.alloc(k / 2 + 1);
+  BufPtr work;
+  int64_t ws = small_svd_workspace(static_cast<int>(m), static_cast<int>(n), 1);
+  if (ws) work = ctx.alloc(ws);
+  small_svd(t.data(), 0, static_cast<int>(m), static_cast<int>(n), static_cast<int>(n), out.u.data(), 0,
+            reinterpret_cast<double*>(sd->p), 0, out.v.data(), 0, 1, ctx.d_status, work ? work->p : nullptr,
+            ctx.stream);
+  ++ctx.launches;
+  out.s.resize(k);
+  PEPSB_CUDA(cudaMemcpyAsync(out.s.data(), sd->p, k * sizeof(double), cudaMemcpyDeviceToHost, ctx.stream));
+  read_status(ctx);
+  ctx.sync();
+  raise_status(*ctx.h_status, false);
+  return out;
+}
+
+SvdTripleD randomized_svd(Ctx& ctx, const ImplicitOp& op, const Trunc& policy, const Rsvd& cfg) {
+  EinsumsvdResultD r = rsvd_core(ctx, op, policy, cfg, -1, {});
+  return SvdTripleD{r.t1, r.t2, r.s, r.rank_clamped};
+}
+
+EinsumsvdResultD einsumsvd(Ctx& ctx, const ImplicitOp& op, const Trunc& policy, int strategy, int absorb,
+                           const Rsvd& cfg, const std::vector<int>& t1_perm) {
+  if (op.rows.empty() || op.cols.empty())
+    throw Error(kShapeError, "einsumsvd needs non-empty row and column groups");
+  const uint64_t f0 = ctx.flops;
+  EinsumsvdResultD out;
+  if (strategy == kImplicitRsvd) {
+    int saved = ctx.orth_mode;
+    try {
+      out = rsvd_core(ctx, op, policy, cfg, absorb, t1_perm);
+    } catch (const Error& e) {
+      ctx.orth_mode = saved;
+      throw;
+    }
+  } else {
+    DTensor mat = implicit_materialize(ctx, op);
+    const int split = static_cast<int>(op.rows.size());
+    SvdD full = svd(ctx, mat, split);
+    const size_t rank = retained_rank(full.s, policy);
+    out.s.assign(full.s.begin(), full.s.begin() + rank);
+    const int64_t m = op.row_extent(), n = op.col_extent(), k = std::min(m, n);
+    out.rank_clamped = policy.max_rank > static_cast<uint64_t>(k);
+    std::vector<double> wl, wr;
+    absorb_weights(out.s, absorb, wl, wr);
+    BufPtr dwl = upload_doubles(ctx, wl), dwr = upload_doubles(ctx, wr);
+    const int64_t r = static_cast<int64_t>(rank);
+    std::vector<int64_t> s1 = op.row_shape(), s2 = {r};
+    s1.push_back(r);
+    for (auto e : op.col_shape()) s2.push_back(e);
+    out.t1 = ctx.empty(s1);
+    out.t2 = ctx.empty(s2);
+    slice_scale_cols(out.t1.data(), full.u.data(), m, r, k, reinterpret_cast<double*>(dwl->p), 0, ctx.stream);
+    slice_scale_cols(out.t2.data(), full.v.data(), r, n, n, nullptr, 0, ctx.stream);
+    scale_axis(out.t2.data(), r * n, n, r, reinterpret_cast<double*>(dwr->p), ctx.stream);
+    ctx.launches += 3;
+    if (!t1_perm.empty()) {
+      std::string lab = unused_labels("", static_cast<int>(t1_perm.size()));
+      std::string o;
+      for (int a : t1_perm) o += lab[a];
+      LTensor r1 = reduce_to(ctx, as_labelled(out.t1, lab), o);
+      out.t1.buf = r1.buf;
+      out.t1.shape = r1.ext;
+    }
+  }
+  ctx.einsumsvd_flops += ctx.flops - f0;
+  return out;
+}
+
+}  // namespace pepsb

@@ -1,0 +1,86 @@
+// einsumsvd and its building blocks on the device (the hot path).
+//
+// Mirrors proj/include/peps/implicit.hpp and proj/include/peps/decomposition.hpp:
+// ImplicitOperator{tensors, labels, row_labels, col_labels} with apply /
+// adjoint_apply / materialize; gram_orthogonalize; randomized_svd; einsumsvd.
+#pragma once
+
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "context.h"
+#include "engine.h"
+
+namespace pepsb {
+
+struct Trunc {
+  uint64_t max_rank = 0;  // 0: unbounded
+  double rel_cutoff = 1e-14;
+};
+
+struct Rsvd {
+  int power_iters = 2;
+  int oversample = -1;  // < 0: max(5, ceil(0.1 * target))
+  uint64_t seed = 0;
+};
+
+enum Strategy { kExact = 0, kImplicitRsvd = 1 };
+enum Absorb { kSplit = 0, kLeft = 1, kRight = 2 };
+
+// implicit.hpp:15-44; validation as implicit.cpp:10-49.  `conj[i]` marks a
+// tensor to be used conjugated (lazily — no copy), e.g. the bra layer.
+class ImplicitOp {
+ public:
+  ImplicitOp(std::vector<DTensor> tensors, std::vector<std::string> labels, std::string rows,
+             std::string cols, std::vector<bool> conj = {});
+  const std::vector<int64_t>& row_shape() const { return row_shape_; }
+  const std::vector<int64_t>& col_shape() const { return col_shape_; }
+  int64_t row_extent() const;
+  int64_t col_extent() const;
+  char fresh_label() const;  // implicit.cpp:54-64
+
+  std::vector<DTensor> tensors;
+  std::vector<std::string> labels;
+  std::string rows, cols;
+  std::vector<bool> conj;
+
+ private:
+  std::vector<int64_t> row_shape_, col_shape_;
+};
+
+DTensor implicit_apply(Ctx& ctx, const ImplicitOp& op, const DTensor& q, bool adjoint);
+DTensor implicit_materialize(Ctx& ctx, const ImplicitOp& op);
+
+struct SvdTripleD {
+  DTensor u, v;
+  std::vector<double> s;
+  bool rank_clamped = false;
+};
+
+struct EinsumsvdResultD {
+  DTensor t1, t2;
+  std::vector<double> s;
+  bool rank_clamped = false;
+};
+
+struct SvdD {
+  DTensor u, v;
+  std::vector<double> s;
+};
+
+// decomposition.cpp:160-193
+std::pair<DTensor, DTensor> gram_orthogonalize(Ctx& ctx, const DTensor& a, int split);
+// decomposition.cpp:259-306
+SvdTripleD randomized_svd(Ctx& ctx, const ImplicitOp& op, const Trunc& policy, const Rsvd& cfg);
+// decomposition.cpp:308-352
+// `t1_perm` (optional) permutes t1's axes on output, like Tensor::permute.
+EinsumsvdResultD einsumsvd(Ctx& ctx, const ImplicitOp& op, const Trunc& policy, int strategy,
+                           int absorb, const Rsvd& cfg, const std::vector<int>& t1_perm = {});
+// linalg.cpp:193-207 (thin SVD of a matricised tensor; small matrices)
+SvdD svd(Ctx& ctx, const DTensor& t, int split);
+
+size_t retained_rank(const std::vector<double>& s, const Trunc& policy);
+size_t effective_oversample(const Rsvd& cfg, size_t target);
+
+}  // namespace pepsb

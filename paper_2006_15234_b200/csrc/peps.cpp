@@ -1,0 +1,410 @@
+// Two-layer boundary contraction, cached environments and band zipper on the
+// device.  Semantics follow proj/src/contraction.cpp:254-338,345-650,
+// proj/src/mps.cpp:102-110 and proj/src/observables.cpp:261-333; every
+// contraction runs through the device engine, every truncation through the
+// device einsumsvd.  Tensors stay resident in HBM between calls.
+#include "peps.h"
+
+#include <algorithm>
+#include <cstring>
+
+#include "tensor_ops.cuh"
+
+namespace pepsb {
+
+namespace {
+
+DTensor reshape(const DTensor& t, std::vector<int64_t> shape) {
+  int64_t n = 1;
+  for (auto e : shape) n *= e;
+  if (n != t.size()) throw Error(kShapeError, "reshape changes element count");
+  DTensor r = t;
+  r.shape = std::move(shape);
+  return r;
+}
+
+LTensor scalar_one(Ctx& ctx) {
+  LTensor l;
+  l.buf = ctx.alloc(1);
+  l.ptr = l.buf->p;
+  const double one[2] = {1.0, 0.0};
+  PEPSB_CUDA(cudaMemcpyAsync(l.buf->p, one, sizeof(one), cudaMemcpyHostToDevice, ctx.stream));
+  return l;
+}
+
+std::pair<double, double> read_scalar(Ctx& ctx, const LTensor& t) {
+  if (t.size() != 1) throw Error(kShapeError, "scalar_value on non-scalar tensor");
+  double v[2];
+  PEPSB_CUDA(cudaMemcpyAsync(v, t.ptr, sizeof(v), cudaMemcpyDeviceToHost, ctx.stream));
+  ctx.sync();
+  return {v[0], v[1]};
+}
+
+}  // namespace
+
+void PepsStateD::validate() const {
+  if (rows <= 0 || cols <= 0) throw Error(kValidationError, "PEPS grid must be non-empty");
+  if (static_cast<int>(sites.size()) != rows * cols) throw Error(kShapeError, "site count does not match grid");
+  for (int r = 0; r < rows; ++r)
+    for (int c = 0; c < cols; ++c) {
+      const auto& t = site(r, c).shape;
+      if (t.size() != 5) throw Error(kShapeError, "PEPS site must be order 5");
+      if (t[0] != d) throw Error(kShapeError, "physical dimension mismatch");
+      if (r == 0 && t[1] != 1) throw Error(kShapeError, "top boundary bond must be 1");
+      if (c == 0 && t[2] != 1) throw Error(kShapeError, "left boundary bond must be 1");
+      if (r == rows - 1 && t[3] != 1) throw Error(kShapeError, "bottom boundary bond must be 1");
+      if (c == cols - 1 && t[4] != 1) throw Error(kShapeError, "right boundary bond must be 1");
+      if (r + 1 < rows && t[3] != site(r + 1, c).shape[1]) throw Error(kShapeError, "vertical bond mismatch");
+      if (c + 1 < cols && t[4] != site(r, c + 1).shape[2]) throw Error(kShapeError, "horizontal bond mismatch");
+    }
+}
+
+void BoundaryD::validate() const {
+  if (sites.empty()) throw Error(kShapeError, "empty MPS");
+  if (sites.front().shape[1] != 1 || sites.back().shape[2] != 1)
+    throw Error(kShapeError, "MPS boundary bonds must have extent 1");
+  for (size_t i = 0; i + 1 < sites.size(); ++i)
+    if (sites[i].shape[2] != sites[i + 1].shape[1])
+      throw Error(kShapeError, "MPS bond mismatch between sites " + std::to_string(i) + " and " + std::to_string(i + 1));
+}
+
+// contraction.cpp:254-267: site = contract("dulbr,dULBR->bBlLrR", bra*, ket) reshaped.
+BoundaryD two_layer_first_row(Ctx& ctx, const PepsStateD& bra, const PepsStateD& ket) {
+  BoundaryD out;
+  for (int c = 0; c < bra.cols; ++c) {
+    const DTensor& b = bra.site(0, c);
+    const DTensor& k = ket.site(0, c);
+    LTensor t = contract_network(ctx, {as_labelled(b, "dulbr", true), as_labelled(k, "dULBR")}, "bBlLrR");
+    DTensor site = materialize(ctx, t, t.labels);
+    out.sites.push_back(reshape(site, {b.shape[3] * k.shape[3], b.shape[2] * k.shape[2], b.shape[4] * k.shape[4]}));
+    out.phys.emplace_back(b.shape[3], k.shape[3]);
+  }
+  return out;
+}
+
+// contraction.cpp:269-311
+BoundaryD two_layer_apply_row(Ctx& ctx, const BoundaryD& top, const PepsStateD& bra, const PepsStateD& ket, int row,
+                              const ContractOptD& opt, uint64_t seed_tag) {
+  const int n = bra.cols;
+  BoundaryD out;
+  out.sites.resize(n);
+  for (int c = 0; c < n; ++c) out.phys.emplace_back(bra.site(row, c).shape[3], ket.site(row, c).shape[3]);
+  const int absorb = opt.canonicalize ? (row % 2 ? kRight : kLeft) : kSplit;
+
+  // pending v: (a, bra-down, ket-down, mps bond, bra-right, ket-right)
+  const DTensor& s0 = top.sites[0];
+  DTensor s0s = reshape(s0, {top.phys[0].first, top.phys[0].second, s0.shape[1], s0.shape[2]});
+  LTensor v0 = contract_network(
+      ctx, {as_labelled(s0s, "uvls"), as_labelled(bra.site(row, 0), "dumbe", true), as_labelled(ket.site(row, 0), "dvncf")},
+      "bcsef");
+  DTensor v = materialize(ctx, v0, v0.labels);
+  v = reshape(v, {1, v.shape[0], v.shape[1], v.shape[2], v.shape[3], v.shape[4]});
+
+  for (int c = 1; c < n; ++c) {
+    const DTensor& sc = top.sites[c];
+    DTensor scs = reshape(sc, {top.phys[c].first, top.phys[c].second, sc.shape[1], sc.shape[2]});
+    ImplicitOp net({v, scs, bra.site(row, c), ket.site(row, c)}, {"apqsmn", "uvst", "dumbe", "dvncf"}, "apq", "bctef",
+                   {false, false, true, false});
+    Trunc policy = opt.trunc;
+    if (policy.max_rank == 0) policy.max_rank = UINT64_MAX;
+    Rsvd cfg = opt.rsvd;
+    cfg.seed = derive_seed1(derive_seed1(derive_seed1(opt.seed, seed_tag), static_cast<uint64_t>(row)),
+                            static_cast<uint64_t>(c));
+    // t1 (a, pb, pk, rho) written directly as (pb, pk, a, rho)
+    EinsumsvdResultD split = einsumsvd(ctx, net, policy, opt.strategy, absorb, cfg, {1, 2, 0, 3});
+    const auto& t1 = split.t1.shape;
+    out.sites[c - 1] = reshape(split.t1, {t1[0] * t1[1], t1[2], t1[3]});
+    v = split.t2;  // (rho, b, c, t, e, f)
+  }
+  // last = v.permute({1,2,0,3,4,5}) -> (pb*pk, rho, t*e*f)
+  LTensor last = reduce_to(ctx, as_labelled(v, "abcdef"), "bcadef");
+  DTensor lastd = materialize(ctx, last, last.labels);
+  const auto& ls = lastd.shape;
+  out.sites[n - 1] = reshape(lastd, {ls[0] * ls[1], ls[2], ls[3] * ls[4] * ls[5]});
+  out.validate();
+  return out;
+}
+
+std::pair<double, double> chain_scalar(Ctx& ctx, const BoundaryD& b) {
+  b.validate();
+  LTensor t = scalar_one(ctx);
+  t.labels = "l";
+  t.ext = {1};
+  t.str = {1};
+  for (const auto& site : b.sites) {
+    if (site.shape[0] != 1) throw Error(kShapeError, "chain_scalar requires physical extents 1");
+    LTensor s = as_labelled(site, "plr");
+    t = contract_network(ctx, {t, s}, "r");
+    t.labels = "l";
+  }
+  t.labels = "";
+  t.ext.clear();
+  t.str.clear();
+  return read_scalar(ctx, t);
+}
+
+std::pair<double, double> contract_two_layer(Ctx& ctx, const PepsStateD& bra, const PepsStateD& ket,
+                                             const ContractOptD& opt) {
+  if (bra.rows != ket.rows || bra.cols != ket.cols || bra.d != ket.d)
+    throw Error(kValidationError, "two-layer contraction needs matching grids");
+  BoundaryD s = two_layer_first_row(ctx, bra, ket);
+  for (int r = 1; r < bra.rows; ++r) s = two_layer_apply_row(ctx, s, bra, ket, r, opt, kTagTop);
+  return chain_scalar(ctx, s);
+}
+
+// observables.cpp:261-270: reverse rows, swap up/down.
+PepsStateD flip_vertical(Ctx& ctx, const PepsStateD& s) {
+  PepsStateD f;
+  f.rows = s.rows;
+  f.cols = s.cols;
+  f.d = s.d;
+  for (int r = s.rows - 1; r >= 0; --r)
+    for (int c = 0; c < s.cols; ++c) {
+      LTensor t = reduce_to(ctx, as_labelled(s.site(r, c), "pudlr"), "pdulr");
+      f.sites.push_back(materialize(ctx, t, t.labels));
+    }
+  return f;
+}
+
+// observables.cpp:272-281,325-333
+RowCacheD build_row_cache(Ctx& ctx, const PepsStateD& s, const ContractOptD& opt) {
+  RowCacheD cache;
+  cache.tops.push_back(two_layer_first_row(ctx, s, s));
+  for (int r = 1; r < s.rows; ++r)
+    cache.tops.push_back(two_layer_apply_row(ctx, cache.tops.back(), s, s, r, opt, kTagTop));
+  PepsStateD fl = flip_vertical(ctx, s);
+  std::vector<BoundaryD> fb;
+  fb.push_back(two_layer_first_row(ctx, fl, fl));
+  for (int r = 1; r < s.rows; ++r) fb.push_back(two_layer_apply_row(ctx, fb.back(), fl, fl, r, opt, kTagBottom));
+  cache.bots.resize(s.rows);
+  for (int k = 0; k < s.rows; ++k) cache.bots[k] = fb[s.rows - 1 - k];
+  return cache;
+}
+
+// ---------------------------------------------------------------------------- band zipper
+
+namespace {
+
+constexpr const char* kIn = "ABCDEFGHIJ";
+constexpr const char* kOut = "MNOPQRSTUV";
+
+struct Layout {
+  bool top = false, bottom = false;
+  int r0 = 0, r1 = 0;
+  int nrows() const { return r1 - r0 + 1; }
+  int roles() const { return (top ? 1 : 0) + 2 * nrows() + (bottom ? 1 : 0); }
+  int top_role() const { return 0; }
+  int bra_role(int br) const { return (top ? 1 : 0) + 2 * br; }
+  int ket_role(int br) const { return (top ? 1 : 0) + 2 * br + 1; }
+  int bottom_role() const { return roles() - 1; }
+};
+
+Layout make_layout(const BoundaryD* top, int r0, int r1, const BoundaryD* bottom) {
+  if (r1 < r0 || r1 - r0 > 1) throw Error(kValidationError, "band must span one or two rows");
+  Layout L;
+  L.top = top != nullptr;
+  L.bottom = bottom != nullptr;
+  L.r0 = r0;
+  L.r1 = r1;
+  return L;
+}
+
+int partner_col(const std::vector<InsertionPieceD>& pieces, const InsertionPieceD* self, int id, bool* found) {
+  int pc = self->col;
+  *found = false;
+  for (const auto& p : pieces) {
+    if (&p == self) continue;
+    for (int o : p.bond_ids)
+      if (o == id) {
+        pc = p.col;
+        *found = true;
+      }
+  }
+  return pc;
+}
+
+// Gate bonds carried across the cut after column c (contraction.cpp:506-529).
+std::vector<int> active_gate_bonds(const std::vector<InsertionPieceD>& pieces, int c) {
+  std::vector<int> out;
+  for (const auto& p : pieces)
+    for (int id : p.bond_ids) {
+      int lo = p.col, hi = p.col;
+      for (const auto& q : pieces) {
+        if (&q == &p) continue;
+        for (int o : q.bond_ids)
+          if (o == id) {
+            lo = std::min(lo, q.col);
+            hi = std::max(hi, q.col);
+          }
+      }
+      if (lo <= c && c < hi && std::find(out.begin(), out.end(), id) == out.end()) out.push_back(id);
+    }
+  std::sort(out.begin(), out.end());
+  return out;
+}
+
+// Column-c transfer network of the band (contraction.cpp:371-474).  With
+// `mirror`, column c is physical column n-1-c with left/right bonds swapped
+// (the right pass of band_environment) — done by relabelling, not copying.
+std::vector<LTensor> band_column(const Layout& L, const BoundaryD* top, const PepsStateD& bra, const PepsStateD& ket,
+                                 const BoundaryD* bottom, const std::vector<InsertionPieceD>& pieces, int c,
+                                 bool mirror, const std::vector<int>& in_gates, const std::vector<int>& out_gates,
+                                 std::string& out_labels) {
+  std::vector<LTensor> net;
+  const int n = bra.cols;
+  const int pc = mirror ? n - 1 - c : c;
+  char dummy = '0';
+  auto fresh = [&]() { return dummy++; };
+  auto h_in = [&](int role) { return c == 0 ? fresh() : kIn[role]; };
+  auto h_out = [&](int role) { return c + 1 == n ? fresh() : kOut[role]; };
+  auto gate_in = [&](int id) {
+    for (size_t i = 0; i < in_gates.size(); ++i)
+      if (in_gates[i] == id) return kIn[L.roles() + i];
+    throw Error(kShapeError, "gate bond not carried into this column");
+  };
+  auto gate_out = [&](int id) {
+    for (size_t i = 0; i < out_gates.size(); ++i)
+      if (out_gates[i] == id) return kOut[L.roles() + i];
+    throw Error(kShapeError, "gate bond not carried out of this column");
+  };
+  auto lr = [&](char lft, char rgt) { return mirror ? std::string{rgt, lft} : std::string{lft, rgt}; };
+
+  if (L.top) {
+    const DTensor& t = top->sites[pc];
+    DTensor v = reshape(t, {top->phys[pc].first, top->phys[pc].second, t.shape[1], t.shape[2]});
+    char i = h_in(L.top_role()), o = h_out(L.top_role());
+    net.push_back(as_labelled(v, std::string("uv") + lr(i, o)));
+  }
+  for (int br = 0; br < L.nrows(); ++br) {
+    const int row = L.r0 + br;
+    const char up_b = br == 0 ? (L.top ? 'u' : fresh()) : 'y';
+    const char up_k = br == 0 ? (L.top ? 'v' : fresh()) : 'z';
+    const bool last = br + 1 == L.nrows();
+    const char dn_b = last ? (L.bottom ? 'k' : fresh()) : 'y';
+    const char dn_k = last ? (L.bottom ? 'l' : fresh()) : 'z';
+    const InsertionPieceD* piece = nullptr;
+    for (const auto& p : pieces)
+      if (p.row == row && p.col == pc) {
+        if (piece) throw Error(kValidationError, "at most one insertion piece per site");
+        piece = &p;
+      }
+    const char ph_b = br == 0 ? 'w' : 'i';
+    const char ph_k = piece ? (br == 0 ? 'x' : 'j') : ph_b;
+    {
+      char i = h_in(L.bra_role(br)), o = h_out(L.bra_role(br));
+      std::string lab = std::string{ph_b, up_b} + lr(i, o).substr(0, 1) + dn_b + lr(i, o).substr(1, 1);
+      net.push_back(as_labelled(bra.site(row, pc), lab, true));
+    }
+    {
+      char i = h_in(L.ket_role(br)), o = h_out(L.ket_role(br));
+      std::string lab = std::string{ph_k, up_k} + lr(i, o).substr(0, 1) + dn_k + lr(i, o).substr(1, 1);
+      net.push_back(as_labelled(ket.site(row, pc), lab));
+    }
+    if (piece) {
+      std::string pl{ph_b, ph_k};
+      for (int id : piece->bond_ids) {
+        bool found = false;
+        int partner = partner_col(pieces, piece, id, &found);
+        if (!found) throw Error(kValidationError, "gate bond has no partner piece");
+        if (partner == pc) pl += 'g';
+        else if (partner > pc) pl += gate_out(id);
+        else pl += gate_in(id);
+      }
+      net.push_back(as_labelled(piece->op, pl));
+    }
+  }
+  if (L.bottom) {
+    const DTensor& t = bottom->sites[pc];
+    DTensor v = reshape(t, {bottom->phys[pc].first, bottom->phys[pc].second, t.shape[1], t.shape[2]});
+    char i = h_in(L.bottom_role()), o = h_out(L.bottom_role());
+    net.push_back(as_labelled(v, std::string("kl") + lr(i, o)));
+  }
+  out_labels.clear();
+  for (int role = 0; role < L.roles(); ++role)
+    if (c + 1 < n) out_labels += kOut[role];
+  for (size_t i = 0; i < out_gates.size(); ++i) out_labels += kOut[L.roles() + i];
+  return net;
+}
+
+std::string to_in(const std::string& s) {
+  std::string o;
+  for (char c : s) o += kIn[std::strchr(kOut, c) - kOut];
+  return o;
+}
+
+LTensor band_step(Ctx& ctx, const Layout& L, const LTensor& l, const BoundaryD* top, const PepsStateD& bra,
+                  const PepsStateD& ket, const BoundaryD* bottom, const std::vector<InsertionPieceD>& pieces, int c,
+                  bool mirror, const std::vector<int>& in_g, const std::vector<int>& out_g) {
+  std::string out;
+  std::vector<LTensor> net = band_column(L, top, bra, ket, bottom, pieces, c, mirror, in_g, out_g, out);
+  net.insert(net.begin(), l);
+  LTensor r = contract_network(ctx, net, out);
+  r.labels = to_in(r.labels);
+  return r;
+}
+
+void check_state_pair(const PepsStateD& bra, const PepsStateD& ket) {
+  if (bra.rows != ket.rows || bra.cols != ket.cols) throw Error(kValidationError, "band needs matching grids");
+}
+
+}  // namespace
+
+std::pair<double, double> band_value(Ctx& ctx, const BoundaryD* top, const PepsStateD& bra, const PepsStateD& ket,
+                                     int r0, int r1, const BoundaryD* bottom,
+                                     const std::vector<InsertionPieceD>& pieces) {
+  check_state_pair(bra, ket);
+  Layout L = make_layout(top, r0, r1, bottom);
+  LTensor l = scalar_one(ctx);
+  std::vector<int> in_g;
+  for (int c = 0; c < bra.cols; ++c) {
+    std::vector<int> out_g = active_gate_bonds(pieces, c);
+    l = band_step(ctx, L, l, top, bra, ket, bottom, pieces, c, false, in_g, out_g);
+    in_g = out_g;
+  }
+  return read_scalar(ctx, l);
+}
+
+BandEnvD band_environment(Ctx& ctx, const BoundaryD* top, const PepsStateD& bra, const PepsStateD& ket, int r0, int r1,
+                          const BoundaryD* bottom) {
+  check_state_pair(bra, ket);
+  Layout L = make_layout(top, r0, r1, bottom);
+  BandEnvD env;
+  env.r0 = r0;
+  env.r1 = r1;
+  const int n = bra.cols;
+  env.left.resize(n);
+  env.right.resize(n);
+  LTensor l = scalar_one(ctx);
+  for (int c = 0; c < n; ++c) {
+    l = band_step(ctx, L, l, top, bra, ket, bottom, {}, c, false, {}, {});
+    env.left[c] = l;
+  }
+  LTensor r = scalar_one(ctx);
+  for (int c = 0; c < n; ++c) {
+    r = band_step(ctx, L, r, top, bra, ket, bottom, {}, c, true, {}, {});
+    env.right[n - 1 - c] = r;
+  }
+  return env;
+}
+
+std::pair<double, double> band_splice(Ctx& ctx, const BandEnvD& env, const BoundaryD* top, const PepsStateD& bra,
+                                      const PepsStateD& ket, const BoundaryD* bottom,
+                                      const std::vector<InsertionPieceD>& pieces, int c0, int c1) {
+  check_state_pair(bra, ket);
+  Layout L = make_layout(top, env.r0, env.r1, bottom);
+  const int n = bra.cols;
+  if (c1 >= n || c0 > c1 || c0 < 0) throw Error(kValidationError, "bad splice column range");
+  LTensor l = c0 == 0 ? scalar_one(ctx) : env.left[c0 - 1];
+  std::vector<int> in_g;
+  for (int c = c0; c <= c1; ++c) {
+    std::vector<int> out_g = active_gate_bonds(pieces, c);
+    l = band_step(ctx, L, l, top, bra, ket, bottom, pieces, c, false, in_g, out_g);
+    in_g = out_g;
+  }
+  if (c1 + 1 == n) return read_scalar(ctx, l);
+  const LTensor& r = env.right[c1 + 1];
+  LTensor v = contract_network(ctx, {l, r}, "");
+  return read_scalar(ctx, v);
+}
+
+}  // namespace pepsb

@@ -1,0 +1,555 @@
+// Single-block small dense solvers (see smalldense.cuh).
+//
+// The k x k problems of einsumsvd (k <= ~100) are far too small for a grid;
+// each runs in one thread block with the matrix in shared memory, one warp
+// per Jacobi rotation pair (round-robin ordering, all pairs of a round
+// disjoint, one __syncthreads per round).
+#include <algorithm>
+#include <cmath>
+
+#include "smalldense.cuh"
+
+namespace pepsb {
+
+namespace {
+
+constexpr int kThreads = 1024;
+constexpr size_t kSmemCap = 200 * 1024;
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__device__ __forceinline__ int rr_pos(int i, int r, int npad) {
+  return i == 0 ? 0 : ((i - 1 + r) % (npad - 1)) + 1;
+}
+
+// One-sided (Hestenes) Jacobi on the n columns (each m long, column stride
+// ldx) of X, accumulating the rotations into V (n x n, column stride ldv,
+// initialised here to I).  Block-wide; every thread must call it.
+__device__ void onesided_jacobi(double2* X, int m, int n, int ldx, double2* V, int ldv, double tol,
+                                double abs_skip, int max_sweeps, int* status) {
+  __shared__ int rotated;
+  for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
+    int c = e / n, r = e % n;
+    V[c * ldv + r] = make_double2(r == c ? 1.0 : 0.0, 0.0);
+  }
+  __syncthreads();
+  if (n < 2) return;
+  const int npad = n + (n & 1);
+  const int pairs = npad / 2;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
+  int sweep = 0;
+  for (; sweep < max_sweeps; ++sweep) {
+    if (threadIdx.x == 0) rotated = 0;
+    __syncthreads();
+    for (int r = 0; r < npad - 1; ++r) {
+      for (int pi = warp; pi < pairs; pi += nwarps) {
+        int p = rr_pos(pi, r, npad), q = rr_pos(npad - 1 - pi, r, npad);
+        if (p >= n || q >= n) continue;
+        if (p > q) { int t = p; p = q; q = t; }
+        double2* xp = X + static_cast<int64_t>(p) * ldx;
+        double2* xq = X + static_cast<int64_t>(q) * ldx;
+        double a = 0.0, b = 0.0, gr = 0.0, gi = 0.0;
+        for (int i = lane; i < m; i += 32) {
+          double2 u = xp[i], v = xq[i];
+          a += cnorm2(u);
+          b += cnorm2(v);
+          gr += u.x * v.x + u.y * v.y;  // conj(u) * v
+          gi += u.x * v.y - u.y * v.x;
+        }
+        a = warp_sum(a);
+        b = warp_sum(b);
+        gr = warp_sum(gr);
+        gi = warp_sum(gi);
+        const double ag = hypot(gr, gi);
+        if (!(ag > tol * sqrt(a * b)) || !(ag > abs_skip)) continue;
+        if (lane == 0) rotated = 1;
+        const double tau = (b - a) / (2.0 * ag);
+        const double t = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
+        const double c = 1.0 / sqrt(1.0 + t * t), s = t * c;
+        const double2 ec = make_double2(gr / ag, -gi / ag);  // conj(e), e = g/|g|
+        for (int i = lane; i < m; i += 32) {
+          double2 u = xp[i], v = cmul(ec, xq[i]);
+          xp[i] = make_double2(c * u.x - s * v.x, c * u.y - s * v.y);
+          xq[i] = make_double2(s * u.x + c * v.x, s * u.y + c * v.y);
+        }
+        double2* vp = V + static_cast<int64_t>(p) * ldv;
+        double2* vq = V + static_cast<int64_t>(q) * ldv;
+        for (int i = lane; i < n; i += 32) {
+          double2 u = vp[i], v = cmul(ec, vq[i]);
+          vp[i] = make_double2(c * u.x - s * v.x, c * u.y - s * v.y);
+          vq[i] = make_double2(s * u.x + c * v.x, s * u.y + c * v.y);
+        }
+      }
+      __syncthreads();
+    }
+    const int any = rotated;
+    __syncthreads();
+    if (!any) break;
+  }
+  if (sweep == max_sweeps && threadIdx.x == 0) atomicOr(status, kSmallNoConverge);
+}
+
+// Descending order of key[0..n) (ties by index) -> order[rank] = column.
+__device__ void sort_desc(const double* key, int* order, int n) {
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const double ki = key[i];
+    int rank = 0;
+    for (int j = 0; j < n; ++j) {
+      const double kj = key[j];
+      rank += (kj > ki) || (kj == ki && j < i);
+    }
+    order[rank] = i;
+  }
+  __syncthreads();
+}
+
+// Column phase fix (linalg.cpp:44-64): for column `col` of a column-major
+// matrix (column stride ld, rows entries) find the first largest-magnitude
+// entry; returns its unit phase (1 if the column is zero).  Warp-level.
+__device__ double2 column_phase(const double2* colp, int rows) {
+  const int lane = threadIdx.x & 31;
+  double best = 0.0;
+  int bi = 0x7fffffff;
+  for (int i = lane; i < rows; i += 32) {
+    double a = hypot(colp[i].x, colp[i].y);
+    if (a > best) { best = a; bi = i; }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    double ob = __shfl_xor_sync(0xffffffffu, best, o);
+    int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+    if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+  }
+  if (best == 0.0) return make_double2(1.0, 0.0);
+  double2 top = colp[bi];
+  return make_double2(top.x / best, top.y / best);
+}
+
+// ------------------------------------------------------------------ gram_factors
+
+__global__ void __launch_bounds__(kThreads) gram_factors_kernel(const double2* G, int n, double2* P,
+                                                                double2* R, int* deficient,
+                                                                int* any_def, int* status,
+                                                                double2* work) {
+  extern __shared__ __align__(16) unsigned char sm[];
+  const bool in_smem = work == nullptr;
+  double2* X = in_smem ? reinterpret_cast<double2*>(sm) : work;  // column-major n x n
+  double2* V = X + n * n;
+  __shared__ double lam[256];
+  __shared__ int order[256];
+  __shared__ double hmax[2];
+  if (threadIdx.x < 2) hmax[threadIdx.x] = 0.0;
+  __syncthreads();
+  // Hermiticity check against the input, as eigh does (linalg.cpp:262-271).
+  double herr = 0.0, scale = 0.0;
+  for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
+    int i = e / n, j = e % n;
+    double2 a = G[i * n + j], b = G[j * n + i];
+    herr = fmax(herr, hypot(a.x - b.x, a.y + b.y));
+    scale = fmax(scale, hypot(a.x, a.y));
+    // symmetrised 0.5 (G + G^H), stored column-major: X[j][i] = A(i, j)
+    X[j * n + i] = make_double2(0.5 * (a.x + b.x), 0.5 * (a.y - b.y));
+  }
+  // block max via atomics on the bit patterns of non-negative doubles
+  atomicMax(reinterpret_cast<unsigned long long*>(&hmax[0]), __double_as_longlong(herr));
+  atomicMax(reinterpret_cast<unsigned long long*>(&hmax[1]), __double_as_longlong(scale));
+  __syncthreads();
+  if (threadIdx.x == 0 && hmax[0] > 1e-10 * fmax(1.0, hmax[1])) atomicOr(status, kSmallNotHermitian);
+
+  double fro = 0.0;
+  for (int e = threadIdx.x; e < n * n; e += blockDim.x) fro += cnorm2(X[e]);
+  // abs skip: rotations below the rounding level of ||G||^2 do not move eigenvalues.
+  __shared__ double fro_sh;
+  if (threadIdx.x == 0) fro_sh = 0.0;
+  __syncthreads();
+  atomicAdd(&fro_sh, fro);
+  __syncthreads();
+  const double abs_skip = 1e-34 * fro_sh;
+  onesided_jacobi(X, n, n, n, V, n, 1e-15, abs_skip, 40, status);
+
+  // eigenvalue j = Re(v_j^H G v_j) = Re(v_j^H x_j)   (X = G V)
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
+  for (int j = warp; j < n; j += nwarps) {
+    double s = 0.0;
+    for (int i = lane; i < n; i += 32) {
+      double2 v = V[j * n + i], x = X[j * n + i];
+      s += v.x * x.x + v.y * x.y;
+    }
+    s = warp_sum(s);
+    if (lane == 0) lam[j] = s;
+  }
+  __syncthreads();
+  sort_desc(lam, order, n);
+  // phase of each sorted eigenvector column
+  __shared__ double2 ph[256];
+  for (int j = warp; j < n; j += nwarps) {
+    double2 p = column_phase(V + order[j] * n, n);
+    if (lane == 0) ph[j] = p;
+  }
+  __syncthreads();
+  const double lmax = lam[order[0]];
+  if (threadIdx.x == 0) {
+    if (!(lmax > 0.0)) atomicOr(status, kSmallZeroGram);
+    int anyd = 0;
+    for (int j = 0; j < n; ++j) {
+      int d = lam[order[j]] < 1e-12 * lmax;
+      deficient[j] = d;
+      anyd |= d;
+    }
+    *any_def = anyd;
+  }
+  for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
+    const int i = e / n, j = e % n;
+    const double lj = fmax(lam[order[j]], 1e-12 * lmax);
+    // eigenvector column j (sorted), phase fixed: x_ij * conj(phase_j)
+    const double2 xij = cmulc(ph[j], V[order[j] * n + i]);
+    const double isq = 1.0 / sqrt(lj);
+    P[i * n + j] = cscale(xij, isq);
+    // R row j = sqrt(l_j) conj(column j of X): R[j][i] = sqrt(l_j) conj(x_ij)
+    R[j * n + i] = cscale(cconj(xij), sqrt(lj));
+  }
+}
+
+// ------------------------------------------------------------------ Cholesky
+
+__global__ void __launch_bounds__(kThreads) chol_kernel(const double2* G, int n, double shift_rel,
+                                                        double2* Rout, double2* Rinv, int* status) {
+  extern __shared__ __align__(16) unsigned char sm[];
+  double2* A = reinterpret_cast<double2*>(sm);  // row-major n x n
+  __shared__ double tr;
+  __shared__ int bad;
+  if (threadIdx.x == 0) { tr = 0.0; bad = 0; }
+  __syncthreads();
+  for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
+    int i = e / n, j = e % n;
+    // symmetrise from the upper triangle
+    double2 v = j >= i ? G[i * n + j] : cconj(G[j * n + i]);
+    A[e] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int i = 0; i < n; ++i) t += A[i * n + i].x;
+    tr = t;
+  }
+  __syncthreads();
+  const double shift = shift_rel * tr;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) A[i * n + i] = make_double2(A[i * n + i].x + shift, 0.0);
+  __syncthreads();
+  for (int k = 0; k < n; ++k) {
+    const double piv = A[k * n + k].x;
+    if (!(piv > 0.0)) {
+      if (threadIdx.x == 0) bad = 1;
+      __syncthreads();
+      break;
+    }
+    const double rkk = sqrt(piv);
+    __syncthreads();
+    for (int j = k + threadIdx.x; j < n; j += blockDim.x)
+      A[k * n + j] = j == k ? make_double2(rkk, 0.0) : cscale(A[k * n + j], 1.0 / rkk);
+    __syncthreads();
+    const int rem = n - k - 1;
+    for (int e = threadIdx.x; e < rem * rem; e += blockDim.x) {
+      const int i = k + 1 + e / rem, j = k + 1 + e % rem;
+      if (j < i) continue;
+      A[i * n + j] = csub(A[i * n + j], cmulc(A[k * n + i], A[k * n + j]));
+    }
+    __syncthreads();
+  }
+  if (bad) {
+    if (threadIdx.x == 0) atomicOr(status, kSmallCholBreakdown);
+    return;
+  }
+  for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
+    int i = e / n, j = e % n;
+    Rout[e] = j >= i ? A[e] : make_double2(0.0, 0.0);
+  }
+  // Rinv column c by back substitution (one thread per column).
+  for (int c = threadIdx.x; c < n; c += blockDim.x) {
+    for (int i = n - 1; i > c; --i) Rinv[i * n + c] = make_double2(0.0, 0.0);
+    // x_c = 1 / R_cc
+    double2 rcc = A[c * n + c];
+    Rinv[c * n + c] = make_double2(1.0 / rcc.x, 0.0);
+    for (int i = c - 1; i >= 0; --i) {
+      double2 s = make_double2(0.0, 0.0);
+      for (int l = i + 1; l <= c; ++l) s = cadd(s, cmul(A[i * n + l], Rinv[l * n + c]));
+      Rinv[i * n + c] = cscale(s, -1.0 / A[i * n + i].x);
+    }
+  }
+}
+
+// ------------------------------------------------------------------ small SVD
+
+__device__ void complete_unit_columns(double2* X, int rows, int cols, int ld, const int* bad,
+                                      int* status) {
+  // Orthonormal completion of flagged columns by Gram-Schmidt of canonical
+  // basis vectors (same rule as decomposition.cpp:88-115), column-major X.
+  __shared__ double red[3];
+  int next_basis = 0;
+  for (int j = 0; j < cols; ++j) {
+    if (!bad[j]) continue;
+    bool done = false;
+    for (; next_basis <= rows && !done; ++next_basis) {
+      if (next_basis == rows) {
+        if (threadIdx.x == 0) atomicOr(status, kSmallCompletionExhausted);
+        return;
+      }
+      double2* v = X + static_cast<int64_t>(j) * ld;
+      for (int r = threadIdx.x; r < rows; r += blockDim.x)
+        v[r] = make_double2(r == next_basis ? 1.0 : 0.0, 0.0);
+      __syncthreads();
+      for (int pass = 0; pass < 2; ++pass) {
+        for (int c = 0; c < cols; ++c) {
+          if (c == j || (bad[c] && c > j)) continue;
+          const double2* qc = X + static_cast<int64_t>(c) * ld;
+          if (threadIdx.x < 2) red[threadIdx.x] = 0.0;
+          __syncthreads();
+          double pr = 0.0, pi = 0.0;
+          for (int r = threadIdx.x; r < rows; r += blockDim.x) {
+            double2 q = qc[r], x = v[r];
+            pr += q.x * x.x + q.y * x.y;
+            pi += q.x * x.y - q.y * x.x;
+          }
+          pr = warp_sum(pr);
+          pi = warp_sum(pi);
+          if ((threadIdx.x & 31) == 0) { atomicAdd(&red[0], pr); atomicAdd(&red[1], pi); }
+          __syncthreads();
+          const double2 proj = make_double2(red[0], red[1]);
+          for (int r = threadIdx.x; r < rows; r += blockDim.x) v[r] = csub(v[r], cmul(proj, qc[r]));
+          __syncthreads();
+        }
+      }
+      if (threadIdx.x == 0) red[2] = 0.0;
+      __syncthreads();
+      double nn = 0.0;
+      for (int r = threadIdx.x; r < rows; r += blockDim.x) nn += cnorm2(v[r]);
+      nn = warp_sum(nn);
+      if ((threadIdx.x & 31) == 0) atomicAdd(&red[2], nn);
+      __syncthreads();
+      const double nrm = sqrt(red[2]);
+      if (nrm > 0.1) {
+        for (int r = threadIdx.x; r < rows; r += blockDim.x) v[r] = cscale(v[r], 1.0 / nrm);
+        done = true;
+      }
+      __syncthreads();
+    }
+  }
+}
+
+struct SvdArgs {
+  const double2* A;
+  int64_t sa;
+  int m, n, lda;
+  double2* U;
+  int64_t su;
+  double* s;
+  int64_t ss;
+  double2* Vh;
+  int64_t sv;
+  int* status;
+  double2* work;
+  int64_t work_stride;
+};
+
+__global__ void __launch_bounds__(kThreads) small_svd_kernel(const SvdArgs a) {
+  extern __shared__ __align__(16) unsigned char sm[];
+  const int b = blockIdx.x;
+  const double2* A = a.A + b * a.sa;
+  const bool tall = a.m >= a.n;
+  const int mr = tall ? a.m : a.n;  // rows of the working matrix
+  const int nc = tall ? a.n : a.m;  // its columns (= k)
+  double2* X = a.work ? a.work + b * a.work_stride : reinterpret_cast<double2*>(sm);
+  double2* V = X + static_cast<int64_t>(mr) * nc;
+  __shared__ double sig[256];
+  __shared__ int order[256];
+  __shared__ int bad[256];
+  __shared__ double2 ph[256];
+  // Working matrix W (mr x nc) column-major: tall -> W = A, wide -> W = A^H.
+  for (int e = threadIdx.x; e < a.m * a.n; e += blockDim.x) {
+    const int i = e / a.n, j = e % a.n;
+    const double2 v = A[static_cast<int64_t>(i) * a.lda + j];
+    if (tall) X[static_cast<int64_t>(j) * mr + i] = v;      // col j, row i
+    else X[static_cast<int64_t>(i) * mr + j] = cconj(v);     // A^H: col i, row j
+  }
+  __syncthreads();
+  onesided_jacobi(X, mr, nc, mr, V, nc, 1e-15, 0.0, 60, a.status);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
+  for (int j = warp; j < nc; j += nwarps) {
+    double s = 0.0;
+    for (int i = lane; i < mr; i += 32) s += cnorm2(X[static_cast<int64_t>(j) * mr + i]);
+    s = warp_sum(s);
+    if (lane == 0) sig[j] = sqrt(s);
+  }
+  __syncthreads();
+  sort_desc(sig, order, nc);
+  const double smax = sig[order[0]];
+  // normalise columns; flag numerically-zero ones for orthonormal completion
+  for (int j = warp; j < nc; j += nwarps) {
+    const double sj = sig[j];
+    const bool zero = !(sj > 0.0) || sj <= 1e-300 || (smax > 0.0 && sj < 1e-300 * smax);
+    if (lane == 0) bad[j] = zero;
+    if (!zero)
+      for (int i = lane; i < mr; i += 32) X[static_cast<int64_t>(j) * mr + i] = cscale(X[static_cast<int64_t>(j) * mr + i], 1.0 / sj);
+  }
+  __syncthreads();
+  // completion works in sorted order semantics only through the flags; the
+  // unsorted storage is fine since completion orthogonalises against all.
+  complete_unit_columns(X, mr, nc, mr, bad, a.status);
+  __syncthreads();
+  // U/Vh in sorted order.  tall: U = X (m x k), V = V (n x k) -> Vh = V^H.
+  //                        wide: U = V (m x k),  Vh = X^H.
+  const double2* Ucols = tall ? X : V;   // column-major, column stride = rows of U
+  const int urows = a.m;
+  const double2* Vcols = tall ? V : X;   // column-major n x k
+  const int vrows = a.n;
+  for (int j = warp; j < nc; j += nwarps) {
+    double2 p = column_phase(Ucols + static_cast<int64_t>(order[j]) * urows, urows);
+    if (lane == 0) ph[j] = p;
+  }
+  __syncthreads();
+  const int k = nc;
+  double2* U = a.U + b * a.su;
+  double2* Vh = a.Vh + b * a.sv;
+  double* s = a.s + b * a.ss;
+  for (int e = threadIdx.x; e < urows * k; e += blockDim.x) {
+    const int i = e / k, j = e % k;
+    U[static_cast<int64_t>(i) * k + j] = cmulc(ph[j], Ucols[static_cast<int64_t>(order[j]) * urows + i]);
+  }
+  for (int e = threadIdx.x; e < k * vrows; e += blockDim.x) {
+    const int j = e / vrows, c = e % vrows;
+    // Vh[j][c] = conj(Vcol_j[c]) * phase_j
+    Vh[static_cast<int64_t>(j) * vrows + c] = cmul(cconj(Vcols[static_cast<int64_t>(order[j]) * vrows + c]), ph[j]);
+  }
+  for (int j = threadIdx.x; j < k; j += blockDim.x) s[j] = sig[order[j]];
+}
+
+// ------------------------------------------------------------------ completion of big Q
+
+__global__ void __launch_bounds__(kThreads) complete_columns_kernel(double2* Q, int64_t rows, int cols,
+                                                                    const int* deficient,
+                                                                    const int* any_def, int* status) {
+  if (*any_def == 0) return;
+  __shared__ double red[3];
+  int64_t next_basis = 0;
+  for (int j = 0; j < cols; ++j) {
+    if (!deficient[j]) continue;
+    bool done = false;
+    for (; next_basis <= rows && !done; ++next_basis) {
+      if (next_basis == rows) {
+        if (threadIdx.x == 0) atomicOr(status, kSmallCompletionExhausted);
+        return;
+      }
+      // use column j of Q as the work vector (it is overwritten anyway)
+      for (int64_t r = threadIdx.x; r < rows; r += blockDim.x)
+        Q[r * cols + j] = make_double2(r == next_basis ? 1.0 : 0.0, 0.0);
+      __syncthreads();
+      for (int pass = 0; pass < 2; ++pass) {
+        for (int c = 0; c < cols; ++c) {
+          if (c == j || (deficient[c] && c > j)) continue;
+          if (threadIdx.x < 2) red[threadIdx.x] = 0.0;
+          __syncthreads();
+          double pr = 0.0, pi = 0.0;
+          for (int64_t r = threadIdx.x; r < rows; r += blockDim.x) {
+            double2 q = Q[r * cols + c], x = Q[r * cols + j];
+            pr += q.x * x.x + q.y * x.y;
+            pi += q.x * x.y - q.y * x.x;
+          }
+          pr = warp_sum(pr);
+          pi = warp_sum(pi);
+          if ((threadIdx.x & 31) == 0) { atomicAdd(&red[0], pr); atomicAdd(&red[1], pi); }
+          __syncthreads();
+          const double2 proj = make_double2(red[0], red[1]);
+          for (int64_t r = threadIdx.x; r < rows; r += blockDim.x)
+            Q[r * cols + j] = csub(Q[r * cols + j], cmul(proj, Q[r * cols + c]));
+          __syncthreads();
+        }
+      }
+      if (threadIdx.x == 0) red[2] = 0.0;
+      __syncthreads();
+      double nn = 0.0;
+      for (int64_t r = threadIdx.x; r < rows; r += blockDim.x) nn += cnorm2(Q[r * cols + j]);
+      nn = warp_sum(nn);
+      if ((threadIdx.x & 31) == 0) atomicAdd(&red[2], nn);
+      __syncthreads();
+      const double nrm = sqrt(red[2]);
+      if (nrm > 0.1) {
+        for (int64_t r = threadIdx.x; r < rows; r += blockDim.x) Q[r * cols + j] = cscale(Q[r * cols + j], 1.0 / nrm);
+        done = true;
+      }
+      __syncthreads();
+    }
+  }
+}
+
+}  // namespace
+
+void gram_factors(const double2* G, int n, double2* P, double2* R, int* deficient, int* any_def,
+                  int* status, double2* work, cudaStream_t stream) {
+  if (n > 256) throw Error(kShapeError, "gram_factors: k > 256 not supported");
+  const size_t smem = 2ull * n * n * sizeof(double2);
+  const bool fits = smem <= kSmemCap;
+  if (!fits && !work) throw Error(kOtherError, "gram_factors: workspace required");
+  static bool attr = false;
+  if (!attr) {
+    PEPSB_CUDA(cudaFuncSetAttribute(gram_factors_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(kSmemCap)));
+    attr = true;
+  }
+  gram_factors_kernel<<<1, kThreads, fits ? smem : 0, stream>>>(G, n, P, R, deficient, any_def, status,
+                                                                fits ? nullptr : work);
+  PEPSB_LAUNCH();
+}
+
+void chol_factors(const double2* G, int n, double shift_rel, double2* R, double2* Rinv, int* status,
+                  cudaStream_t stream) {
+  const size_t smem = static_cast<size_t>(n) * n * sizeof(double2);
+  if (smem > kSmemCap) throw Error(kShapeError, "chol_factors: k too large");
+  static bool attr = false;
+  if (!attr) {
+    PEPSB_CUDA(cudaFuncSetAttribute(chol_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(kSmemCap)));
+    attr = true;
+  }
+  chol_kernel<<<1, kThreads, smem, stream>>>(G, n, shift_rel, R, Rinv, status);
+  PEPSB_LAUNCH();
+}
+
+int64_t small_svd_workspace(int m, int n, int batch) {
+  const int64_t mr = std::max(m, n), nc = std::min(m, n);
+  const size_t smem = static_cast<size_t>(mr * nc + nc * nc) * sizeof(double2);
+  if (smem <= kSmemCap) return 0;
+  return static_cast<int64_t>(batch) * (mr * nc + nc * nc);
+}
+
+void small_svd(const double2* A, int64_t sa, int m, int n, int lda, double2* U, int64_t su, double* s,
+               int64_t ss, double2* Vh, int64_t sv, int batch, int* status, double2* work,
+               cudaStream_t stream) {
+  if (batch <= 0) return;
+  const int64_t mr = std::max(m, n), nc = std::min(m, n);
+  if (nc > 256) throw Error(kShapeError, "small_svd: min(m, n) > 256 not supported");
+  const size_t smem = static_cast<size_t>(mr * nc + nc * nc) * sizeof(double2);
+  const bool fits = smem <= kSmemCap;
+  if (!fits && !work) throw Error(kOtherError, "small_svd: workspace required");
+  static bool attr = false;
+  if (!attr) {
+    PEPSB_CUDA(cudaFuncSetAttribute(small_svd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(kSmemCap)));
+    attr = true;
+  }
+  SvdArgs a{A, sa, m, n, lda, U, su, s, ss, Vh, sv, status, fits ? nullptr : work, mr * nc + nc * nc};
+  const int threads = nc <= 16 ? 256 : kThreads;
+  small_svd_kernel<<<batch, threads, fits ? smem : 0, stream>>>(a);
+  PEPSB_LAUNCH();
+}
+
+void complete_columns(double2* Q, int64_t rows, int cols, const int* deficient, const int* any_def,
+                      int* status, cudaStream_t stream) {
+  complete_columns_kernel<<<1, kThreads, 0, stream>>>(Q, rows, cols, deficient, any_def, status);
+  PEPSB_LAUNCH();
+}
+
+}  // namespace pepsb

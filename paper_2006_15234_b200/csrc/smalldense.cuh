@@ -1,0 +1,52 @@
+// Small dense factorizations that sit between the big contractions of
+// einsumsvd: k x k Gram eigen-factors, Cholesky factors for CholeskyQR2, and
+// (batched) small SVDs.  Each problem runs inside ONE thread block (shared
+// memory resident when it fits), so no host round-trip is needed.
+#pragma once
+
+#include <cstdint>
+
+#include "common.cuh"
+
+namespace pepsb {
+
+// Status words written by the small kernels (device int).
+enum SmallStatus : int {
+  kSmallOk = 0,
+  kSmallZeroGram = 1,       // gram of a zero operator (decomposition.cpp:132)
+  kSmallNotHermitian = 2,   // eigh Hermiticity check (linalg.cpp:268-271)
+  kSmallCholBreakdown = 4,  // Cholesky pivot <= 0
+  kSmallNoConverge = 8,     // Jacobi sweep cap hit
+  kSmallCompletionExhausted = 16,
+};
+
+// Reference gram_factors (proj/src/decomposition.cpp:128-156) on a device n x n
+// Gram matrix G (row-major):  eigh (descending, phase-fixed, linalg.cpp:256-295)
+// -> clamp at 1e-12*lmax -> P = X diag(l^-1/2), R = diag(l^1/2) X^H, deficient
+// flags.  `work` needs 2*n*n complex when n is too large for shared memory.
+void gram_factors(const double2* G, int n, double2* P, double2* R, int* deficient, int* any_def,
+                  int* status, double2* work, cudaStream_t stream);
+
+// CholeskyQR factor: G + shift*I = R^H R (R upper triangular), Rinv = R^{-1}.
+// shift = shift_rel * trace(G).  status |= kSmallCholBreakdown on failure.
+void chol_factors(const double2* G, int n, double shift_rel, double2* R, double2* Rinv,
+                  int* status, cudaStream_t stream);
+
+// Batched thin SVD of small row-major matrices A_b (m x n, leading dim lda,
+// batch stride sa):  A = U diag(s) Vh, k = min(m, n), s descending, U's columns
+// phase-fixed (largest-magnitude entry real positive, Vh rows compensate,
+// linalg.cpp:44-64).  U: m x k (stride su), s: k (stride ss), Vh: k x n (stride sv).
+// One-sided (Hestenes) Jacobi; `work` (>= batch*(m*n + n*n + ...) complex, see
+// small_svd_workspace) is used when the problem does not fit in shared memory.
+void small_svd(const double2* A, int64_t sa, int m, int n, int lda, double2* U, int64_t su,
+               double* s, int64_t ss, double2* Vh, int64_t sv, int batch, int* status,
+               double2* work, cudaStream_t stream);
+int64_t small_svd_workspace(int m, int n, int batch);
+
+// Reference complete_deficient_columns (decomposition.cpp:88-115) on a device
+// rows x cols row-major Q, for the columns flagged in `deficient`; no-op when
+// *any_def == 0 (checked on the device, so no host sync is needed).
+void complete_columns(double2* Q, int64_t rows, int cols, const int* deficient, const int* any_def,
+                      int* status, cudaStream_t stream);
+
+}  // namespace pepsb

@@ -1,0 +1,320 @@
+// Complex-FP64 DMMA GEMM (see zgemm.cuh for the contract).
+//
+// CTA tile BM x BN (complex), K step BK, STAGES-deep cp.async pipeline
+// (LDGSTS.128: one complex element per copy), warps tiled WM x WN, each warp
+// issuing (WM/8) x (WN/4) DMMA.8x8x4 per two complex k.  Fragment layouts of
+// mma.m8n8k4.f64: A a0 = A[lane>>2][lane&3], B b0 = B[lane&3][lane>>2],
+// C {c0,c1} = C[lane>>2][2*(lane&3) + {0,1}].  With the real embedding an
+// 8x8 real C tile is an 8x4 complex tile and each lane owns exactly one
+// complex output (re = c0, im = c1).
+#include <algorithm>
+
+#include "zgemm.cuh"
+
+namespace pepsb {
+
+namespace {
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool pred) {
+  unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  int n = pred ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(n));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+__device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+template <int BM, int BN, int BK, bool AK, bool BNC>
+struct Smem {
+  static constexpr int LDA = AK ? (BK + 2) : BM;   // complex elements per smem row
+  static constexpr int LDB = BNC ? (BN + 4) : (BK + 2);
+  static constexpr int A_ELEMS = AK ? BM * LDA : BK * LDA;
+  static constexpr int B_ELEMS = BNC ? BK * LDB : BN * LDB;
+  static constexpr int STAGE = A_ELEMS + B_ELEMS;
+};
+
+__device__ __forceinline__ int64_t decode_offset(int64_t idx, int n, const int64_t* ext,
+                                                 const int64_t* str) {
+  int64_t off = 0;
+  for (int a = n - 1; a >= 0; --a) {
+    int64_t e = ext[a];
+    int64_t q = idx / e;
+    off += (idx - q * e) * str[a];
+    idx = q;
+  }
+  return off;
+}
+
+template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool AK, bool BNC>
+__global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32)
+    zgemm_dmma_kernel(const ZgemmParams p) {
+  using S = Smem<BM, BN, BK, AK, BNC>;
+  constexpr int NWARP = (BM / WM) * (BN / WN);
+  constexpr int NT = NWARP * 32;
+  constexpr int FM = WM / 8;   // 8-row fragments per warp
+  constexpr int FN = WN / 4;   // 4-complex-column fragments per warp
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double2* smem = reinterpret_cast<double2*>(smem_raw);
+  int64_t* rowoff = reinterpret_cast<int64_t*>(smem + STAGES * S::STAGE);
+  int64_t* coloff = rowoff + BM;
+
+  const int tid = threadIdx.x;
+  const int lane = tid & 31;
+  const int warp = tid >> 5;
+  const int wm0 = (warp % (BM / WM)) * WM;
+  const int wn0 = (warp / (BM / WM)) * WN;
+
+  const int64_t mtiles = (p.M + BM - 1) / BM;
+  const int64_t tile = blockIdx.x;
+  const int64_t m0 = (tile % mtiles) * BM;
+  const int64_t n0 = (tile / mtiles) * BN;
+  const int64_t bz = blockIdx.y / p.splits;
+  const int split = blockIdx.y % p.splits;
+
+  // batch offsets
+  int64_t offA = 0, offB = 0, offC = 0;
+  {
+    int64_t idx = bz;
+    for (int a = p.nb - 1; a >= 0; --a) {
+      int64_t e = p.bext[a];
+      int64_t q = idx / e;
+      int64_t r = idx - q * e;
+      offA += r * p.bsA[a];
+      offB += r * p.bsB[a];
+      offC += r * p.bsC[a];
+      idx = q;
+    }
+  }
+  const double2* A = p.A + offA;
+  const double2* B = p.B + offB;
+
+  const int64_t kbeg = static_cast<int64_t>(split) * p.kchunk;
+  const int64_t kend = min(p.K, kbeg + p.kchunk);
+  const int64_t nk = (kend - kbeg + BK - 1) / BK;
+
+  auto load_stage = [&](int slot, int64_t kt) {
+    double2* As = smem + slot * S::STAGE;
+    double2* Bs = As + S::A_ELEMS;
+    const int64_t k0 = kbeg + kt * BK;
+    // A tile: BM x BK
+#pragma unroll
+    for (int e = tid; e < BM * BK; e += NT) {
+      int i, k;
+      if (AK) { i = e / BK; k = e % BK; } else { k = e / BM; i = e % BM; }
+      const int64_t gi = m0 + i, gk = k0 + k;
+      const bool ok = gi < p.M && gk < kend;
+      const double2* src = ok ? A + gi * p.sAi + gk * p.sAk : A;
+      double2* dst = AK ? As + i * S::LDA + k : As + k * S::LDA + i;
+      cp_async16(dst, src, ok);
+    }
+    // B tile: BK x BN
+#pragma unroll
+    for (int e = tid; e < BK * BN; e += NT) {
+      int k, j;
+      if (BNC) { k = e / BN; j = e % BN; } else { j = e / BK; k = e % BK; }
+      const int64_t gj = n0 + j, gk = k0 + k;
+      const bool ok = gj < p.N && gk < kend;
+      const double2* src = ok ? B + gk * p.sBk + gj * p.sBj : B;
+      double2* dst = BNC ? Bs + k * S::LDB + j : Bs + j * S::LDB + k;
+      cp_async16(dst, src, ok);
+    }
+  };
+
+  // Epilogue scatter offsets for this tile.
+  if (p.splits == 1) {
+    for (int r = tid; r < BM; r += NT) {
+      const int64_t gi = m0 + r;
+      rowoff[r] = gi < p.M ? decode_offset(gi, p.nr, p.rext, p.rstr) : 0;
+    }
+    for (int c = tid; c < BN; c += NT) {
+      const int64_t gj = n0 + c;
+      coloff[c] = gj < p.N ? decode_offset(gj, p.nc, p.cext, p.cstr) : 0;
+    }
+  }
+
+  double acc[FM][FN][2];
+#pragma unroll
+  for (int a = 0; a < FM; ++a)
+#pragma unroll
+    for (int b = 0; b < FN; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < nk) load_stage(s, s);
+    cp_async_commit();
+  }
+
+  const int kk = lane & 3;        // k slot within the 4-wide real k step
+  const int a_row = lane >> 2;    // A fragment row
+  const int b_s = kk & 1;         // real-embedding row parity of B'
+  const int b_nn = lane >> 2;     // B' column (0..7)
+  const int b_t = b_nn & 1;
+  const int b_part = b_s ^ b_t;   // 0: Re(b), 1: Im(b)
+  const bool b_neg = b_part && (b_s ^ p.conjB);
+  const bool a_neg = (kk & 1) && p.conjA;
+
+  for (int64_t kt = 0; kt < nk; ++kt) {
+    cp_async_wait<STAGES - 2>();
+    __syncthreads();
+    {
+      const int64_t pf = kt + STAGES - 1;
+      if (pf < nk) load_stage(static_cast<int>(pf % STAGES), pf);
+      cp_async_commit();
+    }
+    const int slot = static_cast<int>(kt % STAGES);
+    const double* As = reinterpret_cast<const double*>(smem + slot * S::STAGE);
+    const double* Bs = reinterpret_cast<const double*>(smem + slot * S::STAGE + S::A_ELEMS);
+#pragma unroll
+    for (int ks = 0; ks < BK / 2; ++ks) {
+      const int kc = ks * 2 + (kk >> 1);
+      double af[FM], bf[FN];
+#pragma unroll
+      for (int a = 0; a < FM; ++a) {
+        const int row = wm0 + a * 8 + a_row;
+        double v = AK ? As[(row * S::LDA + kc) * 2 + (kk & 1)] : As[(kc * S::LDA + row) * 2 + (kk & 1)];
+        af[a] = a_neg ? -v : v;
+      }
+#pragma unroll
+      for (int b = 0; b < FN; ++b) {
+        const int col = wn0 + b * 4 + (b_nn >> 1);
+        double v = BNC ? Bs[(kc * S::LDB + col) * 2 + b_part] : Bs[(col * S::LDB + kc) * 2 + b_part];
+        bf[b] = b_neg ? -v : v;
+      }
+#pragma unroll
+      for (int a = 0; a < FM; ++a)
+#pragma unroll
+        for (int b = 0; b < FN; ++b) dmma884(acc[a][b][0], acc[a][b][1], af[a], bf[b]);
+    }
+  }
+  cp_async_wait<0>();
+  __syncthreads();
+
+  // Epilogue: each lane owns complex C[a*8 + lane>>2][b*4 + lane&3] of every fragment.
+  if (p.splits == 1) {
+    double2* C = p.C + offC;
+#pragma unroll
+    for (int a = 0; a < FM; ++a) {
+      const int li = wm0 + a * 8 + (lane >> 2);
+      if (m0 + li >= p.M) continue;
+      const int64_t ro = rowoff[li];
+#pragma unroll
+      for (int b = 0; b < FN; ++b) {
+        const int lj = wn0 + b * 4 + (lane & 3);
+        if (n0 + lj >= p.N) continue;
+        double2* dst = C + ro + coloff[lj];
+        double2 v = make_double2(acc[a][b][0], acc[a][b][1]);
+        if (p.accumulate) v = cadd(*dst, v);
+        *dst = v;
+      }
+    }
+  } else {
+    double2* W = p.work + ((static_cast<int64_t>(split) * p.batch + bz) * p.M) * p.N;
+#pragma unroll
+    for (int a = 0; a < FM; ++a) {
+      const int64_t gi = m0 + wm0 + a * 8 + (lane >> 2);
+      if (gi >= p.M) continue;
+#pragma unroll
+      for (int b = 0; b < FN; ++b) {
+        const int64_t gj = n0 + wn0 + b * 4 + (lane & 3);
+        if (gj >= p.N) continue;
+        W[gi * p.N + gj] = make_double2(acc[a][b][0], acc[a][b][1]);
+      }
+    }
+  }
+}
+
+// Deterministic split-K reduction (fixed summation order) + epilogue scatter.
+__global__ void zgemm_splitk_reduce(const ZgemmParams p) {
+  const int64_t total = p.batch * p.M * p.N;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t j = e % p.N;
+    const int64_t i = (e / p.N) % p.M;
+    const int64_t b = e / (p.N * p.M);
+    double2 s = make_double2(0.0, 0.0);
+    for (int sp = 0; sp < p.splits; ++sp) s = cadd(s, p.work[(sp * p.batch + b) * p.M * p.N + i * p.N + j]);
+    int64_t offC = 0, idx = b;
+    for (int a = p.nb - 1; a >= 0; --a) {
+      int64_t q = idx / p.bext[a];
+      offC += (idx - q * p.bext[a]) * p.bsC[a];
+      idx = q;
+    }
+    double2* dst = p.C + offC + decode_offset(i, p.nr, p.rext, p.rstr) + decode_offset(j, p.nc, p.cext, p.cstr);
+    if (p.accumulate) s = cadd(*dst, s);
+    *dst = s;
+  }
+}
+
+template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool AK, bool BNC>
+void launch_cfg(const ZgemmParams& p, cudaStream_t stream) {
+  using S = Smem<BM, BN, BK, AK, BNC>;
+  constexpr int NT = (BM / WM) * (BN / WN) * 32;
+  const size_t smem = static_cast<size_t>(STAGES) * S::STAGE * sizeof(double2) + (BM + BN) * sizeof(int64_t);
+  auto kern = zgemm_dmma_kernel<BM, BN, BK, WM, WN, STAGES, AK, BNC>;
+  static bool attr_set = false;  // per instantiation
+  if (!attr_set) {
+    PEPSB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    attr_set = true;
+  }
+  const int64_t tiles = ((p.M + BM - 1) / BM) * ((p.N + BN - 1) / BN);
+  dim3 grid(static_cast<unsigned>(tiles), static_cast<unsigned>(p.batch * p.splits));
+  kern<<<grid, NT, smem, stream>>>(p);
+  PEPSB_LAUNCH();
+}
+
+constexpr int kBM = 64, kBN = 64, kBK = 16, kWM = 32, kWN = 32, kStages = 3;
+
+}  // namespace
+
+int64_t zgemm_plan_splits(ZgemmParams& p, int num_sms) {
+  const int64_t tiles = ((p.M + kBM - 1) / kBM) * ((p.N + kBN - 1) / kBN) * p.batch;
+  const int64_t target = 2LL * num_sms;
+  int64_t splits = 1;
+  if (tiles < target && p.K > 4 * kBK) {
+    splits = std::min<int64_t>((target + tiles - 1) / tiles, (p.K + 4 * kBK - 1) / (4 * kBK));
+    splits = std::max<int64_t>(1, std::min<int64_t>(splits, 256));
+  }
+  int64_t kchunk = (p.K + splits - 1) / splits;
+  kchunk = ((kchunk + kBK - 1) / kBK) * kBK;
+  splits = (p.K + kchunk - 1) / kchunk;
+  if (splits < 1) splits = 1;
+  p.splits = static_cast<int>(splits);
+  p.kchunk = p.K > 0 ? kchunk : kBK;
+  return splits > 1 ? splits * p.batch * p.M * p.N : 0;
+}
+
+void zgemm_launch(ZgemmParams p, cudaStream_t stream) {
+  if (p.M <= 0 || p.N <= 0 || p.batch <= 0) return;
+  if (p.kchunk <= 0) p.kchunk = std::max<int64_t>(p.K, 1);
+  const bool ak = p.sAk == 1;
+  const bool bnc = p.sBj == 1;
+  if (p.K == 0) {
+    // empty contraction: C = 0 (or unchanged when accumulating)
+    p.splits = 1;
+  }
+  if (ak && bnc)
+    launch_cfg<kBM, kBN, kBK, kWM, kWN, kStages, true, true>(p, stream);
+  else if (ak && !bnc)
+    launch_cfg<kBM, kBN, kBK, kWM, kWN, kStages, true, false>(p, stream);
+  else if (!ak && bnc)
+    launch_cfg<kBM, kBN, kBK, kWM, kWN, kStages, false, true>(p, stream);
+  else
+    launch_cfg<kBM, kBN, kBK, kWM, kWN, kStages, false, false>(p, stream);
+  if (p.splits > 1) {
+    const int64_t total = p.batch * p.M * p.N;
+    const int threads = 256;
+    const int64_t blocks = std::min<int64_t>((total + threads - 1) / threads, 148 * 16);
+    zgemm_splitk_reduce<<<static_cast<unsigned>(blocks), threads, 0, stream>>>(p);
+    PEPSB_LAUNCH();
+  }
+}
+
+}  // namespace pepsb

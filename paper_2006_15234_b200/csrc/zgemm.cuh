@@ -1,0 +1,52 @@
+// Complex-FP64 GEMM on the B200 FP64 tensor cores (DMMA.8x8x4).
+//
+// One pairwise contraction of the implicit-operator chain lowers to
+//   C[b][i][j] = sum_k opA(b,i,k) * opB(b,k,j)
+// (the role of cblas_zgemm in the reference, proj/src/einsum.cpp:41-57,224-227),
+// with two differences that remove the reference's operand permutes
+// (einsum.cpp:203-204, tensor.cpp:99-134):
+//   * operands are addressed through (i,k)/(k,j) strides, either index may be
+//     the contiguous one, conjugation is applied on load;
+//   * the epilogue scatters C through separable mixed-radix row/column offsets,
+//     so the result is written directly in whatever label order the NEXT
+//     contraction wants.
+// Complex products use the real embedding  [Re C | Im C] = [Ar | Ai] x
+// [[Br, Bi], [-Bi, Br]], so the interleaved complex buffer of A is already the
+// real A' operand and each B value expands to a 2x2 real block in registers.
+#pragma once
+
+#include <cstdint>
+
+#include "common.cuh"
+
+namespace pepsb {
+
+struct ZgemmParams {
+  const double2* A = nullptr;
+  const double2* B = nullptr;
+  double2* C = nullptr;
+  double2* work = nullptr;  // split-K partials [splits][batch][M][N]
+  int64_t M = 0, N = 0, K = 0;
+  int64_t sAi = 0, sAk = 0, sBk = 0, sBj = 0;  // complex-element strides
+  int conjA = 0, conjB = 0;
+  // batch modes (row-major decode of the batch index)
+  int nb = 0;
+  int64_t bext[4] = {}, bsA[4] = {}, bsB[4] = {}, bsC[4] = {};
+  int64_t batch = 1;
+  // epilogue scatter: row index i decoded over rext (last fastest) -> sum rstr
+  int nr = 0;
+  int64_t rext[kMaxModes] = {}, rstr[kMaxModes] = {};
+  int nc = 0;
+  int64_t cext[kMaxModes] = {}, cstr[kMaxModes] = {};
+  int splits = 1;
+  int64_t kchunk = 0;
+  int accumulate = 0;  // C += result instead of C = result
+};
+
+// Launches the GEMM (and the deterministic split-K reduction when needed).
+// `work` is allocated by the caller when splits > 1 (see zgemm_workspace).
+void zgemm_launch(ZgemmParams p, cudaStream_t stream);
+// Chooses split-K for the problem; returns the workspace size in complex elements.
+int64_t zgemm_plan_splits(ZgemmParams& p, int num_sms);
+
+}  // namespace pepsb

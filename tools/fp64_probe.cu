@@ -1,0 +1,71 @@
+// FP64 peak probe for B200 (MEASURED_PEAKS.json has no FP64 entry).
+// Measures the DMMA (mma.sync m8n8k4 f64 -> SASS DMMA.8x8x4) and DFMA issue
+// ceilings with register-resident operands, timed with CUDA events.
+#include <cstdio>
+#include <cuda_runtime.h>
+
+__global__ void dmma_loop(double* out, int iters) {
+  double a = threadIdx.x * 1e-9, b = 1.0 + threadIdx.x * 1e-12;
+  double d[8][2] = {};
+  for (int i = 0; i < iters; i++) {
+#pragma unroll
+    for (int j = 0; j < 8; j++)
+      asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                   : "+d"(d[j][0]), "+d"(d[j][1]) : "d"(a), "d"(b));
+  }
+  double s = 0;
+  for (int j = 0; j < 8; j++) s += d[j][0] + d[j][1];
+  if (s == 1234.5) out[0] = s;
+}
+
+__global__ void dfma_loop(double* out, int iters) {
+  double a = threadIdx.x * 1e-9, b = 1.0 - 1e-12;
+  double d[16];
+  for (int j = 0; j < 16; j++) d[j] = j;
+  for (int i = 0; i < iters; i++) {
+#pragma unroll
+    for (int j = 0; j < 16; j++) d[j] = fma(d[j], b, a);
+  }
+  double s = 0;
+  for (int j = 0; j < 16; j++) s += d[j];
+  if (s == 1234.5) out[0] = s;
+}
+
+extern "C" int probe(double* res) {
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  double* out;
+  cudaMalloc(&out, 8);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  const int iters = 20000;
+  float best_dmma = 1e30f, best_dfma = 1e30f;
+  for (int warps = 4; warps <= 16; warps *= 2) {
+    int blocks = sms * 4;
+    for (int rep = 0; rep < 3; rep++) {
+      cudaEventRecord(e0);
+      dmma_loop<<<blocks, warps * 32>>>(out, iters);
+      cudaEventRecord(e1);
+      cudaEventSynchronize(e1);
+      float ms;
+      cudaEventElapsedTime(&ms, e0, e1);
+      // flops per launch: blocks*warps*iters*8 DMMA * (8*8*4*2)
+      double fl = (double)blocks * warps * iters * 8 * 512;
+      double tf = fl / (ms * 1e-3) / 1e12;
+      if (tf > res[0]) res[0] = tf;
+      cudaEventRecord(e0);
+      dfma_loop<<<blocks, warps * 32>>>(out, iters);
+      cudaEventRecord(e1);
+      cudaEventSynchronize(e1);
+      cudaEventElapsedTime(&ms, e0, e1);
+      fl = (double)blocks * warps * 32 * iters * 16 * 2;
+      tf = fl / (ms * 1e-3) / 1e12;
+      if (tf > res[1]) res[1] = tf;
+    }
+  }
+  (void)best_dmma; (void)best_dfma;
+  cudaFree(out);
+  return (int)cudaGetLastError();
+}
