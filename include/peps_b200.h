@@ -85,6 +85,11 @@ int pepsb_ctx_set_option(pepsb_ctx* ctx, const char* key, int64_t value);
  * einsumsvd_flops, peak_elements, kernel launches issued by the library */
 int pepsb_ctx_counters(pepsb_ctx* ctx, uint64_t* out4);
 int pepsb_ctx_reset_counters(pepsb_ctx* ctx);
+/* Per-launch CUDA-event timing of the library's kernels (off by default).
+ * Report: 4 kinds (0 GEMM, 1 small factorizations, 2 gathers, 3 other) x
+ * {launches, device ms, algorithmic real flops, algorithmic bytes}. */
+int pepsb_ctx_profile(pepsb_ctx* ctx, int enable);
+int pepsb_ctx_profile_report(pepsb_ctx* ctx, double* out16);
 /* CUDA stream the library enqueues on (cudaStream_t), for event timing */
 void* pepsb_ctx_stream(pepsb_ctx* ctx);
 
@@ -94,6 +99,8 @@ int pepsb_tensor_from_device(pepsb_ctx* ctx, int ndim, const int64_t* shape, con
 int pepsb_tensor_ndim(const pepsb_tensor* t);
 int pepsb_tensor_shape(const pepsb_tensor* t, int64_t* shape);
 int pepsb_tensor_to_host(pepsb_ctx* ctx, const pepsb_tensor* t, double* out);
+/* stream-ordered copy into (pinned) host memory; completes at pepsb_ctx_sync */
+int pepsb_tensor_to_host_async(pepsb_ctx* ctx, const pepsb_tensor* t, double* out);
 int pepsb_tensor_to_device(pepsb_ctx* ctx, const pepsb_tensor* t, void* dptr);
 void pepsb_tensor_free(pepsb_tensor* t);
 

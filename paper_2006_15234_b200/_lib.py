@@ -49,11 +49,14 @@ _SIGS = {
     "pepsb_ctx_counters": (C.c_int, [_VP, C.POINTER(C.c_uint64)]),
     "pepsb_ctx_reset_counters": (C.c_int, [_VP]),
     "pepsb_ctx_stream": (_VP, [_VP]),
+    "pepsb_ctx_profile": (C.c_int, [_VP, C.c_int]),
+    "pepsb_ctx_profile_report": (C.c_int, [_VP, C.POINTER(C.c_double)]),
     "pepsb_tensor_from_host": (C.c_int, [_VP, C.c_int, C.POINTER(C.c_int64), _VP, C.POINTER(_VP)]),
     "pepsb_tensor_from_device": (C.c_int, [_VP, C.c_int, C.POINTER(C.c_int64), _VP, C.POINTER(_VP)]),
     "pepsb_tensor_ndim": (C.c_int, [_VP]),
     "pepsb_tensor_shape": (C.c_int, [_VP, C.POINTER(C.c_int64)]),
     "pepsb_tensor_to_host": (C.c_int, [_VP, _VP, _VP]),
+    "pepsb_tensor_to_host_async": (C.c_int, [_VP, _VP, _VP]),
     "pepsb_tensor_to_device": (C.c_int, [_VP, _VP, _VP]),
     "pepsb_tensor_free": (None, [_VP]),
     "pepsb_random_tensor": (C.c_int, [_VP, C.c_int, C.POINTER(C.c_int64), C.c_uint64, C.c_int, C.POINTER(_VP)]),

@@ -109,6 +109,16 @@ class Context:
     def reset_counters(self):
         check(lib().pepsb_ctx_reset_counters(self.h))
 
+    def profile(self, enable: bool):
+        check(lib().pepsb_ctx_profile(self.h, int(bool(enable))))
+
+    def profile_report(self) -> dict:
+        a = (C.c_double * 16)()
+        check(lib().pepsb_ctx_profile_report(self.h, a))
+        kinds = ["gemm", "small", "gather", "other"]
+        return {k: dict(launches=int(a[4 * i]), ms=a[4 * i + 1], flops=a[4 * i + 2], bytes=a[4 * i + 3])
+                for i, k in enumerate(kinds)}
+
     @property
     def stream(self) -> int:
         return int(lib().pepsb_ctx_stream(self.h) or 0)

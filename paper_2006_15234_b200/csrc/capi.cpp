@@ -204,6 +204,21 @@ int pepsb_ctx_reset_counters(pepsb_ctx* c) {
   });
 }
 
+int pepsb_ctx_profile(pepsb_ctx* c, int enable) {
+  return guard([&] {
+    need(c, "ctx");
+    c->ctx->profile_clear();
+    c->ctx->profiling = enable != 0;
+  });
+}
+
+int pepsb_ctx_profile_report(pepsb_ctx* c, double* out16) {
+  return guard([&] {
+    need(c, "ctx");
+    c->ctx->profile_report(out16);
+  });
+}
+
 void* pepsb_ctx_stream(pepsb_ctx* c) { return c ? static_cast<void*>(c->ctx->stream) : nullptr; }
 
 int pepsb_tensor_from_host(pepsb_ctx* c, int ndim, const int64_t* shape, const double* data, pepsb_tensor** out) {
@@ -242,6 +257,15 @@ int pepsb_tensor_to_host(pepsb_ctx* c, const pepsb_tensor* t, double* out) {
     if (t->t.size())
       PEPSB_CUDA(cudaMemcpyAsync(out, t->t.data(), t->t.size() * sizeof(double2), cudaMemcpyDeviceToHost, c->ctx->stream));
     c->ctx->sync();
+  });
+}
+
+int pepsb_tensor_to_host_async(pepsb_ctx* c, const pepsb_tensor* t, double* out) {
+  return guard([&] {
+    need(c, "ctx");
+    need(t, "tensor");
+    if (t->t.size())
+      PEPSB_CUDA(cudaMemcpyAsync(out, t->t.data(), t->t.size() * sizeof(double2), cudaMemcpyDeviceToHost, c->ctx->stream));
   });
 }
 

@@ -57,6 +57,8 @@ Ctx::Ctx(int dev) : device(dev) {
 
 Ctx::~Ctx() {
   if (stream) cudaStreamSynchronize(stream);
+  profile_clear();
+  for (auto e : event_pool) cudaEventDestroy(e);
   if (d_status) cudaFree(d_status);
   if (h_status) cudaFreeHost(h_status);
   if (stream) cudaStreamDestroy(stream);
@@ -93,5 +95,49 @@ DTensor Ctx::zeros(const std::vector<int64_t>& shape) {
 }
 
 void Ctx::sync() { PEPSB_CUDA(cudaStreamSynchronize(stream)); }
+
+cudaEvent_t Ctx::take_event() {
+  if (!event_pool.empty()) {
+    cudaEvent_t e = event_pool.back();
+    event_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  PEPSB_CUDA(cudaEventCreate(&e));
+  return e;
+}
+
+void Ctx::profile_clear() {
+  for (auto& r : prof) {
+    event_pool.push_back(r.a);
+    event_pool.push_back(r.b);
+  }
+  prof.clear();
+}
+
+void Ctx::profile_report(double* out) {
+  sync();
+  for (int i = 0; i < 4 * kProfKinds; ++i) out[i] = 0.0;
+  for (auto& r : prof) {
+    float ms = 0.f;
+    PEPSB_CUDA(cudaEventElapsedTime(&ms, r.a, r.b));
+    out[4 * r.kind + 0] += 1.0;
+    out[4 * r.kind + 1] += ms;
+    out[4 * r.kind + 2] += r.flops;
+    out[4 * r.kind + 3] += r.bytes;
+  }
+}
+
+ProfScope::ProfScope(Ctx& c, int kind, double flops, double bytes) : ctx(c) {
+  if (!ctx.profiling) return;
+  Ctx::ProfRec r{ctx.take_event(), ctx.take_event(), kind, flops, bytes};
+  PEPSB_CUDA(cudaEventRecord(r.a, ctx.stream));
+  ctx.prof.push_back(r);
+  idx = static_cast<int>(ctx.prof.size()) - 1;
+}
+
+ProfScope::~ProfScope() {
+  if (idx >= 0) cudaEventRecord(ctx.prof[idx].b, ctx.stream);
+}
 
 }  // namespace pepsb

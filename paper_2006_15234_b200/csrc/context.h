@@ -87,7 +87,33 @@ class Ctx {
     if (n > peak_elements) peak_elements = n;
   }
   // Options
-  int orth_mode = 0;  // 0: reference-faithful Gram eigh; 1: CholeskyQR2
+  // Power-iteration orthogonalisation: 1 = CholeskyQR2 (default; same span as
+  // the reference, different basis -> gauge-invariant parity), 0 = the
+  // reference's Gram-eigh basis (elementwise parity of t1/t2).
+  int orth_mode = 1;
+
+  // Optional per-launch device timing (CUDA events on `stream`), used by the
+  // bench's roofline pass; off in timed runs.
+  enum ProfKind { kProfGemm = 0, kProfSmall = 1, kProfGather = 2, kProfOther = 3, kProfKinds = 4 };
+  struct ProfRec {
+    cudaEvent_t a, b;
+    int kind;
+    double flops, bytes;
+  };
+  bool profiling = false;
+  std::vector<ProfRec> prof;
+  std::vector<cudaEvent_t> event_pool;
+  cudaEvent_t take_event();
+  void profile_report(double* out);  // per kind: count, ms, flops, bytes
+  void profile_clear();
+};
+
+// RAII device-time scope (no-op unless ctx.profiling).
+struct ProfScope {
+  ProfScope(Ctx& c, int kind, double flops = 0.0, double bytes = 0.0);
+  ~ProfScope();
+  Ctx& ctx;
+  int idx = -1;
 };
 
 }  // namespace pepsb

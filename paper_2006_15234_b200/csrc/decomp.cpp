@@ -69,7 +69,10 @@ void mm(Ctx& ctx, double2* C, const double2* A, bool transA, bool conjA, const d
     work = ctx.alloc(ws);
     p.work = work->p;
   }
-  zgemm_launch(p, ctx.stream);
+  {
+    ProfScope ps(ctx, Ctx::kProfGemm, 8.0 * M * N * K, 16.0 * (M * K + K * N + M * N));
+    zgemm_launch(p, ctx.stream);
+  }
   ctx.launches += p.splits > 1 ? 2 : 1;
   ctx.flops += 2ull * M * N * K;
 }
@@ -97,10 +100,17 @@ std::string unused_labels(const std::string& used, int n) {
 }
 
 void read_status(Ctx& ctx) {
-  PEPSB_CUDA(cudaMemcpyAsync(ctx.h_status, ctx.d_status, sizeof(int), cudaMemcpyDeviceToHost, ctx.stream));
+  PEPSB_CUDA(cudaMemcpyAsync(ctx.h_status, ctx.d_status, 2 * sizeof(int), cudaMemcpyDeviceToHost, ctx.stream));
 }
 
+// word 0: factorization status of the current stage; word 1: CholeskyQR
+// breakdowns during the power iterations (orth_mode 1).
 void clear_status(Ctx& ctx) { PEPSB_CUDA(cudaMemsetAsync(ctx.d_status, 0, sizeof(int), ctx.stream)); }
+void clear_all_status(Ctx& ctx) { PEPSB_CUDA(cudaMemsetAsync(ctx.d_status, 0, 2 * sizeof(int), ctx.stream)); }
+
+// Thrown when CholeskyQR met a numerically rank-deficient probe block: the
+// decomposition is redone on the reference-faithful Gram-eigh route.
+struct RedoFaithful {};
 
 void raise_status(int st, bool gram_stage) {
   if (st & kSmallZeroGram) throw Error(kNumericalError, "gram orthogonalization of a zero operator");
@@ -119,10 +129,18 @@ LTensor orth(Ctx& ctx, const LTensor& Y) {
   BufPtr Q = ctx.alloc(rows * k);
   if (ctx.orth_mode == 1) {
     BufPtr R = ctx.alloc(k * k), Ri = ctx.alloc(k * k), G2 = ctx.alloc(k * k), Q1 = ctx.alloc(rows * k);
-    chol_factors(G->p, static_cast<int>(k), 0.0, R->p, Ri->p, ctx.d_status, ctx.stream);
+    {
+      ProfScope ps_(ctx, Ctx::kProfSmall);
+      // breakdowns are flagged in status word 1; rsvd_core then redoes the
+      // decomposition on the reference-faithful route (clamp + completion)
+      chol_factors(G->p, static_cast<int>(k), 0.0, R->p, Ri->p, ctx.d_status + 1, ctx.stream);
+    }
     mm(ctx, Q1->p, Y.ptr, false, false, Ri->p, false, false, rows, k, k);
     mm(ctx, G2->p, Q1->p, true, true, Q1->p, false, false, k, k, rows);
-    chol_factors(G2->p, static_cast<int>(k), 0.0, R->p, Ri->p, ctx.d_status, ctx.stream);
+    {
+      ProfScope ps_(ctx, Ctx::kProfSmall);
+      chol_factors(G2->p, static_cast<int>(k), 0.0, R->p, Ri->p, ctx.d_status + 1, ctx.stream);
+    }
     mm(ctx, Q->p, Q1->p, false, false, Ri->p, false, false, rows, k, k);
     ctx.launches += 2;
   } else {
@@ -131,10 +149,16 @@ LTensor orth(Ctx& ctx, const LTensor& Y) {
     int* d_any = d_def + k;
     BufPtr work;
     if (2 * k * k * 16 > 200 * 1024) work = ctx.alloc(2 * k * k);
-    gram_factors(G->p, static_cast<int>(k), P->p, R->p, d_def, d_any, ctx.d_status, work ? work->p : nullptr,
-                 ctx.stream);
+    {
+      ProfScope ps_(ctx, Ctx::kProfSmall);
+      gram_factors(G->p, static_cast<int>(k), P->p, R->p, d_def, d_any, ctx.d_status, work ? work->p : nullptr,
+                   ctx.stream);
+    }
     mm(ctx, Q->p, Y.ptr, false, Y.conj, P->p, false, false, rows, k, k);
-    complete_columns(Q->p, rows, static_cast<int>(k), d_def, d_any, ctx.d_status, ctx.stream);
+    {
+      ProfScope ps_(ctx, Ctx::kProfSmall);
+      complete_columns(Q->p, rows, static_cast<int>(k), d_def, d_any, ctx.d_status, ctx.stream);
+    }
     ctx.launches += 2;
   }
   LTensor out = Y;
@@ -146,82 +170,83 @@ LTensor orth(Ctx& ctx, const LTensor& Y) {
 }
 
 struct Projected {
-  BufPtr Ut, Wh, Rinv;  // k x k each
+  BufPtr Ut;  // k x k left singular vectors of B = P^H A (phase-fixed)
   std::vector<double> s;
+  bool tsqr = false;  // accurate fallback used
 };
 
-// SVD of B = Z^H (Z: rows x k contiguous): CholeskyQR2 (+shift) then Jacobi on R^H.
-Projected projected_svd(Ctx& ctx, const LTensor& Z) {
+// SVD of B = Z^H (Z: rows x k contiguous) through an R factor of Z
+// (B = R^H Q^H, so B's singular values / left vectors are R^H's):
+//   CholeskyQR2 R when it is provably accurate (no breakdown and the first
+//   `target` singular values above 1e-7 sigma_0, i.e. kappa < u^-1/2);
+//   otherwise the Householder TSQR R (backward stable like the reference's
+//   zgeqrf route, linalg.cpp:87-125, incl. exactly rank-deficient Z).
+Projected projected_svd(Ctx& ctx, const LTensor& Z, int64_t target) {
   const int64_t k = Z.ext.back();
   const int64_t rows = Z.size() / k;
   const int ki = static_cast<int>(k);
+  Projected out;
+  out.Ut = ctx.alloc(k * k);
+  BufPtr Wh = ctx.alloc(k * k);
+  BufPtr sdev = ctx.alloc((k + 1) / 2 + 1);
+  double* d_s = reinterpret_cast<double*>(sdev->p);
+  BufPtr svd_work;
+  if (int64_t ws = small_svd_workspace(ki, ki, 1)) svd_work = ctx.alloc(ws);
+  auto svd_of_rh = [&](const BufPtr& R) {
+    LTensor Rh = reduce_to(ctx, wrap(R, "ab", {k, k}, true), "ba");
+    {
+      ProfScope ps_(ctx, Ctx::kProfSmall);
+      small_svd(Rh.ptr, 0, ki, ki, ki, out.Ut->p, 0, d_s, 0, Wh->p, 0, 1, ctx.d_status,
+                svd_work ? svd_work->p : nullptr, ctx.stream);
+    }
+    ++ctx.launches;
+    out.s.resize(k);
+    PEPSB_CUDA(cudaMemcpyAsync(out.s.data(), d_s, k * sizeof(double), cudaMemcpyDeviceToHost, ctx.stream));
+    read_status(ctx);
+    ctx.sync();
+    return *ctx.h_status;
+  };
   auto gram = [&](const double2* X) {
     BufPtr G = ctx.alloc(k * k);
     mm(ctx, G->p, X, true, true, X, false, false, k, k, rows);
     return G;
   };
-  BufPtr G1 = gram(Z.ptr);
-  BufPtr R1 = ctx.alloc(k * k), R1i = ctx.alloc(k * k);
-  chol_factors(G1->p, ki, 0.0, R1->p, R1i->p, ctx.d_status, ctx.stream);
-  ++ctx.launches;
-  read_status(ctx);
-  ctx.sync();
-  int st = *ctx.h_status;
-  raise_status(st, true);
-  bool shifted = false;
-  if (st & kSmallCholBreakdown) {
-    clear_status(ctx);
-    // shifted CholeskyQR3 (Fukaya et al.): s = 11 (m n + n (n + 1)) u ||Z||_2^2, ||Z||_2^2 <= trace(G)
-    const double u = 1.1102230246251565e-16;
-    const double shift_rel = 11.0 * (static_cast<double>(rows) * k + static_cast<double>(k) * (k + 1)) * u;
-    chol_factors(G1->p, ki, shift_rel, R1->p, R1i->p, ctx.d_status, ctx.stream);
-    ++ctx.launches;
-    shifted = true;
-  }
-  BufPtr Q1 = ctx.alloc(rows * k);
-  mm(ctx, Q1->p, Z.ptr, false, false, R1i->p, false, false, rows, k, k);
-  BufPtr G2 = gram(Q1->p);
-  BufPtr R2 = ctx.alloc(k * k), R2i = ctx.alloc(k * k);
-  chol_factors(G2->p, ki, 0.0, R2->p, R2i->p, ctx.d_status, ctx.stream);
-  ++ctx.launches;
-  BufPtr R = ctx.alloc(k * k), Ri = ctx.alloc(k * k);
-  if (!shifted) {
+  bool ok = false;
+  if (rows >= k) {
+    BufPtr G1 = gram(Z.ptr);
+    BufPtr R1 = ctx.alloc(k * k), R1i = ctx.alloc(k * k);
+    {
+      ProfScope ps_(ctx, Ctx::kProfSmall);
+      chol_factors(G1->p, ki, 0.0, R1->p, R1i->p, ctx.d_status, ctx.stream);
+    }
+    BufPtr Q1 = ctx.alloc(rows * k);
+    mm(ctx, Q1->p, Z.ptr, false, false, R1i->p, false, false, rows, k, k);
+    BufPtr G2 = gram(Q1->p);
+    BufPtr R2 = ctx.alloc(k * k), R2i = ctx.alloc(k * k), R = ctx.alloc(k * k);
+    {
+      ProfScope ps_(ctx, Ctx::kProfSmall);
+      chol_factors(G2->p, ki, 0.0, R2->p, R2i->p, ctx.d_status, ctx.stream);
+    }
+    ctx.launches += 2;
     mm(ctx, R->p, R2->p, false, false, R1->p, false, false, k, k, k);
-    mm(ctx, Ri->p, R1i->p, false, false, R2i->p, false, false, k, k, k);
-  } else {
-    BufPtr Q2 = ctx.alloc(rows * k);
-    mm(ctx, Q2->p, Q1->p, false, false, R2i->p, false, false, rows, k, k);
-    BufPtr G3 = gram(Q2->p);
-    BufPtr R3 = ctx.alloc(k * k), R3i = ctx.alloc(k * k), T = ctx.alloc(k * k);
-    chol_factors(G3->p, ki, 0.0, R3->p, R3i->p, ctx.d_status, ctx.stream);
-    ++ctx.launches;
-    mm(ctx, T->p, R3->p, false, false, R2->p, false, false, k, k, k);
-    mm(ctx, R->p, T->p, false, false, R1->p, false, false, k, k, k);
-    mm(ctx, T->p, R1i->p, false, false, R2i->p, false, false, k, k, k);
-    mm(ctx, Ri->p, T->p, false, false, R3i->p, false, false, k, k, k);
+    const int st = svd_of_rh(R);
+    raise_status(st, false);
+    const int64_t t = std::max<int64_t>(1, std::min<int64_t>(target, k));
+    ok = !(st & kSmallCholBreakdown) && out.s[0] > 0.0 && out.s[t - 1] >= 1e-7 * out.s[0];
+    clear_status(ctx);
   }
-  // Rh = R^H
-  LTensor Rl = wrap(R, "ab", {k, k}, true);
-  LTensor Rh = reduce_to(ctx, Rl, "ba");
-  Projected out;
-  out.Ut = ctx.alloc(k * k);
-  out.Wh = ctx.alloc(k * k);
-  out.Rinv = Ri;
-  BufPtr sdev = ctx.alloc((k + 1) / 2);
-  double* d_s = reinterpret_cast<double*>(sdev->p);
-  BufPtr work;
-  int64_t ws = small_svd_workspace(ki, ki, 1);
-  if (ws) work = ctx.alloc(ws);
-  small_svd(Rh.ptr, 0, ki, ki, ki, out.Ut->p, 0, d_s, 0, out.Wh->p, 0, 1, ctx.d_status, work ? work->p : nullptr,
-            ctx.stream);
-  ++ctx.launches;
-  out.s.resize(k);
-  PEPSB_CUDA(cudaMemcpyAsync(out.s.data(), d_s, k * sizeof(double), cudaMemcpyDeviceToHost, ctx.stream));
-  read_status(ctx);
-  ctx.sync();
-  st = *ctx.h_status;
-  raise_status(st, false);
-  if (st & kSmallCholBreakdown) throw Error(kNumericalError, "SVD failed to converge (CholeskyQR breakdown)");
+  if (!ok) {
+    BufPtr R = ctx.alloc(k * k);
+    BufPtr ws = ctx.alloc(tsqr_workspace(rows, ki));
+    {
+      ProfScope ps_(ctx, Ctx::kProfSmall);
+      tsqr_r(Z.ptr, rows, ki, R->p, ws->p, ctx.stream);
+    }
+    ++ctx.launches;
+    const int st = svd_of_rh(R);
+    raise_status(st, false);
+    out.tsqr = true;
+  }
   return out;
 }
 
@@ -254,7 +279,7 @@ EinsumsvdResultD rsvd_core(Ctx& ctx, const ImplicitOp& op, const Trunc& policy, 
   std::string used = op.rows + op.cols + X;
   for (auto& l : op.labels) used += l;
   const std::string extra = unused_labels(used, 2);
-  const char RK = extra[0], LL = extra[1];
+  const char RK = extra[0];
 
   const size_t nt = op.tensors.size();
   std::vector<LeafMeta> meta_ap, meta_adj;
@@ -297,7 +322,7 @@ EinsumsvdResultD rsvd_core(Ctx& ctx, const ImplicitOp& op, const Trunc& policy, 
   random_fill(om->p, static_cast<int>(qord.size()), pext.data(), lstr.data(), cfg.seed, 0, ctx.stream);
   ++ctx.launches;
   LTensor q = wrap(om, qord, pext);
-  clear_status(ctx);
+  clear_all_status(ctx);
 
   auto apply = [&](const LTensor& qq) {
     leaves_ap.back() = qq;
@@ -315,7 +340,8 @@ EinsumsvdResultD rsvd_core(Ctx& ctx, const ImplicitOp& op, const Trunc& policy, 
   }
   LTensor z = adjoint(p);
   q = LTensor();
-  Projected pr = projected_svd(ctx, z);
+  Projected pr = projected_svd(ctx, z, target);
+  if (ctx.orth_mode == 1 && (ctx.h_status[1] & kSmallCholBreakdown)) throw RedoFaithful{};
 
   Trunc pol = policy;
   int64_t rank = static_cast<int64_t>(retained_rank(pr.s, pol));
@@ -327,20 +353,17 @@ EinsumsvdResultD rsvd_core(Ctx& ctx, const ImplicitOp& op, const Trunc& policy, 
     wl.assign(rank, 1.0);
     wr.assign(rank, 1.0);
   }
-  BufPtr dwl = upload_doubles(ctx, wl), dwr = upload_doubles(ctx, wr);
+  // V_j = Z u_j / s_j  (B = Z^H = U S V^H), so t2 = diag(wr) V^H = conj(Z conj(Mc)) with
+  // Mc = conj(U[:, :rank]) diag(wr / s).
+  std::vector<double> wv(rank);
+  for (int64_t j = 0; j < rank; ++j) wv[j] = s[j] > 0.0 ? wr[j] / s[j] : 0.0;
+  BufPtr dwl = upload_doubles(ctx, wl), dwv = upload_doubles(ctx, wv);
   const int64_t k = probe;
-  // Uw = Ut[:, :rank] diag(wl)   (k x rank)
-  BufPtr Uw = ctx.alloc(k * rank);
+  BufPtr Uw = ctx.alloc(k * rank), Mcb = ctx.alloc(k * rank);
   slice_scale_cols(Uw->p, pr.Ut->p, k, rank, k, reinterpret_cast<double*>(dwl->p), 0, ctx.stream);
-  // Whw = diag(wr) Wh[:rank, :]  (rank x k)
-  BufPtr Whw = ctx.alloc(rank * k);
-  slice_scale_cols(Whw->p, pr.Wh->p, rank, k, k, nullptr, 0, ctx.stream);
-  scale_axis(Whw->p, rank * k, k, rank, reinterpret_cast<double*>(dwr->p), ctx.stream);
-  ctx.launches += 3;
-  // Mc = conj(Rinv) Whw^T  (k x rank):  Mc[a][j] = sum_l conj(Rinv[a][l]) Whw[j][l]
-  LTensor Mc = pairwise_gemm(ctx, wrap(pr.Rinv, std::string(1, X) + LL, {k, k}, true),
-                             wrap(Whw, std::string(1, RK) + LL, {rank, k}), "", std::string(1, LL),
-                             std::string(1, X) + RK);
+  slice_scale_cols(Mcb->p, pr.Ut->p, k, rank, k, reinterpret_cast<double*>(dwv->p), 1, ctx.stream);
+  ctx.launches += 2;
+  LTensor Mc = wrap(Mcb, std::string(1, X) + RK, {k, rank});
   // t1 = P Uw -> (row axes..., rank);  t2 = conj(Z) Mc -> (rank, col axes...)
   std::string t1_order = op.rows + RK;
   if (!t1_perm.empty()) {
@@ -474,15 +497,21 @@ std::pair<DTensor, DTensor> gram_orthogonalize(Ctx& ctx, const DTensor& a, int s
   rshape.insert(rshape.end(), cs.begin(), cs.end());
   R.shape = rshape;
   R.buf = ctx.alloc(cols * cols);
-  gram_factors(G->p, static_cast<int>(cols), P->p, R.data(), d_def, d_any, ctx.d_status, work ? work->p : nullptr,
-               ctx.stream);
+  {
+    ProfScope ps_(ctx, Ctx::kProfSmall);
+    gram_factors(G->p, static_cast<int>(cols), P->p, R.data(), d_def, d_any, ctx.d_status, work ? work->p : nullptr,
+                 ctx.stream);
+  }
   DTensor Q;
   std::vector<int64_t> qshape = rs;
   qshape.insert(qshape.end(), cs.begin(), cs.end());
   Q.shape = qshape;
   Q.buf = ctx.alloc(rows * cols);
   mm(ctx, Q.data(), a.data(), false, false, P->p, false, false, rows, cols, cols);
-  complete_columns(Q.data(), rows, static_cast<int>(cols), d_def, d_any, ctx.d_status, ctx.stream);
+  {
+    ProfScope ps_(ctx, Ctx::kProfSmall);
+    complete_columns(Q.data(), rows, static_cast<int>(cols), d_def, d_any, ctx.d_status, ctx.stream);
+  }
   ctx.launches += 2;
   read_status(ctx);
   ctx.sync();
@@ -506,9 +535,12 @@ SvdD svd(Ctx& ctx, const DTensor& t, int split) {
   BufPtr work;
   int64_t ws = small_svd_workspace(static_cast<int>(m), static_cast<int>(n), 1);
   if (ws) work = ctx.alloc(ws);
-  small_svd(t.data(), 0, static_cast<int>(m), static_cast<int>(n), static_cast<int>(n), out.u.data(), 0,
-            reinterpret_cast<double*>(sd->p), 0, out.v.data(), 0, 1, ctx.d_status, work ? work->p : nullptr,
-            ctx.stream);
+  {
+    ProfScope ps_(ctx, Ctx::kProfSmall);
+    small_svd(t.data(), 0, static_cast<int>(m), static_cast<int>(n), static_cast<int>(n), out.u.data(), 0,
+              reinterpret_cast<double*>(sd->p), 0, out.v.data(), 0, 1, ctx.d_status, work ? work->p : nullptr,
+              ctx.stream);
+  }
   ++ctx.launches;
   out.s.resize(k);
   PEPSB_CUDA(cudaMemcpyAsync(out.s.data(), sd->p, k * sizeof(double), cudaMemcpyDeviceToHost, ctx.stream));
@@ -518,8 +550,28 @@ SvdD svd(Ctx& ctx, const DTensor& t, int split) {
   return out;
 }
 
+namespace {
+EinsumsvdResultD rsvd_faithful_fallback(Ctx& ctx, const ImplicitOp& op, const Trunc& policy, const Rsvd& cfg,
+                                        int absorb, const std::vector<int>& t1_perm) {
+  try {
+    return rsvd_core(ctx, op, policy, cfg, absorb, t1_perm);
+  } catch (const RedoFaithful&) {
+    const int saved = ctx.orth_mode;
+    ctx.orth_mode = 0;
+    try {
+      EinsumsvdResultD r = rsvd_core(ctx, op, policy, cfg, absorb, t1_perm);
+      ctx.orth_mode = saved;
+      return r;
+    } catch (...) {
+      ctx.orth_mode = saved;
+      throw;
+    }
+  }
+}
+}  // namespace
+
 SvdTripleD randomized_svd(Ctx& ctx, const ImplicitOp& op, const Trunc& policy, const Rsvd& cfg) {
-  EinsumsvdResultD r = rsvd_core(ctx, op, policy, cfg, -1, {});
+  EinsumsvdResultD r = rsvd_faithful_fallback(ctx, op, policy, cfg, -1, {});
   return SvdTripleD{r.t1, r.t2, r.s, r.rank_clamped};
 }
 
@@ -530,13 +582,7 @@ EinsumsvdResultD einsumsvd(Ctx& ctx, const ImplicitOp& op, const Trunc& policy, 
   const uint64_t f0 = ctx.flops;
   EinsumsvdResultD out;
   if (strategy == kImplicitRsvd) {
-    int saved = ctx.orth_mode;
-    try {
-      out = rsvd_core(ctx, op, policy, cfg, absorb, t1_perm);
-    } catch (const Error& e) {
-      ctx.orth_mode = saved;
-      throw;
-    }
+    out = rsvd_faithful_fallback(ctx, op, policy, cfg, absorb, t1_perm);
   } else {
     DTensor mat = implicit_materialize(ctx, op);
     const int split = static_cast<int>(op.rows.size());

@@ -128,7 +128,10 @@ LTensor reduce_to(Ctx& ctx, const LTensor& t, const std::string& out_order) {
   out.labels = out_order;
   out.ext = oext;
   out.str = row_major_strides(oext);
-  gather_sum(out.buf->p, t.ptr, p, ctx.stream);
+  {
+    ProfScope ps(ctx, Ctx::kProfGather, 0.0, 32.0 * kept * sum);
+    gather_sum(out.buf->p, t.ptr, p, ctx.stream);
+  }
   ++ctx.launches;
   if (p.nsum) ctx.flops += static_cast<uint64_t>(kept * sum);
   return out;
@@ -219,7 +222,11 @@ LTensor pairwise_gemm(Ctx& ctx, const LTensor& A, const LTensor& B, const std::s
     work = ctx.alloc(ws);
     p.work = work->p;
   }
-  zgemm_launch(p, ctx.stream);
+  {
+    ProfScope ps(ctx, Ctx::kProfGemm, 8.0 * p.batch * p.M * p.N * p.K,
+                 16.0 * (p.batch * (p.M * p.K + p.K * p.N + p.M * p.N)));
+    zgemm_launch(p, ctx.stream);
+  }
   ctx.launches += p.splits > 1 ? 2 : 1;
   const uint64_t macs = static_cast<uint64_t>(p.batch) * p.M * p.N * p.K;
   ctx.flops += 2 * macs;

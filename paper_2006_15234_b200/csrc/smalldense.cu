@@ -22,6 +22,19 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
+// Deterministic block-wide sum (fixed summation order; every thread gets the total).
+__device__ double block_sum(double v) {
+  __shared__ double part[32];
+  v = warp_sum(v);
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  __syncthreads();
+  if (lane == 0) part[w] = v;
+  __syncthreads();
+  double t = 0.0;
+  for (int i = 0; i < nw; ++i) t += part[i];
+  return t;
+}
+
 __device__ __forceinline__ int rr_pos(int i, int r, int npad) {
   return i == 0 ? 0 : ((i - 1 + r) % (npad - 1)) + 1;
 }
@@ -163,12 +176,7 @@ __global__ void __launch_bounds__(kThreads) gram_factors_kernel(const double2* G
   double fro = 0.0;
   for (int e = threadIdx.x; e < n * n; e += blockDim.x) fro += cnorm2(X[e]);
   // abs skip: rotations below the rounding level of ||G||^2 do not move eigenvalues.
-  __shared__ double fro_sh;
-  if (threadIdx.x == 0) fro_sh = 0.0;
-  __syncthreads();
-  atomicAdd(&fro_sh, fro);
-  __syncthreads();
-  const double abs_skip = 1e-34 * fro_sh;
+  const double abs_skip = 1e-34 * block_sum(fro);
   onesided_jacobi(X, n, n, n, V, n, 1e-15, abs_skip, 40, status);
 
   // eigenvalue j = Re(v_j^H G v_j) = Re(v_j^H x_j)   (X = G V)
@@ -288,7 +296,6 @@ __device__ void complete_unit_columns(double2* X, int rows, int cols, int ld, co
                                       int* status) {
   // Orthonormal completion of flagged columns by Gram-Schmidt of canonical
   // basis vectors (same rule as decomposition.cpp:88-115), column-major X.
-  __shared__ double red[3];
   int next_basis = 0;
   for (int j = 0; j < cols; ++j) {
     if (!bad[j]) continue;
@@ -306,31 +313,22 @@ __device__ void complete_unit_columns(double2* X, int rows, int cols, int ld, co
         for (int c = 0; c < cols; ++c) {
           if (c == j || (bad[c] && c > j)) continue;
           const double2* qc = X + static_cast<int64_t>(c) * ld;
-          if (threadIdx.x < 2) red[threadIdx.x] = 0.0;
-          __syncthreads();
           double pr = 0.0, pi = 0.0;
           for (int r = threadIdx.x; r < rows; r += blockDim.x) {
             double2 q = qc[r], x = v[r];
             pr += q.x * x.x + q.y * x.y;
             pi += q.x * x.y - q.y * x.x;
           }
-          pr = warp_sum(pr);
-          pi = warp_sum(pi);
-          if ((threadIdx.x & 31) == 0) { atomicAdd(&red[0], pr); atomicAdd(&red[1], pi); }
-          __syncthreads();
-          const double2 proj = make_double2(red[0], red[1]);
+          pr = block_sum(pr);
+          pi = block_sum(pi);
+          const double2 proj = make_double2(pr, pi);
           for (int r = threadIdx.x; r < rows; r += blockDim.x) v[r] = csub(v[r], cmul(proj, qc[r]));
           __syncthreads();
         }
       }
-      if (threadIdx.x == 0) red[2] = 0.0;
-      __syncthreads();
       double nn = 0.0;
       for (int r = threadIdx.x; r < rows; r += blockDim.x) nn += cnorm2(v[r]);
-      nn = warp_sum(nn);
-      if ((threadIdx.x & 31) == 0) atomicAdd(&red[2], nn);
-      __syncthreads();
-      const double nrm = sqrt(red[2]);
+      const double nrm = sqrt(block_sum(nn));
       if (nrm > 0.1) {
         for (int r = threadIdx.x; r < rows; r += blockDim.x) v[r] = cscale(v[r], 1.0 / nrm);
         done = true;
@@ -429,11 +427,76 @@ __global__ void __launch_bounds__(kThreads) small_svd_kernel(const SvdArgs a) {
 
 // ------------------------------------------------------------------ completion of big Q
 
+// ------------------------------------------------------------------ TSQR R factor
+
+// Householder QR of row block b (rows [b*rpb, b*rpb + rpb)) of a row-major
+// rows x k matrix; writes the k x k upper-triangular R of the block (zero-padded
+// when the block has fewer than k rows).  Column-major working copy in shared
+// memory (or `work` + b * rpb * k when it does not fit).  Backward stable
+// like zgeqrf (linalg.cpp:93), and unaffected by rank deficiency.
+__global__ void __launch_bounds__(kThreads) householder_r_kernel(const double2* A, int64_t rows, int k, int rpb,
+                                                                 double2* Rout, double2* work) {
+  extern __shared__ __align__(16) unsigned char sm[];
+  __shared__ double2 rdiag[256];
+  const int b = blockIdx.x;
+  const int64_t r0 = static_cast<int64_t>(b) * rpb;
+  const int m = static_cast<int>(rows - r0 < rpb ? rows - r0 : rpb);
+  const int mm = max(m, k);
+  double2* X = work ? work + static_cast<int64_t>(b) * max(rpb, k) * k : reinterpret_cast<double2*>(sm);
+  for (int e = threadIdx.x; e < mm * k; e += blockDim.x) {
+    const int r = e / k, c = e % k;
+    X[static_cast<int64_t>(c) * mm + r] = r < m ? A[(r0 + r) * k + c] : make_double2(0.0, 0.0);
+  }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
+  for (int j = 0; j < k; ++j) {
+    double2* xj = X + static_cast<int64_t>(j) * mm;
+    double part = 0.0;
+    for (int r = j + threadIdx.x; r < mm; r += blockDim.x) part += cnorm2(xj[r]);
+    const double alpha = sqrt(block_sum(part));
+    if (!(alpha > 0.0)) {
+      if (threadIdx.x == 0) rdiag[j] = make_double2(0.0, 0.0);
+      __syncthreads();
+      continue;
+    }
+    const double2 x0 = xj[j];
+    const double ax0 = hypot(x0.x, x0.y);
+    const double2 ph = ax0 > 0.0 ? make_double2(x0.x / ax0, x0.y / ax0) : make_double2(1.0, 0.0);
+    const double tau = 1.0 / (alpha * (alpha + ax0));  // 2 / (v^H v)
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      xj[j] = make_double2(x0.x + ph.x * alpha, x0.y + ph.y * alpha);
+      rdiag[j] = make_double2(-ph.x * alpha, -ph.y * alpha);
+    }
+    __syncthreads();
+    for (int c = j + 1 + warp; c < k; c += nwarps) {
+      double2* xc = X + static_cast<int64_t>(c) * mm;
+      double wr = 0.0, wi = 0.0;
+      for (int r = j + lane; r < mm; r += 32) {
+        const double2 v = xj[r], a = xc[r];
+        wr += v.x * a.x + v.y * a.y;  // conj(v) a
+        wi += v.x * a.y - v.y * a.x;
+      }
+      wr = warp_sum(wr) * tau;
+      wi = warp_sum(wi) * tau;
+      for (int r = j + lane; r < mm; r += 32) {
+        const double2 v = xj[r];
+        xc[r] = csub(xc[r], make_double2(v.x * wr - v.y * wi, v.x * wi + v.y * wr));
+      }
+    }
+    __syncthreads();
+  }
+  double2* R = Rout + static_cast<int64_t>(b) * k * k;
+  for (int e = threadIdx.x; e < k * k; e += blockDim.x) {
+    const int i = e / k, c = e % k;
+    R[e] = c > i ? X[static_cast<int64_t>(c) * mm + i] : (c == i ? rdiag[i] : make_double2(0.0, 0.0));
+  }
+}
+
 __global__ void __launch_bounds__(kThreads) complete_columns_kernel(double2* Q, int64_t rows, int cols,
                                                                     const int* deficient,
                                                                     const int* any_def, int* status) {
   if (*any_def == 0) return;
-  __shared__ double red[3];
   int64_t next_basis = 0;
   for (int j = 0; j < cols; ++j) {
     if (!deficient[j]) continue;
@@ -450,32 +513,23 @@ __global__ void __launch_bounds__(kThreads) complete_columns_kernel(double2* Q, 
       for (int pass = 0; pass < 2; ++pass) {
         for (int c = 0; c < cols; ++c) {
           if (c == j || (deficient[c] && c > j)) continue;
-          if (threadIdx.x < 2) red[threadIdx.x] = 0.0;
-          __syncthreads();
           double pr = 0.0, pi = 0.0;
           for (int64_t r = threadIdx.x; r < rows; r += blockDim.x) {
             double2 q = Q[r * cols + c], x = Q[r * cols + j];
             pr += q.x * x.x + q.y * x.y;
             pi += q.x * x.y - q.y * x.x;
           }
-          pr = warp_sum(pr);
-          pi = warp_sum(pi);
-          if ((threadIdx.x & 31) == 0) { atomicAdd(&red[0], pr); atomicAdd(&red[1], pi); }
-          __syncthreads();
-          const double2 proj = make_double2(red[0], red[1]);
+          pr = block_sum(pr);
+          pi = block_sum(pi);
+          const double2 proj = make_double2(pr, pi);
           for (int64_t r = threadIdx.x; r < rows; r += blockDim.x)
             Q[r * cols + j] = csub(Q[r * cols + j], cmul(proj, Q[r * cols + c]));
           __syncthreads();
         }
       }
-      if (threadIdx.x == 0) red[2] = 0.0;
-      __syncthreads();
       double nn = 0.0;
       for (int64_t r = threadIdx.x; r < rows; r += blockDim.x) nn += cnorm2(Q[r * cols + j]);
-      nn = warp_sum(nn);
-      if ((threadIdx.x & 31) == 0) atomicAdd(&red[2], nn);
-      __syncthreads();
-      const double nrm = sqrt(red[2]);
+      const double nrm = sqrt(block_sum(nn));
       if (nrm > 0.1) {
         for (int64_t r = threadIdx.x; r < rows; r += blockDim.x) Q[r * cols + j] = cscale(Q[r * cols + j], 1.0 / nrm);
         done = true;
@@ -544,6 +598,48 @@ void small_svd(const double2* A, int64_t sa, int m, int n, int lda, double2* U, 
   const int threads = nc <= 16 ? 256 : kThreads;
   small_svd_kernel<<<batch, threads, fits ? smem : 0, stream>>>(a);
   PEPSB_LAUNCH();
+}
+
+int64_t tsqr_workspace(int64_t rows, int k) {
+  const size_t cap = 227 * 1024;
+  int64_t rpb0 = std::max<int64_t>(k, static_cast<int64_t>(cap / (16 * k)));
+  int64_t nb = (rows + rpb0 - 1) / rpb0;
+  int64_t ws = 2 * nb * k * k + 16;  // two R stacks
+  if (static_cast<size_t>(2 * k) * k * 16 > cap) ws += nb * 2 * k * k + (rows + 1) * k;  // global work
+  return ws;
+}
+
+void tsqr_r(const double2* A, int64_t rows, int k, double2* R, double2* ws, cudaStream_t stream) {
+  const size_t cap = 227 * 1024;
+  static bool attr = false;
+  if (!attr) {
+    PEPSB_CUDA(cudaFuncSetAttribute(householder_r_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(cap - 8 * 1024)));
+    attr = true;
+  }
+  const size_t usable = cap - 8 * 1024;
+  const bool big = static_cast<size_t>(2 * k) * k * 16 > usable;
+  int64_t rpb = std::max<int64_t>(k, static_cast<int64_t>(usable / (16 * k)));
+  int64_t nb = (rows + rpb - 1) / rpb;
+  double2* stack[2] = {ws, ws + nb * k * k};
+  double2* gwork = big ? ws + 2 * nb * k * k : nullptr;
+  const double2* src = A;
+  int64_t src_rows = rows;
+  int cur = 0;
+  while (true) {
+    const size_t smem = big ? 0 : static_cast<size_t>(std::max<int64_t>(rpb, k)) * k * 16;
+    householder_r_kernel<<<static_cast<unsigned>(nb), kThreads, smem, stream>>>(src, src_rows, k,
+                                                                                 static_cast<int>(rpb),
+                                                                                 stack[cur], gwork);
+    PEPSB_LAUNCH();
+    if (nb == 1) break;
+    src = stack[cur];
+    src_rows = nb * k;
+    cur ^= 1;
+    rpb = 2 * k;
+    nb = (src_rows + rpb - 1) / rpb;
+  }
+  PEPSB_CUDA(cudaMemcpyAsync(R, stack[cur], static_cast<size_t>(k) * k * 16, cudaMemcpyDeviceToDevice, stream));
 }
 
 void complete_columns(double2* Q, int64_t rows, int cols, const int* deficient, const int* any_def,

@@ -43,6 +43,13 @@ void small_svd(const double2* A, int64_t sa, int m, int n, int lda, double2* U, 
                double2* work, cudaStream_t stream);
 int64_t small_svd_workspace(int m, int n, int batch);
 
+// R factor of a tall row-major rows x k matrix by TSQR (Householder per row
+// block, binary tree over the stacked R's).  Robust to rank deficiency; used
+// for the projected SVD when CholeskyQR cannot guarantee accuracy.
+// `ws` must hold tsqr_workspace(rows, k) complex elements.
+void tsqr_r(const double2* A, int64_t rows, int k, double2* R, double2* ws, cudaStream_t stream);
+int64_t tsqr_workspace(int64_t rows, int k);
+
 // Reference complete_deficient_columns (decomposition.cpp:88-115) on a device
 // rows x cols row-major Q, for the columns flagged in `deficient`; no-op when
 // *any_def == 0 (checked on the device, so no host sync is needed).
