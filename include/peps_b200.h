@@ -81,9 +81,10 @@ int pepsb_ctx_destroy(pepsb_ctx* ctx);
 int pepsb_ctx_sync(pepsb_ctx* ctx);
 /* keys: "orth_mode" (0 reference Gram-eigh, 1 CholeskyQR2) */
 int pepsb_ctx_set_option(pepsb_ctx* ctx, const char* key, int64_t value);
-/* out[0..3] = flops (instr::flops convention, instrument.hpp:19-65),
- * einsumsvd_flops, peak_elements, kernel launches issued by the library */
-int pepsb_ctx_counters(pepsb_ctx* ctx, uint64_t* out4);
+/* out[0..5] = flops (instr::flops convention, instrument.hpp:19-65),
+ * einsumsvd_flops, peak_elements, kernel launches issued by the library,
+ * CholeskyQR breakdowns redone on the Gram-eigh route, TSQR fallbacks */
+int pepsb_ctx_counters(pepsb_ctx* ctx, uint64_t* out6);
 int pepsb_ctx_reset_counters(pepsb_ctx* ctx);
 /* Per-launch CUDA-event timing of the library's kernels (off by default).
  * Report: 4 kinds (0 GEMM, 1 small factorizations, 2 gathers, 3 other) x
@@ -159,6 +160,8 @@ int pepsb_chain_scalar(pepsb_ctx* ctx, const pepsb_boundary* b, double* re, doub
 
 /* build_row_cache (observables.hpp:61) */
 int pepsb_build_row_cache(pepsb_ctx* ctx, const pepsb_state* s, const pepsb_contract_opt* opt, pepsb_row_cache** out);
+/* flip_vertical (observables.cpp:261-270): rows reversed, up/down swapped */
+int pepsb_flip_vertical(pepsb_ctx* ctx, const pepsb_state* s, pepsb_state** out);
 /* which 0: tops[k], 1: bots[k] */
 int pepsb_row_cache_get(const pepsb_row_cache* c, int which, int k, pepsb_boundary** out);
 void pepsb_row_cache_free(pepsb_row_cache* c);

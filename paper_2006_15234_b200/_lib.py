@@ -88,6 +88,7 @@ _SIGS = {
                                            C.POINTER(C.c_double)]),
     "pepsb_chain_scalar": (C.c_int, [_VP, _VP, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
     "pepsb_build_row_cache": (C.c_int, [_VP, _VP, C.POINTER(ContractOpt), C.POINTER(_VP)]),
+    "pepsb_flip_vertical": (C.c_int, [_VP, _VP, C.POINTER(_VP)]),
     "pepsb_row_cache_get": (C.c_int, [_VP, C.c_int, C.c_int, C.POINTER(_VP)]),
     "pepsb_row_cache_free": (None, [_VP]),
     "pepsb_band_environment": (C.c_int, [_VP, _VP, _VP, _VP, C.c_int, C.c_int, _VP, C.POINTER(_VP)]),

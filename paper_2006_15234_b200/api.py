@@ -102,9 +102,10 @@ class Context:
         check(lib().pepsb_ctx_set_option(self.h, key.encode(), int(value)))
 
     def counters(self) -> dict:
-        a = (C.c_uint64 * 4)()
+        a = (C.c_uint64 * 6)()
         check(lib().pepsb_ctx_counters(self.h, a))
-        return dict(flops=int(a[0]), einsumsvd_flops=int(a[1]), peak_elements=int(a[2]), launches=int(a[3]))
+        return dict(flops=int(a[0]), einsumsvd_flops=int(a[1]), peak_elements=int(a[2]), launches=int(a[3]),
+                    faithful_redos=int(a[4]), tsqr_fallbacks=int(a[5]))
 
     def reset_counters(self):
         check(lib().pepsb_ctx_reset_counters(self.h))
@@ -403,6 +404,21 @@ def chain_scalar(b: TwoLayerBoundary) -> complex:
     re, im = C.c_double(), C.c_double()
     check(lib().pepsb_chain_scalar(b.ctx.h, b.h, C.byref(re), C.byref(im)))
     return complex(re.value, im.value)
+
+
+def flip_vertical(s: PepsState) -> PepsState:
+    """observables.cpp:261-270 — rows reversed, up/down bonds swapped."""
+    h = _VP()
+    check(lib().pepsb_flip_vertical(s.ctx.h, s.h, C.byref(h)))
+    out = PepsState.__new__(PepsState)
+    out.ctx, out.rows, out.cols, out.d, out.h = s.ctx, s.rows, s.cols, s.d, h
+    out.sites = []
+    for r in range(s.rows):
+        for c in range(s.cols):
+            t = _VP()
+            check(lib().pepsb_state_site(h, r, c, C.byref(t)))
+            out.sites.append(DeviceTensor(t, s.ctx))
+    return out
 
 
 @dataclass

@@ -193,6 +193,8 @@ int pepsb_ctx_counters(pepsb_ctx* c, uint64_t* out) {
     out[1] = c->ctx->einsumsvd_flops;
     out[2] = c->ctx->peak_elements;
     out[3] = static_cast<uint64_t>(c->ctx->launches);
+    out[4] = static_cast<uint64_t>(c->ctx->faithful_redos);
+    out[5] = static_cast<uint64_t>(c->ctx->tsqr_fallbacks);
   });
 }
 
@@ -201,6 +203,7 @@ int pepsb_ctx_reset_counters(pepsb_ctx* c) {
     need(c, "ctx");
     c->ctx->flops = c->ctx->einsumsvd_flops = c->ctx->peak_elements = 0;
     c->ctx->launches = 0;
+    c->ctx->faithful_redos = c->ctx->tsqr_fallbacks = 0;
   });
 }
 
@@ -492,6 +495,16 @@ int pepsb_build_row_cache(pepsb_ctx* c, const pepsb_state* s, const pepsb_contra
     need(c, "ctx");
     need(s, "state");
     *out = new pepsb_row_cache{build_row_cache(*c->ctx, s->s, opt_of(opt))};
+  });
+}
+
+int pepsb_flip_vertical(pepsb_ctx* c, const pepsb_state* s, pepsb_state** out) {
+  return guard([&] {
+    need(c, "ctx");
+    need(s, "state");
+    PepsStateD f = flip_vertical(*c->ctx, s->s);
+    f.validate();
+    *out = new pepsb_state{f};
   });
 }
 

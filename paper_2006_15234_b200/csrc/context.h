@@ -78,6 +78,8 @@ class Ctx {
   int* h_status = nullptr;  // pinned
   // Launch accounting (for the bench's gpu_launches claim).
   int64_t launches = 0;
+  int64_t faithful_redos = 0;  // CholeskyQR breakdowns redone on the Gram-eigh route
+  int64_t tsqr_fallbacks = 0;  // projected SVDs that needed the TSQR R factor
   // Cost counters (reference instr::flops definition: 2 per complex MAC,
   // proj/include/peps/instrument.hpp:19-65).
   uint64_t flops = 0;
@@ -87,10 +89,14 @@ class Ctx {
     if (n > peak_elements) peak_elements = n;
   }
   // Options
-  // Power-iteration orthogonalisation: 1 = CholeskyQR2 (default; same span as
-  // the reference, different basis -> gauge-invariant parity), 0 = the
-  // reference's Gram-eigh basis (elementwise parity of t1/t2).
-  int orth_mode = 1;
+  // Power-iteration orthogonalisation: 0 = the reference's Gram-eigh basis
+  // (default).  The basis fixes the column phases of U, i.e. the bond gauge of
+  // emitted boundary sites, and the NEXT row's sketch Omega is drawn in the
+  // reference layout of those bonds -- so multi-row contractions only agree
+  // with the reference if the basis does.  1 = CholeskyQR2 (same spans, other
+  // basis): identical within one row / one einsumsvd, but across rows it
+  // differs from the reference by the sketch-dependent rSVD error.
+  int orth_mode = 0;
 
   // Optional per-launch device timing (CUDA events on `stream`), used by the
   // bench's roofline pass; off in timed runs.

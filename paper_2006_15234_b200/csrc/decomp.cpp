@@ -133,7 +133,9 @@ LTensor orth(Ctx& ctx, const LTensor& Y) {
       ProfScope ps_(ctx, Ctx::kProfSmall);
       // breakdowns are flagged in status word 1; rsvd_core then redoes the
       // decomposition on the reference-faithful route (clamp + completion)
-      chol_factors(G->p, static_cast<int>(k), 0.0, R->p, Ri->p, ctx.d_status + 1, ctx.stream);
+      // pivot floor 1e-9 max_diag: flags every Gram the reference would clamp
+      // (lambda < 1e-12 lambda_max implies a pivot < 1e-12 max_diag) with margin
+      chol_factors(G->p, static_cast<int>(k), 1e-9, R->p, Ri->p, ctx.d_status + 1, ctx.stream);
     }
     mm(ctx, Q1->p, Y.ptr, false, false, Ri->p, false, false, rows, k, k);
     mm(ctx, G2->p, Q1->p, true, true, Q1->p, false, false, k, k, rows);
@@ -246,6 +248,7 @@ Projected projected_svd(Ctx& ctx, const LTensor& Z, int64_t target) {
     const int st = svd_of_rh(R);
     raise_status(st, false);
     out.tsqr = true;
+    ++ctx.tsqr_fallbacks;
   }
   return out;
 }
@@ -341,7 +344,10 @@ EinsumsvdResultD rsvd_core(Ctx& ctx, const ImplicitOp& op, const Trunc& policy, 
   LTensor z = adjoint(p);
   q = LTensor();
   Projected pr = projected_svd(ctx, z, target);
-  if (ctx.orth_mode == 1 && (ctx.h_status[1] & kSmallCholBreakdown)) throw RedoFaithful{};
+  if (ctx.orth_mode == 1 && (ctx.h_status[1] & kSmallCholBreakdown)) {
+    ++ctx.faithful_redos;
+    throw RedoFaithful{};
+  }
 
   Trunc pol = policy;
   int64_t rank = static_cast<int64_t>(retained_rank(pr.s, pol));

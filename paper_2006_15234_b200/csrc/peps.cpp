@@ -160,7 +160,8 @@ PepsStateD flip_vertical(Ctx& ctx, const PepsStateD& s) {
   f.d = s.d;
   for (int r = s.rows - 1; r >= 0; --r)
     for (int c = 0; c < s.cols; ++c) {
-      LTensor t = reduce_to(ctx, as_labelled(s.site(r, c), "pudlr"), "pdlur");
+      // site axes (phys, up, left, down, right) -> (phys, down, left, up, right)
+      LTensor t = reduce_to(ctx, as_labelled(s.site(r, c), "puldr"), "pdlur");
       f.sites.push_back(materialize(ctx, t, t.labels));
     }
   return f;

@@ -144,14 +144,10 @@ __device__ double2 column_phase(const double2* colp, int rows) {
 
 // ------------------------------------------------------------------ gram_factors
 
-__global__ void __launch_bounds__(kThreads) gram_factors_kernel(const double2* G, int n, double2* P,
-                                                                double2* R, int* deficient,
-                                                                int* any_def, int* status,
-                                                                double2* work) {
-  extern __shared__ __align__(16) unsigned char sm[];
-  const bool in_smem = work == nullptr;
-  double2* X = in_smem ? reinterpret_cast<double2*>(sm) : work;  // column-major n x n
-  double2* V = X + n * n;
+// Block-level gram_factors; X, V: n*n complex scratch each (column-major).
+// Outputs (P, R, deficient, any_def) are complete after the trailing barrier.
+__device__ void gram_factors_dev(const double2* G, int n, double2* X, double2* V, double2* P, double2* R,
+                                 int* deficient, int* any_def, int* status) {
   __shared__ double lam[256];
   __shared__ int order[256];
   __shared__ double hmax[2];
@@ -177,7 +173,11 @@ __global__ void __launch_bounds__(kThreads) gram_factors_kernel(const double2* G
   for (int e = threadIdx.x; e < n * n; e += blockDim.x) fro += cnorm2(X[e]);
   // abs skip: rotations below the rounding level of ||G||^2 do not move eigenvalues.
   const double abs_skip = 1e-34 * block_sum(fro);
-  onesided_jacobi(X, n, n, n, V, n, 1e-15, abs_skip, 40, status);
+  // Convergence at the rounding level of the column inner products
+  // (8 eps sqrt(n), cf. LAPACK zgesvj's sqrt(m) eps): a tighter threshold only
+  // chases noise and never terminates early.
+  onesided_jacobi(X, n, n, n, V, n, 8.0 * 2.220446049250313e-16 * sqrt(static_cast<double>(n)), abs_skip, 40,
+                  status);
 
   // eigenvalue j = Re(v_j^H G v_j) = Re(v_j^H x_j)   (X = G V)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
@@ -220,6 +220,16 @@ __global__ void __launch_bounds__(kThreads) gram_factors_kernel(const double2* G
     // R row j = sqrt(l_j) conj(column j of X): R[j][i] = sqrt(l_j) conj(x_ij)
     R[j * n + i] = cscale(cconj(xij), sqrt(lj));
   }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(kThreads) gram_factors_kernel(const double2* G, int n, double2* P,
+                                                                double2* R, int* deficient,
+                                                                int* any_def, int* status,
+                                                                double2* work) {
+  extern __shared__ __align__(16) unsigned char sm[];
+  double2* X = work ? work : reinterpret_cast<double2*>(sm);  // column-major n x n
+  gram_factors_dev(G, n, X, X + n * n, P, R, deficient, any_def, status);
 }
 
 // ------------------------------------------------------------------ Cholesky
@@ -241,16 +251,16 @@ __global__ void __launch_bounds__(kThreads) chol_kernel(const double2* G, int n,
   __syncthreads();
   if (threadIdx.x == 0) {
     double t = 0.0;
-    for (int i = 0; i < n; ++i) t += A[i * n + i].x;
-    tr = t;
+    for (int i = 0; i < n; ++i) t = fmax(t, A[i * n + i].x);
+    tr = t;  // largest diagonal entry
   }
   __syncthreads();
-  const double shift = shift_rel * tr;
-  for (int i = threadIdx.x; i < n; i += blockDim.x) A[i * n + i] = make_double2(A[i * n + i].x + shift, 0.0);
-  __syncthreads();
+  // A pivot below pivot_rel * max_diag counts as a breakdown: the Gram matrix is
+  // then (close to) rank deficient where the reference's eigh route would clamp.
+  const double floor = shift_rel * tr;
   for (int k = 0; k < n; ++k) {
     const double piv = A[k * n + k].x;
-    if (!(piv > 0.0)) {
+    if (!(piv > floor) || !(piv > 0.0)) {
       if (threadIdx.x == 0) bad = 1;
       __syncthreads();
       break;
@@ -353,14 +363,18 @@ struct SvdArgs {
   int64_t work_stride;
 };
 
-__global__ void __launch_bounds__(kThreads) small_svd_kernel(const SvdArgs a) {
-  extern __shared__ __align__(16) unsigned char sm[];
-  const int b = blockIdx.x;
-  const double2* A = a.A + b * a.sa;
+// Block-level thin SVD of a row-major m x n matrix A (leading dim lda):
+// A = U diag(s) Vh, U m x k, Vh k x n (both row-major, k = min(m, n)).
+// X: scratch of max(m,n)*min(m,n) + min(m,n)^2 complex.
+__device__ void small_svd_dev(const double2* A, int m_, int n_, int lda, double2* X, double2* U, double* s,
+                              double2* Vh, int* status) {
+  struct {
+    int m, n, lda;
+    int* status;
+  } a{m_, n_, lda, status};
   const bool tall = a.m >= a.n;
   const int mr = tall ? a.m : a.n;  // rows of the working matrix
   const int nc = tall ? a.n : a.m;  // its columns (= k)
-  double2* X = a.work ? a.work + b * a.work_stride : reinterpret_cast<double2*>(sm);
   double2* V = X + static_cast<int64_t>(mr) * nc;
   __shared__ double sig[256];
   __shared__ int order[256];
@@ -374,7 +388,8 @@ __global__ void __launch_bounds__(kThreads) small_svd_kernel(const SvdArgs a) {
     else X[static_cast<int64_t>(i) * mr + j] = cconj(v);     // A^H: col i, row j
   }
   __syncthreads();
-  onesided_jacobi(X, mr, nc, mr, V, nc, 1e-15, 0.0, 60, a.status);
+  onesided_jacobi(X, mr, nc, mr, V, nc, 8.0 * 2.220446049250313e-16 * sqrt(static_cast<double>(mr)), 0.0, 60,
+                  a.status);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
   for (int j = warp; j < nc; j += nwarps) {
     double s = 0.0;
@@ -410,9 +425,6 @@ __global__ void __launch_bounds__(kThreads) small_svd_kernel(const SvdArgs a) {
   }
   __syncthreads();
   const int k = nc;
-  double2* U = a.U + b * a.su;
-  double2* Vh = a.Vh + b * a.sv;
-  double* s = a.s + b * a.ss;
   for (int e = threadIdx.x; e < urows * k; e += blockDim.x) {
     const int i = e / k, j = e % k;
     U[static_cast<int64_t>(i) * k + j] = cmulc(ph[j], Ucols[static_cast<int64_t>(order[j]) * urows + i]);
@@ -423,6 +435,14 @@ __global__ void __launch_bounds__(kThreads) small_svd_kernel(const SvdArgs a) {
     Vh[static_cast<int64_t>(j) * vrows + c] = cmul(cconj(Vcols[static_cast<int64_t>(order[j]) * vrows + c]), ph[j]);
   }
   for (int j = threadIdx.x; j < k; j += blockDim.x) s[j] = sig[order[j]];
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(kThreads) small_svd_kernel(const SvdArgs a) {
+  extern __shared__ __align__(16) unsigned char sm[];
+  const int b = blockIdx.x;
+  double2* X = a.work ? a.work + b * a.work_stride : reinterpret_cast<double2*>(sm);
+  small_svd_dev(a.A + b * a.sa, a.m, a.n, a.lda, X, a.U + b * a.su, a.s + b * a.ss, a.Vh + b * a.sv, a.status);
 }
 
 // ------------------------------------------------------------------ completion of big Q
@@ -539,7 +559,228 @@ __global__ void __launch_bounds__(kThreads) complete_columns_kernel(double2* Q, 
   }
 }
 
+// ------------------------------------------------------------------ simple update (state.cpp:89-204)
+//
+// One thread block per site (reduce / restore) or per bond (split); a whole
+// colour of disjoint bonds is one launch of each, ragged shapes included.
+
+__global__ void __launch_bounds__(512) su_reduce_kernel(const SuSiteDesc* descs, int* status) {
+  extern __shared__ __align__(16) unsigned char sm[];
+  __shared__ int anyd;
+  const SuSiteDesc D = descs[blockIdx.x];
+  const int E = D.e[0] * D.e[1] * D.e[2], S = D.d * D.s;
+  double2* Y = reinterpret_cast<double2*>(sm);  // column-major E x S (site in env form)
+  for (int idx = threadIdx.x; idx < E * S; idx += blockDim.x) {
+    const int c = idx / E, e = idx % E;
+    const int i2 = e % D.e[2], t = e / D.e[2], i1 = t % D.e[1], i0 = t / D.e[1];
+    const int p = c / D.s, q = c % D.s;
+    Y[idx] = D.src[i0 * D.str[0] + i1 * D.str[1] + i2 * D.str[2] + p * D.str[3] + q * D.str[4]];
+  }
+  __syncthreads();
+  if (!D.reduced) {  // env < d * shared: no QR (state.cpp:132-136), R = site (E, d, s)
+    for (int idx = threadIdx.x; idx < E * S; idx += blockDim.x) D.R[idx] = Y[(idx % S) * E + idx / S];
+    return;
+  }
+  double2* G = Y + E * S;
+  double2* X = G + S * S;
+  double2* V = X + S * S;
+  double2* P = V + S * S;
+  double2* Rm = P + S * S;
+  int* def = reinterpret_cast<int*>(Rm + S * S);
+  for (int idx = threadIdx.x; idx < S * S; idx += blockDim.x) {
+    const int i = idx / S, j = idx % S;
+    double re = 0.0, im = 0.0;
+    for (int e = 0; e < E; ++e) {
+      const double2 a = Y[i * E + e], b = Y[j * E + e];
+      re += a.x * b.x + a.y * b.y;
+      im += a.x * b.y - a.y * b.x;
+    }
+    G[idx] = make_double2(re, im);
+  }
+  __syncthreads();
+  // gram_orthogonalize(site as (env, d*s)) — decomposition.cpp:160-193
+  gram_factors_dev(G, S, X, V, P, Rm, def, &anyd, status);
+  for (int idx = threadIdx.x; idx < E * S; idx += blockDim.x) {
+    const int j = idx / E, e = idx % E;
+    double2 acc = make_double2(0.0, 0.0);
+    for (int i = 0; i < S; ++i) acc = cadd(acc, cmul(Y[i * E + e], P[i * S + j]));
+    D.Q[idx] = acc;  // column-major
+  }
+  __syncthreads();
+  if (anyd) complete_unit_columns(D.Q, E, S, E, def, status);
+  for (int idx = threadIdx.x; idx < S * S; idx += blockDim.x) D.R[idx] = Rm[idx];
+}
+
+__global__ void __launch_bounds__(256) su_split_kernel(const SuBondDesc* descs, int* ranks, int* status) {
+  extern __shared__ __align__(16) unsigned char sm[];
+  __shared__ int rank_sh;
+  const SuBondDesc B = descs[blockIdx.x];
+  const int d = B.d, m = B.ta * d, n = d * B.tb, k = min(m, n);
+  double2* M = reinterpret_cast<double2*>(sm);
+  double2* U = M + m * n;
+  double2* Vh = U + m * k;
+  double2* X = Vh + k * n;
+  double* sv = reinterpret_cast<double*>(X + max(m, n) * k + k * k);
+  // M[(a,o),(p,b)] = sum_{i,j,q} g[o,p,i,j] Ra[a,i,q] Rb[b,j,q]   (network {g, Ra, Rb}, state.cpp:192-194)
+  for (int idx = threadIdx.x; idx < m * n; idx += blockDim.x) {
+    const int row = idx / n, col = idx % n;
+    const int a = row / d, o = row % d, p = col / B.tb, b = col % B.tb;
+    double2 acc = make_double2(0.0, 0.0);
+    for (int i = 0; i < d; ++i)
+      for (int j = 0; j < d; ++j) {
+        const double2 g = B.gate[((o * d + p) * d + i) * d + j];
+        double2 sum = make_double2(0.0, 0.0);
+        for (int q = 0; q < B.s; ++q)
+          sum = cadd(sum, cmul(B.Ra[(a * d + i) * B.s + q], B.Rb[(b * d + j) * B.s + q]));
+        acc = cadd(acc, cmul(g, sum));
+      }
+    M[idx] = acc;
+  }
+  __syncthreads();
+  small_svd_dev(M, m, n, n, X, U, sv, Vh, status);
+  if (threadIdx.x == 0) {  // retained_rank (decomposition.cpp:20-29)
+    int above = 0;
+    for (int j = 0; j < k; ++j) above += sv[j] >= B.cutoff * sv[0];
+    int64_t r = above;
+    if (B.cap > 0 && B.cap < r) r = B.cap;
+    rank_sh = static_cast<int>(r < 1 ? 1 : r);
+    ranks[blockIdx.x] = rank_sh;
+  }
+  __syncthreads();
+  const int rank = rank_sh;
+  // Absorb::split: t1 = U sqrt(S) as (a, o, rho); t2 = sqrt(S) Vh as (b, p, rho)
+  for (int idx = threadIdx.x; idx < m * rank; idx += blockDim.x) {
+    const int row = idx / rank, r = idx % rank;
+    B.t1[row * B.rmax + r] = cscale(U[row * k + r], sqrt(sv[r]));
+  }
+  for (int idx = threadIdx.x; idx < n * rank; idx += blockDim.x) {
+    const int col = idx / rank, r = idx % rank;  // col = (p, b)
+    const int p = col / B.tb, b = col % B.tb;
+    B.t2[(b * d + p) * B.rmax + r] = cscale(Vh[r * n + col], sqrt(sv[r]));
+  }
+}
+
+__global__ void __launch_bounds__(256) su_restore_kernel(const SuRestoreDesc* descs, const int* ranks) {
+  const SuRestoreDesc D = descs[blockIdx.x];
+  const int rank = ranks[D.bond];
+  const int E = D.e[0] * D.e[1] * D.e[2];
+  for (int idx = threadIdx.x; idx < E * D.d * rank; idx += blockDim.x) {
+    const int e = idx / (D.d * rank), rem = idx % (D.d * rank), o = rem / rank, r = rem % rank;
+    double2 v;
+    if (D.reduced) {  // contract("et,tov->eov", q, t) (state.cpp:150-157)
+      v = make_double2(0.0, 0.0);
+      for (int c = 0; c < D.S; ++c) v = cadd(v, cmul(D.Q[c * E + e], D.t[(c * D.d + o) * D.rmax + r]));
+    } else {
+      v = D.t[(e * D.d + o) * D.rmax + r];
+    }
+    const int i2 = e % D.e[2], t = e / D.e[2], i1 = t % D.e[1], i0 = t / D.e[1];
+    D.dst[i0 * D.dstr[0] + i1 * D.dstr[1] + i2 * D.dstr[2] + o * D.dstr[3] + r * D.dstr[4]] = v;
+  }
+}
+
+__global__ void su_one_site_kernel(const SuOneSiteDesc* descs) {
+  const SuOneSiteDesc D = descs[blockIdx.x];
+  for (int64_t idx = threadIdx.x; idx < D.d * D.rest; idx += blockDim.x) {
+    const int64_t i = idx / D.rest, r = idx % D.rest;
+    double2 acc = make_double2(0.0, 0.0);
+    for (int j = 0; j < D.d; ++j) acc = cadd(acc, cmul(D.gate[i * D.d + j], D.src[j * D.rest + r]));
+    D.dst[idx] = acc;  // contract("ij,juldr->iuldr") (state.cpp:75-85)
+  }
+}
+
+// hermitian_function(coeff*H, exp(-tau x)) (linalg.cpp:297-314) for n <= 16:
+// serial two-sided Jacobi in one thread (gate construction, negligible work).
+__global__ void herm_exp_kernel(const double2* H, int n, double coeff, double tau, double2* out) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  double2 A[16 * 16], V[16 * 16];
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < n; ++j) {
+      const double2 a = H[i * n + j], b = H[j * n + i];
+      A[i * n + j] = make_double2(0.5 * coeff * (a.x + b.x), 0.5 * coeff * (a.y - b.y));
+      V[i * n + j] = make_double2(i == j ? 1.0 : 0.0, 0.0);
+    }
+  for (int sweep = 0; sweep < 100; ++sweep) {
+    double off = 0.0, tot = 0.0;
+    for (int i = 0; i < n; ++i)
+      for (int j = 0; j < n; ++j) {
+        tot += cnorm2(A[i * n + j]);
+        if (i != j) off += cnorm2(A[i * n + j]);
+      }
+    if (!(off > 1e-32 * tot)) break;
+    for (int p = 0; p < n; ++p)
+      for (int q = p + 1; q < n; ++q) {
+        const double2 apq = A[p * n + q];
+        const double ag = hypot(apq.x, apq.y);
+        if (!(ag > 1e-300)) continue;
+        const double tau_ = (A[q * n + q].x - A[p * n + p].x) / (2.0 * ag);
+        const double t = (tau_ >= 0.0 ? 1.0 : -1.0) / (fabs(tau_) + sqrt(1.0 + tau_ * tau_));
+        const double c = 1.0 / sqrt(1.0 + t * t), s = t * c;
+        const double2 e = make_double2(apq.x / ag, apq.y / ag), ec = cconj(e);
+        for (int k = 0; k < n; ++k) {  // columns p, q
+          const double2 akp = A[k * n + p], akq = cmul(A[k * n + q], ec);
+          A[k * n + p] = csub(cscale(akp, c), cscale(akq, s));
+          A[k * n + q] = cadd(cscale(akp, s), cscale(akq, c));
+          const double2 vkp = V[k * n + p], vkq = cmul(V[k * n + q], ec);
+          V[k * n + p] = csub(cscale(vkp, c), cscale(vkq, s));
+          V[k * n + q] = cadd(cscale(vkp, s), cscale(vkq, c));
+        }
+        for (int k = 0; k < n; ++k) {  // rows p, q
+          const double2 apk = A[p * n + k], aqk = cmul(A[q * n + k], e);
+          A[p * n + k] = csub(cscale(apk, c), cscale(aqk, s));
+          A[q * n + k] = cadd(cscale(apk, s), cscale(aqk, c));
+        }
+        A[p * n + q] = A[q * n + p] = make_double2(0.0, 0.0);
+      }
+  }
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < n; ++j) {
+      double2 acc = make_double2(0.0, 0.0);
+      for (int l = 0; l < n; ++l) acc = cadd(acc, cscale(cmulc(V[j * n + l], V[i * n + l]), exp(-tau * A[l * n + l].x)));
+      out[i * n + j] = acc;  // X f(L) X^H
+    }
+}
+
 }  // namespace
+
+void su_reduce(const SuSiteDesc* d, int n, size_t smem, int* status, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    PEPSB_CUDA(cudaFuncSetAttribute(su_reduce_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    attr = true;
+  }
+  if (n == 0) return;
+  su_reduce_kernel<<<n, 512, smem, st>>>(d, status);
+  PEPSB_LAUNCH();
+}
+
+void su_split(const SuBondDesc* d, int n, size_t smem, int* ranks, int* status, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    PEPSB_CUDA(cudaFuncSetAttribute(su_split_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    attr = true;
+  }
+  if (n == 0) return;
+  su_split_kernel<<<n, 256, smem, st>>>(d, ranks, status);
+  PEPSB_LAUNCH();
+}
+
+void su_restore(const SuRestoreDesc* d, int n, const int* ranks, cudaStream_t st) {
+  if (n == 0) return;
+  su_restore_kernel<<<n, 256, 0, st>>>(d, ranks);
+  PEPSB_LAUNCH();
+}
+
+void su_one_site(const SuOneSiteDesc* d, int n, cudaStream_t st) {
+  if (n == 0) return;
+  su_one_site_kernel<<<n, 256, 0, st>>>(d);
+  PEPSB_LAUNCH();
+}
+
+void herm_exp(const double2* H, int n, double coeff, double tau, double2* out, cudaStream_t st) {
+  if (n > 16) throw Error(kShapeError, "gate construction supports local dimension <= 16");
+  herm_exp_kernel<<<1, 32, 0, st>>>(H, n, coeff, tau, out);
+  PEPSB_LAUNCH();
+}
 
 void gram_factors(const double2* G, int n, double2* P, double2* R, int* deficient, int* any_def,
                   int* status, double2* work, cudaStream_t stream) {

@@ -28,8 +28,9 @@ void gram_factors(const double2* G, int n, double2* P, double2* R, int* deficien
                   int* status, double2* work, cudaStream_t stream);
 
 // CholeskyQR factor: G + shift*I = R^H R (R upper triangular), Rinv = R^{-1}.
-// shift = shift_rel * trace(G).  status |= kSmallCholBreakdown on failure.
-void chol_factors(const double2* G, int n, double shift_rel, double2* R, double2* Rinv,
+// CholeskyQR factor G = R^H R; status |= kSmallCholBreakdown when a pivot
+// falls below pivot_rel * max_i G_ii (or is not positive).
+void chol_factors(const double2* G, int n, double pivot_rel, double2* R, double2* Rinv,
                   int* status, cudaStream_t stream);
 
 // Batched thin SVD of small row-major matrices A_b (m x n, leading dim lda,
@@ -49,6 +50,52 @@ int64_t small_svd_workspace(int m, int n, int batch);
 // `ws` must hold tsqr_workspace(rows, k) complex elements.
 void tsqr_r(const double2* A, int64_t rows, int k, double2* R, double2* ws, cudaStream_t stream);
 int64_t tsqr_workspace(int64_t rows, int k);
+
+// ---- batched QR-reduced simple update (state.cpp:89-204), one colour per launch
+struct SuSiteDesc {
+  const double2* src;  // site tensor (phys, up, left, down, right)
+  int64_t str[5];      // source strides of (env0, env1, env2, phys, shared)
+  int e[3];            // env extents
+  int d, s;            // phys and shared-bond extents
+  int reduced;         // env >= d*s: Gram QR (state.cpp:132-140), else R = site
+  double2* Q;          // E x (d*s) column-major (reduced)
+  double2* R;          // reduced: (d*s) x (d*s); else E x (d*s), row-major (t, d, s)
+};
+struct SuBondDesc {
+  const double2* gate;  // (o, p, i, j)
+  const double2* Ra;
+  const double2* Rb;
+  int ta, tb, d, s;
+  int64_t cap;  // rank cap (policy.max_rank, or d * pre_bond when 0)
+  double cutoff;
+  double2* t1;  // (ta, d, rank) with row stride rmax
+  double2* t2;  // (tb, d, rank) with row stride rmax  [= split.t2.permute({2,1,0})]
+  int rmax;
+};
+struct SuRestoreDesc {
+  const double2* Q;
+  int reduced, S;
+  const double2* t;
+  int rmax;
+  int bond;
+  int e[3];
+  int d;
+  double2* dst;
+  int64_t dstr[5];  // destination strides of (env0, env1, env2, out-phys, new bond)
+};
+struct SuOneSiteDesc {
+  const double2* src;
+  double2* dst;
+  int64_t rest;
+  int d;
+  const double2* gate;
+};
+void su_reduce(const SuSiteDesc* d_descs, int n, size_t smem, int* status, cudaStream_t stream);
+void su_split(const SuBondDesc* d_descs, int n, size_t smem, int* ranks, int* status, cudaStream_t stream);
+void su_restore(const SuRestoreDesc* d_descs, int n, const int* ranks, cudaStream_t stream);
+void su_one_site(const SuOneSiteDesc* d_descs, int n, cudaStream_t stream);
+// out = exp(-tau * coeff * H) for Hermitian n x n H (hermitian_function, linalg.cpp:297-314)
+void herm_exp(const double2* H, int n, double coeff, double tau, double2* out, cudaStream_t stream);
 
 // Reference complete_deficient_columns (decomposition.cpp:88-115) on a device
 // rows x cols row-major Q, for the columns flagged in `deficient`; no-op when

@@ -47,7 +47,16 @@ def faithful(A):
     ctx = A.default_context()
     ctx.set_option("orth_mode", 0)
     yield A
+    ctx.set_option("orth_mode", 0)
+
+
+@pytest.fixture
+def cholqr(A):
+    """CholeskyQR2 orthogonalisation (same spans, other basis)."""
+    ctx = A.default_context()
     ctx.set_option("orth_mode", 1)
+    yield A
+    ctx.set_option("orth_mode", 0)
 
 
 def mps_fidelity(a, b):

@@ -140,9 +140,10 @@ def test_rsvd_error_within_optimal_bound(A):
 
 
 @pytest.mark.parametrize("absorb", ["split", "left", "right"])
-def test_einsumsvd_two_layer_gauge_invariant_default(A, golden, absorb):
-    """Default CholeskyQR2 orthogonalisation: same spans as the reference, so
-    singular values, ranks and the product t1 t2 agree (north_star bar)."""
+def test_einsumsvd_two_layer_gauge_invariant_cholqr(cholqr, golden, absorb):
+    """CholeskyQR2 orthogonalisation: same spans as the reference, so singular
+    values, ranks and the product t1 t2 agree (north_star bar)."""
+    A = cholqr
     ts, labs = _two_layer(3, 6, 100)
     res = A.einsumsvd(A.ImplicitOperator(ts, labs, "apq", "bctef"), A.TruncationPolicy(6, 1e-14),
                       A.SvdStrategy.implicit_rsvd, A.Absorb[absorb], A.RsvdConfig(2, -1, 11))
@@ -233,7 +234,7 @@ def test_einsumsvd_vs_live_reference_larger(A, refo, mode):
             assert rel(t1.reshape(-1, k) @ t2.reshape(k, -1),
                        want["t1"].reshape(-1, k) @ want["t2"].reshape(k, -1)) < 1e-9
     finally:
-        ctx.set_option("orth_mode", 1)
+        ctx.set_option("orth_mode", 0)
 
 
 def test_rank_deficient_probe_falls_back_to_faithful(A, refo):
@@ -249,7 +250,7 @@ def test_rank_deficient_probe_falls_back_to_faithful(A, refo):
         assert t.s.shape == want["s"].shape  # rank metadata: 3 retained of target 6
         assert rel(t.s, want["s"]) < 1e-10
         assert rel((t.u.numpy() * t.s) @ t.v.numpy(), a) < 1e-10
-    A.default_context().set_option("orth_mode", 1)
+    A.default_context().set_option("orth_mode", 0)
 
 
 def test_errors_mirror_reference(A):
