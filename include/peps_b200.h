@@ -91,6 +91,8 @@ int pepsb_ctx_reset_counters(pepsb_ctx* ctx);
  * {launches, device ms, algorithmic real flops, algorithmic bytes}. */
 int pepsb_ctx_profile(pepsb_ctx* ctx, int enable);
 int pepsb_ctx_profile_report(pepsb_ctx* ctx, double* out16);
+/* Diagnostics: device status word idx (word 7 = cumulative Jacobi sweeps). */
+int pepsb_ctx_debug_word(pepsb_ctx* ctx, int idx, int reset);
 /* CUDA stream the library enqueues on (cudaStream_t), for event timing */
 void* pepsb_ctx_stream(pepsb_ctx* ctx);
 
@@ -180,6 +182,20 @@ int pepsb_band_value(pepsb_ctx* ctx, const pepsb_boundary* top, const pepsb_stat
                      int r1, const pepsb_boundary* bottom, int npieces, const int* rc, pepsb_tensor* const* ops,
                      const int* nbonds, const int* bond_ids, double* re, double* im);
 void pepsb_band_env_free(pepsb_band_env* e);
+
+/* ---------------------------------------------------------------- simple update / ITE (state.hpp:64-76) */
+/* hermitian_function(coeff * op, exp(-tau x)) (linalg.hpp:44): the ITE gate rule of drivers.cpp:56-71 */
+int pepsb_hermitian_exp(pepsb_ctx* ctx, const pepsb_tensor* op, double coeff, double tau, pepsb_tensor** out);
+/* apply_one_site (state.hpp:64-65) on nsites sites (row, col pairs in rc); returns a new state */
+int pepsb_apply_one_site(pepsb_ctx* ctx, const pepsb_state* s, const pepsb_tensor* gate, int nsites, const int* rc,
+                         pepsb_state** out);
+/* apply_two_site (state.hpp:69-70; UpdateStrategy::qr_svd_gram) on nbonds disjoint adjacent bonds
+ * (ar, ac, br, bc per bond), batched; policy NULL = {0, 1e-14} (cap d * pre-gate bond) */
+int pepsb_apply_two_site(pepsb_ctx* ctx, const pepsb_state* s, const pepsb_tensor* gate, int nbonds,
+                         const int* bonds, const pepsb_trunc* policy, pepsb_state** out);
+/* TFIM imaginary-time evolution (drivers.cpp:75-98 loop; H = -J sum ZZ - h sum X, colour-ordered terms) */
+int pepsb_ite_tfim(pepsb_ctx* ctx, const pepsb_state* s, double J, double h, double tau, int steps, uint64_t rank,
+                   pepsb_state** out);
 
 #ifdef __cplusplus
 }

@@ -307,15 +307,21 @@ def mps_overlap(a, b) -> complex:
 
 def inner_exact(sites, rows, cols) -> complex:
     """Exact <psi|psi> by full dense contraction (small lattices only)."""
+    return inner_exact_pair(sites, sites, rows, cols)
+
+
+def inner_exact_pair(bra, ket, rows, cols) -> complex:
+    """Exact <bra|ket> by full dense contraction of the merged grid
+    (merge_two_layer, contraction.cpp:670-688; small lattices only)."""
     letters = iter("ABCDEFGHIJKLMNOPQRSTUVWXYZabcdefghijklmnopqrstuvwxyz")
-    # build the merged one-layer grid as einsum over bra*/ket pairs
     tens, specs = [], []
     hb = {}
     for r in range(rows):
         for c in range(cols):
-            t = sites[r * cols + c]
-            m = np.einsum("dulbr,dULBR->uUlLbBrR", t.conj(), t)
-            m = m.reshape(t.shape[1] ** 2, t.shape[2] ** 2, t.shape[3] ** 2, t.shape[4] ** 2)
+            b, t = bra[r * cols + c], ket[r * cols + c]
+            m = np.einsum("dulbr,dULBR->uUlLbBrR", b.conj(), t)
+            m = m.reshape(b.shape[1] * t.shape[1], b.shape[2] * t.shape[2], b.shape[3] * t.shape[3],
+                          b.shape[4] * t.shape[4])
             key_u, key_l, key_d, key_r = ("v", r, c), ("h", r, c), ("v", r + 1, c), ("h", r, c + 1)
             lab = ""
             for k in (key_u, key_l, key_d, key_r):

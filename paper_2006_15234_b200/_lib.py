@@ -49,6 +49,7 @@ _SIGS = {
     "pepsb_ctx_counters": (C.c_int, [_VP, C.POINTER(C.c_uint64)]),
     "pepsb_ctx_reset_counters": (C.c_int, [_VP]),
     "pepsb_ctx_stream": (_VP, [_VP]),
+    "pepsb_ctx_debug_word": (C.c_int, [_VP, C.c_int, C.c_int]),
     "pepsb_ctx_profile": (C.c_int, [_VP, C.c_int]),
     "pepsb_ctx_profile_report": (C.c_int, [_VP, C.POINTER(C.c_double)]),
     "pepsb_tensor_from_host": (C.c_int, [_VP, C.c_int, C.POINTER(C.c_int64), _VP, C.POINTER(_VP)]),
@@ -99,6 +100,12 @@ _SIGS = {
                                    C.POINTER(_VP), C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_double),
                                    C.POINTER(C.c_double)]),
     "pepsb_band_env_free": (None, [_VP]),
+    "pepsb_hermitian_exp": (C.c_int, [_VP, _VP, C.c_double, C.c_double, C.POINTER(_VP)]),
+    "pepsb_apply_one_site": (C.c_int, [_VP, _VP, _VP, C.c_int, C.POINTER(C.c_int), C.POINTER(_VP)]),
+    "pepsb_apply_two_site": (C.c_int, [_VP, _VP, _VP, C.c_int, C.POINTER(C.c_int), C.POINTER(Trunc),
+                                       C.POINTER(_VP)]),
+    "pepsb_ite_tfim": (C.c_int, [_VP, _VP, C.c_double, C.c_double, C.c_double, C.c_int, C.c_uint64,
+                                 C.POINTER(_VP)]),
 }
 
 

@@ -502,4 +502,53 @@ def band_value(top, bra: PepsState, ket: PepsState, r0: int, r1: int, bottom, pi
     return complex(re.value, im.value)
 
 
+def _wrap_state(h, like: PepsState) -> PepsState:
+    out = PepsState.__new__(PepsState)
+    out.ctx, out.rows, out.cols, out.d, out.h = like.ctx, like.rows, like.cols, like.d, h
+    out.sites = []
+    for r in range(like.rows):
+        for c in range(like.cols):
+            t = _VP()
+            check(lib().pepsb_state_site(h, r, c, C.byref(t)))
+            out.sites.append(DeviceTensor(t, like.ctx))
+    return out
+
+
+def hermitian_exp(op, coeff: float, tau: float, ctx: Optional[Context] = None) -> DeviceTensor:
+    """hermitian_function(coeff*op, exp(-tau x)) (linalg.cpp:297-314), evaluated on the device."""
+    ctx = ctx or default_context()
+    d = to_device(op, ctx)
+    h = _VP()
+    check(lib().pepsb_hermitian_exp(ctx.h, d.h, float(coeff), float(tau), C.byref(h)))
+    return DeviceTensor(h, ctx)
+
+
+def apply_one_site(s: PepsState, gate, sites: Sequence[Tuple[int, int]]) -> PepsState:
+    """apply_one_site (state.cpp:75-85) on every listed site, one batched launch."""
+    g = to_device(gate, s.ctx)
+    rc = (C.c_int * max(1, 2 * len(sites)))(*[int(x) for p in sites for x in p])
+    h = _VP()
+    check(lib().pepsb_apply_one_site(s.ctx.h, s.h, g.h, len(sites), rc, C.byref(h)))
+    return _wrap_state(h, s)
+
+
+def apply_two_site(s: PepsState, gate, bonds: Sequence[Tuple[int, int, int, int]],
+                   policy: Optional[TruncationPolicy] = None) -> PepsState:
+    """apply_two_site (state.cpp:161-204, qr_svd_gram) on disjoint adjacent bonds (ar, ac, br, bc)."""
+    g = to_device(gate, s.ctx)
+    b = (C.c_int * max(1, 4 * len(bonds)))(*[int(x) for t in bonds for x in t])
+    pol = (policy or TruncationPolicy(0, 1e-14)).c()
+    h = _VP()
+    check(lib().pepsb_apply_two_site(s.ctx.h, s.h, g.h, len(bonds), b, C.byref(pol), C.byref(h)))
+    return _wrap_state(h, s)
+
+
+def ite_tfim(s: PepsState, J: float, h: float, tau: float, steps: int, rank: int) -> PepsState:
+    """TFIM imaginary-time evolution by batched simple update (config 4)."""
+    out = _VP()
+    check(lib().pepsb_ite_tfim(s.ctx.h, s.h, float(J), float(h), float(tau), int(steps), int(rank),
+                               C.byref(out)))
+    return _wrap_state(out, s)
+
+
 __all__ = [n for n in dir() if not n.startswith("_")] + ["PepsError"]

@@ -4,6 +4,7 @@
 #include <string>
 
 #include "../../include/peps_b200.h"
+#include "ite.h"
 #include "peps.h"
 #include "tensor_ops.cuh"
 
@@ -220,6 +221,18 @@ int pepsb_ctx_profile_report(pepsb_ctx* c, double* out16) {
     need(c, "ctx");
     c->ctx->profile_report(out16);
   });
+}
+
+int pepsb_ctx_debug_word(pepsb_ctx* c, int idx, int reset) {
+  int v = -1;
+  guard([&] {
+    need(c, "ctx");
+    if (idx < 0 || idx >= 64) throw Error(kValidationError, "debug word index out of range");
+    c->ctx->sync();
+    PEPSB_CUDA(cudaMemcpy(&v, c->ctx->d_status + idx, sizeof(int), cudaMemcpyDeviceToHost));
+    if (reset) PEPSB_CUDA(cudaMemset(c->ctx->d_status + idx, 0, sizeof(int)));
+  });
+  return v;
 }
 
 void* pepsb_ctx_stream(pepsb_ctx* c) { return c ? static_cast<void*>(c->ctx->stream) : nullptr; }
@@ -555,5 +568,48 @@ int pepsb_band_value(pepsb_ctx* c, const pepsb_boundary* top, const pepsb_state*
 }
 
 void pepsb_band_env_free(pepsb_band_env* e) { delete e; }
+
+int pepsb_hermitian_exp(pepsb_ctx* c, const pepsb_tensor* op, double coeff, double tau, pepsb_tensor** out) {
+  return guard([&] {
+    need(c, "ctx");
+    need(op, "operator");
+    *out = wrap(hermitian_exp(*c->ctx, op->t, coeff, tau));
+  });
+}
+
+int pepsb_apply_one_site(pepsb_ctx* c, const pepsb_state* s, const pepsb_tensor* gate, int nsites, const int* rc,
+                         pepsb_state** out) {
+  return guard([&] {
+    need(c, "ctx");
+    need(s, "state");
+    need(gate, "gate");
+    std::vector<std::pair<int, int>> sites;
+    for (int i = 0; i < nsites; ++i) sites.push_back({rc[2 * i], rc[2 * i + 1]});
+    *out = new pepsb_state{apply_one_site_batch(*c->ctx, s->s, gate->t, sites)};
+  });
+}
+
+int pepsb_apply_two_site(pepsb_ctx* c, const pepsb_state* s, const pepsb_tensor* gate, int nbonds, const int* bonds,
+                         const pepsb_trunc* policy, pepsb_state** out) {
+  return guard([&] {
+    need(c, "ctx");
+    need(s, "state");
+    need(gate, "gate");
+    std::vector<std::array<int, 4>> bl;
+    for (int i = 0; i < nbonds; ++i) bl.push_back({bonds[4 * i], bonds[4 * i + 1], bonds[4 * i + 2], bonds[4 * i + 3]});
+    Trunc t = trunc_of(policy);
+    if (!policy) t = Trunc{0, 1e-14};
+    *out = new pepsb_state{apply_two_site_batch(*c->ctx, s->s, gate->t, bl, t)};
+  });
+}
+
+int pepsb_ite_tfim(pepsb_ctx* c, const pepsb_state* s, double J, double h, double tau, int steps, uint64_t rank,
+                   pepsb_state** out) {
+  return guard([&] {
+    need(c, "ctx");
+    need(s, "state");
+    *out = new pepsb_state{ite_tfim(*c->ctx, s->s, J, h, tau, steps, rank)};
+  });
+}
 
 }  // extern "C"

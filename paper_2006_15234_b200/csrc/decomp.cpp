@@ -20,6 +20,9 @@
 
 #include <algorithm>
 #include <cmath>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <set>
@@ -150,7 +153,7 @@ LTensor orth(Ctx& ctx, const LTensor& Y) {
     int* d_def = reinterpret_cast<int*>(def->p);
     int* d_any = d_def + k;
     BufPtr work;
-    if (2 * k * k * 16 > 200 * 1024) work = ctx.alloc(2 * k * k);
+    if (2 * k * (k + 1) * 16 > 200 * 1024) work = ctx.alloc(2 * k * (k + 1));
     {
       ProfScope ps_(ctx, Ctx::kProfSmall);
       gram_factors(G->p, static_cast<int>(k), P->p, R->p, d_def, d_any, ctx.d_status, work ? work->p : nullptr,
@@ -336,6 +339,9 @@ EinsumsvdResultD rsvd_core(Ctx& ctx, const ImplicitOp& op, const Trunc& policy, 
     return plan_adj.execute(ctx, leaves_adj);
   };
 
+  static const bool trace = getenv("PEPSB_TRACE") != nullptr;
+  auto now = [] { return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count(); };
+  const double tr0 = trace ? now() : 0.0;
   LTensor p = orth(ctx, apply(q));
   for (int i = 0; i < cfg.power_iters; ++i) {
     q = orth(ctx, adjoint(p));
@@ -343,7 +349,14 @@ EinsumsvdResultD rsvd_core(Ctx& ctx, const ImplicitOp& op, const Trunc& policy, 
   }
   LTensor z = adjoint(p);
   q = LTensor();
+  const double tr1 = trace ? now() : 0.0;
+  if (trace) {
+    ctx.sync();
+    fprintf(stderr, "[pepsb] rsvd enqueue %.3f ms, drain %.3f ms\n", tr1 - tr0, now() - tr1);
+  }
+  const double tr2 = trace ? now() : 0.0;
   Projected pr = projected_svd(ctx, z, target);
+  if (trace) fprintf(stderr, "[pepsb] projected_svd %.3f ms (tsqr %d)\n", now() - tr2, pr.tsqr ? 1 : 0);
   if (ctx.orth_mode == 1 && (ctx.h_status[1] & kSmallCholBreakdown)) {
     ++ctx.faithful_redos;
     throw RedoFaithful{};
@@ -497,7 +510,7 @@ std::pair<DTensor, DTensor> gram_orthogonalize(Ctx& ctx, const DTensor& a, int s
   int* d_def = reinterpret_cast<int*>(def->p);
   int* d_any = d_def + cols;
   BufPtr work;
-  if (2 * cols * cols * 16 > 200 * 1024) work = ctx.alloc(2 * cols * cols);
+  if (2 * cols * (cols + 1) * 16 > 200 * 1024) work = ctx.alloc(2 * cols * (cols + 1));
   DTensor R;
   std::vector<int64_t> rshape = cs;
   rshape.insert(rshape.end(), cs.begin(), cs.end());

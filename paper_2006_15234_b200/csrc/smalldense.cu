@@ -104,6 +104,7 @@ __device__ void onesided_jacobi(double2* X, int m, int n, int ldx, double2* V, i
     if (!any) break;
   }
   if (sweep == max_sweeps && threadIdx.x == 0) atomicOr(status, kSmallNoConverge);
+  if (threadIdx.x == 0) atomicAdd(status + 7, sweep + 1);  // diagnostics: total sweeps
 }
 
 // Descending order of key[0..n) (ties by index) -> order[rank] = column.
@@ -144,6 +145,111 @@ __device__ double2 column_phase(const double2* colp, int rows) {
 
 // ------------------------------------------------------------------ gram_factors
 
+// Two-sided parallel (round-robin) Jacobi for a Hermitian n x n matrix A stored
+// column-major (A(i,j) = A[j*n+i]); on return A is diagonal (eigenvalues) and
+// V (column-major) holds the eigenvectors.  Each round applies n/2 disjoint
+// rotations A <- J^H A J with one thread per 2x2 block of (pair_i, pair_j)
+// coordinates, so a round costs two barriers and no reductions.
+__device__ void herm_jacobi(double2* A, double2* V, int n, int ld, double tol, double abs_skip, int max_sweeps,
+                            int* status) {
+  __shared__ double jc[128], js[128];
+  __shared__ double2 je[128];
+  __shared__ int jp[128], jq[128];
+  __shared__ int rotated, flag[3];
+  for (int e = threadIdx.x; e < n * n; e += blockDim.x)
+    V[(e / n) * ld + e % n] = make_double2((e / n) == (e % n) ? 1.0 : 0.0, 0.0);
+  if (threadIdx.x < 3) flag[threadIdx.x] = 0;
+  __syncthreads();
+  if (n < 2) return;
+  const int npad = n + (n & 1);
+  const int pairs = npad / 2;
+  const int nblk = pairs * pairs;
+  const double tol2 = tol * tol, skip2 = abs_skip * abs_skip;
+  int sweep = 0, round = 0;
+  for (; sweep < max_sweeps; ++sweep) {
+    if (threadIdx.x == 0) rotated = 0;
+    __syncthreads();
+    for (int r = 0; r < npad - 1; ++r, ++round) {
+      // phase 1: rotation parameters of the round's disjoint pairs (reads A only)
+      if (threadIdx.x == 0) flag[(round + 1) % 3] = 0;  // last read two rounds ago
+      for (int pi = threadIdx.x; pi < pairs; pi += blockDim.x) {
+        int p = rr_pos(pi, r, npad), q = rr_pos(npad - 1 - pi, r, npad);
+        if (p > q) { int t = p; p = q; q = t; }
+        double c = 1.0, s = 0.0;
+        double2 e = make_double2(1.0, 0.0);
+        if (q < n) {
+          const double2 apq = A[q * ld + p];
+          const double ag2 = apq.x * apq.x + apq.y * apq.y;
+          const double app = A[p * ld + p].x, aqq = A[q * ld + q].x;
+          if (ag2 > tol2 * fabs(app * aqq) && ag2 > skip2) {
+            const double rag = rsqrt(ag2);  // 1 / |a_pq|
+            const double tau = 0.5 * (aqq - app) * rag;
+            const double t = copysign(1.0, tau) / (fabs(tau) + sqrt(fma(tau, tau, 1.0)));
+            c = rsqrt(fma(t, t, 1.0));
+            s = t * c;
+            e = make_double2(apq.x * rag, apq.y * rag);
+            rotated = 1;
+            flag[round % 3] = 1;
+          }
+        }
+        jp[pi] = p;
+        jq[pi] = q;
+        jc[pi] = c;
+        js[pi] = s;
+        je[pi] = e;
+      }
+      __syncthreads();
+      if (!flag[round % 3]) continue;  // nothing rotated: no writes, no second barrier
+      // phase 2: A <- J^H A J per 2x2 block, J = [[c, s], [-s conj(e), c conj(e)]],
+      // and V <- V J, as one balanced task list
+      for (int task = threadIdx.x; task < nblk + n * pairs; task += blockDim.x) {
+        if (task < nblk) {
+          const int i = task / pairs, j = task - (task / pairs) * pairs;
+          const double sI = js[i], sJ = js[j];
+          if (sI == 0.0 && sJ == 0.0) continue;
+          const int ri0 = jp[i], ri1 = jq[i], cj0 = jp[j], cj1 = jq[j];
+          const bool v0 = ri1 < n, v1 = cj1 < n;  // (q may be the padding index)
+          double2 a00 = A[cj0 * ld + ri0];
+          double2 a01 = v1 ? A[cj1 * ld + ri0] : make_double2(0.0, 0.0);
+          double2 a10 = v0 ? A[cj0 * ld + ri1] : make_double2(0.0, 0.0);
+          double2 a11 = (v0 && v1) ? A[cj1 * ld + ri1] : make_double2(0.0, 0.0);
+          const double cJ = jc[j], cI = jc[i];
+          const double2 eJc = cconj(je[j]), eI = je[i];
+          // M = a J_j
+          double2 t0 = cmul(eJc, a01), t1 = cmul(eJc, a11);
+          const double2 m00 = csub(cscale(a00, cJ), cscale(t0, sJ)), m01 = cadd(cscale(a00, sJ), cscale(t0, cJ));
+          const double2 m10 = csub(cscale(a10, cJ), cscale(t1, sJ)), m11 = cadd(cscale(a10, sJ), cscale(t1, cJ));
+          // out = J_i^H M
+          t0 = cmul(eI, m10);
+          t1 = cmul(eI, m11);
+          a00 = csub(cscale(m00, cI), cscale(t0, sI));
+          a10 = cadd(cscale(m00, sI), cscale(t0, cI));
+          a01 = csub(cscale(m01, cI), cscale(t1, sI));
+          a11 = cadd(cscale(m01, sI), cscale(t1, cI));
+          if (i == j && sI != 0.0) a01 = a10 = make_double2(0.0, 0.0);  // annihilated by construction
+          A[cj0 * ld + ri0] = a00;
+          if (v1) A[cj1 * ld + ri0] = a01;
+          if (v0) A[cj0 * ld + ri1] = a10;
+          if (v0 && v1) A[cj1 * ld + ri1] = a11;
+        } else {
+          const int t = task - nblk, k = t / pairs, j = t - (t / pairs) * pairs;
+          const int p = jp[j], q = jq[j];
+          if (q >= n || js[j] == 0.0) continue;
+          const double2 vkp = V[p * ld + k], vkq = cmul(cconj(je[j]), V[q * ld + k]);
+          V[p * ld + k] = csub(cscale(vkp, jc[j]), cscale(vkq, js[j]));
+          V[q * ld + k] = cadd(cscale(vkp, js[j]), cscale(vkq, jc[j]));
+        }
+      }
+      __syncthreads();
+    }
+    const int any = rotated;
+    __syncthreads();
+    if (!any) break;
+  }
+  if (sweep == max_sweeps && threadIdx.x == 0) atomicOr(status, kSmallNoConverge);
+  if (threadIdx.x == 0) atomicAdd(status + 7, sweep + 1);  // diagnostics: total sweeps
+}
+
 // Block-level gram_factors; X, V: n*n complex scratch each (column-major).
 // Outputs (P, R, deficient, any_def) are complete after the trailing barrier.
 __device__ void gram_factors_dev(const double2* G, int n, double2* X, double2* V, double2* P, double2* R,
@@ -151,6 +257,7 @@ __device__ void gram_factors_dev(const double2* G, int n, double2* X, double2* V
   __shared__ double lam[256];
   __shared__ int order[256];
   __shared__ double hmax[2];
+  const int ld = n + 1;  // padded column stride: conflict-free strided column access
   if (threadIdx.x < 2) hmax[threadIdx.x] = 0.0;
   __syncthreads();
   // Hermiticity check against the input, as eigh does (linalg.cpp:262-271).
@@ -160,8 +267,8 @@ __device__ void gram_factors_dev(const double2* G, int n, double2* X, double2* V
     double2 a = G[i * n + j], b = G[j * n + i];
     herr = fmax(herr, hypot(a.x - b.x, a.y + b.y));
     scale = fmax(scale, hypot(a.x, a.y));
-    // symmetrised 0.5 (G + G^H), stored column-major: X[j][i] = A(i, j)
-    X[j * n + i] = make_double2(0.5 * (a.x + b.x), 0.5 * (a.y - b.y));
+    // symmetrised 0.5 (G + G^H), stored column-major (ld = n + 1): X[j][i] = A(i, j)
+    X[j * ld + i] = make_double2(0.5 * (a.x + b.x), 0.5 * (a.y - b.y));
   }
   // block max via atomics on the bit patterns of non-negative doubles
   atomicMax(reinterpret_cast<unsigned long long*>(&hmax[0]), __double_as_longlong(herr));
@@ -170,32 +277,23 @@ __device__ void gram_factors_dev(const double2* G, int n, double2* X, double2* V
   if (threadIdx.x == 0 && hmax[0] > 1e-10 * fmax(1.0, hmax[1])) atomicOr(status, kSmallNotHermitian);
 
   double fro = 0.0;
-  for (int e = threadIdx.x; e < n * n; e += blockDim.x) fro += cnorm2(X[e]);
-  // abs skip: rotations below the rounding level of ||G||^2 do not move eigenvalues.
-  const double abs_skip = 1e-34 * block_sum(fro);
-  // Convergence at the rounding level of the column inner products
-  // (8 eps sqrt(n), cf. LAPACK zgesvj's sqrt(m) eps): a tighter threshold only
-  // chases noise and never terminates early.
-  onesided_jacobi(X, n, n, n, V, n, 8.0 * 2.220446049250313e-16 * sqrt(static_cast<double>(n)), abs_skip, 40,
-                  status);
-
-  // eigenvalue j = Re(v_j^H G v_j) = Re(v_j^H x_j)   (X = G V)
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
-  for (int j = warp; j < n; j += nwarps) {
-    double s = 0.0;
-    for (int i = lane; i < n; i += 32) {
-      double2 v = V[j * n + i], x = X[j * n + i];
-      s += v.x * x.x + v.y * x.y;
-    }
-    s = warp_sum(s);
-    if (lane == 0) lam[j] = s;
-  }
+  for (int e = threadIdx.x; e < n * n; e += blockDim.x) fro += cnorm2(X[(e / n) * ld + e % n]);
+  // Off-diagonals below the rounding level of ||G|| are noise (G itself carries
+  // absolute errors ~eps ||G||, as does zheevd's output); rotating them only
+  // chases noise on the small-eigenvalue block.
+  // Both thresholds at n*eps: the accumulated rounding of O(n^2) rotations,
+  // and the accuracy class of zheevd (|d lambda| ~ n eps ||G||).
+  const double neps = static_cast<double>(n) * 2.220446049250313e-16;
+  const double abs_skip = neps * sqrt(block_sum(fro));
+  herm_jacobi(X, V, n, ld, neps, abs_skip, 40, status);
+  for (int j = threadIdx.x; j < n; j += blockDim.x) lam[j] = X[j * ld + j].x;
   __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
   sort_desc(lam, order, n);
   // phase of each sorted eigenvector column
   __shared__ double2 ph[256];
   for (int j = warp; j < n; j += nwarps) {
-    double2 p = column_phase(V + order[j] * n, n);
+    double2 p = column_phase(V + order[j] * ld, n);
     if (lane == 0) ph[j] = p;
   }
   __syncthreads();
@@ -214,7 +312,7 @@ __device__ void gram_factors_dev(const double2* G, int n, double2* X, double2* V
     const int i = e / n, j = e % n;
     const double lj = fmax(lam[order[j]], 1e-12 * lmax);
     // eigenvector column j (sorted), phase fixed: x_ij * conj(phase_j)
-    const double2 xij = cmulc(ph[j], V[order[j] * n + i]);
+    const double2 xij = cmulc(ph[j], V[order[j] * ld + i]);
     const double isq = 1.0 / sqrt(lj);
     P[i * n + j] = cscale(xij, isq);
     // R row j = sqrt(l_j) conj(column j of X): R[j][i] = sqrt(l_j) conj(x_ij)
@@ -228,8 +326,8 @@ __global__ void __launch_bounds__(kThreads) gram_factors_kernel(const double2* G
                                                                 int* any_def, int* status,
                                                                 double2* work) {
   extern __shared__ __align__(16) unsigned char sm[];
-  double2* X = work ? work : reinterpret_cast<double2*>(sm);  // column-major n x n
-  gram_factors_dev(G, n, X, X + n * n, P, R, deficient, any_def, status);
+  double2* X = work ? work : reinterpret_cast<double2*>(sm);  // column-major n x (n+1)
+  gram_factors_dev(G, n, X, X + n * (n + 1), P, R, deficient, any_def, status);
 }
 
 // ------------------------------------------------------------------ Cholesky
@@ -388,7 +486,12 @@ __device__ void small_svd_dev(const double2* A, int m_, int n_, int lda, double2
     else X[static_cast<int64_t>(i) * mr + j] = cconj(v);     // A^H: col i, row j
   }
   __syncthreads();
-  onesided_jacobi(X, mr, nc, mr, V, nc, 8.0 * 2.220446049250313e-16 * sqrt(static_cast<double>(mr)), 0.0, 60,
+  // skip rotations between columns whose inner product is below (eps ||A||_F)^2:
+  // numerically-null columns (rank-deficient A) are left alone, as gesdd would.
+  double fro = 0.0;
+  for (int e = threadIdx.x; e < mr * nc; e += blockDim.x) fro += cnorm2(X[e]);
+  const double abs_skip = 4.930380657631324e-32 * block_sum(fro);
+  onesided_jacobi(X, mr, nc, mr, V, nc, 8.0 * 2.220446049250313e-16 * sqrt(static_cast<double>(mr)), abs_skip, 60,
                   a.status);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
   for (int j = warp; j < nc; j += nwarps) {
@@ -583,8 +686,8 @@ __global__ void __launch_bounds__(512) su_reduce_kernel(const SuSiteDesc* descs,
   }
   double2* G = Y + E * S;
   double2* X = G + S * S;
-  double2* V = X + S * S;
-  double2* P = V + S * S;
+  double2* V = X + S * (S + 1);
+  double2* P = V + S * (S + 1);
   double2* Rm = P + S * S;
   int* def = reinterpret_cast<int*>(Rm + S * S);
   for (int idx = threadIdx.x; idx < S * S; idx += blockDim.x) {
@@ -785,7 +888,7 @@ void herm_exp(const double2* H, int n, double coeff, double tau, double2* out, c
 void gram_factors(const double2* G, int n, double2* P, double2* R, int* deficient, int* any_def,
                   int* status, double2* work, cudaStream_t stream) {
   if (n > 256) throw Error(kShapeError, "gram_factors: k > 256 not supported");
-  const size_t smem = 2ull * n * n * sizeof(double2);
+  const size_t smem = 2ull * n * (n + 1) * sizeof(double2);
   const bool fits = smem <= kSmemCap;
   if (!fits && !work) throw Error(kOtherError, "gram_factors: workspace required");
   static bool attr = false;
@@ -794,7 +897,8 @@ void gram_factors(const double2* G, int n, double2* P, double2* R, int* deficien
                                     static_cast<int>(kSmemCap)));
     attr = true;
   }
-  gram_factors_kernel<<<1, kThreads, fits ? smem : 0, stream>>>(G, n, P, R, deficient, any_def, status,
+  const int threads = kThreads;
+  gram_factors_kernel<<<1, threads, fits ? smem : 0, stream>>>(G, n, P, R, deficient, any_def, status,
                                                                 fits ? nullptr : work);
   PEPSB_LAUNCH();
 }

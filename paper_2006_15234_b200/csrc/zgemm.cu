@@ -270,12 +270,41 @@ void launch_cfg(const ZgemmParams& p, cudaStream_t stream) {
   PEPSB_LAUNCH();
 }
 
-constexpr int kBM = 64, kBN = 64, kBK = 16, kWM = 32, kWN = 32, kStages = 3;
+constexpr int kBK = 16, kStages = 3;
+
+// Tile configurations (BM x BN complex, warps WM x WN): the 72-wide ones cover
+// the k = 72 probe dimension of config 2 in one tile (no 8/64 tail waste).
+struct TileCfg {
+  int bm, bn;
+};
+constexpr TileCfg kCfgs[] = {{64, 64}, {64, 72}, {72, 64}, {72, 72}, {128, 64}};
+
+int choose_cfg(int64_t M, int64_t N) {
+  const bool m72 = M > 48 && M <= 72, n72 = N > 48 && N <= 72;
+  if (m72 && n72) return 3;
+  if (n72) return 1;
+  if (m72) return 2;
+  if (M > 64 && M <= 128 && N >= 4096) return 4;
+  return 0;
+}
+
+template <bool AK, bool BNC>
+void launch_any(const ZgemmParams& p, cudaStream_t stream) {
+  switch (p.cfg) {
+    case 1: launch_cfg<64, 72, kBK, 32, 36, kStages, AK, BNC>(p, stream); break;
+    case 2: launch_cfg<72, 64, kBK, 24, 32, kStages, AK, BNC>(p, stream); break;
+    case 3: launch_cfg<72, 72, kBK, 24, 36, kStages, AK, BNC>(p, stream); break;
+    case 4: launch_cfg<128, 64, kBK, 32, 32, kStages, AK, BNC>(p, stream); break;
+    default: launch_cfg<64, 64, kBK, 32, 32, kStages, AK, BNC>(p, stream); break;
+  }
+}
 
 }  // namespace
 
 int64_t zgemm_plan_splits(ZgemmParams& p, int num_sms) {
-  const int64_t tiles = ((p.M + kBM - 1) / kBM) * ((p.N + kBN - 1) / kBN) * p.batch;
+  p.cfg = choose_cfg(p.M, p.N);
+  const int64_t bm = kCfgs[p.cfg].bm, bn = kCfgs[p.cfg].bn;
+  const int64_t tiles = ((p.M + bm - 1) / bm) * ((p.N + bn - 1) / bn) * p.batch;
   const int64_t target = 2LL * num_sms;
   int64_t splits = 1;
   if (tiles < target && p.K > 4 * kBK) {
@@ -294,6 +323,7 @@ int64_t zgemm_plan_splits(ZgemmParams& p, int num_sms) {
 void zgemm_launch(ZgemmParams p, cudaStream_t stream) {
   if (p.M <= 0 || p.N <= 0 || p.batch <= 0) return;
   if (p.kchunk <= 0) p.kchunk = std::max<int64_t>(p.K, 1);
+  if (p.cfg < 0 || p.cfg > 4) p.cfg = 0;
   const bool ak = p.sAk == 1;
   const bool bnc = p.sBj == 1;
   if (p.K == 0) {
@@ -301,13 +331,13 @@ void zgemm_launch(ZgemmParams p, cudaStream_t stream) {
     p.splits = 1;
   }
   if (ak && bnc)
-    launch_cfg<kBM, kBN, kBK, kWM, kWN, kStages, true, true>(p, stream);
+    launch_any<true, true>(p, stream);
   else if (ak && !bnc)
-    launch_cfg<kBM, kBN, kBK, kWM, kWN, kStages, true, false>(p, stream);
+    launch_any<true, false>(p, stream);
   else if (!ak && bnc)
-    launch_cfg<kBM, kBN, kBK, kWM, kWN, kStages, false, true>(p, stream);
+    launch_any<false, true>(p, stream);
   else
-    launch_cfg<kBM, kBN, kBK, kWM, kWN, kStages, false, false>(p, stream);
+    launch_any<false, false>(p, stream);
   if (p.splits > 1) {
     const int64_t total = p.batch * p.M * p.N;
     const int threads = 256;

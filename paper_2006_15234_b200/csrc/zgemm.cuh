@@ -41,6 +41,7 @@ struct ZgemmParams {
   int splits = 1;
   int64_t kchunk = 0;
   int accumulate = 0;  // C += result instead of C = result
+  int cfg = 0;         // tile configuration (set by zgemm_plan_splits)
 };
 
 // Launches the GEMM (and the deterministic split-K reduction when needed).
