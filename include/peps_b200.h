@@ -91,6 +91,8 @@ int pepsb_ctx_reset_counters(pepsb_ctx* ctx);
  * {launches, device ms, algorithmic real flops, algorithmic bytes}. */
 int pepsb_ctx_profile(pepsb_ctx* ctx, int enable);
 int pepsb_ctx_profile_report(pepsb_ctx* ctx, double* out16);
+/* Per-launch records of the profile (kind, device ms, algorithmic flops) x n; returns n */
+int pepsb_ctx_profile_records(pepsb_ctx* ctx, double* out, int cap);
 /* Diagnostics: device status word idx (word 7 = cumulative Jacobi sweeps). */
 int pepsb_ctx_debug_word(pepsb_ctx* ctx, int idx, int reset);
 /* CUDA stream the library enqueues on (cudaStream_t), for event timing */

@@ -50,6 +50,7 @@ _SIGS = {
     "pepsb_ctx_reset_counters": (C.c_int, [_VP]),
     "pepsb_ctx_stream": (_VP, [_VP]),
     "pepsb_ctx_debug_word": (C.c_int, [_VP, C.c_int, C.c_int]),
+    "pepsb_ctx_profile_records": (C.c_int, [_VP, C.POINTER(C.c_double), C.c_int]),
     "pepsb_ctx_profile": (C.c_int, [_VP, C.c_int]),
     "pepsb_ctx_profile_report": (C.c_int, [_VP, C.POINTER(C.c_double)]),
     "pepsb_tensor_from_host": (C.c_int, [_VP, C.c_int, C.POINTER(C.c_int64), _VP, C.POINTER(_VP)]),

@@ -223,6 +223,24 @@ int pepsb_ctx_profile_report(pepsb_ctx* c, double* out16) {
   });
 }
 
+int pepsb_ctx_profile_records(pepsb_ctx* c, double* out, int cap) {
+  int n = 0;
+  guard([&] {
+    need(c, "ctx");
+    c->ctx->sync();
+    for (auto& r : c->ctx->prof) {
+      if (n >= cap) break;
+      float ms = 0.f;
+      PEPSB_CUDA(cudaEventElapsedTime(&ms, r.a, r.b));
+      out[3 * n] = r.kind;
+      out[3 * n + 1] = ms;
+      out[3 * n + 2] = r.flops;
+      ++n;
+    }
+  });
+  return n;
+}
+
 int pepsb_ctx_debug_word(pepsb_ctx* c, int idx, int reset) {
   int v = -1;
   guard([&] {

@@ -217,8 +217,36 @@ Projected projected_svd(Ctx& ctx, const LTensor& Z, int64_t target) {
     return G;
   };
   bool ok = false;
+  const int64_t tgt = std::max<int64_t>(1, std::min<int64_t>(target, k));
+  BufPtr G1;
   if (rows >= k) {
-    BufPtr G1 = gram(Z.ptr);
+    // Stage 1: eigendecomposition of G1 = Z^H Z = B B^H gives B's left singular
+    // vectors and sigma^2 directly.  Accepted when the retained part of the
+    // spectrum is well inside the Gram route's accuracy (sigma_{target-1} >=
+    // 1e-4 sigma_0: relative error of the kept sigma_j <= eps (s0/sj)^2 ~ 1e-8).
+    G1 = gram(Z.ptr);
+    BufPtr P = ctx.alloc(k * k), R = ctx.alloc(k * k), def = ctx.alloc(k / 4 + 2);
+    int* d_def = reinterpret_cast<int*>(def->p);
+    BufPtr work;
+    if (2 * k * (k + 1) * 16 > 200 * 1024) work = ctx.alloc(2 * k * (k + 1));
+    {
+      ProfScope ps_(ctx, Ctx::kProfSmall);
+      gram_factors(G1->p, ki, P->p, R->p, d_def, d_def + k, ctx.d_status, work ? work->p : nullptr, ctx.stream,
+                   d_s, out.Ut->p);
+    }
+    ++ctx.launches;
+    std::vector<double> lam(k);
+    PEPSB_CUDA(cudaMemcpyAsync(lam.data(), d_s, k * sizeof(double), cudaMemcpyDeviceToHost, ctx.stream));
+    read_status(ctx);
+    ctx.sync();
+    const int st = *ctx.h_status & ~kSmallZeroGram;  // a zero Z is judged below
+    raise_status(st, false);
+    out.s.resize(k);
+    for (int64_t j = 0; j < k; ++j) out.s[j] = std::sqrt(std::max(lam[j], 0.0));
+    ok = out.s[0] > 0.0 && out.s[tgt - 1] >= 1e-4 * out.s[0];
+    clear_status(ctx);
+  }
+  if (!ok && rows >= k) {
     BufPtr R1 = ctx.alloc(k * k), R1i = ctx.alloc(k * k);
     {
       ProfScope ps_(ctx, Ctx::kProfSmall);
@@ -236,8 +264,7 @@ Projected projected_svd(Ctx& ctx, const LTensor& Z, int64_t target) {
     mm(ctx, R->p, R2->p, false, false, R1->p, false, false, k, k, k);
     const int st = svd_of_rh(R);
     raise_status(st, false);
-    const int64_t t = std::max<int64_t>(1, std::min<int64_t>(target, k));
-    ok = !(st & kSmallCholBreakdown) && out.s[0] > 0.0 && out.s[t - 1] >= 1e-7 * out.s[0];
+    ok = !(st & kSmallCholBreakdown) && out.s[0] > 0.0 && out.s[tgt - 1] >= 1e-7 * out.s[0];
     clear_status(ctx);
   }
   if (!ok) {

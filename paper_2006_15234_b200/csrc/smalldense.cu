@@ -200,45 +200,63 @@ __device__ void herm_jacobi(double2* A, double2* V, int n, int ld, double tol, d
       }
       __syncthreads();
       if (!flag[round % 3]) continue;  // nothing rotated: no writes, no second barrier
-      // phase 2: A <- J^H A J per 2x2 block, J = [[c, s], [-s conj(e), c conj(e)]],
-      // and V <- V J, as one balanced task list
-      for (int task = threadIdx.x; task < nblk + n * pairs; task += blockDim.x) {
-        if (task < nblk) {
-          const int i = task / pairs, j = task - (task / pairs) * pairs;
-          const double sI = js[i], sJ = js[j];
-          if (sI == 0.0 && sJ == 0.0) continue;
-          const int ri0 = jp[i], ri1 = jq[i], cj0 = jp[j], cj1 = jq[j];
-          const bool v0 = ri1 < n, v1 = cj1 < n;  // (q may be the padding index)
-          double2 a00 = A[cj0 * ld + ri0];
-          double2 a01 = v1 ? A[cj1 * ld + ri0] : make_double2(0.0, 0.0);
-          double2 a10 = v0 ? A[cj0 * ld + ri1] : make_double2(0.0, 0.0);
-          double2 a11 = (v0 && v1) ? A[cj1 * ld + ri1] : make_double2(0.0, 0.0);
-          const double cJ = jc[j], cI = jc[i];
-          const double2 eJc = cconj(je[j]), eI = je[i];
-          // M = a J_j
-          double2 t0 = cmul(eJc, a01), t1 = cmul(eJc, a11);
-          const double2 m00 = csub(cscale(a00, cJ), cscale(t0, sJ)), m01 = cadd(cscale(a00, sJ), cscale(t0, cJ));
-          const double2 m10 = csub(cscale(a10, cJ), cscale(t1, sJ)), m11 = cadd(cscale(a10, sJ), cscale(t1, cJ));
-          // out = J_i^H M
-          t0 = cmul(eI, m10);
-          t1 = cmul(eI, m11);
-          a00 = csub(cscale(m00, cI), cscale(t0, sI));
-          a10 = cadd(cscale(m00, sI), cscale(t0, cI));
-          a01 = csub(cscale(m01, cI), cscale(t1, sI));
-          a11 = cadd(cscale(m01, sI), cscale(t1, cI));
-          if (i == j && sI != 0.0) a01 = a10 = make_double2(0.0, 0.0);  // annihilated by construction
-          A[cj0 * ld + ri0] = a00;
-          if (v1) A[cj1 * ld + ri0] = a01;
-          if (v0) A[cj0 * ld + ri1] = a10;
-          if (v0 && v1) A[cj1 * ld + ri1] = a11;
-        } else {
-          const int t = task - nblk, k = t / pairs, j = t - (t / pairs) * pairs;
-          const int p = jp[j], q = jq[j];
-          if (q >= n || js[j] == 0.0) continue;
-          const double2 vkp = V[p * ld + k], vkq = cmul(cconj(je[j]), V[q * ld + k]);
-          V[p * ld + k] = csub(cscale(vkp, jc[j]), cscale(vkq, js[j]));
-          V[q * ld + k] = cadd(cscale(vkp, js[j]), cscale(vkq, jc[j]));
+      // phase 2: A <- J^H A J per 2x2 block of pairs (i <= j, the mirror block is
+      // its conjugate transpose), J = [[c, s], [-s conj(e), c conj(e)]]; V <- V J.
+      {
+        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+        for (int i = warp; i < pairs; i += nw) {
+          const double sI = js[i], cI = jc[i];
+          const double2 eI = je[i];
+          const int ri0 = jp[i], ri1 = jq[i];
+          const bool v0 = ri1 < n;
+          for (int j = i + lane; j < pairs; j += 32) {
+            const double sJ = js[j];
+            if (sI == 0.0 && sJ == 0.0) continue;
+            const double cJ = jc[j];
+            const double2 eJc = cconj(je[j]);
+            const int cj0 = jp[j], cj1 = jq[j];
+            const bool v1 = cj1 < n;
+            double2 a00 = A[cj0 * ld + ri0];
+            double2 a01 = v1 ? A[cj1 * ld + ri0] : make_double2(0.0, 0.0);
+            double2 a10 = v0 ? A[cj0 * ld + ri1] : make_double2(0.0, 0.0);
+            double2 a11 = (v0 && v1) ? A[cj1 * ld + ri1] : make_double2(0.0, 0.0);
+            double2 t0 = cmul(eJc, a01), t1 = cmul(eJc, a11);
+            const double2 m00 = csub(cscale(a00, cJ), cscale(t0, sJ)), m01 = cadd(cscale(a00, sJ), cscale(t0, cJ));
+            const double2 m10 = csub(cscale(a10, cJ), cscale(t1, sJ)), m11 = cadd(cscale(a10, sJ), cscale(t1, cJ));
+            t0 = cmul(eI, m10);
+            t1 = cmul(eI, m11);
+            a00 = csub(cscale(m00, cI), cscale(t0, sI));
+            a10 = cadd(cscale(m00, sI), cscale(t0, cI));
+            a01 = csub(cscale(m01, cI), cscale(t1, sI));
+            a11 = cadd(cscale(m01, sI), cscale(t1, cI));
+            if (i == j) {
+              if (sI != 0.0) a01 = a10 = make_double2(0.0, 0.0);  // annihilated by construction
+              a00.y = 0.0;
+              a11.y = 0.0;
+            }
+            A[cj0 * ld + ri0] = a00;
+            if (v1) A[cj1 * ld + ri0] = a01;
+            if (v0) A[cj0 * ld + ri1] = a10;
+            if (v0 && v1) A[cj1 * ld + ri1] = a11;
+            if (i != j) {  // mirror block (rows of pair j, columns of pair i)
+              A[ri0 * ld + cj0] = cconj(a00);
+              if (v1) A[ri0 * ld + cj1] = cconj(a01);
+              if (v0) A[ri1 * ld + cj0] = cconj(a10);
+              if (v0 && v1) A[ri1 * ld + cj1] = cconj(a11);
+            }
+          }
         }
+        for (int k = warp; k < n; k += nw)
+          for (int j = lane; j < pairs; j += 32) {
+            const double sj = js[j];
+            const int q = jq[j];
+            if (q >= n || sj == 0.0) continue;
+            const int p = jp[j];
+            const double cjv = jc[j];
+            const double2 vkp = V[p * ld + k], vkq = cmul(cconj(je[j]), V[q * ld + k]);
+            V[p * ld + k] = csub(cscale(vkp, cjv), cscale(vkq, sj));
+            V[q * ld + k] = cadd(cscale(vkp, sj), cscale(vkq, cjv));
+          }
       }
       __syncthreads();
     }
@@ -253,7 +271,8 @@ __device__ void herm_jacobi(double2* A, double2* V, int n, int ld, double tol, d
 // Block-level gram_factors; X, V: n*n complex scratch each (column-major).
 // Outputs (P, R, deficient, any_def) are complete after the trailing barrier.
 __device__ void gram_factors_dev(const double2* G, int n, double2* X, double2* V, double2* P, double2* R,
-                                 int* deficient, int* any_def, int* status) {
+                                 int* deficient, int* any_def, int* status, double* lam_out = nullptr,
+                                 double2* vec_out = nullptr) {
   __shared__ double lam[256];
   __shared__ int order[256];
   __shared__ double hmax[2];
@@ -317,17 +336,21 @@ __device__ void gram_factors_dev(const double2* G, int n, double2* X, double2* V
     P[i * n + j] = cscale(xij, isq);
     // R row j = sqrt(l_j) conj(column j of X): R[j][i] = sqrt(l_j) conj(x_ij)
     R[j * n + i] = cscale(cconj(xij), sqrt(lj));
+    if (vec_out) vec_out[i * n + j] = xij;  // eigenvector j (descending), phase-fixed
   }
+  if (lam_out)
+    for (int j = threadIdx.x; j < n; j += blockDim.x) lam_out[j] = lam[order[j]];
   __syncthreads();
 }
 
 __global__ void __launch_bounds__(kThreads) gram_factors_kernel(const double2* G, int n, double2* P,
                                                                 double2* R, int* deficient,
                                                                 int* any_def, int* status,
-                                                                double2* work) {
+                                                                double2* work, double* lam_out,
+                                                                double2* vec_out) {
   extern __shared__ __align__(16) unsigned char sm[];
   double2* X = work ? work : reinterpret_cast<double2*>(sm);  // column-major n x (n+1)
-  gram_factors_dev(G, n, X, X + n * (n + 1), P, R, deficient, any_def, status);
+  gram_factors_dev(G, n, X, X + n * (n + 1), P, R, deficient, any_def, status, lam_out, vec_out);
 }
 
 // ------------------------------------------------------------------ Cholesky
@@ -886,7 +909,7 @@ void herm_exp(const double2* H, int n, double coeff, double tau, double2* out, c
 }
 
 void gram_factors(const double2* G, int n, double2* P, double2* R, int* deficient, int* any_def,
-                  int* status, double2* work, cudaStream_t stream) {
+                  int* status, double2* work, cudaStream_t stream, double* lam_out, double2* vec_out) {
   if (n > 256) throw Error(kShapeError, "gram_factors: k > 256 not supported");
   const size_t smem = 2ull * n * (n + 1) * sizeof(double2);
   const bool fits = smem <= kSmemCap;
@@ -899,7 +922,7 @@ void gram_factors(const double2* G, int n, double2* P, double2* R, int* deficien
   }
   const int threads = kThreads;
   gram_factors_kernel<<<1, threads, fits ? smem : 0, stream>>>(G, n, P, R, deficient, any_def, status,
-                                                                fits ? nullptr : work);
+                                                                fits ? nullptr : work, lam_out, vec_out);
   PEPSB_LAUNCH();
 }
 

@@ -24,8 +24,11 @@ enum SmallStatus : int {
 // Gram matrix G (row-major):  eigh (descending, phase-fixed, linalg.cpp:256-295)
 // -> clamp at 1e-12*lmax -> P = X diag(l^-1/2), R = diag(l^1/2) X^H, deficient
 // flags.  `work` needs 2*n*n complex when n is too large for shared memory.
+// Optionally also returns the sorted eigenvalues (lam_out, n doubles) and the
+// phase-fixed eigenvectors (vec_out, row-major n x n, column j = vector j).
 void gram_factors(const double2* G, int n, double2* P, double2* R, int* deficient, int* any_def,
-                  int* status, double2* work, cudaStream_t stream);
+                  int* status, double2* work, cudaStream_t stream, double* lam_out = nullptr,
+                  double2* vec_out = nullptr);
 
 // CholeskyQR factor: G + shift*I = R^H R (R upper triangular), Rinv = R^{-1}.
 // CholeskyQR factor G = R^H R; status |= kSmallCholBreakdown when a pivot

@@ -8,6 +8,8 @@
 // 8x8 real C tile is an 8x4 complex tile and each lane owns exactly one
 // complex output (re = c0, im = c1).
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 
 #include "zgemm.cuh"
 
@@ -280,7 +282,7 @@ struct TileCfg {
 constexpr TileCfg kCfgs[] = {{64, 64}, {64, 72}, {72, 64}, {72, 72}, {128, 64}};
 
 int choose_cfg(int64_t M, int64_t N) {
-  const bool m72 = M > 48 && M <= 72, n72 = N > 48 && N <= 72;
+  const bool m72 = M > 64 && M <= 72, n72 = N > 64 && N <= 72;
   if (m72 && n72) return 3;
   if (n72) return 1;
   if (m72) return 2;
@@ -324,6 +326,11 @@ void zgemm_launch(ZgemmParams p, cudaStream_t stream) {
   if (p.M <= 0 || p.N <= 0 || p.batch <= 0) return;
   if (p.kchunk <= 0) p.kchunk = std::max<int64_t>(p.K, 1);
   if (p.cfg < 0 || p.cfg > 4) p.cfg = 0;
+  static const bool trace = getenv("PEPSB_TRACE_GEMM") != nullptr;
+  if (trace)
+    fprintf(stderr, "[zgemm] M=%ld N=%ld K=%ld batch=%ld cfg=%d splits=%d AK=%d BNC=%d conjA=%d conjB=%d\n",
+            (long)p.M, (long)p.N, (long)p.K, (long)p.batch, p.cfg, p.splits, p.sAk == 1, p.sBj == 1, p.conjA,
+            p.conjB);
   const bool ak = p.sAk == 1;
   const bool bnc = p.sBj == 1;
   if (p.K == 0) {
