@@ -6,6 +6,8 @@
 // disjoint, one __syncthreads per round).
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
+#include <string>
 
 #include "smalldense.cuh"
 
@@ -268,11 +270,201 @@ __device__ void herm_jacobi(double2* A, double2* V, int n, int ld, double tol, d
   if (threadIdx.x == 0) atomicAdd(status + 7, sweep + 1);  // diagnostics: total sweeps
 }
 
+// Hermitian eigensolver for one thread block: Householder tridiagonalisation
+// (the zhetd2 recurrence: A <- H^H A H with H = I - tau v v^H, rank-2 updates),
+// implicit QL with Wilkinson shifts on the real tridiagonal run by ONE warp
+// (every lane evaluates the scalar Givens chain redundantly and rotates its own
+// rows of Z, so the chain needs no barriers), and back-transformation X = Q Z.
+// A (column-major, ld) is destroyed; on return its diagonal holds the
+// eigenvalues (unsorted) and V (column-major, ld) the eigenvectors.
+// Backward stable like zheevd; O(n) barriers instead of Jacobi's O(n * sweeps).
+__device__ void herm_eig_tridiag(double2* A, double2* V, int n, int ld, int* status) {
+  __shared__ double d[128], e[128];
+  __shared__ double2 vv[128], pw[128], tauv[128];
+  __shared__ double2 sh_tau, sh_scal;
+  __shared__ double sh_beta;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  const long long clk0 = clock64();
+  // ---- 1. tridiagonalisation, j = 0 .. n-2 (reflector H_j acts on rows/cols j+1..n-1)
+  for (int j = 0; j + 1 < n; ++j) {
+    double part = 0.0;
+    for (int i = j + 2 + tid; i < n; i += blockDim.x) part += cnorm2(A[j * ld + i]);
+    const double xnorm2 = block_sum(part);
+    if (tid == 0) {
+      const double2 alpha = A[j * ld + j + 1];
+      if (xnorm2 == 0.0 && alpha.y == 0.0) {
+        sh_tau = make_double2(0.0, 0.0);
+        sh_beta = alpha.x;
+      } else {
+        const double beta = -copysign(sqrt(alpha.x * alpha.x + alpha.y * alpha.y + xnorm2), alpha.x);
+        sh_tau = make_double2((beta - alpha.x) / beta, -alpha.y / beta);
+        const double2 den = make_double2(alpha.x - beta, alpha.y);  // scal = 1 / (alpha - beta)
+        const double dn = 1.0 / cnorm2(den);
+        sh_scal = make_double2(den.x * dn, -den.y * dn);
+        sh_beta = beta;
+      }
+    }
+    __syncthreads();
+    const double2 tau = sh_tau;
+    if (tid == 0) {
+      d[j] = A[j * ld + j].x;
+      e[j] = sh_beta;
+      tauv[j] = tau;
+    }
+    if (tau.x == 0.0 && tau.y == 0.0) {
+      __syncthreads();
+      continue;
+    }
+    const double2 scal = sh_scal;
+    for (int i = j + 1 + tid; i < n; i += blockDim.x) {
+      const double2 vi = i == j + 1 ? make_double2(1.0, 0.0) : cmul(A[j * ld + i], scal);
+      vv[i] = vi;
+      A[j * ld + i] = vi;  // reflector kept in column j for the back-transformation
+    }
+    __syncthreads();
+    // p = tau A22 v   (row i: sum_l A(i,l) v_l, one warp per row)
+    for (int i = j + 1 + warp; i < n; i += nw) {
+      double re = 0.0, im = 0.0;
+      for (int l = j + 1 + lane; l < n; l += 32) {
+        const double2 a = A[l * ld + i], v = vv[l];
+        re += a.x * v.x - a.y * v.y;
+        im += a.x * v.y + a.y * v.x;
+      }
+      re = warp_sum(re);
+      im = warp_sum(im);
+      if (lane == 0) pw[i] = cmul(tau, make_double2(re, im));
+    }
+    __syncthreads();
+    // alpha2 = -1/2 tau (p^H v);  w = p + alpha2 v
+    double pr = 0.0, pi = 0.0;
+    for (int i = j + 1 + tid; i < n; i += blockDim.x) {
+      const double2 p = pw[i], v = vv[i];
+      pr += p.x * v.x + p.y * v.y;
+      pi += p.x * v.y - p.y * v.x;
+    }
+    pr = block_sum(pr);
+    pi = block_sum(pi);
+    const double2 alpha2 = cscale(cmul(tau, make_double2(pr, pi)), -0.5);
+    for (int i = j + 1 + tid; i < n; i += blockDim.x) pw[i] = cadd(pw[i], cmul(alpha2, vv[i]));
+    __syncthreads();
+    // A22 -= v w^H + w v^H
+    const int m = n - j - 1;
+    for (int t = tid; t < m * m; t += blockDim.x) {
+      const int l = j + 1 + t / m, i = j + 1 + t % m;  // column l, row i (contiguous rows)
+      const double2 vi = vv[i], wi = pw[i], vl = vv[l], wl = pw[l];
+      A[l * ld + i] = csub(A[l * ld + i], cadd(cmulc(wl, vi), cmulc(vl, wi)));
+    }
+    __syncthreads();
+  }
+  if (tid == 0) {
+    d[n - 1] = A[(n - 1) * ld + n - 1].x;
+    e[n - 1] = 0.0;
+  }
+  const long long clk1 = clock64();
+  // ---- 2. implicit QL with Wilkinson shifts on (d, e), Z = I, by warp 0.  All
+  // lanes evaluate the same scalar recurrence (identical values), lane 0 stores
+  // shared scalars, and each lane rotates its own rows of Z.
+  for (int t = tid; t < n * n; t += blockDim.x) V[(t / n) * ld + t % n] = make_double2((t / n) == (t % n) ? 1.0 : 0.0, 0.0);
+  __syncthreads();
+  if (warp == 0) {
+    const double eps = 2.220446049250313e-16;
+    for (int l = 0; l < n; ++l) {
+      int iter = 0;
+      while (true) {
+        int m = l;
+        for (; m < n - 1; ++m) {
+          const double dd = fabs(d[m]) + fabs(d[m + 1]);
+          if (fabs(e[m]) <= eps * dd) break;
+        }
+        if (m == l) break;
+        if (++iter > 60) {
+          if (lane == 0) atomicOr(status, kSmallNoConverge);
+          break;
+        }
+        double g = (d[l + 1] - d[l]) / (2.0 * e[l]);
+        double r = sqrt(g * g + 1.0);
+        g = d[m] - d[l] + e[l] / (g + copysign(r, g));
+        double s = 1.0, c = 1.0, p = 0.0;
+        int i = m - 1;
+        bool underflow = false;
+        for (; i >= l; --i) {
+          const double f = s * e[i], b = c * e[i];
+          r = sqrt(f * f + g * g);
+          __syncwarp();
+          if (lane == 0) e[i + 1] = r;
+          if (r == 0.0) {
+            underflow = true;
+            break;
+          }
+          s = f / r;
+          c = g / r;
+          g = d[i + 1] - p;
+          r = (d[i] - g) * s + 2.0 * c * b;
+          p = s * r;
+          __syncwarp();
+          if (lane == 0) d[i + 1] = g + p;
+          g = c * r - b;
+          for (int k = lane; k < n; k += 32) {  // rotate columns i, i+1 of Z
+            const double zi = V[i * ld + k].x, zi1 = V[(i + 1) * ld + k].x;
+            V[(i + 1) * ld + k].x = s * zi + c * zi1;
+            V[i * ld + k].x = c * zi - s * zi1;
+          }
+        }
+        __syncwarp();
+        if (lane == 0) {
+          if (underflow) {
+            d[i + 1] -= p;
+          } else {
+            d[l] -= p;
+            e[l] = g;
+          }
+          e[m] = 0.0;
+        }
+        __syncwarp();
+      }
+    }
+  }
+  __syncthreads();
+  const long long clk2 = clock64();
+  // ---- 3. back-transformation X = H_0 H_1 ... H_{n-2} Z  (apply H_{n-2} first)
+  for (int j = n - 2; j >= 0; --j) {
+    const double2 tau = tauv[j];
+    if (tau.x == 0.0 && tau.y == 0.0) continue;
+    // t_c = sum_{s > j} conj(v_s) X(s, c)   (one warp per column)
+    for (int c = warp; c < n; c += nw) {
+      double re = 0.0, im = 0.0;
+      for (int s = j + 1 + lane; s < n; s += 32) {
+        const double2 v = A[j * ld + s], x = V[c * ld + s];
+        re += v.x * x.x + v.y * x.y;
+        im += v.x * x.y - v.y * x.x;
+      }
+      re = warp_sum(re);
+      im = warp_sum(im);
+      if (lane == 0) pw[c] = cmul(tau, make_double2(re, im));
+    }
+    __syncthreads();
+    const int m = n - j - 1;
+    for (int t = tid; t < n * m; t += blockDim.x) {
+      const int c = t / m, s = j + 1 + t % m;
+      V[c * ld + s] = csub(V[c * ld + s], cmul(A[j * ld + s], pw[c]));
+    }
+    __syncthreads();
+  }
+  if (tid == 0) {  // diagnostics: stage cycles (kcycles) in status words 8..10
+    const long long clk3 = clock64();
+    atomicAdd(status + 8, static_cast<int>((clk1 - clk0) / 1000));
+    atomicAdd(status + 9, static_cast<int>((clk2 - clk1) / 1000));
+    atomicAdd(status + 10, static_cast<int>((clk3 - clk2) / 1000));
+  }
+  for (int j = tid; j < n; j += blockDim.x) A[j * ld + j] = make_double2(d[j], 0.0);
+  __syncthreads();
+}
+
 // Block-level gram_factors; X, V: n*n complex scratch each (column-major).
 // Outputs (P, R, deficient, any_def) are complete after the trailing barrier.
 __device__ void gram_factors_dev(const double2* G, int n, double2* X, double2* V, double2* P, double2* R,
                                  int* deficient, int* any_def, int* status, double* lam_out = nullptr,
-                                 double2* vec_out = nullptr) {
+                                 double2* vec_out = nullptr, bool use_jacobi = false) {
   __shared__ double lam[256];
   __shared__ int order[256];
   __shared__ double hmax[2];
@@ -304,7 +496,10 @@ __device__ void gram_factors_dev(const double2* G, int n, double2* X, double2* V
   // and the accuracy class of zheevd (|d lambda| ~ n eps ||G||).
   const double neps = static_cast<double>(n) * 2.220446049250313e-16;
   const double abs_skip = neps * sqrt(block_sum(fro));
-  herm_jacobi(X, V, n, ld, neps, abs_skip, 40, status);
+  if (use_jacobi)
+    herm_jacobi(X, V, n, ld, neps, abs_skip, 40, status);
+  else
+    herm_eig_tridiag(X, V, n, ld, status);
   for (int j = threadIdx.x; j < n; j += blockDim.x) lam[j] = X[j * ld + j].x;
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
@@ -346,11 +541,11 @@ __device__ void gram_factors_dev(const double2* G, int n, double2* X, double2* V
 __global__ void __launch_bounds__(kThreads) gram_factors_kernel(const double2* G, int n, double2* P,
                                                                 double2* R, int* deficient,
                                                                 int* any_def, int* status,
-                                                                double2* work, double* lam_out,
+                                                                double2* work, int use_jacobi, double* lam_out,
                                                                 double2* vec_out) {
   extern __shared__ __align__(16) unsigned char sm[];
   double2* X = work ? work : reinterpret_cast<double2*>(sm);  // column-major n x (n+1)
-  gram_factors_dev(G, n, X, X + n * (n + 1), P, R, deficient, any_def, status, lam_out, vec_out);
+  gram_factors_dev(G, n, X, X + n * (n + 1), P, R, deficient, any_def, status, lam_out, vec_out, use_jacobi != 0);
 }
 
 // ------------------------------------------------------------------ Cholesky
@@ -920,9 +1115,13 @@ void gram_factors(const double2* G, int n, double2* P, double2* R, int* deficien
                                     static_cast<int>(kSmemCap)));
     attr = true;
   }
-  const int threads = kThreads;
+  static const int env_threads = getenv("PEPSB_EIG_THREADS") ? atoi(getenv("PEPSB_EIG_THREADS")) : 0;
+  const int threads = env_threads > 0 ? env_threads : kThreads;
+  // PEPSB_EIG=tridiag selects Householder tridiagonalisation + QL (default: two-sided Jacobi)
+  static const int use_jacobi = !(getenv("PEPSB_EIG") && std::string(getenv("PEPSB_EIG")) == "tridiag");
   gram_factors_kernel<<<1, threads, fits ? smem : 0, stream>>>(G, n, P, R, deficient, any_def, status,
-                                                                fits ? nullptr : work, lam_out, vec_out);
+                                                                fits ? nullptr : work, use_jacobi, lam_out,
+                                                                vec_out);
   PEPSB_LAUNCH();
 }
 

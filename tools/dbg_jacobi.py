@@ -17,3 +17,5 @@ for k in (16, 41, 64, 72):
     sw2 = lib().pepsb_ctx_debug_word(ctx.h, 7, 1)
     qq = q.numpy()
     print(k, "small ms", rep["small"]["ms"], "sweeps", sw, "svd sweeps", sw2, "orth err", np.abs(qq.conj().T @ qq - np.eye(k)).max(), flush=True)
+for w in (8, 9, 10):
+    print("stage word", w, lib().pepsb_ctx_debug_word(ctx.h, w, 1), "kcycles (cumulative)")
