@@ -282,13 +282,35 @@ struct TileCfg {
 constexpr TileCfg kCfgs[] = {{64, 64}, {64, 72}, {72, 64}, {72, 72}, {128, 64}};
 
 int choose_cfg(int64_t M, int64_t N) {
+  static const bool cfg4 = getenv("PEPSB_CFG4") != nullptr;
   const bool m72 = M > 64 && M <= 72, n72 = N > 64 && N <= 72;
   if (m72 && n72) return 3;
   if (n72) return 1;
   if (m72) return 2;
-  if (M > 64 && M <= 128 && N >= 4096) return 4;
+  if (cfg4 && M > 64 && M <= 128 && N >= 4096) return 4;
   return 0;
 }
+
+// C^T = B^T A^T: swap the operand roles (and the epilogue's row/column decode)
+// so that a 72-wide side becomes N and the 4-warp 64x72 tile applies.
+void transpose_problem(ZgemmParams& p) {
+  std::swap(p.A, p.B);
+  const int64_t sAi = p.sAi, sAk = p.sAk;
+  p.sAi = p.sBj;
+  p.sAk = p.sBk;
+  p.sBk = sAk;
+  p.sBj = sAi;
+  std::swap(p.conjA, p.conjB);
+  std::swap(p.M, p.N);
+  for (int a = 0; a < 4; ++a) std::swap(p.bsA[a], p.bsB[a]);
+  std::swap(p.nr, p.nc);
+  for (int a = 0; a < kMaxModes; ++a) {
+    std::swap(p.rext[a], p.cext[a]);
+    std::swap(p.rstr[a], p.cstr[a]);
+  }
+}
+
+int ctas_per_sm(int cfg) { return cfg <= 1 ? 2 : 1; }
 
 template <bool AK, bool BNC>
 void launch_any(const ZgemmParams& p, cudaStream_t stream) {
@@ -304,13 +326,15 @@ void launch_any(const ZgemmParams& p, cudaStream_t stream) {
 }  // namespace
 
 int64_t zgemm_plan_splits(ZgemmParams& p, int num_sms) {
+  if (p.M > 64 && p.M <= 72 && p.N > 72) transpose_problem(p);
   p.cfg = choose_cfg(p.M, p.N);
   const int64_t bm = kCfgs[p.cfg].bm, bn = kCfgs[p.cfg].bn;
   const int64_t tiles = ((p.M + bm - 1) / bm) * ((p.N + bn - 1) / bn) * p.batch;
-  const int64_t target = 2LL * num_sms;
+  // one full wave of resident CTAs (no partial second wave)
+  const int64_t target = static_cast<int64_t>(ctas_per_sm(p.cfg)) * num_sms;
   int64_t splits = 1;
   if (tiles < target && p.K > 4 * kBK) {
-    splits = std::min<int64_t>((target + tiles - 1) / tiles, (p.K + 4 * kBK - 1) / (4 * kBK));
+    splits = std::min<int64_t>(std::max<int64_t>(1, target / tiles), (p.K + 4 * kBK - 1) / (4 * kBK));
     splits = std::max<int64_t>(1, std::min<int64_t>(splits, 256));
   }
   int64_t kchunk = (p.K + splits - 1) / splits;
