@@ -1,13 +1,60 @@
 #include "context.h"
 
+#include <chrono>
 #include <cstdint>
+#include <cstdlib>
 
 #include "tensor_ops.cuh"
 
 namespace pepsb {
 
 Buf::~Buf() {
-  if (p && ctx) cudaFreeAsync(p, ctx->stream);
+  if (p && pool) pool->release(p, bytes);
+}
+
+void* Pool::alloc(size_t bytes, size_t* reserved) {
+  // size classes: 512 B granules below 1 MiB, 2 MiB granules above
+  const size_t g = bytes <= (1u << 20) ? 512 : (2u << 20);
+  const size_t want = ((bytes + g - 1) / g) * g;
+  auto it = free_blocks.lower_bound(want);
+  if (it != free_blocks.end() && it->first <= want + want / 4 + g) {
+    void* p = it->second;
+    *reserved = it->first;
+    cached_bytes -= it->first;
+    free_blocks.erase(it);
+    return p;
+  }
+  void* p = nullptr;
+  cudaError_t e = cudaMalloc(&p, want);
+  if (e != cudaSuccess) {  // release the cache and retry once
+    cudaGetLastError();
+    trim();
+    e = cudaMalloc(&p, want);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      throw Error(kResourceError, "device allocation of " + std::to_string(bytes) + " bytes failed: " +
+                                      cudaGetErrorString(e));
+    }
+  }
+  reserved_bytes += want;
+  *reserved = want;
+  return p;
+}
+
+void Pool::release(void* p, size_t bytes) {
+  free_blocks.emplace(bytes, p);
+  cached_bytes += bytes;
+}
+
+void Pool::trim() {
+  if (stream) cudaStreamSynchronize(stream);
+  else cudaDeviceSynchronize();
+  for (auto& [sz, p] : free_blocks) {
+    cudaFree(p);
+    reserved_bytes -= sz;
+  }
+  free_blocks.clear();
+  cached_bytes = 0;
 }
 
 int64_t LTensor::extent_of(char c) const {
@@ -42,14 +89,20 @@ LTensor as_labelled(const DTensor& t, const std::string& labels, bool conj) {
   return l;
 }
 
+HostTimer::HostTimer(double* a) : acc(a), t0(0.0) {
+  if (acc) t0 = std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+HostTimer::~HostTimer() {
+  if (acc) *acc += std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count() - t0;
+}
+
 Ctx::Ctx(int dev) : device(dev) {
+  trace = getenv("PEPSB_TRACE") != nullptr;
   PEPSB_CUDA(cudaSetDevice(dev));
   PEPSB_CUDA(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev));
   PEPSB_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
-  cudaMemPool_t pool;
-  PEPSB_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
-  uint64_t thr = UINT64_MAX;
-  PEPSB_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+  pool = std::make_shared<Pool>();
+  pool->stream = stream;
   PEPSB_CUDA(cudaMalloc(&d_status, 64 * sizeof(int)));
   PEPSB_CUDA(cudaMemset(d_status, 0, 64 * sizeof(int)));
   PEPSB_CUDA(cudaMallocHost(&h_status, 64 * sizeof(int)));
@@ -57,6 +110,8 @@ Ctx::Ctx(int dev) : device(dev) {
 
 Ctx::~Ctx() {
   if (stream) cudaStreamSynchronize(stream);
+  pool->trim();
+  pool->stream = nullptr;  // buffers that outlive the context release into a stream-less pool
   profile_clear();
   for (auto e : event_pool) cudaEventDestroy(e);
   if (d_status) cudaFree(d_status);
@@ -67,14 +122,10 @@ Ctx::~Ctx() {
 BufPtr Ctx::alloc(int64_t n) {
   auto b = std::make_shared<Buf>();
   b->n = n;
-  b->ctx = this;
+  b->pool = pool;
   if (n > 0) {
-    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&b->p), static_cast<size_t>(n) * sizeof(double2), stream);
-    if (e != cudaSuccess) {
-      cudaGetLastError();
-      throw Error(kResourceError, "device allocation of " + std::to_string(n) + " complex elements failed: " +
-                                      cudaGetErrorString(e));
-    }
+    HostTimer ht(trace ? &t_alloc : nullptr);
+    b->p = static_cast<double2*>(pool->alloc(static_cast<size_t>(n) * sizeof(double2), &b->bytes));
   }
   record_intermediate(static_cast<uint64_t>(n));
   return b;
@@ -94,7 +145,10 @@ DTensor Ctx::zeros(const std::vector<int64_t>& shape) {
   return t;
 }
 
-void Ctx::sync() { PEPSB_CUDA(cudaStreamSynchronize(stream)); }
+void Ctx::sync() {
+  HostTimer ht(trace ? &t_sync : nullptr);
+  PEPSB_CUDA(cudaStreamSynchronize(stream));
+}
 
 cudaEvent_t Ctx::take_event() {
   if (!event_pool.empty()) {

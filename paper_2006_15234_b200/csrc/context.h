@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <map>
 #include <memory>
 #include <string>
 #include <vector>
@@ -14,12 +15,35 @@ namespace pepsb {
 
 class Ctx;
 
+// Accumulates host wall time into *acc (no-op when acc is null).
+struct HostTimer {
+  explicit HostTimer(double* acc);
+  ~HostTimer();
+  double* acc;
+  double t0;
+};
+
 // Stream-ordered device buffer (cudaMallocAsync from the device pool; freed
 // with cudaFreeAsync on the context stream when the last reference drops).
+// Caching device allocator.  Every buffer is used on the single context stream,
+// so a freed block can be handed to the next allocation immediately (stream
+// order protects it); cudaMalloc is only called when no cached block fits.
+// Shared by the context and its buffers, so buffers may outlive the context.
+struct Pool {
+  std::multimap<size_t, void*> free_blocks;
+  size_t cached_bytes = 0, reserved_bytes = 0;
+  cudaStream_t stream = nullptr;  // cleared when the owning context goes away
+  void* alloc(size_t bytes, size_t* reserved);
+  void release(void* p, size_t bytes);
+  void trim();  // synchronises, then returns every cached block to the driver
+  ~Pool() { trim(); }
+};
+
 struct Buf {
   double2* p = nullptr;
   int64_t n = 0;
-  Ctx* ctx = nullptr;
+  size_t bytes = 0;  // size class actually reserved
+  std::shared_ptr<Pool> pool;
   ~Buf();
 };
 using BufPtr = std::shared_ptr<Buf>;
@@ -65,6 +89,7 @@ class Ctx {
   Ctx& operator=(const Ctx&) = delete;
 
   BufPtr alloc(int64_t n);  // n complex elements (uninitialised)
+  std::shared_ptr<struct Pool> pool;
   DTensor empty(const std::vector<int64_t>& shape);
   DTensor zeros(const std::vector<int64_t>& shape);
   void sync();
@@ -78,6 +103,9 @@ class Ctx {
   int* h_status = nullptr;  // pinned
   // Launch accounting (for the bench's gpu_launches claim).
   int64_t launches = 0;
+  // Host-side tracing (PEPSB_TRACE): seconds spent in allocation, free and sync.
+  bool trace = false;
+  double t_alloc = 0.0, t_free = 0.0, t_sync = 0.0;
   int64_t faithful_redos = 0;  // CholeskyQR breakdowns redone on the Gram-eigh route
   int64_t tsqr_fallbacks = 0;  // projected SVDs that needed the TSQR R factor
   // Cost counters (reference instr::flops definition: 2 per complex MAC,

@@ -6,6 +6,7 @@
 #include "peps.h"
 
 #include <algorithm>
+#include <cstdio>
 #include <cstring>
 
 #include "tensor_ops.cuh"
@@ -122,6 +123,10 @@ BoundaryD two_layer_apply_row(Ctx& ctx, const BoundaryD& top, const PepsStateD& 
   const auto& ls = lastd.shape;
   out.sites[n - 1] = reshape(lastd, {ls[0] * ls[1], ls[2], ls[3] * ls[4] * ls[5]});
   out.validate();
+  if (ctx.trace) {
+    fprintf(stderr, "[pepsb] row %d: host alloc %.2f ms, free %.2f ms, sync-wait %.2f ms (cumulative)\n", row,
+            ctx.t_alloc * 1e3, ctx.t_free * 1e3, ctx.t_sync * 1e3);
+  }
   return out;
 }
 
