@@ -159,6 +159,13 @@ LTensor orth(Ctx& ctx, const LTensor& Y) {
       gram_factors(G->p, static_cast<int>(k), P->p, R->p, d_def, d_any, ctx.d_status, work ? work->p : nullptr,
                    ctx.stream);
     }
+    if (ctx.trace) {
+      int sw = 0;
+      ctx.sync();
+      PEPSB_CUDA(cudaMemcpy(&sw, ctx.d_status + 7, sizeof(int), cudaMemcpyDeviceToHost));
+      PEPSB_CUDA(cudaMemset(ctx.d_status + 7, 0, sizeof(int)));
+      fprintf(stderr, "[pepsb] orth rows=%ld k=%ld sweeps=%d\n", (long)rows, (long)k, sw);
+    }
     mm(ctx, Q->p, Y.ptr, false, Y.conj, P->p, false, false, rows, k, k);
     {
       ProfScope ps_(ctx, Ctx::kProfSmall);
