@@ -124,6 +124,11 @@ int pepsb_implicit(pepsb_ctx* ctx, int n, pepsb_tensor* const* ts, const char* l
 /* gram_orthogonalize(Tensor, split) (decomposition.hpp:52) */
 int pepsb_gram_orthogonalize(pepsb_ctx* ctx, const pepsb_tensor* a, int split, pepsb_tensor** q, pepsb_tensor** r);
 
+/* eigh(Tensor) (linalg.hpp:41, linalg.cpp:256-295): values descending (capacity cap),
+ * vectors n x n with column j the phase-fixed eigenvector j.  n <= 256.  The
+ * solver is process-wide option "eig_solver" (0 divide and conquer, 1 Jacobi). */
+int pepsb_eigh(pepsb_ctx* ctx, const pepsb_tensor* a, double* values, int64_t cap, pepsb_tensor** vectors);
+
 /* svd(Tensor, split) (linalg.hpp:21-22); s has capacity s_cap, *k = min extent */
 int pepsb_svd(pepsb_ctx* ctx, const pepsb_tensor* a, int split, pepsb_tensor** u, double* s, int64_t s_cap,
               int64_t* k, pepsb_tensor** v);

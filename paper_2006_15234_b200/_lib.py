@@ -66,6 +66,7 @@ _SIGS = {
     "pepsb_implicit": (C.c_int, [_VP, C.c_int, C.POINTER(_VP), C.c_char_p, C.c_char_p, C.c_char_p, _VP, C.c_int,
                                  C.POINTER(_VP)]),
     "pepsb_gram_orthogonalize": (C.c_int, [_VP, _VP, C.c_int, C.POINTER(_VP), C.POINTER(_VP)]),
+    "pepsb_eigh": (C.c_int, [_VP, _VP, C.POINTER(C.c_double), C.c_int64, C.POINTER(_VP)]),
     "pepsb_svd": (C.c_int, [_VP, _VP, C.c_int, C.POINTER(_VP), C.POINTER(C.c_double), C.c_int64,
                             C.POINTER(C.c_int64), C.POINTER(_VP)]),
     "pepsb_randomized_svd": (C.c_int, [_VP, C.c_int, C.POINTER(_VP), C.c_char_p, C.c_char_p, C.c_char_p,

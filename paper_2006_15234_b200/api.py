@@ -295,6 +295,17 @@ def gram_orthogonalize(a, split: int, ctx: Optional[Context] = None):
     return DeviceTensor(q, ctx), DeviceTensor(r, ctx)
 
 
+def eigh(a, ctx: Optional[Context] = None):
+    """linalg.cpp:256-295 — (values descending, vectors with phase-fixed columns)."""
+    ctx = ctx or default_context()
+    d = to_device(a, ctx)
+    n = d.shape[0] if len(d.shape) == 2 else 0
+    w = np.zeros(max(n, 1))
+    v = _VP()
+    check(lib().pepsb_eigh(ctx.h, d.h, w.ctypes.data_as(C.POINTER(C.c_double)), len(w), C.byref(v)))
+    return w[:n].copy(), DeviceTensor(v, ctx)
+
+
 def svd(a, split: int, ctx: Optional[Context] = None):
     """linalg.cpp:193-207 — returns (u, s, v) with phase-fixed u."""
     ctx = ctx or default_context()

@@ -6,6 +6,7 @@
 #include "../../include/peps_b200.h"
 #include "ite.h"
 #include "peps.h"
+#include "smalldense.cuh"
 #include "tensor_ops.cuh"
 
 using namespace pepsb;
@@ -183,6 +184,7 @@ int pepsb_ctx_set_option(pepsb_ctx* c, const char* key, int64_t value) {
     need(c, "ctx");
     std::string k = key ? key : "";
     if (k == "orth_mode") c->ctx->orth_mode = static_cast<int>(value);
+    else if (k == "eig_solver") set_eig_solver(static_cast<int>(value));
     else throw Error(kConfigError, "unknown option '" + k + "'");
   });
 }
@@ -366,6 +368,19 @@ int pepsb_gram_orthogonalize(pepsb_ctx* c, const pepsb_tensor* a, int split, pep
     auto [Q, R] = gram_orthogonalize(*c->ctx, a->t, split);
     *q = wrap(Q);
     *r = wrap(R);
+  });
+}
+
+int pepsb_eigh(pepsb_ctx* c, const pepsb_tensor* a, double* values, int64_t cap, pepsb_tensor** vectors) {
+  return guard([&] {
+    need(c, "ctx");
+    need(a, "tensor");
+    need(values, "values");
+    need(vectors, "vectors");
+    EighD r = eigh(*c->ctx, a->t);
+    if (static_cast<int64_t>(r.values.size()) > cap) throw Error(kValidationError, "eigenvalue buffer too small");
+    std::memcpy(values, r.values.data(), r.values.size() * sizeof(double));
+    *vectors = wrap(r.vectors);
   });
 }
 

@@ -153,7 +153,7 @@ LTensor orth(Ctx& ctx, const LTensor& Y) {
     int* d_def = reinterpret_cast<int*>(def->p);
     int* d_any = d_def + k;
     BufPtr work;
-    if (2 * k * (k + 1) * 16 > 200 * 1024) work = ctx.alloc(2 * k * (k + 1));
+    if (2 * k * (k + 1) * 16 > 176 * 1024) work = ctx.alloc(2 * k * (k + 1));
     {
       ProfScope ps_(ctx, Ctx::kProfSmall);
       gram_factors(G->p, static_cast<int>(k), P->p, R->p, d_def, d_any, ctx.d_status, work ? work->p : nullptr,
@@ -165,6 +165,16 @@ LTensor orth(Ctx& ctx, const LTensor& Y) {
       PEPSB_CUDA(cudaMemcpy(&sw, ctx.d_status + 7, sizeof(int), cudaMemcpyDeviceToHost));
       PEPSB_CUDA(cudaMemset(ctx.d_status + 7, 0, sizeof(int)));
       fprintf(stderr, "[pepsb] orth rows=%ld k=%ld sweeps=%d\n", (long)rows, (long)k, sw);
+      static int dumped = 0;
+      if (sw >= 12 && getenv("PEPSB_DUMP_GRAM") && dumped < 4) {  // developer aid: slow-converging Grams
+        std::vector<double2> h(static_cast<size_t>(k * k));
+        PEPSB_CUDA(cudaMemcpy(h.data(), G->p, h.size() * sizeof(double2), cudaMemcpyDeviceToHost));
+        const std::string fn = std::string(getenv("PEPSB_DUMP_GRAM")) + std::to_string(dumped++) + ".bin";
+        if (FILE* f = fopen(fn.c_str(), "wb")) {
+          fwrite(h.data(), sizeof(double2), h.size(), f);
+          fclose(f);
+        }
+      }
     }
     mm(ctx, Q->p, Y.ptr, false, Y.conj, P->p, false, false, rows, k, k);
     {
@@ -235,7 +245,7 @@ Projected projected_svd(Ctx& ctx, const LTensor& Z, int64_t target) {
     BufPtr P = ctx.alloc(k * k), R = ctx.alloc(k * k), def = ctx.alloc(k / 4 + 2);
     int* d_def = reinterpret_cast<int*>(def->p);
     BufPtr work;
-    if (2 * k * (k + 1) * 16 > 200 * 1024) work = ctx.alloc(2 * k * (k + 1));
+    if (2 * k * (k + 1) * 16 > 176 * 1024) work = ctx.alloc(2 * k * (k + 1));
     {
       ProfScope ps_(ctx, Ctx::kProfSmall);
       gram_factors(G1->p, ki, P->p, R->p, d_def, d_def + k, ctx.d_status, work ? work->p : nullptr, ctx.stream,
@@ -544,7 +554,7 @@ std::pair<DTensor, DTensor> gram_orthogonalize(Ctx& ctx, const DTensor& a, int s
   int* d_def = reinterpret_cast<int*>(def->p);
   int* d_any = d_def + cols;
   BufPtr work;
-  if (2 * cols * (cols + 1) * 16 > 200 * 1024) work = ctx.alloc(2 * cols * (cols + 1));
+  if (2 * cols * (cols + 1) * 16 > 176 * 1024) work = ctx.alloc(2 * cols * (cols + 1));
   DTensor R;
   std::vector<int64_t> rshape = cs;
   rshape.insert(rshape.end(), cs.begin(), cs.end());
@@ -570,6 +580,30 @@ std::pair<DTensor, DTensor> gram_orthogonalize(Ctx& ctx, const DTensor& a, int s
   ctx.sync();
   raise_status(*ctx.h_status, true);
   return {Q, R};
+}
+
+EighD eigh(Ctx& ctx, const DTensor& m) {
+  if (m.shape.size() != 2 || m.shape[0] != m.shape[1]) throw Error(kShapeError, "eigh expects a square matrix");
+  const int64_t n = m.shape[0];
+  if (n > 256) throw Error(kShapeError, "eigh: n > 256 not supported");
+  EighD out;
+  out.vectors = ctx.empty({n, n});
+  if (n == 0) return out;
+  clear_status(ctx);
+  BufPtr w = ctx.alloc(n / 2 + 1), work;
+  if (2 * n * (n + 1) * 16 > 176 * 1024) work = ctx.alloc(2 * n * (n + 1));
+  {
+    ProfScope ps_(ctx, Ctx::kProfSmall);
+    eigh_dense(m.data(), static_cast<int>(n), reinterpret_cast<double*>(w->p), out.vectors.data(), ctx.d_status,
+               work ? work->p : nullptr, ctx.stream);
+  }
+  ++ctx.launches;
+  out.values.resize(n);
+  PEPSB_CUDA(cudaMemcpyAsync(out.values.data(), w->p, n * sizeof(double), cudaMemcpyDeviceToHost, ctx.stream));
+  read_status(ctx);
+  ctx.sync();
+  raise_status(*ctx.h_status, false);
+  return out;
 }
 
 SvdD svd(Ctx& ctx, const DTensor& t, int split) {

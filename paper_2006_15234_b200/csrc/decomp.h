@@ -64,6 +64,11 @@ struct EinsumsvdResultD {
   bool rank_clamped = false;
 };
 
+struct EighD {
+  std::vector<double> values;  // descending
+  DTensor vectors;             // n x n, column j = phase-fixed eigenvector j
+};
+
 struct SvdD {
   DTensor u, v;
   std::vector<double> s;
@@ -77,6 +82,8 @@ SvdTripleD randomized_svd(Ctx& ctx, const ImplicitOp& op, const Trunc& policy, c
 // `t1_perm` (optional) permutes t1's axes on output, like Tensor::permute.
 EinsumsvdResultD einsumsvd(Ctx& ctx, const ImplicitOp& op, const Trunc& policy, int strategy,
                            int absorb, const Rsvd& cfg, const std::vector<int>& t1_perm = {});
+// linalg.cpp:256-295 (Hermitian eigendecomposition of a square matrix, n <= 256)
+EighD eigh(Ctx& ctx, const DTensor& m);
 // linalg.cpp:193-207 (thin SVD of a matricised tensor; small matrices)
 SvdD svd(Ctx& ctx, const DTensor& t, int split);
 

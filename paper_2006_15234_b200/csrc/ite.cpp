@@ -128,7 +128,7 @@ PepsStateD apply_two_site_batch(Ctx& ctx, const PepsStateD& s, const DTensor& ga
       if (D.reduced) smem_reduce = std::max<size_t>(smem_reduce, (E * S + 5 * S * S + 2 * S) * 16 + S * 4 + 64);
       else smem_reduce = std::max<size_t>(smem_reduce, E * S * 16);
     }
-  if (smem_reduce > 200 * 1024) throw Error(kShapeError, "simple update: site too large for the batched kernel");
+  if (smem_reduce > 176 * 1024)  // + the eigensolver's static shared memory throw Error(kShapeError, "simple update: site too large for the batched kernel");
   if (sd[0].s != sd[1].s) throw Error(kShapeError, "shared bond mismatch");
 
   // ---- exact einsumsvd of {g, Ra, Rb} (state.cpp:186-194)

@@ -4,6 +4,7 @@
 // each runs in one thread block with the matrix in shared memory, one warp
 // per Jacobi rotation pair (round-robin ordering, all pairs of a round
 // disjoint, one __syncthreads per round).
+#include <atomic>
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
@@ -152,8 +153,12 @@ __device__ double2 column_phase(const double2* colp, int rows) {
 // V (column-major) holds the eigenvectors.  Each round applies n/2 disjoint
 // rotations A <- J^H A J with one thread per 2x2 block of (pair_i, pair_j)
 // coordinates, so a round costs two barriers and no reductions.
-__device__ void herm_jacobi(double2* A, double2* V, int n, int ld, double tol, double abs_skip, int max_sweeps,
-                            int* status) {
+// Pairs whose diagonal entries are both below low_skip are not rotated: at
+// termination they form a block whose eigenvalues are bounded by its trace, which
+// the caller sizes below its deficiency cut, so only the (discarded) basis of
+// that numerically-null block is left unresolved (0 disables).
+__device__ void herm_jacobi(double2* A, double2* V, int n, int ld, double tol, double abs_skip, double low_skip,
+                            int max_sweeps, int* status) {
   __shared__ double jc[128], js[128];
   __shared__ double2 je[128];
   __shared__ int jp[128], jq[128];
@@ -183,7 +188,8 @@ __device__ void herm_jacobi(double2* A, double2* V, int n, int ld, double tol, d
           const double2 apq = A[q * ld + p];
           const double ag2 = apq.x * apq.x + apq.y * apq.y;
           const double app = A[p * ld + p].x, aqq = A[q * ld + q].x;
-          if (ag2 > tol2 * fabs(app * aqq) && ag2 > skip2) {
+          if (ag2 > tol2 * fabs(app * aqq) && ag2 > skip2 &&
+              (low_skip <= 0.0 || app >= low_skip || aqq >= low_skip)) {
             const double rag = rsqrt(ag2);  // 1 / |a_pq|
             const double tau = 0.5 * (aqq - app) * rag;
             const double t = copysign(1.0, tau) / (fabs(tau) + sqrt(fma(tau, tau, 1.0)));
@@ -270,193 +276,566 @@ __device__ void herm_jacobi(double2* A, double2* V, int n, int ld, double tol, d
   if (threadIdx.x == 0) atomicAdd(status + 7, sweep + 1);  // diagnostics: total sweeps
 }
 
-// Hermitian eigensolver for one thread block: Householder tridiagonalisation
-// (the zhetd2 recurrence: A <- H^H A H with H = I - tau v v^H, rank-2 updates),
-// implicit QL with Wilkinson shifts on the real tridiagonal run by ONE warp
-// (every lane evaluates the scalar Givens chain redundantly and rotates its own
-// rows of Z, so the chain needs no barriers), and back-transformation X = Q Z.
-// A (column-major, ld) is destroyed; on return its diagonal holds the
-// eigenvalues (unsorted) and V (column-major, ld) the eigenvectors.
-// Backward stable like zheevd; O(n) barriers instead of Jacobi's O(n * sweeps).
-__device__ void herm_eig_tridiag(double2* A, double2* V, int n, int ld, int* status) {
-  __shared__ double d[128], e[128];
-  __shared__ double2 vv[128], pw[128], tauv[128];
-  __shared__ double2 sh_tau, sh_scal;
-  __shared__ double sh_beta;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
-  const long long clk0 = clock64();
-  // ---- 1. tridiagonalisation, j = 0 .. n-2 (reflector H_j acts on rows/cols j+1..n-1)
-  for (int j = 0; j + 1 < n; ++j) {
-    double part = 0.0;
-    for (int i = j + 2 + tid; i < n; i += blockDim.x) part += cnorm2(A[j * ld + i]);
-    const double xnorm2 = block_sum(part);
-    if (tid == 0) {
-      const double2 alpha = A[j * ld + j + 1];
-      if (xnorm2 == 0.0 && alpha.y == 0.0) {
-        sh_tau = make_double2(0.0, 0.0);
-        sh_beta = alpha.x;
-      } else {
-        const double beta = -copysign(sqrt(alpha.x * alpha.x + alpha.y * alpha.y + xnorm2), alpha.x);
-        sh_tau = make_double2((beta - alpha.x) / beta, -alpha.y / beta);
-        const double2 den = make_double2(alpha.x - beta, alpha.y);  // scal = 1 / (alpha - beta)
-        const double dn = 1.0 / cnorm2(den);
-        sh_scal = make_double2(den.x * dn, -den.y * dn);
-        sh_beta = beta;
+// ------------------------------------------------------------------ tridiagonal divide and conquer
+// Real symmetric tridiagonal eigenproblem (d, e; e[i] couples i and i+1) by
+// Cuppen's divide and conquer with Gu-Eisenstat eigenvectors, the algorithm of
+// LAPACK dstedc/dlaed0-4 restated for one thread block: every split point m
+// removes |e[m-1]| from d[m-1] and d[m] up front, leaves are 1x1, and each merge
+// of two solved halves is the rank-one problem D + rho z z^T:
+//   deflation (|rho z_i| <= tol, or Givens-merged nearby poles), the secular
+//   equation solved per root by a safeguarded two-pole rational model around
+//   the nearer pole (all differences d_i - lambda_j formed as (d_i - sigma) - tau,
+//   which is what keeps the vectors orthogonal), z recomputed from the roots
+//   (Loewner), vectors z_i / (d_i - lambda_j), and the block of Z updated by
+//   one small GEMM.
+// Subtrees of <= 32 rows are merged by a single warp (all of them
+// concurrently), larger merges by the whole block.  Z lives in V[c*ld + r].x;
+// V[.].y is scratch for the merge vectors and is zeroed on exit.
+struct DcScratch {
+  double *zb, *dk, *zk, *zh, *sig, *tau, *rc, *rs;
+  int *ndx, *perm, *ra, *rb, *meta;
+  int* prof;  // diagnostics: per-phase kcycles (status words 12..)
+};
+
+
+// 1/x to full double precision: MUFU seed + two Newton steps (~6 pipelined
+// instructions instead of the IEEE division's slow path).  x normal, nonzero.
+__device__ __forceinline__ double fast_rcp(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
+
+// Sum / product over the T-lane segment (T a power of two, segment-aligned).
+__device__ __forceinline__ double seg_sum(double v, int T, unsigned mask) {
+  for (int o = T >> 1; o > 0; o >>= 1) v += __shfl_xor_sync(mask, v, o);
+  return v;
+}
+__device__ __forceinline__ double seg_prod(double v, int T, unsigned mask) {
+  for (int o = T >> 1; o > 0; o >>= 1) v *= __shfl_xor_sync(mask, v, o);
+  return v;
+}
+
+// Root j (ascending) of 1/rho + sum_i zk_i^2 / (dk_i - lambda) = 0, returned as
+// lambda = sigma + tau with sigma a pole.  Warp-synchronous: all 32 lanes call
+// it together (valid == false for padding lanes); the T lanes of a segment
+// split the sums over i (lane `sub` takes i = sub, sub + T, ...) and run the
+// scalar iteration redundantly; the iteration count is uniform over the warp
+// (until every segment has converged), so the full-mask shuffles never see a
+// diverged warp.
+__device__ void dc_secular_root(bool valid, int j, int K, const double* dk, const double* zk, double rho, int sub,
+                                int T, double* sig_out, double* tau_out, int* prof) {
+  const unsigned full = 0xffffffffu;
+  const double eps = 2.220446049250313e-16;
+  if (!valid) {  // padding lane: harmless in-range values, converged from the start
+    j = 0;
+    K = 2;
+    rho = 1.0;
+  }
+  const double irho = 1.0 / rho;
+  double sig, lo_t, hi_t;
+  int pl, pr;
+  if (j < K - 1) {
+    const double gap = dk[j + 1] - dk[j], mid = 0.5 * gap;
+    double f = 0.0;
+    if (valid)
+#pragma unroll 4
+      for (int i = sub; i < K; i += T) f += zk[i] * zk[i] * fast_rcp((dk[i] - dk[j]) - mid);
+    f = irho + seg_sum(f, T, full);
+    if (f >= 0.0) {  // root in (d_j, d_j + gap/2]: origin d_j
+      sig = dk[j];
+      lo_t = 0.0;
+      hi_t = mid;
+    } else {  // root in (d_j + gap/2, d_j+1): origin d_j+1
+      sig = dk[j + 1];
+      lo_t = -mid;
+      hi_t = 0.0;
+    }
+    pl = j;
+    pr = j + 1;
+  } else {
+    double zz = 0.0;
+    if (valid)
+      for (int i = sub; i < K; i += T) zz += zk[i] * zk[i];
+    zz = seg_sum(zz, T, full);
+    sig = dk[K - 1];
+    lo_t = 0.0;
+    hi_t = rho * zz;
+    pl = K - 2;
+    pr = K - 1;
+  }
+  double tau = 0.5 * (lo_t + hi_t);
+  bool done = !valid || K == 1;
+  if (valid && K == 1) {
+    sig = dk[0];
+    tau = rho * zk[0] * zk[0];
+  }
+  const int i1 = pl + 1 + ((sub - (pl + 1)) % T + T) % T;  // first i > pl in this lane's stride
+  for (int it = 0; it < 100; ++it) {
+    if (!__any_sync(full, !done)) break;
+    double psi = 0.0, dpsi = 0.0, phi = 0.0, dphi = 0.0;
+    if (!done) {
+#pragma unroll 4
+      for (int i = sub; i <= pl; i += T) {
+        const double inv = fast_rcp((dk[i] - sig) - tau);
+        const double t = zk[i] * zk[i] * inv;
+        psi += t;
+        dpsi += t * inv;
+      }
+#pragma unroll 4
+      for (int i = i1; i < K; i += T) {
+        const double inv = fast_rcp((dk[i] - sig) - tau);
+        const double t = zk[i] * zk[i] * inv;
+        phi += t;
+        dphi += t * inv;
       }
     }
-    __syncthreads();
-    const double2 tau = sh_tau;
-    if (tid == 0) {
-      d[j] = A[j * ld + j].x;
-      e[j] = sh_beta;
-      tauv[j] = tau;
-    }
-    if (tau.x == 0.0 && tau.y == 0.0) {
-      __syncthreads();
+    psi = seg_sum(psi, T, full);
+    dpsi = seg_sum(dpsi, T, full);
+    phi = seg_sum(phi, T, full);
+    dphi = seg_sum(dphi, T, full);
+    if (done) continue;
+    if (sub == 0) atomicAdd(prof, 1);
+    const double f = irho + psi + phi;
+    if (f < 0.0) lo_t = tau;
+    else hi_t = tau;
+    if (f == 0.0 || fabs(f) <= 8.0 * eps * K * (irho + fabs(psi) + fabs(phi)) ||
+        hi_t - lo_t <= 2.0 * eps * fmax(fabs(lo_t), fabs(hi_t))) {
+      done = true;
       continue;
     }
-    const double2 scal = sh_scal;
-    for (int i = j + 1 + tid; i < n; i += blockDim.x) {
-      const double2 vi = i == j + 1 ? make_double2(1.0, 0.0) : cmul(A[j * ld + i], scal);
-      vv[i] = vi;
-      A[j * ld + i] = vi;  // reflector kept in column j for the back-transformation
-    }
-    __syncthreads();
-    // p = tau A22 v   (row i: sum_l A(i,l) v_l, one warp per row)
-    for (int i = j + 1 + warp; i < n; i += nw) {
-      double re = 0.0, im = 0.0;
-      for (int l = j + 1 + lane; l < n; l += 32) {
-        const double2 a = A[l * ld + i], v = vv[l];
-        re += a.x * v.x - a.y * v.y;
-        im += a.x * v.y + a.y * v.x;
+    const double lo_e = lo_t - tau, hi_e = hi_t - tau;
+    double eta = 0.5 * (lo_e + hi_e);  // bisection unless the model step lands inside
+    if (it < 40) {
+      // f(lambda + eta) ~ c + B / (Dl - eta) + D / (Dr - eta):  c eta^2 - a eta + b = 0
+      const double Dl = (dk[pl] - sig) - tau, Dr = (dk[pr] - sig) - tau;
+      const double B = Dl * Dl * dpsi, D = Dr * Dr * dphi;
+      const double c = f - Dl * dpsi - Dr * dphi;
+      const double a = c * (Dl + Dr) + B + D, b = Dl * Dr * f;
+      if (c == 0.0) {
+        if (a != 0.0) {
+          const double r = b / a;
+          if (r > lo_e && r < hi_e) eta = r;
+        }
+      } else {
+        const double disc = fmax(a * a - 4.0 * b * c, 0.0);
+        const double q = 0.5 * (a + copysign(sqrt(disc), a));
+        const double r1 = q / c, r2 = q != 0.0 ? b / q : 0.0;
+        if (r1 > lo_e && r1 < hi_e) eta = r1;
+        else if (r2 > lo_e && r2 < hi_e) eta = r2;
       }
-      re = warp_sum(re);
-      im = warp_sum(im);
-      if (lane == 0) pw[i] = cmul(tau, make_double2(re, im));
     }
-    __syncthreads();
-    // alpha2 = -1/2 tau (p^H v);  w = p + alpha2 v
-    double pr = 0.0, pi = 0.0;
-    for (int i = j + 1 + tid; i < n; i += blockDim.x) {
-      const double2 p = pw[i], v = vv[i];
-      pr += p.x * v.x + p.y * v.y;
-      pi += p.x * v.y - p.y * v.x;
+    const double tn = tau + eta;
+    if (tn == tau) done = true;
+    tau = tn;
+  }
+  if (valid && sub == 0) {
+    atomicAdd(prof + 1, 1);
+    *sig_out = sig;
+    *tau_out = tau;
+  }
+}
+
+// One merge of the two solved halves of node [lo, lo + N) (split at n1) by a
+// group of G threads (thread gt of the group; active == false: a padding
+// group).  Every group of one tree level runs in lock step -- all block
+// barriers are executed by every thread the same number of times.
+// Z(r, c) lives in V[c*ld + r].x; V[.].y of the node's diagonal block holds the
+// merge vectors; the GEMM result is staged in the free upper triangle of A.
+__device__ void dc_merge(bool active, int lo, int n1, int N, int gt, int G, double* d, const double* e, double2* V,
+                         double2* A, int ld, const DcScratch& S) {
+  const int lane = threadIdx.x & 31;
+  const double eps = 2.220446049250313e-16;
+  const double beta = active ? e[lo + n1 - 1] : 0.0;
+  const double rho = 2.0 * fabs(beta);
+  const double sg = beta >= 0.0 ? 1.0 : -1.0;
+  long long tk = clock64();
+  auto mark = [&](int w) {
+    if (threadIdx.x == 0) {
+      const long long t2 = clock64();
+      atomicAdd(S.prof + w, static_cast<int>((t2 - tk) / 100));
+      tk = t2;
     }
-    pr = block_sum(pr);
-    pi = block_sum(pi);
-    const double2 alpha2 = cscale(cmul(tau, make_double2(pr, pi)), -0.5);
-    for (int i = j + 1 + tid; i < n; i += blockDim.x) pw[i] = cadd(pw[i], cmul(alpha2, vv[i]));
-    __syncthreads();
-    // A22 -= v w^H + w v^H
+  };
+  // z = Q^T (e_last(T1) + sg e_first(T2)) / sqrt(2); ascending order of d
+  if (active)
+    for (int c = gt; c < N; c += G) {
+      const int col = lo + c;
+      S.zb[col] = (c < n1 ? V[col * ld + lo + n1 - 1].x : sg * V[col * ld + lo + n1].x) * 0.70710678118654752440;
+      const double dc = d[col];
+      int r = 0;
+      for (int c2 = 0; c2 < N; ++c2) {
+        const double d2 = d[lo + c2];
+        r += (d2 < dc) || (d2 == dc && c2 < c);
+      }
+      S.perm[lo + r] = col;
+    }
+  __syncthreads();
+  // deflation (sequential, dlaed2's rules)
+  if (active && gt == 0) {
+    double dmax = 0.0;
+    for (int c = 0; c < N; ++c) dmax = fmax(dmax, fabs(d[lo + c]));
+    const double tol = 8.0 * eps * fmax(dmax, rho);
+    int K = 0, nrot = 0, prev = -1;
+    for (int q = 0; q < N; ++q) {
+      const int c = S.perm[lo + q];
+      const double zc = S.zb[c];
+      if (rho * fabs(zc) <= tol) continue;  // eigenpair (d_c, column c) deflates
+      if (prev < 0) {
+        prev = c;
+        continue;
+      }
+      const double zp = S.zb[prev];
+      const double dp = d[prev], dcv = d[c];
+      // |(d_c - d_p) a b| <= tol with a b = -z_c z_p / (z_p^2 + z_c^2), division-free
+      if (fabs((dcv - dp) * zc * zp) <= tol * (zp * zp + zc * zc)) {  // nearby poles: rotate z_prev into z_c
+        const double t = hypot(zp, zc);
+        const double a = zc / t, b = -zp / t;
+        S.ra[lo + nrot] = prev;
+        S.rb[lo + nrot] = c;
+        S.rc[lo + nrot] = a;
+        S.rs[lo + nrot] = b;
+        ++nrot;
+        S.zb[c] = t;
+        S.zb[prev] = 0.0;
+        d[prev] = a * a * dp + b * b * dcv;
+        d[c] = b * b * dp + a * a * dcv;
+      } else {
+        S.ndx[lo + K++] = prev;
+      }
+      prev = c;
+    }
+    if (prev >= 0) S.ndx[lo + K++] = prev;
+    S.meta[2 * lo] = K;
+    S.meta[2 * lo + 1] = nrot;
+  }
+  __syncthreads();
+  const int K = active ? S.meta[2 * lo] : 0, nrot = active ? S.meta[2 * lo + 1] : 0;
+  for (int r = lo + gt; r < lo + N && nrot > 0; r += G)
+    for (int t = 0; t < nrot; ++t) {  // Q <- Q R^T, rotations in order
+      const int pa = S.ra[lo + t], pb = S.rb[lo + t];
+      const double a = S.rc[lo + t], b = S.rs[lo + t];
+      const double xp = V[pa * ld + r].x, xc = V[pb * ld + r].x;
+      V[pa * ld + r].x = a * xp + b * xc;
+      V[pb * ld + r].x = a * xc - b * xp;
+    }
+  for (int i = gt; i < K; i += G) {
+    const int c = S.ndx[lo + i];
+    S.dk[lo + i] = d[c];
+    S.zk[lo + i] = S.zb[c];
+  }
+  __syncthreads();
+  mark(0);
+  // T lanes per root / per vector: the largest power of two with 2 T K <= G
+  int T = 1;
+  while (T < 32 && T < G && 2 * T * K <= G) T <<= 1;
+  T = __reduce_min_sync(0xffffffffu, T);  // warp-uniform: groups sharing a warp run the same shuffles
+  const int sub = lane & (T - 1), seg = gt / T, nseg = G / T;
+  const unsigned mask = 0xffffffffu;  // every loop below has a warp-uniform trip count
+  const double* dk = S.dk + lo;
+  const double* zk = S.zk + lo;
+  const int nq = __reduce_max_sync(mask, K > seg ? (K - seg + nseg - 1) / nseg : 0);
+  for (int q = 0; q < nq; ++q) {
+    const int j = seg + q * nseg;
+    dc_secular_root(j < K, j, K, dk, zk, rho, sub, T, S.sig + lo + j, S.tau + lo + j, S.prof + 12);
+  }
+  __syncthreads();
+  mark(1);
+  const double* sg_ = S.sig + lo;
+  const double* tu_ = S.tau + lo;
+  // z recomputed from the roots: zh_i^2 = prod_j (lambda_j - d_i) / (rho prod_{j != i} (d_j - d_i))
+  for (int q = 0; q < nq; ++q) {
+    const int i = seg + q * nseg;
+    double w = 1.0;
+    if (i < K) {
+      const double di = dk[i];
+#pragma unroll 4
+      for (int j = sub; j < K; j += T)
+        w *= -((di - sg_[j]) - tu_[j]) * (j == i ? 1.0 / rho : fast_rcp(dk[j] - di));
+    }
+    w = seg_prod(w, T, mask);
+    if (i < K && sub == 0) S.zh[lo + i] = copysign(sqrt(fmax(w, 0.0)), zk[i]);
+  }
+  __syncthreads();
+  // merge vectors v_j[i] = zh_i / (d_i - lambda_j), normalised; stored W^T in V.y:
+  // v_j[i] at V[(lo + i) * ld + lo + j].y
+  const double* zh = S.zh + lo;
+  for (int q = 0; q < nq; ++q) {
+    const int j = seg + q * nseg;
+    double nrm = 0.0;
+    if (j < K)
+#pragma unroll 4
+      for (int i = sub; i < K; i += T) {
+        const double v = zh[i] * fast_rcp((dk[i] - sg_[j]) - tu_[j]);
+        V[(lo + i) * ld + lo + j].y = v;
+        nrm += v * v;
+      }
+    const double inv = rsqrt(seg_sum(nrm, T, mask));
+    if (j < K)
+      for (int i = sub; i < K; i += T) V[(lo + i) * ld + lo + j].y *= inv;
+  }
+  __syncthreads();
+  mark(2);
+  for (int j = gt; j < K; j += G) d[S.ndx[lo + j]] = sg_[j] + tu_[j];
+  // Zt(r, ndx[j]) = sum_i Z(r, ndx[i]) v_j[i] staged in A's upper triangle
+  // (local (r, c): r <= c at A(lo + r, lo + c).x, r > c at A(lo + c, lo + r).y),
+  // then copied back over Z.
+  const int* ndx = S.ndx + lo;
+  for (int o = gt; o < N * K; o += G) {
+    const int r = o / K, j = o % K;
+    double acc = 0.0;
+#pragma unroll 4
+    for (int i = 0; i < K; ++i) acc += V[ndx[i] * ld + lo + r].x * V[(lo + i) * ld + lo + j].y;
+    const int c = ndx[j] - lo;
+    if (r <= c) A[(lo + c) * ld + lo + r].x = acc;
+    else A[(lo + r) * ld + lo + c].y = acc;
+  }
+  __syncthreads();
+  for (int o = gt; o < N * K; o += G) {
+    const int r = o / K, c = ndx[o % K] - lo;
+    V[(lo + c) * ld + lo + r].x = r <= c ? A[(lo + c) * ld + lo + r].x : A[(lo + r) * ld + lo + c].y;
+  }
+  __syncthreads();
+  mark(3);
+}
+
+// d, e in shared memory; V column-major (ld); A: the tridiagonalised matrix
+// (only its upper triangle is used, as staging).  On return d holds the
+// eigenvalues (unsorted) and V[c*ld + r] = (Z(r, c), 0).
+__device__ void tridiag_dc(double* d, double* e, double2* V, double2* A, int n, int ld, const DcScratch& S) {
+  // Merge schedule: internal nodes grouped by depth; the nodes of one depth
+  // are merged concurrently (block split into equal power-of-two groups),
+  // deepest first.
+  __shared__ short2 nodes[256];  // (lo, N), depth-major
+  __shared__ int dstart[17];
+  __shared__ int ndepth;
+  const int tid = threadIdx.x;
+  for (int t = tid; t < n * n; t += blockDim.x)
+    V[(t / n) * ld + t % n] = make_double2((t / n) == (t % n) ? 1.0 : 0.0, 0.0);
+  if (tid == 0) {
+    for (int m = 1; m < n; ++m) {  // Cuppen's rank-one tear at every split point
+      const double r = fabs(e[m - 1]);
+      d[m - 1] -= r;
+      d[m] -= r;
+    }
+    // breadth-first over the halving tree: depth t occupies nodes[dstart[t] .. dstart[t+1])
+    int cnt = 0, nd = 0;
+    if (n >= 2) nodes[cnt++] = make_short2(0, static_cast<short>(n));
+    int b = 0;
+    while (b < cnt) {
+      dstart[nd++] = b;
+      const int e_ = cnt;
+      for (int q = b; q < e_; ++q) {
+        const short2 x = nodes[q];
+        const short h = static_cast<short>(x.y / 2);
+        if (h >= 2) nodes[cnt++] = make_short2(x.x, h);
+        if (x.y - h >= 2) nodes[cnt++] = make_short2(static_cast<short>(x.x + h), static_cast<short>(x.y - h));
+      }
+      b = e_;
+    }
+    dstart[nd] = cnt;
+    ndepth = nd;
+  }
+  __syncthreads();
+  for (int t = ndepth - 1; t >= 0; --t) {
+    const int first = dstart[t], m = dstart[t + 1] - first;
+    int G = 1;
+    while (2 * G * m <= static_cast<int>(blockDim.x)) G <<= 1;
+    const int g = tid / G;
+    const bool active = g < m;
+    const short2 x = active ? nodes[first + g] : make_short2(0, 2);
+    dc_merge(active, x.x, x.y / 2, x.y, tid % G, G, d, e, V, A, ld, S);
+  }
+  for (int t = tid; t < n * n; t += blockDim.x) V[(t / n) * ld + t % n].y = 0.0;
+  __syncthreads();
+}
+
+// Hermitian eigensolver for one thread block: Householder tridiagonalisation
+// (the zhetd2 recurrence: A <- H^H A H with H = I - tau v v^H, rank-2 updates),
+// divide and conquer on the real tridiagonal (tridiag_dc), and
+// back-transformation X = Q Z.  A (column-major, ld) is destroyed; on return its
+// diagonal holds the eigenvalues (unsorted) and V (column-major, ld) the
+// eigenvectors.  Backward stable like zheevd; O(n) barriers instead of Jacobi's
+// O(n * sweeps).  n <= 256.
+//  * tridiagonalisation: warp 0 forms each reflector (no block reductions), the
+//    matvec p = tau A22 v is split over row x column-chunk threads, 4 barriers
+//    per column;
+//  * back-transformation: columns of X are independent, so each column is owned
+//    by an 8-lane group that applies H_{n-2} .. H_0 with shuffle reductions and
+//    no block barriers at all.
+__device__ void herm_eig_tridiag(double2* A, double2* V, int n, int ld, int* status) {
+  constexpr int kChunks = 4;
+  __shared__ double d[256], e[256];
+  __shared__ double2 vv[256], pw[256], tauv[256];
+  // matvec partials (tridiagonalisation), then divide-and-conquer scratch
+  __shared__ double2 scratch[kChunks * 256];
+  double2(*part)[256] = reinterpret_cast<double2(*)[256]>(scratch);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nthr = blockDim.x;
+  const long long clk0 = clock64();
+  // ---- 1. tridiagonalisation, j = 0 .. n-2 (reflector H_j acts on rows/cols j+1..n-1).
+  // Two barriers per column: the rank-2 update of step j-1 (v, w in vv / pw) is
+  // applied lazily inside step j's matvec (each thread updates the elements it
+  // multiplies), while warp 0 forms the updated column x = A(j+1:, j) on the fly;
+  // then warp 0 turns (x, A x) into the reflector v = scal (x - beta e1) and
+  // w = p + alpha2 v with p = tau A v = tau scal (A x - beta A(:, j+1)).
+  for (int j = 0; j + 1 < n; ++j) {
     const int m = n - j - 1;
-    for (int t = tid; t < m * m; t += blockDim.x) {
-      const int l = j + 1 + t / m, i = j + 1 + t % m;  // column l, row i (contiguous rows)
-      const double2 vi = vv[i], wi = pw[i], vl = vv[l], wl = pw[l];
-      A[l * ld + i] = csub(A[l * ld + i], cadd(cmulc(wl, vi), cmulc(vl, wi)));
+    const bool pend = j > 0 && (tauv[j - 1].x != 0.0 || tauv[j - 1].y != 0.0);
+    double2* xs = part[kChunks - 1];  // the updated column x (warp 0's, phase A -> B)
+    double xn = 0.0;
+    double2 alpha = make_double2(0.0, 0.0);
+    const int nch = 1;
+    if (warp == 0) {
+      const double2 vj = pend ? vv[j] : make_double2(0.0, 0.0), wj = pend ? pw[j] : make_double2(0.0, 0.0);
+      for (int l = j + 1 + lane; l < n; l += 32) {
+        double2 x = A[j * ld + l];
+        if (pend) x = csub(x, cadd(cmulc(wj, vv[l]), cmulc(vj, pw[l])));
+        xs[l] = x;
+        if (l >= j + 2) xn += cnorm2(x);
+        if (l == j + 1) alpha = x;
+      }
+      xn = warp_sum(xn);
+      alpha = make_double2(__shfl_sync(0xffffffffu, alpha.x, 0), __shfl_sync(0xffffffffu, alpha.y, 0));
+      if (lane == 0) d[j] = A[j * ld + j].x - (pend ? 2.0 * (vj.x * wj.x + vj.y * wj.y) : 0.0);
+    } else {
+      // rows i >= j+1 (8 lanes per row, interleaved columns): apply the pending
+      // update, accumulate A x, reduce over the 8 lanes
+      const int t = tid - 32, gl = t & 7;
+      for (int i0 = j + 1; i0 < n; i0 += (nthr - 32) >> 3) {
+        const int i = i0 + (t >> 3);
+        double re0 = 0.0, im0 = 0.0;
+        if (i < n) {
+          const double2 vi = pend ? vv[i] : make_double2(0.0, 0.0), wi = pend ? pw[i] : make_double2(0.0, 0.0);
+          const double2 vj = pend ? vv[j] : make_double2(0.0, 0.0), wj = pend ? pw[j] : make_double2(0.0, 0.0);
+          for (int l = j + 1 + gl; l < n; l += 8) {
+            double2 a = A[l * ld + i], x = A[j * ld + l];
+            if (pend) {
+              const double2 vl = vv[l], wl = pw[l];
+              a = csub(a, cadd(cmulc(wl, vi), cmulc(vl, wi)));
+              A[l * ld + i] = a;
+              x = csub(x, cadd(cmulc(wj, vl), cmulc(vj, wl)));
+            }
+            re0 += a.x * x.x - a.y * x.y;
+            im0 += a.x * x.y + a.y * x.x;
+          }
+        }
+#pragma unroll
+        for (int o = 4; o > 0; o >>= 1) {
+          re0 += __shfl_xor_sync(0xffffffffu, re0, o);
+          im0 += __shfl_xor_sync(0xffffffffu, im0, o);
+        }
+        if (i < n && gl == 0) part[0][i] = make_double2(re0, im0);
+      }
+    }
+    __syncthreads();
+    if (warp == 0) {
+      double2 tau, scal = make_double2(0.0, 0.0);
+      double beta;
+      if (xn == 0.0 && alpha.y == 0.0) {
+        tau = make_double2(0.0, 0.0);
+        beta = alpha.x;
+      } else {
+        beta = -copysign(sqrt(alpha.x * alpha.x + alpha.y * alpha.y + xn), alpha.x);
+        tau = make_double2((beta - alpha.x) / beta, -alpha.y / beta);
+        const double2 den = make_double2(alpha.x - beta, alpha.y);  // scal = 1 / (alpha - beta)
+        const double dn = 1.0 / cnorm2(den);
+        scal = make_double2(den.x * dn, -den.y * dn);
+      }
+      const bool zero = tau.x == 0.0 && tau.y == 0.0;
+      const double2 ts = cmul(tau, scal);
+      double hr = 0.0, hi = 0.0;
+      for (int l = j + 1 + lane; l < n && !zero; l += 32) {
+        {
+          const double2 v = l == j + 1 ? make_double2(1.0, 0.0) : cmul(xs[l], scal);
+          A[j * ld + l] = v;  // reflector kept in column j for the back-transformation
+          vv[l] = v;
+          double2 s = part[0][l];
+          for (int c = 1; c < nch; ++c) s = cadd(s, part[c][l]);
+          const double2 a1 = A[(j + 1) * ld + l];  // updated A(l, j+1)
+          const double2 p = cmul(ts, make_double2(s.x - beta * a1.x, s.y - beta * a1.y));
+          pw[l] = p;
+          hr += p.x * v.x + p.y * v.y;
+          hi += p.x * v.y - p.y * v.x;
+        }
+      }
+      hr = warp_sum(hr);
+      hi = warp_sum(hi);
+      const double2 alpha2 = cscale(cmul(tau, make_double2(hr, hi)), -0.5);
+      for (int l = j + 1 + lane; l < n; l += 32) {
+        {
+          if (zero) {
+            vv[l] = make_double2(0.0, 0.0);
+            pw[l] = make_double2(0.0, 0.0);
+          } else {
+            pw[l] = cadd(pw[l], cmul(alpha2, vv[l]));
+          }
+        }
+      }
+      if (lane == 0) {
+        e[j] = beta;
+        tauv[j] = tau;
+      }
     }
     __syncthreads();
   }
   if (tid == 0) {
-    d[n - 1] = A[(n - 1) * ld + n - 1].x;
+    const bool pend = n >= 2 && (tauv[n - 2].x != 0.0 || tauv[n - 2].y != 0.0);
+    const double2 vl = pend ? vv[n - 1] : make_double2(0.0, 0.0), wl = pend ? pw[n - 1] : make_double2(0.0, 0.0);
+    d[n - 1] = A[(n - 1) * ld + n - 1].x - 2.0 * (vl.x * wl.x + vl.y * wl.y);
     e[n - 1] = 0.0;
   }
+  __syncthreads();
   const long long clk1 = clock64();
-  // ---- 2. implicit QL with Wilkinson shifts on (d, e), Z = I, by warp 0.  All
-  // lanes evaluate the same scalar recurrence (identical values), lane 0 stores
-  // shared scalars, and each lane rotates its own rows of Z.
-  for (int t = tid; t < n * n; t += blockDim.x) V[(t / n) * ld + t % n] = make_double2((t / n) == (t % n) ? 1.0 : 0.0, 0.0);
-  __syncthreads();
-  if (warp == 0) {
-    const double eps = 2.220446049250313e-16;
-    for (int l = 0; l < n; ++l) {
-      int iter = 0;
-      while (true) {
-        int m = l;
-        for (; m < n - 1; ++m) {
-          const double dd = fabs(d[m]) + fabs(d[m + 1]);
-          if (fabs(e[m]) <= eps * dd) break;
-        }
-        if (m == l) break;
-        if (++iter > 60) {
-          if (lane == 0) atomicOr(status, kSmallNoConverge);
-          break;
-        }
-        double g = (d[l + 1] - d[l]) / (2.0 * e[l]);
-        double r = sqrt(g * g + 1.0);
-        g = d[m] - d[l] + e[l] / (g + copysign(r, g));
-        double s = 1.0, c = 1.0, p = 0.0;
-        int i = m - 1;
-        bool underflow = false;
-        for (; i >= l; --i) {
-          const double f = s * e[i], b = c * e[i];
-          r = sqrt(f * f + g * g);
-          __syncwarp();
-          if (lane == 0) e[i + 1] = r;
-          if (r == 0.0) {
-            underflow = true;
-            break;
-          }
-          s = f / r;
-          c = g / r;
-          g = d[i + 1] - p;
-          r = (d[i] - g) * s + 2.0 * c * b;
-          p = s * r;
-          __syncwarp();
-          if (lane == 0) d[i + 1] = g + p;
-          g = c * r - b;
-          for (int k = lane; k < n; k += 32) {  // rotate columns i, i+1 of Z
-            const double zi = V[i * ld + k].x, zi1 = V[(i + 1) * ld + k].x;
-            V[(i + 1) * ld + k].x = s * zi + c * zi1;
-            V[i * ld + k].x = c * zi - s * zi1;
-          }
-        }
-        __syncwarp();
-        if (lane == 0) {
-          if (underflow) {
-            d[i + 1] -= p;
-          } else {
-            d[l] -= p;
-            e[l] = g;
-          }
-          e[m] = 0.0;
-        }
-        __syncwarp();
-      }
-    }
+  // ---- 2. divide and conquer on (d, e): eigenvalues in d, Z in V.x
+  {
+    double* sd = reinterpret_cast<double*>(scratch);  // 8 x 256 doubles
+    int* si = reinterpret_cast<int*>(vv);              // vv: 4 x 256 ints
+    int* sm = reinterpret_cast<int*>(pw);              // pw: 512 ints of per-merge counts
+    const DcScratch S{sd, sd + 256, sd + 512, sd + 768, sd + 1024, sd + 1280, sd + 1536, sd + 1792,
+                      si, si + 256, si + 512, si + 768, sm, status + 12};
+    tridiag_dc(d, e, V, A, n, ld, S);
   }
-  __syncthreads();
   const long long clk2 = clock64();
-  // ---- 3. back-transformation X = H_0 H_1 ... H_{n-2} Z  (apply H_{n-2} first)
-  for (int j = n - 2; j >= 0; --j) {
-    const double2 tau = tauv[j];
-    if (tau.x == 0.0 && tau.y == 0.0) continue;
-    // t_c = sum_{s > j} conj(v_s) X(s, c)   (one warp per column)
-    for (int c = warp; c < n; c += nw) {
-      double re = 0.0, im = 0.0;
-      for (int s = j + 1 + lane; s < n; s += 32) {
-        const double2 v = A[j * ld + s], x = V[c * ld + s];
-        re += v.x * x.x + v.y * x.y;
-        im += v.x * x.y - v.y * x.x;
+  // ---- 3. back-transformation X = H_0 H_1 ... H_{n-2} Z, one 8-lane group per column
+  {
+    const int grp = tid >> 3, gl = tid & 7, ngrp = nthr >> 3;
+    for (int cbase = 0; cbase < n; cbase += ngrp) {
+      const int c = cbase + grp;
+      const bool act = c < n;
+      double2* xc = V + (act ? c : 0) * ld;
+      for (int j = n - 2; j >= 0; --j) {
+        const double2 tau = tauv[j];
+        if (tau.x == 0.0 && tau.y == 0.0) continue;
+        double re = 0.0, im = 0.0;
+        if (act)
+          for (int s = j + 1 + gl; s < n; s += 8) {
+            const double2 v = A[j * ld + s], x = xc[s];
+            re += v.x * x.x + v.y * x.y;
+            im += v.x * x.y - v.y * x.x;
+          }
+#pragma unroll
+        for (int o = 4; o > 0; o >>= 1) {
+          re += __shfl_xor_sync(0xffffffffu, re, o);
+          im += __shfl_xor_sync(0xffffffffu, im, o);
+        }
+        const double2 t = cmul(tau, make_double2(re, im));
+        if (act)
+          for (int s = j + 1 + gl; s < n; s += 8) xc[s] = csub(xc[s], cmul(A[j * ld + s], t));
       }
-      re = warp_sum(re);
-      im = warp_sum(im);
-      if (lane == 0) pw[c] = cmul(tau, make_double2(re, im));
     }
-    __syncthreads();
-    const int m = n - j - 1;
-    for (int t = tid; t < n * m; t += blockDim.x) {
-      const int c = t / m, s = j + 1 + t % m;
-      V[c * ld + s] = csub(V[c * ld + s], cmul(A[j * ld + s], pw[c]));
-    }
-    __syncthreads();
   }
+  __syncthreads();
   if (tid == 0) {  // diagnostics: stage cycles (kcycles) in status words 8..10
     const long long clk3 = clock64();
     atomicAdd(status + 8, static_cast<int>((clk1 - clk0) / 1000));
     atomicAdd(status + 9, static_cast<int>((clk2 - clk1) / 1000));
     atomicAdd(status + 10, static_cast<int>((clk3 - clk2) / 1000));
   }
-  for (int j = tid; j < n; j += blockDim.x) A[j * ld + j] = make_double2(d[j], 0.0);
+  for (int j = tid; j < n; j += nthr) A[j * ld + j] = make_double2(d[j], 0.0);
   __syncthreads();
 }
 
@@ -496,8 +875,19 @@ __device__ void gram_factors_dev(const double2* G, int n, double2* X, double2* V
   // and the accuracy class of zheevd (|d lambda| ~ n eps ||G||).
   const double neps = static_cast<double>(n) * 2.220446049250313e-16;
   const double abs_skip = neps * sqrt(block_sum(fro));
+  // Deficiency cut below is 1e-12 lambda_max >= 1e-12 max_i G_ii: an unresolved
+  // block of pairs with G_pp < 1e-12 max G_ii / n has all eigenvalues under it.
+  // Only when the caller needs just the kept eigenvectors (not vec_out).
+  double dmax = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) dmax = fmax(dmax, X[i * ld + i].x);
+  __shared__ double sh_dmax;
+  if (threadIdx.x == 0) sh_dmax = 0.0;
+  __syncthreads();
+  atomicMax(reinterpret_cast<unsigned long long*>(&sh_dmax), __double_as_longlong(dmax));
+  __syncthreads();
+  const double low_skip = vec_out ? 0.0 : 1e-12 * sh_dmax / n;
   if (use_jacobi)
-    herm_jacobi(X, V, n, ld, neps, abs_skip, 40, status);
+    herm_jacobi(X, V, n, ld, neps, abs_skip, low_skip, 40, status);
   else
     herm_eig_tridiag(X, V, n, ld, status);
   for (int j = threadIdx.x; j < n; j += blockDim.x) lam[j] = X[j * ld + j].x;
@@ -512,7 +902,7 @@ __device__ void gram_factors_dev(const double2* G, int n, double2* X, double2* V
   }
   __syncthreads();
   const double lmax = lam[order[0]];
-  if (threadIdx.x == 0) {
+  if (threadIdx.x == 0 && P) {  // (P == nullptr: plain eigh, no Gram factors)
     if (!(lmax > 0.0)) atomicOr(status, kSmallZeroGram);
     int anyd = 0;
     for (int j = 0; j < n; ++j) {
@@ -527,10 +917,12 @@ __device__ void gram_factors_dev(const double2* G, int n, double2* X, double2* V
     const double lj = fmax(lam[order[j]], 1e-12 * lmax);
     // eigenvector column j (sorted), phase fixed: x_ij * conj(phase_j)
     const double2 xij = cmulc(ph[j], V[order[j] * ld + i]);
-    const double isq = 1.0 / sqrt(lj);
-    P[i * n + j] = cscale(xij, isq);
-    // R row j = sqrt(l_j) conj(column j of X): R[j][i] = sqrt(l_j) conj(x_ij)
-    R[j * n + i] = cscale(cconj(xij), sqrt(lj));
+    if (P) {
+      const double isq = 1.0 / sqrt(lj);
+      P[i * n + j] = cscale(xij, isq);
+      // R row j = sqrt(l_j) conj(column j of X): R[j][i] = sqrt(l_j) conj(x_ij)
+      R[j * n + i] = cscale(cconj(xij), sqrt(lj));
+    }
     if (vec_out) vec_out[i * n + j] = xij;  // eigenvector j (descending), phase-fixed
   }
   if (lam_out)
@@ -1066,7 +1458,7 @@ __global__ void herm_exp_kernel(const double2* H, int n, double coeff, double ta
 void su_reduce(const SuSiteDesc* d, int n, size_t smem, int* status, cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
-    PEPSB_CUDA(cudaFuncSetAttribute(su_reduce_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    PEPSB_CUDA(cudaFuncSetAttribute(su_reduce_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 176 * 1024));
     attr = true;
   }
   if (n == 0) return;
@@ -1107,22 +1499,45 @@ void gram_factors(const double2* G, int n, double2* P, double2* R, int* deficien
                   int* status, double2* work, cudaStream_t stream, double* lam_out, double2* vec_out) {
   if (n > 256) throw Error(kShapeError, "gram_factors: k > 256 not supported");
   const size_t smem = 2ull * n * (n + 1) * sizeof(double2);
-  const bool fits = smem <= kSmemCap;
+  constexpr size_t kCap = 176 * 1024;  // + ~45 KB static shared memory of the eigensolvers
+  const bool fits = smem <= kCap;
   if (!fits && !work) throw Error(kOtherError, "gram_factors: workspace required");
   static bool attr = false;
   if (!attr) {
     PEPSB_CUDA(cudaFuncSetAttribute(gram_factors_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    static_cast<int>(kSmemCap)));
+                                    static_cast<int>(kCap)));
     attr = true;
   }
   static const int env_threads = getenv("PEPSB_EIG_THREADS") ? atoi(getenv("PEPSB_EIG_THREADS")) : 0;
-  const int threads = env_threads > 0 ? env_threads : kThreads;
-  // PEPSB_EIG=tridiag selects Householder tridiagonalisation + QL (default: two-sided Jacobi)
-  static const int use_jacobi = !(getenv("PEPSB_EIG") && std::string(getenv("PEPSB_EIG")) == "tridiag");
+  const int threads = env_threads >= 64 ? env_threads : kThreads;
+  const int use_jacobi = eig_solver() == kEigJacobi;
   gram_factors_kernel<<<1, threads, fits ? smem : 0, stream>>>(G, n, P, R, deficient, any_def, status,
                                                                 fits ? nullptr : work, use_jacobi, lam_out,
                                                                 vec_out);
   PEPSB_LAUNCH();
+}
+
+namespace {
+std::atomic<int> g_eig_solver{-1};
+}
+
+int eig_solver() {
+  int v = g_eig_solver.load();
+  if (v < 0) {  // PEPSB_EIG=jacobi selects the Jacobi solver before any option is set
+    const char* e = getenv("PEPSB_EIG");
+    v = (e && std::string(e) == "jacobi") ? kEigJacobi : kEigDivideConquer;
+    g_eig_solver.store(v);
+  }
+  return v;
+}
+
+void set_eig_solver(int s) {
+  if (s != kEigJacobi && s != kEigDivideConquer) throw Error(kValidationError, "eig_solver must be 0 or 1");
+  g_eig_solver.store(s);
+}
+
+void eigh_dense(const double2* G, int n, double* w, double2* vec, int* status, double2* work, cudaStream_t stream) {
+  gram_factors(G, n, nullptr, nullptr, nullptr, nullptr, status, work, stream, w, vec);
 }
 
 void chol_factors(const double2* G, int n, double shift_rel, double2* R, double2* Rinv, int* status,

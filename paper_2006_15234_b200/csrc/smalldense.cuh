@@ -30,6 +30,17 @@ void gram_factors(const double2* G, int n, double2* P, double2* R, int* deficien
                   int* status, double2* work, cudaStream_t stream, double* lam_out = nullptr,
                   double2* vec_out = nullptr);
 
+// Hermitian k x k eigensolver used by gram_factors / eigh_dense (process-wide):
+// kEigDivideConquer = Householder tridiagonalisation + divide and conquer (the
+// zheevd route), kEigJacobi = two-sided cyclic Jacobi.
+enum EigSolver { kEigDivideConquer = 0, kEigJacobi = 1 };
+int eig_solver();
+void set_eig_solver(int s);
+
+// Hermitian eigendecomposition (linalg.cpp:256-295): w descending, vec row-major
+// n x n with column j = phase-fixed eigenvector j.  Same `work` rule as above.
+void eigh_dense(const double2* G, int n, double* w, double2* vec, int* status, double2* work, cudaStream_t stream);
+
 // CholeskyQR factor: G + shift*I = R^H R (R upper triangular), Rinv = R^{-1}.
 // CholeskyQR factor G = R^H R; status |= kSmallCholBreakdown when a pivot
 // falls below pivot_rel * max_i G_ii (or is not positive).
