@@ -17,6 +17,9 @@ namespace pepsb {
 namespace {
 
 constexpr int kThreads = 1024;
+// k x k eigensolver block: 512 threads leave 128 registers per thread for the
+// register-resident tridiagonalisation / back-transformation.
+constexpr int kEigThreads = 512;
 constexpr size_t kSmemCap = 200 * 1024;
 
 __device__ __forceinline__ double warp_sum(double v) {
@@ -398,7 +401,6 @@ __device__ void dc_secular_root(bool valid, int j, int K, const double* dk, cons
     phi = seg_sum(phi, T, full);
     dphi = seg_sum(dphi, T, full);
     if (done) continue;
-    if (sub == 0) atomicAdd(prof, 1);
     const double f = irho + psi + phi;
     if (f < 0.0) lo_t = tau;
     else hi_t = tau;
@@ -433,7 +435,6 @@ __device__ void dc_secular_root(bool valid, int j, int K, const double* dk, cons
     tau = tn;
   }
   if (valid && sub == 0) {
-    atomicAdd(prof + 1, 1);
     *sig_out = sig;
     *tau_out = tau;
   }
@@ -452,14 +453,7 @@ __device__ void dc_merge(bool active, int lo, int n1, int N, int gt, int G, doub
   const double beta = active ? e[lo + n1 - 1] : 0.0;
   const double rho = 2.0 * fabs(beta);
   const double sg = beta >= 0.0 ? 1.0 : -1.0;
-  long long tk = clock64();
-  auto mark = [&](int w) {
-    if (threadIdx.x == 0) {
-      const long long t2 = clock64();
-      atomicAdd(S.prof + w, static_cast<int>((t2 - tk) / 100));
-      tk = t2;
-    }
-  };
+
   // z = Q^T (e_last(T1) + sg e_first(T2)) / sqrt(2); ascending order of d
   if (active)
     for (int c = gt; c < N; c += G) {
@@ -528,7 +522,6 @@ __device__ void dc_merge(bool active, int lo, int n1, int N, int gt, int G, doub
     S.zk[lo + i] = S.zb[c];
   }
   __syncthreads();
-  mark(0);
   // T lanes per root / per vector: the largest power of two with 2 T K <= G
   int T = 1;
   while (T < 32 && T < G && 2 * T * K <= G) T <<= 1;
@@ -543,7 +536,6 @@ __device__ void dc_merge(bool active, int lo, int n1, int N, int gt, int G, doub
     dc_secular_root(j < K, j, K, dk, zk, rho, sub, T, S.sig + lo + j, S.tau + lo + j, S.prof + 12);
   }
   __syncthreads();
-  mark(1);
   const double* sg_ = S.sig + lo;
   const double* tu_ = S.tau + lo;
   // z recomputed from the roots: zh_i^2 = prod_j (lambda_j - d_i) / (rho prod_{j != i} (d_j - d_i))
@@ -578,20 +570,46 @@ __device__ void dc_merge(bool active, int lo, int n1, int N, int gt, int G, doub
       for (int i = sub; i < K; i += T) V[(lo + i) * ld + lo + j].y *= inv;
   }
   __syncthreads();
-  mark(2);
   for (int j = gt; j < K; j += G) d[S.ndx[lo + j]] = sg_[j] + tu_[j];
   // Zt(r, ndx[j]) = sum_i Z(r, ndx[i]) v_j[i] staged in A's upper triangle
   // (local (r, c): r <= c at A(lo + r, lo + c).x, r > c at A(lo + c, lo + r).y),
   // then copied back over Z.
   const int* ndx = S.ndx + lo;
-  for (int o = gt; o < N * K; o += G) {
-    const int r = o / K, j = o % K;
-    double acc = 0.0;
-#pragma unroll 4
-    for (int i = 0; i < K; ++i) acc += V[ndx[i] * ld + lo + r].x * V[(lo + i) * ld + lo + j].y;
-    const int c = ndx[j] - lo;
-    if (r <= c) A[(lo + c) * ld + lo + r].x = acc;
-    else A[(lo + r) * ld + lo + c].y = acc;
+  {
+    // 4 x 4 register tiles: 9 shared loads per 16 FMAs
+    const int tr = (N + 3) >> 2, tc = (K + 3) >> 2;
+    for (int o = gt; o < tr * tc; o += G) {
+      const int r0 = (o / tc) * 4, j0 = (o % tc) * 4;
+      double acc[4][4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+      for (int i = 0; i < K; ++i) {
+        const double2* zc = V + ndx[i] * ld + lo + r0;
+        const double2* wr = V + (lo + i) * ld + lo + j0;
+        double zv[4], wv[4];
+#pragma unroll
+        for (int a = 0; a < 4; ++a) zv[a] = r0 + a < N ? zc[a].x : 0.0;
+#pragma unroll
+        for (int b = 0; b < 4; ++b) wv[b] = j0 + b < K ? wr[b].y : 0.0;
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int b = 0; b < 4; ++b) acc[a][b] = fma(zv[a], wv[b], acc[a][b]);
+      }
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          const int r = r0 + a, j = j0 + b;
+          if (r < N && j < K) {
+            const int c = ndx[j] - lo;
+            if (r <= c) A[(lo + c) * ld + lo + r].x = acc[a][b];
+            else A[(lo + r) * ld + lo + c].y = acc[a][b];
+          }
+        }
+    }
   }
   __syncthreads();
   for (int o = gt; o < N * K; o += G) {
@@ -599,7 +617,6 @@ __device__ void dc_merge(bool active, int lo, int n1, int N, int gt, int G, doub
     V[(lo + c) * ld + lo + r].x = r <= c ? A[(lo + c) * ld + lo + r].x : A[(lo + r) * ld + lo + c].y;
   }
   __syncthreads();
-  mark(3);
 }
 
 // d, e in shared memory; V column-major (ld); A: the tridiagonalised matrix
@@ -653,6 +670,55 @@ __device__ void tridiag_dc(double* d, double* e, double2* V, double2* A, int n, 
   __syncthreads();
 }
 
+// Back-transformation X = H_0 ... H_{n-2} Z with each column of X held in the
+// registers of an 8-lane group (rows s = gl + 8k), n <= 8 * ES: reflectors are
+// read from shared memory as broadcasts, X never round-trips through it.
+template <int ES, int GS>
+__device__ void back_transform_reg(const double2* A, double2* V, int n, int ld, const double2* tauv) {
+  const int tid = threadIdx.x, grp = tid / GS, gl = tid % GS, ngrp = blockDim.x / GS;
+  for (int cbase = 0; cbase < n; cbase += ngrp) {
+    const int c = cbase + grp;
+    const bool act = c < n;
+    double2 x[ES];
+#pragma unroll
+    for (int k = 0; k < ES; ++k) {
+      const int s = gl + GS * k;
+      x[k] = (act && s < n) ? V[c * ld + s] : make_double2(0.0, 0.0);
+    }
+    for (int j = n - 2; j >= 0; --j) {
+      const double2 tau = tauv[j];
+      if (tau.x == 0.0 && tau.y == 0.0) continue;
+      double re = 0.0, im = 0.0;
+#pragma unroll
+      for (int k = 0; k < ES; ++k) {
+        const int s = gl + GS * k;
+        if (s > j && s < n) {
+          const double2 v = A[j * ld + s];
+          re += v.x * x[k].x + v.y * x[k].y;
+          im += v.x * x[k].y - v.y * x[k].x;
+        }
+      }
+#pragma unroll
+      for (int o = GS / 2; o > 0; o >>= 1) {
+        re += __shfl_xor_sync(0xffffffffu, re, o);
+        im += __shfl_xor_sync(0xffffffffu, im, o);
+      }
+      const double2 t = cmul(tau, make_double2(re, im));
+#pragma unroll
+      for (int k = 0; k < ES; ++k) {
+        const int s = gl + GS * k;
+        if (s > j && s < n) x[k] = csub(x[k], cmul(A[j * ld + s], t));
+      }
+    }
+    if (act)
+#pragma unroll
+      for (int k = 0; k < ES; ++k) {
+        const int s = gl + GS * k;
+        if (s < n) V[c * ld + s] = x[k];
+      }
+  }
+}
+
 // Hermitian eigensolver for one thread block: Householder tridiagonalisation
 // (the zhetd2 recurrence: A <- H^H A H with H = I - tau v v^H, rank-2 updates),
 // divide and conquer on the real tridiagonal (tridiag_dc), and
@@ -679,108 +745,122 @@ __device__ void herm_eig_tridiag(double2* A, double2* V, int n, int ld, int* sta
   // ---- 1. tridiagonalisation, j = 0 .. n-2 (reflector H_j acts on rows/cols j+1..n-1).
   // Two barriers per column: the rank-2 update of step j-1 (v, w in vv / pw) is
   // applied lazily inside step j's matvec (each thread updates the elements it
-  // multiplies), while warp 0 forms the updated column x = A(j+1:, j) on the fly;
-  // then warp 0 turns (x, A x) into the reflector v = scal (x - beta e1) and
-  // w = p + alpha2 v with p = tau A v = tau scal (A x - beta A(:, j+1)).
-  for (int j = 0; j + 1 < n; ++j) {
-    const int m = n - j - 1;
-    const bool pend = j > 0 && (tauv[j - 1].x != 0.0 || tauv[j - 1].y != 0.0);
-    double2* xs = part[kChunks - 1];  // the updated column x (warp 0's, phase A -> B)
-    double xn = 0.0;
-    double2 alpha = make_double2(0.0, 0.0);
-    const int nch = 1;
-    if (warp == 0) {
-      const double2 vj = pend ? vv[j] : make_double2(0.0, 0.0), wj = pend ? pw[j] : make_double2(0.0, 0.0);
-      for (int l = j + 1 + lane; l < n; l += 32) {
-        double2 x = A[j * ld + l];
-        if (pend) x = csub(x, cadd(cmulc(wj, vv[l]), cmulc(vj, pw[l])));
-        xs[l] = x;
-        if (l >= j + 2) xn += cnorm2(x);
-        if (l == j + 1) alpha = x;
-      }
-      xn = warp_sum(xn);
-      alpha = make_double2(__shfl_sync(0xffffffffu, alpha.x, 0), __shfl_sync(0xffffffffu, alpha.y, 0));
-      if (lane == 0) d[j] = A[j * ld + j].x - (pend ? 2.0 * (vj.x * wj.x + vj.y * wj.y) : 0.0);
-    } else {
-      // rows i >= j+1 (8 lanes per row, interleaved columns): apply the pending
-      // update, accumulate A x, reduce over the 8 lanes
-      const int t = tid - 32, gl = t & 7;
-      for (int i0 = j + 1; i0 < n; i0 += (nthr - 32) >> 3) {
-        const int i = i0 + (t >> 3);
-        double re0 = 0.0, im0 = 0.0;
-        if (i < n) {
-          const double2 vi = pend ? vv[i] : make_double2(0.0, 0.0), wi = pend ? pw[i] : make_double2(0.0, 0.0);
-          const double2 vj = pend ? vv[j] : make_double2(0.0, 0.0), wj = pend ? pw[j] : make_double2(0.0, 0.0);
-          for (int l = j + 1 + gl; l < n; l += 8) {
-            double2 a = A[l * ld + i], x = A[j * ld + l];
-            if (pend) {
-              const double2 vl = vv[l], wl = pw[l];
-              a = csub(a, cadd(cmulc(wl, vi), cmulc(vl, wi)));
-              A[l * ld + i] = a;
-              x = csub(x, cadd(cmulc(wj, vl), cmulc(vj, wl)));
-            }
-            re0 += a.x * x.x - a.y * x.y;
-            im0 += a.x * x.y + a.y * x.x;
-          }
+  // multiplies), while warp 0 forms the updated column x = A(j+1:, j), its norm
+  // and the reflector scalars; then warp 0 turns (x, A x) into v = scal (x - beta e1)
+  // and w = p + alpha2 v with p = tau A v = tau scal (A x - beta A(:, j+1)).
+  {
+    double2* xs = part[1];  // the updated column x (warp 0's, phase A -> B)
+    double2* qs = part[0];  // q = A22 x
+    const int mt = nthr - 32;
+    int lpr = 8;  // lanes per row of the matvec: one pass over the rows when possible
+    while (lpr > 2 && (mt / lpr) < n - 1) lpr >>= 1;
+    const unsigned gmask = 0xffffffffu;
+    for (int j = 0; j + 1 < n; ++j) {
+      const bool pend = j > 0 && (tauv[j - 1].x != 0.0 || tauv[j - 1].y != 0.0);
+      const double2 z0 = make_double2(0.0, 0.0);
+      const double2 vj = pend ? vv[j] : z0, wj = pend ? pw[j] : z0;
+      double2 tau = z0, scal = z0;
+      double beta = 0.0;
+      if (warp == 0) {
+        double xn = 0.0;
+        double2 alpha = z0;
+        for (int l = j + 1 + lane; l < n; l += 32) {
+          double2 x = A[j * ld + l];
+          if (pend) x = csub(x, cadd(cmulc(wj, vv[l]), cmulc(vj, pw[l])));
+          xs[l] = x;
+          if (l >= j + 2) xn += cnorm2(x);
+          if (l == j + 1) alpha = x;
         }
-#pragma unroll
-        for (int o = 4; o > 0; o >>= 1) {
-          re0 += __shfl_xor_sync(0xffffffffu, re0, o);
-          im0 += __shfl_xor_sync(0xffffffffu, im0, o);
+        xn = warp_sum(xn);
+        alpha = make_double2(__shfl_sync(0xffffffffu, alpha.x, 0), __shfl_sync(0xffffffffu, alpha.y, 0));
+        if (lane == 0) d[j] = A[j * ld + j].x - (pend ? 2.0 * (vj.x * wj.x + vj.y * wj.y) : 0.0);
+        if (xn == 0.0 && alpha.y == 0.0) {
+          beta = alpha.x;
+        } else {
+          beta = -copysign(sqrt(alpha.x * alpha.x + alpha.y * alpha.y + xn), alpha.x);
+          const double rb = 1.0 / beta;
+          tau = make_double2((beta - alpha.x) * rb, -alpha.y * rb);
+          const double2 den = make_double2(alpha.x - beta, alpha.y);  // scal = 1 / (alpha - beta)
+          const double dn = 1.0 / cnorm2(den);
+          scal = make_double2(den.x * dn, -den.y * dn);
         }
-        if (i < n && gl == 0) part[0][i] = make_double2(re0, im0);
-      }
-    }
-    __syncthreads();
-    if (warp == 0) {
-      double2 tau, scal = make_double2(0.0, 0.0);
-      double beta;
-      if (xn == 0.0 && alpha.y == 0.0) {
-        tau = make_double2(0.0, 0.0);
-        beta = alpha.x;
       } else {
-        beta = -copysign(sqrt(alpha.x * alpha.x + alpha.y * alpha.y + xn), alpha.x);
-        tau = make_double2((beta - alpha.x) / beta, -alpha.y / beta);
-        const double2 den = make_double2(alpha.x - beta, alpha.y);  // scal = 1 / (alpha - beta)
-        const double dn = 1.0 / cnorm2(den);
-        scal = make_double2(den.x * dn, -den.y * dn);
-      }
-      const bool zero = tau.x == 0.0 && tau.y == 0.0;
-      const double2 ts = cmul(tau, scal);
-      double hr = 0.0, hi = 0.0;
-      for (int l = j + 1 + lane; l < n && !zero; l += 32) {
-        {
-          const double2 v = l == j + 1 ? make_double2(1.0, 0.0) : cmul(xs[l], scal);
-          A[j * ld + l] = v;  // reflector kept in column j for the back-transformation
-          vv[l] = v;
-          double2 s = part[0][l];
-          for (int c = 1; c < nch; ++c) s = cadd(s, part[c][l]);
-          const double2 a1 = A[(j + 1) * ld + l];  // updated A(l, j+1)
-          const double2 p = cmul(ts, make_double2(s.x - beta * a1.x, s.y - beta * a1.y));
-          pw[l] = p;
-          hr += p.x * v.x + p.y * v.y;
-          hi += p.x * v.y - p.y * v.x;
+        // rows i >= j+1 (lpr lanes per row, interleaved columns): apply the
+        // pending update, accumulate A x, reduce over the row's lanes
+        const int t = tid - 32, gl = t % lpr;
+        for (int i0 = j + 1; i0 < n; i0 += mt / lpr) {
+          const int i = i0 + t / lpr;
+          double re0 = 0.0, im0 = 0.0, re1 = 0.0, im1 = 0.0;
+          if (i < n) {
+            const double2 vi = pend ? vv[i] : z0, wi = pend ? pw[i] : z0;
+            int l = j + 1 + gl;
+            for (; l < n; l += 2 * lpr) {
+              const int l2 = l + lpr;
+              const bool two = l2 < n;
+              double2 a = A[l * ld + i], x = A[j * ld + l];
+              double2 b = two ? A[l2 * ld + i] : z0, y = two ? A[j * ld + l2] : z0;
+              if (pend) {
+                const double2 vl = vv[l], wl = pw[l];
+                a = csub(a, cadd(cmulc(wl, vi), cmulc(vl, wi)));
+                A[l * ld + i] = a;
+                x = csub(x, cadd(cmulc(wj, vl), cmulc(vj, wl)));
+                if (two) {
+                  const double2 vl2 = vv[l2], wl2 = pw[l2];
+                  b = csub(b, cadd(cmulc(wl2, vi), cmulc(vl2, wi)));
+                  A[l2 * ld + i] = b;
+                  y = csub(y, cadd(cmulc(wj, vl2), cmulc(vj, wl2)));
+                }
+              }
+              re0 += a.x * x.x - a.y * x.y;
+              im0 += a.x * x.y + a.y * x.x;
+              re1 += b.x * y.x - b.y * y.y;
+              im1 += b.x * y.y + b.y * y.x;
+            }
+          }
+          re0 += re1;
+          im0 += im1;
+          for (int o = lpr >> 1; o > 0; o >>= 1) {
+            re0 += __shfl_xor_sync(gmask, re0, o);
+            im0 += __shfl_xor_sync(gmask, im0, o);
+          }
+          if (i < n && gl == 0) qs[i] = make_double2(re0, im0);
         }
       }
-      hr = warp_sum(hr);
-      hi = warp_sum(hi);
-      const double2 alpha2 = cscale(cmul(tau, make_double2(hr, hi)), -0.5);
-      for (int l = j + 1 + lane; l < n; l += 32) {
-        {
+      __syncthreads();
+      if (warp == 0) {
+        const bool zero = tau.x == 0.0 && tau.y == 0.0;
+        const double2 ts = cmul(tau, scal);
+        double hr = 0.0, hi = 0.0;
+        if (!zero) {
+          for (int l = j + 1 + lane; l < n; l += 32) {
+            const double2 xl = xs[l], s = qs[l], a1 = A[(j + 1) * ld + l];  // a1: updated A(l, j+1)
+            const double2 v = l == j + 1 ? make_double2(1.0, 0.0) : cmul(xl, scal);
+            const double2 p = cmul(ts, make_double2(s.x - beta * a1.x, s.y - beta * a1.y));
+            A[j * ld + l] = v;  // reflector kept in column j for the back-transformation
+            vv[l] = v;
+            pw[l] = p;
+            hr += p.x * v.x + p.y * v.y;
+            hi += p.x * v.y - p.y * v.x;
+          }
+          hr = warp_sum(hr);
+          hi = warp_sum(hi);
+        }
+        const double2 alpha2 = cscale(cmul(tau, make_double2(hr, hi)), -0.5);
+        for (int l = j + 1 + lane; l < n; l += 32) {
           if (zero) {
-            vv[l] = make_double2(0.0, 0.0);
-            pw[l] = make_double2(0.0, 0.0);
+            vv[l] = z0;
+            pw[l] = z0;
           } else {
             pw[l] = cadd(pw[l], cmul(alpha2, vv[l]));
           }
         }
+        if (lane == 0) {
+          e[j] = beta;
+          tauv[j] = tau;
+        }
       }
-      if (lane == 0) {
-        e[j] = beta;
-        tauv[j] = tau;
-      }
+      __syncthreads();
     }
-    __syncthreads();
   }
   if (tid == 0) {
     const bool pend = n >= 2 && (tauv[n - 2].x != 0.0 || tauv[n - 2].y != 0.0);
@@ -801,7 +881,18 @@ __device__ void herm_eig_tridiag(double2* A, double2* V, int n, int ld, int* sta
   }
   const long long clk2 = clock64();
   // ---- 3. back-transformation X = H_0 H_1 ... H_{n-2} Z, one 8-lane group per column
-  {
+  if (n <= 24 * 4 && 4 * n <= nthr) {
+    if (n <= nthr / 8) {
+      const int esb = (n + 7) / 8;
+      if (esb <= 4) back_transform_reg<4, 8>(A, V, n, ld, tauv);
+      else if (esb <= 8) back_transform_reg<8, 8>(A, V, n, ld, tauv);
+      else back_transform_reg<12, 8>(A, V, n, ld, tauv);
+    } else {
+      const int esb = (n + 3) / 4;
+      if (esb <= 18) back_transform_reg<18, 4>(A, V, n, ld, tauv);
+      else back_transform_reg<24, 4>(A, V, n, ld, tauv);
+    }
+  } else {
     const int grp = tid >> 3, gl = tid & 7, ngrp = nthr >> 3;
     for (int cbase = 0; cbase < n; cbase += ngrp) {
       const int c = cbase + grp;
@@ -930,7 +1021,7 @@ __device__ void gram_factors_dev(const double2* G, int n, double2* X, double2* V
   __syncthreads();
 }
 
-__global__ void __launch_bounds__(kThreads) gram_factors_kernel(const double2* G, int n, double2* P,
+__global__ void __launch_bounds__(kEigThreads) gram_factors_kernel(const double2* G, int n, double2* P,
                                                                 double2* R, int* deficient,
                                                                 int* any_def, int* status,
                                                                 double2* work, int use_jacobi, double* lam_out,
@@ -1509,7 +1600,7 @@ void gram_factors(const double2* G, int n, double2* P, double2* R, int* deficien
     attr = true;
   }
   static const int env_threads = getenv("PEPSB_EIG_THREADS") ? atoi(getenv("PEPSB_EIG_THREADS")) : 0;
-  const int threads = env_threads >= 64 ? env_threads : kThreads;
+  const int threads = env_threads >= 64 && env_threads <= kEigThreads ? env_threads : kEigThreads;
   const int use_jacobi = eig_solver() == kEigJacobi;
   gram_factors_kernel<<<1, threads, fits ? smem : 0, stream>>>(G, n, P, R, deficient, any_def, status,
                                                                 fits ? nullptr : work, use_jacobi, lam_out,

@@ -26,4 +26,4 @@ for n in (16, 32, 64, 72, 128):
     ctx.profile(False)
     words = [lib().pepsb_ctx_debug_word(ctx.h, w, 1) for w in range(8, 40)]
     print(n, "ms %.3f" % rep["small"]["ms"], "tri/dc/back kcyc", words[0:3], "block merge hcyc", words[4:8],
-          "secular its/roots", words[16:18], "tri hcyc", words[22:24], flush=True)
+          "secular its/roots", words[16:18], flush=True)
