@@ -7,6 +7,7 @@
 #include "ite.h"
 #include "peps.h"
 #include "smalldense.cuh"
+#include "zgemm.cuh"
 #include "tensor_ops.cuh"
 
 using namespace pepsb;
@@ -185,6 +186,7 @@ int pepsb_ctx_set_option(pepsb_ctx* c, const char* key, int64_t value) {
     std::string k = key ? key : "";
     if (k == "orth_mode") c->ctx->orth_mode = static_cast<int>(value);
     else if (k == "eig_solver") set_eig_solver(static_cast<int>(value));
+    else if (k == "gemm_algo") zgemm_set_algo(static_cast<int>(value));
     else throw Error(kConfigError, "unknown option '" + k + "'");
   });
 }

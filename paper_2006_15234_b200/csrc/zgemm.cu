@@ -8,6 +8,8 @@
 // 8x8 real C tile is an 8x4 complex tile and each lane owns exactly one
 // complex output (re = c0, im = c1).
 #include <algorithm>
+#include <atomic>
+#include <string>
 #include <cstdio>
 #include <cstdlib>
 
@@ -280,6 +282,8 @@ struct TileCfg {
   int bm, bn;
 };
 constexpr TileCfg kCfgs[] = {{64, 64}, {64, 72}, {72, 64}, {72, 72}, {128, 64}};
+constexpr TileCfg kCfgs3m[] = {{64, 32}, {64, 72}, {72, 64}, {72, 72}, {64, 32}};
+constexpr TileCfg kCfgs4c[] = {{64, 64}, {64, 72}, {72, 64}, {72, 72}, {64, 64}};
 
 int choose_cfg(int64_t M, int64_t N) {
   static const bool cfg4 = getenv("PEPSB_CFG4") != nullptr;
@@ -311,6 +315,9 @@ void transpose_problem(ZgemmParams& p) {
 }
 
 int ctas_per_sm(int cfg) { return cfg <= 1 ? 2 : 1; }
+int ctas_per_sm3m(int cfg) { return cfg == 0 ? 2 : 1; }
+
+std::atomic<int> g_algo{-1};
 
 template <bool AK, bool BNC>
 void launch_any(const ZgemmParams& p, cudaStream_t stream) {
@@ -323,15 +330,379 @@ void launch_any(const ZgemmParams& p, cudaStream_t stream) {
   }
 }
 
+// ---------------------------------------------------------------- 3M (Gauss) variant
+// C = A B over complex k with three real products per 8x8 complex block,
+//   P1 = Ar Br,  P2 = Ai Bi,  P3 = (Ar + Ai)(Br + Bi),
+//   Re C = P1 - P2,  Im C = P3 - P1 - P2      (conjugation: Ai -> -Ai, Bi -> -Bi),
+// i.e. 3 real MACs per complex MAC instead of the real embedding's 4 (the
+// zgemm3m scheme).  One DMMA.8x8x4 covers 8 x 8 complex outputs over 4 complex
+// k; each lane loads its A / B fragment element as one complex value (LDS.128)
+// and forms (r, i, r + i) in registers.  Smem strides are padded so every
+// quarter-warp's 8 LDS.128 hit distinct 16-byte bank groups.
+template <int BM, int BN, int BK, bool AK, bool BNC>
+struct Smem3 {
+  static constexpr int LDA = AK ? (BK + 4) : (BM + 2);
+  static constexpr int LDB = BNC ? (BN + 2) : (BK + 4);
+  static constexpr int A_ELEMS = AK ? BM * LDA : BK * LDA;
+  static constexpr int B_ELEMS = BNC ? BK * LDB : BN * LDB;
+  static constexpr int STAGE = A_ELEMS + B_ELEMS;
+};
+
+template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool AK, bool BNC, int ALG, int MINB>
+__global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32, MINB)
+    zgemm_cx_kernel(const ZgemmParams p) {
+  constexpr int NACC = ALG == 3 ? 3 : 2;  // 3M: P1, P2, P3;  4M: Re, Im
+  using S = Smem3<BM, BN, BK, AK, BNC>;
+  constexpr int NT = (BM / WM) * (BN / WN) * 32;
+  constexpr int FM = WM / 8;  // 8-row blocks per warp
+  constexpr int FN = WN / 8;  // 8-column blocks per warp
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double2* smem = reinterpret_cast<double2*>(smem_raw);
+  int64_t* rowoff = reinterpret_cast<int64_t*>(smem + STAGES * S::STAGE);
+  int64_t* coloff = rowoff + BM;
+
+  const int tid = threadIdx.x;
+  const int lane = tid & 31;
+  const int warp = tid >> 5;
+  const int wm0 = (warp % (BM / WM)) * WM;
+  const int wn0 = (warp / (BM / WM)) * WN;
+
+  const int64_t mtiles = (p.M + BM - 1) / BM;
+  const int64_t tile = blockIdx.x;
+  const int64_t m0 = (tile % mtiles) * BM;
+  const int64_t n0 = (tile / mtiles) * BN;
+  const int64_t bz = blockIdx.y / p.splits;
+  const int split = blockIdx.y % p.splits;
+
+  int64_t offA = 0, offB = 0, offC = 0;
+  {
+    int64_t idx = bz;
+    for (int a = p.nb - 1; a >= 0; --a) {
+      int64_t e = p.bext[a];
+      int64_t q = idx / e;
+      int64_t r = idx - q * e;
+      offA += r * p.bsA[a];
+      offB += r * p.bsB[a];
+      offC += r * p.bsC[a];
+      idx = q;
+    }
+  }
+  const double2* A = p.A + offA;
+  const double2* B = p.B + offB;
+
+  const int64_t kbeg = static_cast<int64_t>(split) * p.kchunk;
+  const int64_t kend = min(p.K, kbeg + p.kchunk);
+  const int64_t nk = (kend - kbeg + BK - 1) / BK;
+
+  // Operand tile loaders, strength-reduced: thread tid copies the elements
+  // e = tid + u * NT of the [outer][inner] smem tile, so when NT is a multiple
+  // of the inner extent its inner index is fixed and the outer index advances
+  // by NT / inner -- one 64-bit base per operand, a constant stride per u, a
+  // k-tile stride per stage, and row-validity bits computed once.
+  constexpr int AIN = AK ? BK : BM, AOUT = AK ? BM : BK;
+  constexpr int BIN = BNC ? BN : BK, BOUT = BNC ? BK : BN;
+  constexpr bool AREG = (NT % AIN) == 0, BREG = (NT % BIN) == 0;
+  constexpr int UA = (BM * BK + NT - 1) / NT, UB = (BK * BN + NT - 1) / NT;
+  constexpr int AOS = AREG ? NT / AIN : 1, BOS = BREG ? NT / BIN : 1;
+  const int a_in = tid % AIN, a_o0 = tid / AIN, b_in = tid % BIN, b_o0 = tid / BIN;
+  int64_t a_base, a_ustr, b_base, b_ustr;
+  unsigned a_ok = 0, b_ok = 0;  // AK: row bits per u / !AK: row ok in bit 0 (and BNC likewise)
+  if (AK) {
+    a_base = (m0 + a_o0) * p.sAi + (kbeg + a_in) * p.sAk;
+    a_ustr = AOS * p.sAi;
+#pragma unroll
+    for (int u = 0; u < UA; ++u)
+      if (a_o0 + u * AOS < AOUT && m0 + a_o0 + u * AOS < p.M) a_ok |= 1u << u;
+  } else {
+    a_base = (m0 + a_in) * p.sAi + (kbeg + a_o0) * p.sAk;
+    a_ustr = AOS * p.sAk;
+    a_ok = m0 + a_in < p.M ? 1u : 0u;
+  }
+  if (BNC) {
+    b_base = (kbeg + b_o0) * p.sBk + (n0 + b_in) * p.sBj;
+    b_ustr = BOS * p.sBk;
+    b_ok = n0 + b_in < p.N ? 1u : 0u;
+  } else {
+    b_base = (n0 + b_o0) * p.sBj + (kbeg + b_in) * p.sBk;
+    b_ustr = BOS * p.sBj;
+#pragma unroll
+    for (int u = 0; u < UB; ++u)
+      if (b_o0 + u * BOS < BOUT && n0 + b_o0 + u * BOS < p.N) b_ok |= 1u << u;
+  }
+  auto load_stage = [&](int slot, int64_t kt) {
+    double2* As = smem + slot * S::STAGE;
+    double2* Bs = As + S::A_ELEMS;
+    const int64_t k0 = kbeg + kt * BK;
+    if constexpr (AREG) {
+      const double2* src = A + a_base + kt * BK * p.sAk;
+#pragma unroll
+      for (int u = 0; u < UA; ++u) {
+        const int o = a_o0 + u * AOS;
+        if ((AOUT % AOS) != 0 && o >= AOUT) break;  // past the tile (a zero-fill copy would land in B)
+        const bool ok = AK ? (((a_ok >> u) & 1u) && k0 + a_in < kend) : (a_ok && k0 + o < kend);
+        cp_async16(As + o * S::LDA + a_in, ok ? src + u * a_ustr : A, ok);
+      }
+    } else {
+#pragma unroll
+      for (int e = tid; e < BM * BK; e += NT) {
+        int i, k;
+        if (AK) { i = e / BK; k = e % BK; } else { k = e / BM; i = e % BM; }
+        const int64_t gi = m0 + i, gk = k0 + k;
+        const bool ok = gi < p.M && gk < kend;
+        const double2* src = ok ? A + gi * p.sAi + gk * p.sAk : A;
+        double2* dst = AK ? As + i * S::LDA + k : As + k * S::LDA + i;
+        cp_async16(dst, src, ok);
+      }
+    }
+    if constexpr (BREG) {
+      const double2* src = B + b_base + kt * BK * p.sBk;
+#pragma unroll
+      for (int u = 0; u < UB; ++u) {
+        const int o = b_o0 + u * BOS;
+        if ((BOUT % BOS) != 0 && o >= BOUT) break;  // past the tile (would spill into the next stage)
+        const bool ok = BNC ? (b_ok && k0 + o < kend) : (((b_ok >> u) & 1u) && k0 + b_in < kend);
+        cp_async16(Bs + o * S::LDB + b_in, ok ? src + u * b_ustr : B, ok);
+      }
+    } else {
+#pragma unroll
+      for (int e = tid; e < BK * BN; e += NT) {
+        int k, j;
+        if (BNC) { k = e / BN; j = e % BN; } else { j = e / BK; k = e % BK; }
+        const int64_t gj = n0 + j, gk = k0 + k;
+        const bool ok = gj < p.N && gk < kend;
+        const double2* src = ok ? B + gk * p.sBk + gj * p.sBj : B;
+        double2* dst = BNC ? Bs + k * S::LDB + j : Bs + j * S::LDB + k;
+        cp_async16(dst, src, ok);
+      }
+    }
+  };
+
+
+  if (p.splits == 1) {
+    for (int r = tid; r < BM; r += NT) {
+      const int64_t gi = m0 + r;
+      rowoff[r] = gi < p.M ? decode_offset(gi, p.nr, p.rext, p.rstr) : 0;
+    }
+    for (int c = tid; c < BN; c += NT) {
+      const int64_t gj = n0 + c;
+      coloff[c] = gj < p.N ? decode_offset(gj, p.nc, p.cext, p.cstr) : 0;
+    }
+  }
+
+  double acc[FM][FN][NACC][2];
+#pragma unroll
+  for (int a = 0; a < FM; ++a)
+#pragma unroll
+    for (int b = 0; b < FN; ++b)
+#pragma unroll
+      for (int t = 0; t < NACC; ++t) acc[a][b][t][0] = acc[a][b][t][1] = 0.0;
+
+#pragma unroll
+  for (int s = 0; s < STAGES; ++s) {  // every slot filled up front
+    if (s < nk) load_stage(s, s);
+    cp_async_commit();
+  }
+
+  const int kq = lane & 3;   // k within the 4-wide step (A column / B row of the fragment)
+  const int rq = lane >> 2;  // A fragment row / B fragment column
+  // conjugation: flip the sign bit of the imaginary parts (integer XOR, keeps
+  // the FP64 pipe free for nothing but the DMMAs)
+  const long long sga = p.conjA ? (long long)0x8000000000000000ULL : 0LL;
+  const long long sgb = p.conjB ? (long long)0x8000000000000000ULL : 0LL;
+  auto flip = [](double v, long long m) { return __longlong_as_double(__double_as_longlong(v) ^ m); };
+  // Fragments double-buffered in registers: the LDS for step s+1 are issued
+  // before the DMMAs of step s; one barrier per k-tile (before the first
+  // fragment load of the next slot, which also frees the current slot for the
+  // prefetch of stage kt + STAGES).
+  double2 fa[2][FM], fb[2][FN];
+  auto load_frags = [&](int buf, int slot, int ks) {
+    const double2* As = smem + slot * S::STAGE;
+    const double2* Bs = As + S::A_ELEMS;
+    const int kc = ks * 4 + kq;
+#pragma unroll
+    for (int a = 0; a < FM; ++a) {
+      const int row = wm0 + a * 8 + rq;
+      fa[buf][a] = AK ? As[row * S::LDA + kc] : As[kc * S::LDA + row];
+    }
+#pragma unroll
+    for (int b = 0; b < FN; ++b) {
+      const int col = wn0 + b * 8 + rq;
+      fb[buf][b] = BNC ? Bs[kc * S::LDB + col] : Bs[col * S::LDB + kc];
+    }
+  };
+  auto compute = [&](int buf) {
+    if constexpr (ALG == 3) {
+      double ar[FM], ai[FM], as[FM], br[FN], bi[FN], bs[FN];
+#pragma unroll
+      for (int a = 0; a < FM; ++a) {
+        ar[a] = fa[buf][a].x;
+        ai[a] = flip(fa[buf][a].y, sga);
+        as[a] = ar[a] + ai[a];
+      }
+#pragma unroll
+      for (int b = 0; b < FN; ++b) {
+        br[b] = fb[buf][b].x;
+        bi[b] = flip(fb[buf][b].y, sgb);
+        bs[b] = br[b] + bi[b];
+      }
+#pragma unroll
+      for (int a = 0; a < FM; ++a)
+#pragma unroll
+        for (int b = 0; b < FN; ++b) {
+          dmma884(acc[a][b][0][0], acc[a][b][0][1], ar[a], br[b]);
+          dmma884(acc[a][b][1][0], acc[a][b][1][1], ai[a], bi[b]);
+          dmma884(acc[a][b][2][0], acc[a][b][2][1], as[a], bs[b]);
+        }
+    } else {
+      // Re += Ar Br - Ai Bi,  Im += Ar Bi + Ai Br
+      double ai[FM], nai[FM], bi[FN];
+#pragma unroll
+      for (int a = 0; a < FM; ++a) {
+        ai[a] = flip(fa[buf][a].y, sga);
+        nai[a] = flip(fa[buf][a].y, sga ^ (long long)0x8000000000000000ULL);
+      }
+#pragma unroll
+      for (int b = 0; b < FN; ++b) bi[b] = flip(fb[buf][b].y, sgb);
+#pragma unroll
+      for (int a = 0; a < FM; ++a)
+#pragma unroll
+        for (int b = 0; b < FN; ++b) {
+          dmma884(acc[a][b][0][0], acc[a][b][0][1], fa[buf][a].x, fb[buf][b].x);
+          dmma884(acc[a][b][1][0], acc[a][b][1][1], fa[buf][a].x, bi[b]);
+          dmma884(acc[a][b][0][0], acc[a][b][0][1], nai[a], bi[b]);
+          dmma884(acc[a][b][1][0], acc[a][b][1][1], ai[a], fb[buf][b].x);
+        }
+    }
+  };
+  constexpr int KS = BK / 4;
+  if (nk > 0) {
+    cp_async_wait<STAGES - 1>();
+    __syncthreads();
+    load_frags(0, 0, 0);
+  }
+  static_assert(KS % 2 == 0, "k steps per tile must be even (static fragment buffers)");
+  for (int64_t kt = 0; kt < nk; ++kt) {
+    const int slot = static_cast<int>(kt % STAGES);
+#pragma unroll 1
+    for (int kp = 0; kp < KS; kp += 2) {
+      load_frags(1, slot, kp + 1);
+      compute(0);
+      if (kp + 2 < KS) {
+        load_frags(0, slot, kp + 2);
+      } else if (kt + 1 < nk) {
+        cp_async_wait<STAGES - 2>();
+        __syncthreads();
+        if (kt + STAGES < nk) load_stage(slot, kt + STAGES);
+        cp_async_commit();
+        load_frags(0, static_cast<int>((kt + 1) % STAGES), 0);
+      }
+      compute(1);
+    }
+  }
+  cp_async_wait<0>();
+  __syncthreads();
+
+  // Epilogue: lane owns C[a*8 + lane>>2][b*8 + 2*(lane&3) + {0,1}] of every block.
+#pragma unroll
+  for (int a = 0; a < FM; ++a) {
+    const int li = wm0 + a * 8 + (lane >> 2);
+    if (m0 + li >= p.M) continue;
+#pragma unroll
+    for (int b = 0; b < FN; ++b)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int lj = wn0 + b * 8 + 2 * (lane & 3) + h;
+        if (n0 + lj >= p.N) continue;
+        double2 v;
+        if constexpr (ALG == 3) {
+          const double p1 = acc[a][b][0][h], p2 = acc[a][b][1][h], p3 = acc[a][b][NACC - 1][h];
+          v = make_double2(p1 - p2, p3 - p1 - p2);
+        } else {
+          v = make_double2(acc[a][b][0][h], acc[a][b][1][h]);
+        }
+        if (p.splits == 1) {
+          double2* dst = p.C + offC + rowoff[li] + coloff[lj];
+          if (p.accumulate) v = cadd(*dst, v);
+          *dst = v;
+        } else {
+          double2* W = p.work + ((static_cast<int64_t>(split) * p.batch + bz) * p.M) * p.N;
+          W[(m0 + li) * p.N + n0 + lj] = v;
+        }
+      }
+  }
+}
+
+template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool AK, bool BNC, int ALG, int MINB>
+void launch_cx(const ZgemmParams& p, cudaStream_t stream) {
+  using S = Smem3<BM, BN, BK, AK, BNC>;
+  constexpr int NT = (BM / WM) * (BN / WN) * 32;
+  const size_t smem = static_cast<size_t>(STAGES) * S::STAGE * sizeof(double2) + (BM + BN) * sizeof(int64_t);
+  auto kern = zgemm_cx_kernel<BM, BN, BK, WM, WN, STAGES, AK, BNC, ALG, MINB>;
+  static bool attr_set = false;  // per instantiation
+  if (!attr_set) {
+    PEPSB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    attr_set = true;
+  }
+  const int64_t tiles = ((p.M + BM - 1) / BM) * ((p.N + BN - 1) / BN);
+  dim3 grid(static_cast<unsigned>(tiles), static_cast<unsigned>(p.batch * p.splits));
+  kern<<<grid, NT, smem, stream>>>(p);
+  PEPSB_LAUNCH();
+}
+
+template <bool AK, bool BNC>
+void launch_any3m(const ZgemmParams& p, cudaStream_t stream) {
+  switch (p.cfg) {
+    case 1: launch_cx<64, 72, kBK, 16, 24, kStages, AK, BNC, 3, 1>(p, stream); break;
+    case 2: launch_cx<72, 64, kBK, 24, 16, kStages, AK, BNC, 3, 1>(p, stream); break;
+    case 3: launch_cx<72, 72, kBK, 24, 24, kStages, AK, BNC, 3, 1>(p, stream); break;
+    default: launch_cx<64, 32, kBK, 32, 16, kStages, AK, BNC, 3, 2>(p, stream); break;
+  }
+}
+
+// 4M with complex fragments (one LDS.128 per fragment element, four DMMAs per
+// 8 x 8 complex block into Re / Im accumulators), the CUTLASS z884 scheme.
+template <bool AK, bool BNC>
+void launch_any4c(const ZgemmParams& p, cudaStream_t stream) {
+  switch (p.cfg) {
+    case 1: launch_cx<64, 72, kBK, 32, 24, kStages, AK, BNC, 4, 1>(p, stream); break;
+    case 2: launch_cx<72, 64, kBK, 24, 32, kStages, AK, BNC, 4, 1>(p, stream); break;
+    case 3: launch_cx<72, 72, kBK, 24, 24, kStages, AK, BNC, 4, 1>(p, stream); break;
+    default: launch_cx<64, 64, kBK, 32, 32, kStages, AK, BNC, 4, 2>(p, stream); break;
+  }
+}
+
 }  // namespace
+
+int zgemm_algo() {
+  int v = g_algo.load();
+  if (v < 0) {  // PEPSB_GEMM=4m selects the real-embedding kernels before any option is set
+    const char* e = getenv("PEPSB_GEMM");
+    v = (e && std::string(e) == "4m") ? kGemm4M : (e && std::string(e) == "4c") ? kGemm4C : kGemm3M;
+    g_algo.store(v);
+  }
+  return v;
+}
+
+void zgemm_set_algo(int a) {
+  if (a != kGemm4M && a != kGemm3M && a != kGemm4C)
+    throw Error(kValidationError, "gemm_algo must be 0 (4M), 1 (3M) or 2 (4M complex fragments)");
+  g_algo.store(a);
+}
 
 int64_t zgemm_plan_splits(ZgemmParams& p, int num_sms) {
   if (p.M > 64 && p.M <= 72 && p.N > 72) transpose_problem(p);
   p.cfg = choose_cfg(p.M, p.N);
-  const int64_t bm = kCfgs[p.cfg].bm, bn = kCfgs[p.cfg].bn;
+  p.algo = zgemm_algo();
+  if (p.algo != kGemm4M && p.cfg == 4) p.cfg = 0;
+  // Short-K problems on the 64-wide tiles are epilogue-heavy: the 4M
+  // complex-fragment kernel's 64 x 64 tile (twice the 3M tile) wins there.
+  if (p.algo == kGemm3M && p.cfg == 0 && p.K <= 64) p.algo = kGemm4C;
+  const TileCfg tc = p.algo == kGemm3M ? kCfgs3m[p.cfg] : p.algo == kGemm4C ? kCfgs4c[p.cfg] : kCfgs[p.cfg];
+  const int64_t bm = tc.bm, bn = tc.bn;
   const int64_t tiles = ((p.M + bm - 1) / bm) * ((p.N + bn - 1) / bn) * p.batch;
   // one full wave of resident CTAs (no partial second wave)
-  const int64_t target = static_cast<int64_t>(ctas_per_sm(p.cfg)) * num_sms;
+  const int64_t target =
+      static_cast<int64_t>(p.algo == kGemm4M ? ctas_per_sm(p.cfg) : ctas_per_sm3m(p.cfg)) * num_sms;
   int64_t splits = 1;
   if (tiles < target && p.K > 4 * kBK) {
     splits = std::min<int64_t>(std::max<int64_t>(1, target / tiles), (p.K + 4 * kBK - 1) / (4 * kBK));
@@ -352,16 +723,36 @@ void zgemm_launch(ZgemmParams p, cudaStream_t stream) {
   if (p.cfg < 0 || p.cfg > 4) p.cfg = 0;
   static const bool trace = getenv("PEPSB_TRACE_GEMM") != nullptr;
   if (trace)
-    fprintf(stderr, "[zgemm] M=%ld N=%ld K=%ld batch=%ld cfg=%d splits=%d AK=%d BNC=%d conjA=%d conjB=%d\n",
+    fprintf(stderr, "[zgemm] M=%ld N=%ld K=%ld batch=%ld cfg=%d splits=%d AK=%d BNC=%d conjA=%d conjB=%d algo=%d\n",
             (long)p.M, (long)p.N, (long)p.K, (long)p.batch, p.cfg, p.splits, p.sAk == 1, p.sBj == 1, p.conjA,
-            p.conjB);
+            p.conjB, p.algo);
   const bool ak = p.sAk == 1;
   const bool bnc = p.sBj == 1;
   if (p.K == 0) {
     // empty contraction: C = 0 (or unchanged when accumulating)
     p.splits = 1;
   }
-  if (ak && bnc)
+  if (p.algo == kGemm3M) {
+    if (p.cfg == 4) p.cfg = 0;
+    if (ak && bnc)
+      launch_any3m<true, true>(p, stream);
+    else if (ak && !bnc)
+      launch_any3m<true, false>(p, stream);
+    else if (!ak && bnc)
+      launch_any3m<false, true>(p, stream);
+    else
+      launch_any3m<false, false>(p, stream);
+  } else if (p.algo == kGemm4C) {
+    if (p.cfg == 4) p.cfg = 0;
+    if (ak && bnc)
+      launch_any4c<true, true>(p, stream);
+    else if (ak && !bnc)
+      launch_any4c<true, false>(p, stream);
+    else if (!ak && bnc)
+      launch_any4c<false, true>(p, stream);
+    else
+      launch_any4c<false, false>(p, stream);
+  } else if (ak && bnc)
     launch_any<true, true>(p, stream);
   else if (ak && !bnc)
     launch_any<true, false>(p, stream);

@@ -42,7 +42,16 @@ struct ZgemmParams {
   int64_t kchunk = 0;
   int accumulate = 0;  // C += result instead of C = result
   int cfg = 0;         // tile configuration (set by zgemm_plan_splits)
+  int algo = 0;        // kGemm4M / kGemm3M (set by zgemm_plan_splits)
 };
+
+// Complex product scheme (process-wide): kGemm4M = real embedding, 4 real MACs
+// per complex MAC (the zgemm arithmetic); kGemm3M = Gauss / zgemm3m, 3 real MACs
+// per complex MAC (Im C = (Ar+Ai)(Br+Bi) - ArBr - AiBi).  Default 3M;
+// PEPSB_GEMM=4m or option "gemm_algo" = 0 selects 4M.
+enum GemmAlgo { kGemm4M = 0, kGemm3M = 1, kGemm4C = 2 };
+int zgemm_algo();
+void zgemm_set_algo(int a);
 
 // Launches the GEMM (and the deterministic split-K reduction when needed).
 // `work` is allocated by the caller when splits > 1 (see zgemm_workspace).

@@ -261,3 +261,30 @@ def test_errors_mirror_reference(A):
     with pytest.raises(A.PepsError, match="ValidationError"):
         A.randomized_svd(A.ImplicitOperator([np.eye(2, dtype=complex)], ["rc"], "r", "c"),
                          A.TruncationPolicy(0, 1e-14))
+
+
+@pytest.mark.parametrize("algo", [0, 1, 2], ids=["4m_embed", "3m", "4m_cfrag"])
+def test_gemm_kernels_all_layouts(A, algo):
+    """Every complex GEMM kernel (real embedding, 3M/Gauss, 4M complex
+    fragments) on every tile configuration (64/72-wide, transposed problems,
+    ragged edges, split-K) and operand layout, against numpy at rounding level."""
+    ctx = A.default_context()
+    ctx.set_option("gemm_algo", algo)
+    try:
+        shapes = [(70, 90, 300), (64, 64, 64), (72, 72, 72), (128, 300, 64), (65, 70, 17), (5, 7, 3),
+                  (200, 72, 130), (72, 200, 33), (64, 72, 64), (72, 64, 48), (33, 65, 129), (1, 1, 1),
+                  (8, 300, 256), (300, 8, 256), (72, 72, 5000)]
+        for (m, n, k) in shapes:
+            for sp in ["ik,kj->ij", "ki,kj->ij", "ik,jk->ij", "ki,jk->ij"]:
+                a = O.random_tensor((m, k) if sp[:2] == "ik" else (k, m), m * 7 + k)
+                b = O.random_tensor((k, n) if sp[3:5] == "kj" else (n, k), n * 5 + k)
+                got = A.contract(sp, a, b).numpy()
+                ref = np.einsum(sp, a, b)
+                assert np.abs(got - ref).max() <= 1e-12 * np.abs(ref).max(), (algo, sp, m, n, k)
+            # conjugated operand (the adjoint applies of the implicit operator)
+            a = O.random_tensor((m, k), m + k)
+            b = O.random_tensor((k, n), n + k)
+            got = A.contract("ik,kj->ij", a.conj(), b).numpy()
+            assert np.abs(got - a.conj() @ b).max() <= 1e-12 * np.abs(a.conj() @ b).max()
+    finally:
+        ctx.set_option("gemm_algo", 1)
