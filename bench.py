@@ -278,14 +278,21 @@ def run_b200(args, rank, world, local_rank):
     value = world * flops / dt / 1e12
     peak = _fp64_peak()
     g = rep["gemm"]
-    achieved = g["flops"] / (g["ms"] / 1e3) / 1e12 if g["ms"] > 0 else None
+    # achieved = real flops the DMMAs execute (3M launches: 6 per complex MAC,
+    # 4M launches: 8) / device time -- the tensor-pipe roofline; the algorithmic
+    # rate (8 per complex MAC, the reference's count) is reported beside it.
+    achieved = g["exec_flops"] / (g["ms"] / 1e3) / 1e12 if g["ms"] > 0 else None
+    achieved_alg = g["flops"] / (g["ms"] / 1e3) / 1e12 if g["ms"] > 0 else None
     total_ms = sum(v["ms"] for v in rep.values())
     roof = {"bound": "tensor", "achieved": achieved, "peak": peak["tflops"], "unit": "TFLOP/s",
             "frac": achieved / peak["tflops"] if achieved else None, "traffic": _ncu_traffic(),
-            "kernel": "zgemm_dmma_kernel (complex FP64 DMMA.8x8x4 GEMM, all instantiations)",
+            "kernel": "zgemm_cx_kernel (complex FP64 GEMM on DMMA.8x8x4: 3M/Gauss and 4M complex-fragment "
+                      "instantiations, all launches of the step)",
+            "achieved_algorithmic": achieved_alg,
             "kernel_share_of_step": g["ms"] / total_ms if total_ms else None,
             "launches_per_step": g["launches"], "avg_launch_ms": g["ms"] / max(1, g["launches"]),
-            "algorithmic_flops_per_step": g["flops"], "peak_source": peak["source"],
+            "algorithmic_flops_per_step": g["flops"], "executed_flops_per_step": g["exec_flops"],
+            "peak_source": peak["source"],
             "whole_step_frac": (flops / dt / 1e12) / peak["tflops"],
             "breakdown_ms": {k: round(v["ms"], 3) for k, v in rep.items()}}
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,

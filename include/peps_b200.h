@@ -91,6 +91,9 @@ int pepsb_ctx_reset_counters(pepsb_ctx* ctx);
  * {launches, device ms, algorithmic real flops, algorithmic bytes}. */
 int pepsb_ctx_profile(pepsb_ctx* ctx, int enable);
 int pepsb_ctx_profile_report(pepsb_ctx* ctx, double* out16);
+/* Same with a fifth value per kind: the real flops the hardware executes (the
+ * 3M GEMM runs 6 real flops per complex MAC where the algorithmic count is 8). */
+int pepsb_ctx_profile_report_ex(pepsb_ctx* ctx, double* out20);
 /* Per-launch records of the profile (kind, device ms, algorithmic flops) x n; returns n */
 int pepsb_ctx_profile_records(pepsb_ctx* ctx, double* out, int cap);
 /* Diagnostics: device status word idx (word 7 = cumulative Jacobi sweeps). */

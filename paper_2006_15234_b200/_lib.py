@@ -53,6 +53,7 @@ _SIGS = {
     "pepsb_ctx_profile_records": (C.c_int, [_VP, C.POINTER(C.c_double), C.c_int]),
     "pepsb_ctx_profile": (C.c_int, [_VP, C.c_int]),
     "pepsb_ctx_profile_report": (C.c_int, [_VP, C.POINTER(C.c_double)]),
+    "pepsb_ctx_profile_report_ex": (C.c_int, [_VP, C.POINTER(C.c_double)]),
     "pepsb_tensor_from_host": (C.c_int, [_VP, C.c_int, C.POINTER(C.c_int64), _VP, C.POINTER(_VP)]),
     "pepsb_tensor_from_device": (C.c_int, [_VP, C.c_int, C.POINTER(C.c_int64), _VP, C.POINTER(_VP)]),
     "pepsb_tensor_ndim": (C.c_int, [_VP]),

@@ -114,11 +114,11 @@ class Context:
         check(lib().pepsb_ctx_profile(self.h, int(bool(enable))))
 
     def profile_report(self) -> dict:
-        a = (C.c_double * 16)()
-        check(lib().pepsb_ctx_profile_report(self.h, a))
+        a = (C.c_double * 20)()
+        check(lib().pepsb_ctx_profile_report_ex(self.h, a))
         kinds = ["gemm", "small", "gather", "other"]
-        return {k: dict(launches=int(a[4 * i]), ms=a[4 * i + 1], flops=a[4 * i + 2], bytes=a[4 * i + 3])
-                for i, k in enumerate(kinds)}
+        return {k: dict(launches=int(a[5 * i]), ms=a[5 * i + 1], flops=a[5 * i + 2], bytes=a[5 * i + 3],
+                        exec_flops=a[5 * i + 4]) for i, k in enumerate(kinds)}
 
     @property
     def stream(self) -> int:

@@ -220,6 +220,13 @@ int pepsb_ctx_profile(pepsb_ctx* c, int enable) {
   });
 }
 
+int pepsb_ctx_profile_report_ex(pepsb_ctx* c, double* out20) {
+  return guard([&] {
+    need(c, "ctx");
+    c->ctx->profile_report_ex(out20);
+  });
+}
+
 int pepsb_ctx_profile_report(pepsb_ctx* c, double* out16) {
   return guard([&] {
     need(c, "ctx");

@@ -169,6 +169,20 @@ void Ctx::profile_clear() {
   prof.clear();
 }
 
+void Ctx::profile_report_ex(double* out) {
+  sync();
+  for (int i = 0; i < 5 * kProfKinds; ++i) out[i] = 0.0;
+  for (auto& r : prof) {
+    float ms = 0.f;
+    PEPSB_CUDA(cudaEventElapsedTime(&ms, r.a, r.b));
+    out[5 * r.kind + 0] += 1.0;
+    out[5 * r.kind + 1] += ms;
+    out[5 * r.kind + 2] += r.flops;
+    out[5 * r.kind + 3] += r.bytes;
+    out[5 * r.kind + 4] += r.exec_flops;
+  }
+}
+
 void Ctx::profile_report(double* out) {
   sync();
   for (int i = 0; i < 4 * kProfKinds; ++i) out[i] = 0.0;
@@ -182,9 +196,9 @@ void Ctx::profile_report(double* out) {
   }
 }
 
-ProfScope::ProfScope(Ctx& c, int kind, double flops, double bytes) : ctx(c) {
+ProfScope::ProfScope(Ctx& c, int kind, double flops, double bytes, double exec_flops) : ctx(c) {
   if (!ctx.profiling) return;
-  Ctx::ProfRec r{ctx.take_event(), ctx.take_event(), kind, flops, bytes};
+  Ctx::ProfRec r{ctx.take_event(), ctx.take_event(), kind, flops, bytes, exec_flops < 0.0 ? flops : exec_flops};
   PEPSB_CUDA(cudaEventRecord(r.a, ctx.stream));
   ctx.prof.push_back(r);
   idx = static_cast<int>(ctx.prof.size()) - 1;

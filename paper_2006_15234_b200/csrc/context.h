@@ -133,18 +133,20 @@ class Ctx {
     cudaEvent_t a, b;
     int kind;
     double flops, bytes;
+    double exec_flops;  // flops the hardware executes (3M GEMM: 6 per complex MAC, not 8)
   };
   bool profiling = false;
   std::vector<ProfRec> prof;
   std::vector<cudaEvent_t> event_pool;
   cudaEvent_t take_event();
   void profile_report(double* out);  // per kind: count, ms, flops, bytes
+  void profile_report_ex(double* out);  // per kind: count, ms, flops, bytes, executed flops
   void profile_clear();
 };
 
 // RAII device-time scope (no-op unless ctx.profiling).
 struct ProfScope {
-  ProfScope(Ctx& c, int kind, double flops = 0.0, double bytes = 0.0);
+  ProfScope(Ctx& c, int kind, double flops = 0.0, double bytes = 0.0, double exec_flops = -1.0);
   ~ProfScope();
   Ctx& ctx;
   int idx = -1;

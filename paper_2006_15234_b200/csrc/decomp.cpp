@@ -73,7 +73,7 @@ void mm(Ctx& ctx, double2* C, const double2* A, bool transA, bool conjA, const d
     p.work = work->p;
   }
   {
-    ProfScope ps(ctx, Ctx::kProfGemm, 8.0 * M * N * K, 16.0 * (M * K + K * N + M * N));
+    ProfScope ps(ctx, Ctx::kProfGemm, 8.0 * M * N * K, 16.0 * (M * K + K * N + M * N), zgemm_exec_flops(p));
     zgemm_launch(p, ctx.stream);
   }
   ctx.launches += p.splits > 1 ? 2 : 1;

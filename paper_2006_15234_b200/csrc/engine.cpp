@@ -224,7 +224,7 @@ LTensor pairwise_gemm(Ctx& ctx, const LTensor& A, const LTensor& B, const std::s
   }
   {
     ProfScope ps(ctx, Ctx::kProfGemm, 8.0 * p.batch * p.M * p.N * p.K,
-                 16.0 * (p.batch * (p.M * p.K + p.K * p.N + p.M * p.N)));
+                 16.0 * (p.batch * (p.M * p.K + p.K * p.N + p.M * p.N)), zgemm_exec_flops(p));
     zgemm_launch(p, ctx.stream);
   }
   ctx.launches += p.splits > 1 ? 2 : 1;

@@ -51,6 +51,10 @@ struct ZgemmParams {
 // PEPSB_GEMM=4m or option "gemm_algo" = 0 selects 4M.
 enum GemmAlgo { kGemm4M = 0, kGemm3M = 1, kGemm4C = 2 };
 int zgemm_algo();
+// Real flops the DMMAs execute for a planned problem (8 per complex MAC, 6 for 3M).
+inline double zgemm_exec_flops(const ZgemmParams& p) {
+  return (p.algo == kGemm3M ? 6.0 : 8.0) * static_cast<double>(p.batch) * p.M * p.N * p.K;
+}
 void zgemm_set_algo(int a);
 
 // Launches the GEMM (and the deterministic split-K reduction when needed).
