@@ -429,7 +429,9 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32, MINB)
     for (int u = 0; u < UB; ++u)
       if (b_o0 + u * BOS < BOUT && n0 + b_o0 + u * BOS < p.N) b_ok |= 1u << u;
   }
-  auto load_stage = [&](int slot, int64_t kt) {
+  // Issues part `part` of `nparts` of stage kt's copies (the main loop spreads
+  // one stage over the k-steps of the previous tile, CUTLASS-style).
+  auto load_stage = [&](int slot, int64_t kt, int part, int nparts) {
     double2* As = smem + slot * S::STAGE;
     double2* Bs = As + S::A_ELEMS;
     const int64_t k0 = kbeg + kt * BK;
@@ -437,12 +439,13 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32, MINB)
       const double2* src = A + a_base + kt * BK * p.sAk;
 #pragma unroll
       for (int u = 0; u < UA; ++u) {
+        if (u < part * UA / nparts || u >= (part + 1) * UA / nparts) continue;
         const int o = a_o0 + u * AOS;
         if ((AOUT % AOS) != 0 && o >= AOUT) break;  // past the tile (a zero-fill copy would land in B)
         const bool ok = AK ? (((a_ok >> u) & 1u) && k0 + a_in < kend) : (a_ok && k0 + o < kend);
         cp_async16(As + o * S::LDA + a_in, ok ? src + u * a_ustr : A, ok);
       }
-    } else {
+    } else if (part == 0) {
 #pragma unroll
       for (int e = tid; e < BM * BK; e += NT) {
         int i, k;
@@ -458,12 +461,13 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32, MINB)
       const double2* src = B + b_base + kt * BK * p.sBk;
 #pragma unroll
       for (int u = 0; u < UB; ++u) {
+        if (u < part * UB / nparts || u >= (part + 1) * UB / nparts) continue;
         const int o = b_o0 + u * BOS;
         if ((BOUT % BOS) != 0 && o >= BOUT) break;  // past the tile (would spill into the next stage)
         const bool ok = BNC ? (b_ok && k0 + o < kend) : (((b_ok >> u) & 1u) && k0 + b_in < kend);
         cp_async16(Bs + o * S::LDB + b_in, ok ? src + u * b_ustr : B, ok);
       }
-    } else {
+    } else if (part == 0) {
 #pragma unroll
       for (int e = tid; e < BK * BN; e += NT) {
         int k, j;
@@ -498,8 +502,8 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32, MINB)
       for (int t = 0; t < NACC; ++t) acc[a][b][t][0] = acc[a][b][t][1] = 0.0;
 
 #pragma unroll
-  for (int s = 0; s < STAGES; ++s) {  // every slot filled up front
-    if (s < nk) load_stage(s, s);
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < nk) load_stage(s, s, 0, 1);
     cp_async_commit();
   }
 
@@ -563,38 +567,53 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32, MINB)
       }
 #pragma unroll
       for (int b = 0; b < FN; ++b) bi[b] = flip(fb[buf][b].y, sgb);
+      // pass-major order: the two DMMAs into the same accumulator are
+      // FM * FN * 2 instructions apart (DMMA accumulator latency)
 #pragma unroll
       for (int a = 0; a < FM; ++a)
 #pragma unroll
         for (int b = 0; b < FN; ++b) {
           dmma884(acc[a][b][0][0], acc[a][b][0][1], fa[buf][a].x, fb[buf][b].x);
           dmma884(acc[a][b][1][0], acc[a][b][1][1], fa[buf][a].x, bi[b]);
+        }
+#pragma unroll
+      for (int a = 0; a < FM; ++a)
+#pragma unroll
+        for (int b = 0; b < FN; ++b) {
           dmma884(acc[a][b][0][0], acc[a][b][0][1], nai[a], bi[b]);
           dmma884(acc[a][b][1][0], acc[a][b][1][1], ai[a], fb[buf][b].x);
         }
     }
   };
   constexpr int KS = BK / 4;
+  // Stage kt + STAGES - 1 is copied into the slot freed by the previous tile's
+  // closing barrier, a quarter per k-step of tile kt; one barrier per tile.
   if (nk > 0) {
-    cp_async_wait<STAGES - 1>();
+    cp_async_wait<STAGES - 2>();
     __syncthreads();
     load_frags(0, 0, 0);
   }
   static_assert(KS % 2 == 0, "k steps per tile must be even (static fragment buffers)");
   for (int64_t kt = 0; kt < nk; ++kt) {
     const int slot = static_cast<int>(kt % STAGES);
-#pragma unroll 1
+    const int64_t pf = kt + STAGES - 1;
+    const int pslot = static_cast<int>(pf % STAGES);
+    const bool do_pf = pf < nk;
+#pragma unroll
     for (int kp = 0; kp < KS; kp += 2) {
       load_frags(1, slot, kp + 1);
+      if (do_pf) load_stage(pslot, pf, kp, KS);
       compute(0);
+      if (do_pf) load_stage(pslot, pf, kp + 1, KS);
       if (kp + 2 < KS) {
         load_frags(0, slot, kp + 2);
-      } else if (kt + 1 < nk) {
-        cp_async_wait<STAGES - 2>();
-        __syncthreads();
-        if (kt + STAGES < nk) load_stage(slot, kt + STAGES);
+      } else {
         cp_async_commit();
-        load_frags(0, static_cast<int>((kt + 1) % STAGES), 0);
+        if (kt + 1 < nk) {
+          cp_async_wait<STAGES - 2>();
+          __syncthreads();
+          load_frags(0, static_cast<int>((kt + 1) % STAGES), 0);
+        }
       }
       compute(1);
     }
