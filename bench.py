@@ -353,6 +353,80 @@ def _ncu_traffic():
         return None
 
 
+def run_sharded(args, rank, world, local_rank):
+    """--sharded: ONE config-2 row absorb split across the N ranks along the
+    boundary bond (paper_2006_15234_b200/sharded.py, NCCL collectives);
+    scaling "strong", value = the row's algorithmic flops / max-over-ranks time."""
+    import torch
+    import torch.distributed as dist
+    import paper_2006_15234_b200.api as A
+    from paper_2006_15234_b200 import sharded as SH
+
+    torch.cuda.set_device(local_rank)
+    ctx = A.Context(local_rank)
+    stream = torch.cuda.ExternalStream(ctx.stream, device=torch.device("cuda", local_rank))
+    ops = SH.DeviceOps(SH.Comm(), ctx)
+    c2 = inputs.config2(seed=2)
+    row = [A.to_device(c2["sites"][1 * L + c], ctx) for c in range(L)]
+    tops = [A.to_device(t, ctx) for t in c2["top"]]
+    opt = A.ContractOption.two_layer_opt(M, c2["seed"], Q, OS)
+
+    def step(tp, rw):
+        return SH.sharded_two_layer_apply_row(ops, tp, c2["phys"], rw, rw, 1, M, opt.seed, Q, OS, True, 0x20)
+
+    for _ in range(max(args.warmup, 0)):
+        out = step(tops, row)
+    ctx.sync()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ctx.reset_counters()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            out = step(tops, row)
+        e1.record(stream)
+        ctx.sync()
+        torch.cuda.synchronize()
+    dt = e0.elapsed_time(e1) / 1e3 / args.steps
+    launches = ctx.counters()["launches"]
+    # e2e: inputs from pinned host memory, boundary copied back every step
+    pinned_in = [torch.from_numpy(np.ascontiguousarray(x).view(np.float64)).pin_memory()
+                 for x in [c2["sites"][1 * L + c] for c in range(L)] + list(c2["top"])]
+    shapes = [c2["sites"][1 * L + c].shape for c in range(L)] + [t.shape for t in c2["top"]]
+    h2d = sum(p.numel() * 8 for p in pinned_in)
+    d2h = 0
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        dev = [A.DeviceTensor(_from_pinned(ctx, p, sh), ctx) for p, sh in zip(pinned_in, shapes)]
+        o, _ = step(dev[L:], dev[:L])
+        host = [x.numpy() for x in o]
+        d2h = sum(h.nbytes for h in host)
+    ctx.sync()
+    dt_e2e = (time.perf_counter() - t0) / args.steps
+    if world > 1:
+        t = torch.tensor([dt, dt_e2e], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dt, dt_e2e = float(t[0]), float(t[1])
+    if rank != 0:
+        return 0
+    flops = alg_flops_row()
+    line = {"metric": METRIC, "value": flops / dt / 1e12, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "c128", "data": "synthetic (seeded N(0,1) Box-Muller over SplitMix64)",
+            "config": workload_config({"parallelism": f"bond-sharded x{world} (t / s of the boundary bond)",
+                                       "s_per_row_absorb": dt}),
+            "clocks": clk.summary(), "gpu_launches": launches,
+            "e2e": {"value": flops / dt_e2e / 1e12, "unit": UNIT, "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h, "s_per_step": dt_e2e}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -360,6 +434,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--sharded", action="store_true",
+                    help="N>1: split one row absorb across the ranks along the boundary bond (strong scaling) "
+                         "instead of N independent replicas")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -372,6 +449,8 @@ def main():
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl")
     try:
+        if args.sharded:
+            return run_sharded(args, rank, world, local_rank)
         return run_b200(args, rank, world, local_rank)
     finally:
         if world > 1:

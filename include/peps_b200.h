@@ -127,6 +127,29 @@ int pepsb_implicit(pepsb_ctx* ctx, int n, pepsb_tensor* const* ts, const char* l
 /* gram_orthogonalize(Tensor, split) (decomposition.hpp:52) */
 int pepsb_gram_orthogonalize(pepsb_ctx* ctx, const pepsb_tensor* a, int split, pepsb_tensor** q, pepsb_tensor** r);
 
+/* ---- building blocks of the bond-sharded einsumsvd (paper_2006_15234_b200/sharded.py) */
+/* Slice [start, start+count) along `axis` of random_tensor(shape, seed) (tensor.cpp:192-201):
+ * bit-identical to the same elements of the full tensor (counter-based stream). */
+int pepsb_random_slice(pepsb_ctx* ctx, int ndim, const int64_t* shape, int axis, int64_t start, int64_t count,
+                       uint64_t seed, int real, pepsb_tensor** out);
+int pepsb_tensor_conj(pepsb_ctx* ctx, const pepsb_tensor* a, pepsb_tensor** out);
+/* Copy of [start, start+count) along `axis`. */
+int pepsb_tensor_slice(pepsb_ctx* ctx, const pepsb_tensor* a, int axis, int64_t start, int64_t count,
+                       pepsb_tensor** out);
+/* New handle sharing the buffer with a different shape (same element count). */
+int pepsb_tensor_reshape(const pepsb_tensor* a, int ndim, const int64_t* shape, pepsb_tensor** out);
+/* Device pointer of the tensor's contiguous row-major complex128 buffer. */
+int pepsb_tensor_data_ptr(const pepsb_tensor* a, void** ptr);
+/* G = Z^H Z over all leading axes of z (the last axis is the probe axis). */
+int pepsb_gram(pepsb_ctx* ctx, const pepsb_tensor* z, pepsb_tensor** g);
+/* gram_factors (decomposition.cpp:128-156) of a k x k Gram matrix: P = X l^-1/2,
+ * R = l^1/2 X^H, X (phase-fixed eigenvectors), lam (descending), deficient flags. */
+int pepsb_gram_factors(pepsb_ctx* ctx, const pepsb_tensor* g, pepsb_tensor** p, pepsb_tensor** r,
+                       pepsb_tensor** vecs, double* lam, int* deficient, int64_t cap);
+/* Projected SVD of B = Z^H (the rSVD's last stage): k x k left vectors and sigma. */
+int pepsb_projected_svd(pepsb_ctx* ctx, const pepsb_tensor* z, int64_t target, pepsb_tensor** ut, double* s,
+                        int64_t cap);
+
 /* eigh(Tensor) (linalg.hpp:41, linalg.cpp:256-295): values descending (capacity cap),
  * vectors n x n with column j the phase-fixed eigenvector j.  n <= 256.  The
  * solver is process-wide option "eig_solver" (0 divide and conquer, 1 Jacobi). */

@@ -68,6 +68,16 @@ _SIGS = {
                                  C.POINTER(_VP)]),
     "pepsb_gram_orthogonalize": (C.c_int, [_VP, _VP, C.c_int, C.POINTER(_VP), C.POINTER(_VP)]),
     "pepsb_eigh": (C.c_int, [_VP, _VP, C.POINTER(C.c_double), C.c_int64, C.POINTER(_VP)]),
+    "pepsb_random_slice": (C.c_int, [_VP, C.c_int, C.POINTER(C.c_int64), C.c_int, C.c_int64, C.c_int64, C.c_uint64,
+                                     C.c_int, C.POINTER(_VP)]),
+    "pepsb_tensor_conj": (C.c_int, [_VP, _VP, C.POINTER(_VP)]),
+    "pepsb_tensor_slice": (C.c_int, [_VP, _VP, C.c_int, C.c_int64, C.c_int64, C.POINTER(_VP)]),
+    "pepsb_tensor_reshape": (C.c_int, [_VP, C.c_int, C.POINTER(C.c_int64), C.POINTER(_VP)]),
+    "pepsb_tensor_data_ptr": (C.c_int, [_VP, C.POINTER(_VP)]),
+    "pepsb_gram": (C.c_int, [_VP, _VP, C.POINTER(_VP)]),
+    "pepsb_gram_factors": (C.c_int, [_VP, _VP, C.POINTER(_VP), C.POINTER(_VP), C.POINTER(_VP), C.POINTER(C.c_double),
+                                     C.POINTER(C.c_int), C.c_int64]),
+    "pepsb_projected_svd": (C.c_int, [_VP, _VP, C.c_int64, C.POINTER(_VP), C.POINTER(C.c_double), C.c_int64]),
     "pepsb_svd": (C.c_int, [_VP, _VP, C.c_int, C.POINTER(_VP), C.POINTER(C.c_double), C.c_int64,
                             C.POINTER(C.c_int64), C.POINTER(_VP)]),
     "pepsb_randomized_svd": (C.c_int, [_VP, C.c_int, C.POINTER(_VP), C.c_char_p, C.c_char_p, C.c_char_p,

@@ -171,6 +171,36 @@ class DeviceTensor:
     def __repr__(self):
         return f"DeviceTensor{self.shape}"
 
+    @property
+    def data_ptr(self) -> int:
+        p = _VP()
+        check(lib().pepsb_tensor_data_ptr(self.h, C.byref(p)))
+        return int(p.value or 0)
+
+    @property
+    def __cuda_array_interface__(self):
+        """Zero-copy view for torch / NCCL (the library stream must be idle: ctx.sync())."""
+        return {"shape": self.shape, "typestr": "<c16", "data": (self.data_ptr, False), "version": 3,
+                "strides": None}
+
+    def reshape(self, *shape) -> "DeviceTensor":
+        if len(shape) == 1 and isinstance(shape[0], (tuple, list)):
+            shape = tuple(shape[0])
+        shp = (C.c_int64 * max(1, len(shape)))(*shape)
+        h = _VP()
+        check(lib().pepsb_tensor_reshape(self.h, len(shape), shp, C.byref(h)))
+        return DeviceTensor(h, self.ctx)
+
+    def slice(self, axis: int, start: int, stop: int) -> "DeviceTensor":
+        h = _VP()
+        check(lib().pepsb_tensor_slice(self.ctx.h, self.h, int(axis), int(start), int(stop - start), C.byref(h)))
+        return DeviceTensor(h, self.ctx)
+
+    def conj(self) -> "DeviceTensor":
+        h = _VP()
+        check(lib().pepsb_tensor_conj(self.ctx.h, self.h, C.byref(h)))
+        return DeviceTensor(h, self.ctx)
+
 
 def to_device(a, ctx: Optional[Context] = None) -> DeviceTensor:
     ctx = ctx or default_context()
@@ -180,6 +210,15 @@ def to_device(a, ctx: Optional[Context] = None) -> DeviceTensor:
     shp = (C.c_int64 * max(1, a.ndim))(*a.shape)
     h = _VP()
     check(lib().pepsb_tensor_from_host(ctx.h, a.ndim, shp, a.ctypes.data_as(_VP), C.byref(h)))
+    return DeviceTensor(h, ctx)
+
+
+def from_device_ptr(ptr: int, shape, ctx: Optional[Context] = None) -> DeviceTensor:
+    """Copy a contiguous complex128 device buffer (e.g. a torch tensor's) into a library tensor."""
+    ctx = ctx or default_context()
+    shp = (C.c_int64 * max(1, len(shape)))(*shape)
+    h = _VP()
+    check(lib().pepsb_tensor_from_device(ctx.h, len(shape), shp, _VP(int(ptr)), C.byref(h)))
     return DeviceTensor(h, ctx)
 
 
@@ -304,6 +343,52 @@ def eigh(a, ctx: Optional[Context] = None):
     v = _VP()
     check(lib().pepsb_eigh(ctx.h, d.h, w.ctypes.data_as(C.POINTER(C.c_double)), len(w), C.byref(v)))
     return w[:n].copy(), DeviceTensor(v, ctx)
+
+
+def random_slice(shape, axis: int, start: int, count: int, seed: int, real: bool = False,
+                 ctx: Optional[Context] = None) -> DeviceTensor:
+    """Elements [start, start+count) along `axis` of random_tensor(shape, seed),
+    bit-identical to slicing the full tensor (tensor.cpp:192-201 counter stream)."""
+    ctx = ctx or default_context()
+    shp = (C.c_int64 * max(1, len(shape)))(*shape)
+    h = _VP()
+    check(lib().pepsb_random_slice(ctx.h, len(shape), shp, int(axis), int(start), int(count),
+                                   C.c_uint64(seed & 0xFFFFFFFFFFFFFFFF), int(real), C.byref(h)))
+    return DeviceTensor(h, ctx)
+
+
+def gram(z, ctx: Optional[Context] = None) -> DeviceTensor:
+    """G = Z^H Z over the leading axes of z (last axis = probe axis)."""
+    ctx = ctx or default_context()
+    d = to_device(z, ctx)
+    h = _VP()
+    check(lib().pepsb_gram(ctx.h, d.h, C.byref(h)))
+    return DeviceTensor(h, ctx)
+
+
+def gram_factors(g, ctx: Optional[Context] = None):
+    """decomposition.cpp:128-156 on a given Gram matrix: (P, R, X, lam, deficient)."""
+    ctx = ctx or default_context()
+    d = to_device(g, ctx)
+    k = d.shape[0]
+    lam = np.zeros(k)
+    dfc = np.zeros(k, dtype=np.int32)
+    p, r, x = _VP(), _VP(), _VP()
+    check(lib().pepsb_gram_factors(ctx.h, d.h, C.byref(p), C.byref(r), C.byref(x),
+                                   lam.ctypes.data_as(C.POINTER(C.c_double)),
+                                   dfc.ctypes.data_as(C.POINTER(C.c_int)), k))
+    return DeviceTensor(p, ctx), DeviceTensor(r, ctx), DeviceTensor(x, ctx), lam, dfc.astype(bool)
+
+
+def projected_svd(z, target: int, ctx: Optional[Context] = None):
+    """Last rSVD stage: SVD of B = Z^H -> (Ut k x k left vectors, sigma)."""
+    ctx = ctx or default_context()
+    d = to_device(z, ctx)
+    k = d.shape[-1]
+    s = np.zeros(k)
+    u = _VP()
+    check(lib().pepsb_projected_svd(ctx.h, d.h, int(target), C.byref(u), s.ctypes.data_as(C.POINTER(C.c_double)), k))
+    return DeviceTensor(u, ctx), s
 
 
 def svd(a, split: int, ctx: Optional[Context] = None):

@@ -380,6 +380,110 @@ int pepsb_gram_orthogonalize(pepsb_ctx* c, const pepsb_tensor* a, int split, pep
   });
 }
 
+int pepsb_random_slice(pepsb_ctx* c, int ndim, const int64_t* shape, int axis, int64_t start, int64_t count,
+                       uint64_t seed, int real, pepsb_tensor** out) {
+  return guard([&] {
+    need(c, "ctx");
+    std::vector<int64_t> full = shape_of(ndim, shape);
+    if (axis < 0 || axis >= ndim) throw Error(kShapeError, "random_slice: axis out of range");
+    if (start < 0 || count < 0 || start + count > full[axis]) throw Error(kShapeError, "random_slice: bad range");
+    std::vector<int64_t> lstr = row_major_strides(full);
+    std::vector<int64_t> ext = full;
+    ext[axis] = count;
+    DTensor t = c->ctx->empty(ext);
+    if (t.size() > 0) {
+      random_fill(t.data(), ndim, ext.data(), lstr.data(), seed, real, c->ctx->stream,
+                  static_cast<uint64_t>(start) * static_cast<uint64_t>(lstr[axis]));
+      ++c->ctx->launches;
+    }
+    *out = wrap(t);
+  });
+}
+
+int pepsb_tensor_conj(pepsb_ctx* c, const pepsb_tensor* a, pepsb_tensor** out) {
+  return guard([&] {
+    need(c, "ctx");
+    need(a, "tensor");
+    std::string lab;
+    for (size_t i = 0; i < a->t.shape.size(); ++i) lab += static_cast<char>('a' + i);
+    LTensor l = reduce_to(*c->ctx, as_labelled(a->t, lab, true), lab);
+    *out = wrap(materialize(*c->ctx, l, lab));
+  });
+}
+
+int pepsb_tensor_slice(pepsb_ctx* c, const pepsb_tensor* a, int axis, int64_t start, int64_t count,
+                       pepsb_tensor** out) {
+  return guard([&] {
+    need(c, "ctx");
+    need(a, "tensor");
+    const int nd = static_cast<int>(a->t.shape.size());
+    if (axis < 0 || axis >= nd) throw Error(kShapeError, "slice: axis out of range");
+    if (start < 0 || count < 0 || start + count > a->t.shape[axis]) throw Error(kShapeError, "slice: bad range");
+    std::string lab;
+    for (int i = 0; i < nd; ++i) lab += static_cast<char>('a' + i);
+    LTensor l = as_labelled(a->t, lab);
+    l.ptr += start * l.str[axis];
+    l.ext[axis] = count;
+    if (l.size() == 0) {
+      *out = wrap(c->ctx->empty(l.ext));
+      return;
+    }
+    *out = wrap(materialize(*c->ctx, reduce_to(*c->ctx, l, lab), lab));
+  });
+}
+
+int pepsb_tensor_reshape(const pepsb_tensor* a, int ndim, const int64_t* shape, pepsb_tensor** out) {
+  return guard([&] {
+    need(a, "tensor");
+    DTensor t = a->t;
+    t.shape = shape_of(ndim, shape);
+    if (t.size() != a->t.size()) throw Error(kShapeError, "reshape changes the element count");
+    *out = wrap(t);
+  });
+}
+
+int pepsb_tensor_data_ptr(const pepsb_tensor* a, void** ptr) {
+  return guard([&] {
+    need(a, "tensor");
+    *ptr = a->t.data();
+  });
+}
+
+int pepsb_gram(pepsb_ctx* c, const pepsb_tensor* z, pepsb_tensor** g) {
+  return guard([&] {
+    need(c, "ctx");
+    need(z, "tensor");
+    *g = wrap(gram_matrix(*c->ctx, z->t));
+  });
+}
+
+int pepsb_gram_factors(pepsb_ctx* c, const pepsb_tensor* g, pepsb_tensor** p, pepsb_tensor** r, pepsb_tensor** vecs,
+                       double* lam, int* deficient, int64_t cap) {
+  return guard([&] {
+    need(c, "ctx");
+    need(g, "tensor");
+    GramFactorsD f = gram_factors_full(*c->ctx, g->t);
+    if (static_cast<int64_t>(f.lam.size()) > cap) throw Error(kValidationError, "buffer too small");
+    std::memcpy(lam, f.lam.data(), f.lam.size() * sizeof(double));
+    std::memcpy(deficient, f.deficient.data(), f.deficient.size() * sizeof(int));
+    *p = wrap(f.P);
+    *r = wrap(f.R);
+    *vecs = wrap(f.vecs);
+  });
+}
+
+int pepsb_projected_svd(pepsb_ctx* c, const pepsb_tensor* z, int64_t target, pepsb_tensor** ut, double* s,
+                        int64_t cap) {
+  return guard([&] {
+    need(c, "ctx");
+    need(z, "tensor");
+    auto [u, sv] = projected_svd_full(*c->ctx, z->t, target);
+    if (static_cast<int64_t>(sv.size()) > cap) throw Error(kValidationError, "buffer too small");
+    std::memcpy(s, sv.data(), sv.size() * sizeof(double));
+    *ut = wrap(u);
+  });
+}
+
 int pepsb_eigh(pepsb_ctx* c, const pepsb_tensor* a, double* values, int64_t cap, pepsb_tensor** vectors) {
   return guard([&] {
     need(c, "ctx");

@@ -582,6 +582,59 @@ std::pair<DTensor, DTensor> gram_orthogonalize(Ctx& ctx, const DTensor& a, int s
   return {Q, R};
 }
 
+// ---------------------------------------------------------------------------- sharded-driver blocks
+
+DTensor gram_matrix(Ctx& ctx, const DTensor& z) {
+  if (z.shape.empty()) throw Error(kShapeError, "gram_matrix needs a tensor with a column axis");
+  const int64_t k = z.shape.back();
+  const int64_t rows = k ? z.size() / k : 0;
+  DTensor g = ctx.zeros({k, k});
+  if (rows > 0 && k > 0) mm(ctx, g.data(), z.data(), true, true, z.data(), false, false, k, k, rows);
+  return g;
+}
+
+GramFactorsD gram_factors_full(Ctx& ctx, const DTensor& g) {
+  if (g.shape.size() != 2 || g.shape[0] != g.shape[1]) throw Error(kShapeError, "gram_factors needs k x k");
+  const int64_t k = g.shape[0];
+  if (k < 1 || k > 256) throw Error(kShapeError, "gram_factors: 1 <= k <= 256");
+  clear_status(ctx);
+  GramFactorsD out;
+  out.P = ctx.empty({k, k});
+  out.R = ctx.empty({k, k});
+  out.vecs = ctx.empty({k, k});
+  BufPtr def = ctx.alloc(k / 4 + 2), lam = ctx.alloc(k / 2 + 1), work;
+  if (2 * k * (k + 1) * 16 > 176 * 1024) work = ctx.alloc(2 * k * (k + 1));
+  int* d_def = reinterpret_cast<int*>(def->p);
+  {
+    ProfScope ps_(ctx, Ctx::kProfSmall);
+    gram_factors(g.data(), static_cast<int>(k), out.P.data(), out.R.data(), d_def, d_def + k, ctx.d_status,
+                 work ? work->p : nullptr, ctx.stream, reinterpret_cast<double*>(lam->p), out.vecs.data());
+  }
+  ++ctx.launches;
+  out.lam.resize(k);
+  out.deficient.resize(k);
+  PEPSB_CUDA(cudaMemcpyAsync(out.lam.data(), lam->p, k * sizeof(double), cudaMemcpyDeviceToHost, ctx.stream));
+  PEPSB_CUDA(cudaMemcpyAsync(out.deficient.data(), d_def, k * sizeof(int), cudaMemcpyDeviceToHost, ctx.stream));
+  read_status(ctx);
+  ctx.sync();
+  raise_status(*ctx.h_status, true);
+  return out;
+}
+
+std::pair<DTensor, std::vector<double>> projected_svd_full(Ctx& ctx, const DTensor& z, int64_t target) {
+  const int64_t k = z.shape.back();
+  DTensor z2;
+  z2.buf = z.buf;
+  z2.shape = {k ? z.size() / k : 0, k};
+  LTensor zl = as_labelled(z2, "ab");
+  clear_all_status(ctx);
+  Projected pr = projected_svd(ctx, zl, target);
+  DTensor ut;
+  ut.buf = pr.Ut;
+  ut.shape = {k, k};
+  return {ut, pr.s};
+}
+
 EighD eigh(Ctx& ctx, const DTensor& m) {
   if (m.shape.size() != 2 || m.shape[0] != m.shape[1]) throw Error(kShapeError, "eigh expects a square matrix");
   const int64_t n = m.shape[0];

@@ -69,6 +69,12 @@ struct EighD {
   DTensor vectors;             // n x n, column j = phase-fixed eigenvector j
 };
 
+struct GramFactorsD {
+  DTensor P, R, vecs;              // k x k: X diag(l^-1/2), diag(l^1/2) X^H, phase-fixed X
+  std::vector<double> lam;         // descending
+  std::vector<int> deficient;      // l_j < 1e-12 l_max
+};
+
 struct SvdD {
   DTensor u, v;
   std::vector<double> s;
@@ -82,6 +88,13 @@ SvdTripleD randomized_svd(Ctx& ctx, const ImplicitOp& op, const Trunc& policy, c
 // `t1_perm` (optional) permutes t1's axes on output, like Tensor::permute.
 EinsumsvdResultD einsumsvd(Ctx& ctx, const ImplicitOp& op, const Trunc& policy, int strategy,
                            int absorb, const Rsvd& cfg, const std::vector<int>& t1_perm = {});
+// Building blocks of the bond-sharded einsumsvd (sharded.py): G = Z^H Z over the
+// leading axes of z (the last axis is the probe axis); the reference's Gram
+// factors (decomposition.cpp:128-156) of a given Gram matrix; and the projected
+// SVD of B = Z^H (left singular vectors Ut, k x k, and sigma).
+DTensor gram_matrix(Ctx& ctx, const DTensor& z);
+GramFactorsD gram_factors_full(Ctx& ctx, const DTensor& g);
+std::pair<DTensor, std::vector<double>> projected_svd_full(Ctx& ctx, const DTensor& z, int64_t target);
 // linalg.cpp:256-295 (Hermitian eigendecomposition of a square matrix, n <= 256)
 EighD eigh(Ctx& ctx, const DTensor& m);
 // linalg.cpp:193-207 (thin SVD of a matricised tensor; small matrices)

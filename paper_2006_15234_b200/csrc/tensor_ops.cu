@@ -44,6 +44,7 @@ __device__ __forceinline__ double sym_unit(uint64_t x) {
 
 struct RandParams {
   int nd;
+  uint64_t base;  // logical index of the first element (slices of a larger tensor)
   int64_t pext[kMaxModes];
   int64_t lstr[kMaxModes];
 };
@@ -52,7 +53,7 @@ __global__ void random_kernel(double2* dst, const RandParams p, int64_t total, u
   for (int64_t o = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; o < total;
        o += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     int64_t idx = o;
-    uint64_t j = 0;
+    uint64_t j = p.base;
     for (int a = p.nd - 1; a >= 0; --a) {
       int64_t q = idx / p.pext[a];
       j += static_cast<uint64_t>(idx - q * p.pext[a]) * static_cast<uint64_t>(p.lstr[a]);
@@ -105,9 +106,10 @@ void gather_sum(double2* dst, const double2* src, const GatherParams& p, cudaStr
 }
 
 void random_fill(double2* dst, int nd, const int64_t* pext, const int64_t* lstr, uint64_t seed, int real,
-                 cudaStream_t st) {
+                 cudaStream_t st, uint64_t base) {
   RandParams p{};
   p.nd = nd;
+  p.base = base;
   int64_t total = 1;
   for (int a = 0; a < nd; ++a) {
     p.pext[a] = pext[a];

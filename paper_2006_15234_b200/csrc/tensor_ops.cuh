@@ -27,8 +27,9 @@ void gather_sum(double2* dst, const double2* src, const GatherParams& p, cudaStr
 // Sketch generator: element at physical position p has logical (reference)
 // linear index j = sum_a idx_a(p) * lstr[a]; complex: re = sym(mix(seed+(2j+1)g)),
 // im = sym(mix(seed+(2j+2)g)); real: re = sym(mix(seed+(j+1)g)), im = 0.
+// `base` offsets the logical index (a slice of a larger random tensor).
 void random_fill(double2* dst, int nd, const int64_t* pext, const int64_t* lstr, uint64_t seed,
-                 int real, cudaStream_t st);
+                 int real, cudaStream_t st, uint64_t base = 0);
 
 // t[i] *= w[(i / inner) % ext]  (scale one axis by real weights held on device)
 void scale_axis(double2* t, int64_t total, int64_t inner, int64_t ext, const double* w,

@@ -1,0 +1,317 @@
+"""Bond-sharded two-layer row absorb: one einsumsvd per column
+split across ranks along the boundary-MPS bond, collectives over
+torch.distributed (NCCL between GPUs).
+
+Reference algorithm: `two_layer_apply_row` (proj/src/contraction.cpp:254-311)
+calling `einsumsvd` / `randomized_svd` (proj/src/decomposition.cpp:259-352) on
+the network {v(apqsmn), S(uvst), bra*(dumbe), ket(dvncf)}, rows "apq", cols
+"bctef".  The column side is sharded along t (the top-boundary bond leaving the
+column); the pending tensor v, which is the previous column's t2, arrives
+sharded along s.  Per rank r with t in T_r and s in S_r:
+
+  apply  A Q:   (1) bra*(dum|be) Q_r(be|ctfX)   local
+                (2) ket(vn|dcf) (1)              local
+                (3) S(s|uv t_r) (2)              partial over t_r  -> all-reduce (s,n,m,X)
+                (4) v_r(apq|s_r mn) (3)[s_r]     partial over s_r  -> all-reduce Y (a,p,q,X)
+  adjoint A^H P: v_r^* P -> (s_r,n,m,X) -> all-gather over s; then S^*, ket^*,
+                bra locally on t_r -> Z_r (b,c,t_r,e,f,X)
+  big-side orth: G = all-reduce(Z_r^H Z_r) (k x k), replicated gram_factors
+                (the paper's Gram-matrix orthogonalisation, Alg. 5),
+                Q_r = Z_r P locally
+  small side (Y, P): replicated (identical on every rank)
+  projected SVD: G = all-reduce(Z_r^H Z_r), replicated eigendecomposition;
+                t1 = P U w_l replicated, t2_r = conj(Z_r) conj(U) w_r / s local.
+
+Ω_r is the t-slice of the reference's random_tensor(col_shape + [k], seed),
+bit-identical to the unsharded sketch, so a sharded run reproduces the
+single-device result up to the summation order of the all-reduces.  Columns
+whose t extent is smaller than the world size (the last column, t = 1) run
+replicated after an all-gather of v.
+
+The compute backend is the device library (`DeviceOps`); the host code here is
+only orchestration.  tests/test_sharded.py runs the same driver with a
+numpy backend on world-size-2 gloo groups.
+"""
+from __future__ import annotations
+
+import math
+from typing import List, Optional, Sequence, Tuple
+
+import numpy as np
+
+MASK = (1 << 64) - 1
+GAMMA = 0x9E3779B97F4A7C15
+
+
+def _splitmix_next(state: int) -> int:
+    """rng.hpp:17-23 (one step)."""
+    z = (state + GAMMA) & MASK
+    z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & MASK
+    z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & MASK
+    return z ^ (z >> 31)
+
+
+def derive_seed(base: int, *parts: int) -> int:
+    """rng.hpp:38-44: per-einsumsvd seed derive_seed(opt.seed, tag, row, col)."""
+    s = base & MASK
+    for p in parts:
+        s = _splitmix_next((s ^ ((p + GAMMA) & MASK)) & MASK)
+    return s
+
+
+def shard_range(extent: int, world: int, rank: int) -> Tuple[int, int]:
+    """Contiguous balanced partition of [0, extent): sizes differ by at most one."""
+    base, extra = divmod(extent, world)
+    start = rank * base + min(rank, extra)
+    return start, start + base + (1 if rank < extra else 0)
+
+
+def effective_oversample(oversample: int, target: int) -> int:
+    """decomposition.cpp:15-22."""
+    return oversample if oversample >= 0 else max(5, int(math.ceil(0.1 * target)))
+
+
+def retained_rank(s: Sequence[float], max_rank: int, rel_cutoff: float) -> int:
+    """decomposition.cpp:24-29 (max_rank 0 = unbounded)."""
+    if len(s) == 0:
+        return 0
+    floor = rel_cutoff * s[0]
+    above = sum(1 for v in s if v >= floor)
+    cap = len(s) if max_rank == 0 else max_rank
+    return max(1, min(above, cap))
+
+
+class Comm:
+    """Rank / world of a torch.distributed group (world 1 when not initialised)."""
+
+    def __init__(self, group=None):
+        self.group = group
+        try:
+            import torch.distributed as dist
+            self.dist = dist if dist.is_available() and dist.is_initialized() else None
+        except Exception:  # pragma: no cover - torch without distributed
+            self.dist = None
+        self.rank = self.dist.get_rank(group) if self.dist else 0
+        self.world = self.dist.get_world_size(group) if self.dist else 1
+
+
+class DeviceOps:
+    """Product backend: the device library's building blocks; collectives run
+    through torch.distributed on zero-copy views of the library's buffers."""
+
+    def __init__(self, comm: Comm, ctx=None):
+        from . import api as A
+        self.A = A
+        self.ctx = ctx or A.default_context()
+        self.comm = comm
+
+    # --- tensors
+    def shape(self, t):
+        return t.shape
+
+    def reshape(self, t, shape):
+        return t.reshape(tuple(shape))
+
+    def conj(self, t):
+        return t.conj()
+
+    def slice(self, t, axis, start, stop):
+        return t.slice(axis, start, stop)
+
+    def contract(self, spec, *ts):
+        return self.A.contract(spec, *ts, ctx=self.ctx)
+
+    def random_slice(self, shape, axis, start, stop, seed):
+        return self.A.random_slice(shape, axis, start, stop - start, seed, ctx=self.ctx)
+
+    def scale_cols(self, m, w):
+        wd = self.A.to_device(np.asarray(w, dtype=np.complex128), self.ctx)
+        return self.A.contract("XR,R->XR", m, wd, ctx=self.ctx)
+
+    # --- factorizations
+    def gram(self, z):
+        return self.A.gram(z, self.ctx)
+
+    def gram_factors(self, g):
+        return self.A.gram_factors(g, self.ctx)
+
+    def orth(self, y):
+        return self.A.gram_orthogonalize(y, len(y.shape) - 1, self.ctx)[0]
+
+    def projected_svd(self, z, target):
+        return self.A.projected_svd(z, target, self.ctx)
+
+    def einsumsvd(self, tensors, labels, rows, cols, max_rank, rel_cutoff, absorb, power_iters, oversample, seed):
+        A = self.A
+        net = A.ImplicitOperator(tensors, labels, rows, cols, ctx=self.ctx)
+        r = A.einsumsvd(net, A.TruncationPolicy(max_rank, rel_cutoff), A.SvdStrategy.implicit_rsvd,
+                        A.Absorb(absorb), A.RsvdConfig(power_iters, oversample, seed))
+        return r.t1, r.t2, r.s
+
+    # --- collectives (in place on the library's buffer / new tensor)
+    def _torch(self, t):
+        import torch
+        self.ctx.sync()
+        return torch.as_tensor(t, device="cuda")
+
+    def allreduce(self, t):
+        if self.comm.world == 1:
+            return t
+        import torch
+        x = self._torch(t)
+        self.comm.dist.all_reduce(x, group=self.comm.group)
+        torch.cuda.current_stream().synchronize()
+        return t
+
+    def allgather(self, t, axis, extent):
+        if self.comm.world == 1:
+            return t
+        import torch
+        x = self._torch(t)
+        w = self.comm.world
+        sizes = [shard_range(extent, w, r) for r in range(w)]
+        mx = max(b - a for a, b in sizes)
+        pad = list(x.shape)
+        pad[axis] = mx
+        buf = torch.zeros(pad, dtype=x.dtype, device=x.device)
+        buf.narrow(axis, 0, x.shape[axis]).copy_(x)
+        parts = [torch.empty_like(buf) for _ in range(w)]
+        self.comm.dist.all_gather(parts, buf, group=self.comm.group)
+        full = torch.cat([p.narrow(axis, 0, b - a) for p, (a, b) in zip(parts, sizes)], dim=axis).contiguous()
+        torch.cuda.current_stream().synchronize()
+        out = self.A.from_device_ptr(full.data_ptr(), tuple(full.shape), self.ctx)
+        self.ctx.sync()  # the copy has landed before `full` returns to torch's allocator
+        return out
+
+
+def _absorb_weights(s, absorb):
+    """decomposition.cpp:336-346 (0 split, 1 left, 2 right)."""
+    s = np.asarray(s, dtype=float)
+    one = np.ones_like(s)
+    if absorb == 0:
+        return np.sqrt(s), np.sqrt(s)
+    if absorb == 1:
+        return s, one
+    return one, s
+
+
+def sharded_column_einsumsvd(ops, v_r, S, Bc, K, s_range, T, max_rank, rel_cutoff, absorb, power_iters,
+                             oversample, seed):
+    """One column of the row absorb, sharded along t (see the module docstring).
+
+    v_r: (a, p, q, s_r, m, n) local slice; S: (u, v, s, t) full; Bc = conj(bra)
+    (d, u, m, b, e); K = ket (d, v, n, c, f).  Returns t1 (pb, pk, a, rank)
+    replicated, t2_r (rank, b, c, t_r, e, f) local, and the kept sigma."""
+    comm = ops.comm
+    a, p, q, _, m_, n_ = ops.shape(v_r)
+    b, e = ops.shape(Bc)[3], ops.shape(Bc)[4]
+    c, f = ops.shape(K)[3], ops.shape(K)[4]
+    s_full = ops.shape(S)[2]
+    rows, cols = a * p * q, b * c * T * e * f
+    mindim = min(rows, cols)
+    target = min(max_rank if max_rank else mindim, mindim)
+    probe = min(target + effective_oversample(oversample, target), mindim)
+    t0, t1 = shard_range(T, comm.world, comm.rank)
+    s0, s1 = s_range
+
+    S_t = ops.slice(S, 3, t0, t1)
+    S_tc = ops.conj(S_t)
+    vc = ops.conj(v_r)
+    Kc = ops.conj(K)
+    B = ops.conj(Bc)
+
+    def apply(x):  # x: (b, c, t_r, e, f, X) -> Y (a, p, q, X), replicated
+        w1 = ops.contract("dumbe,bctefX->dumctfX", Bc, x)
+        w2 = ops.contract("dvncf,dumctfX->vnumtX", K, w1)
+        w3 = ops.allreduce(ops.contract("uvst,vnumtX->snmX", S_t, w2))
+        w3s = ops.slice(w3, 0, s0, s1)
+        return ops.allreduce(ops.contract("apqsmn,snmX->apqX", v_r, w3s))
+
+    def adjoint(pp):  # pp: (a, p, q, X) replicated -> Z_r (b, c, t_r, e, f, X)
+        r = ops.allgather(ops.contract("apqsmn,apqX->snmX", vc, pp), 0, s_full)
+        w2 = ops.contract("uvst,snmX->vnumtX", S_tc, r)
+        w1 = ops.contract("dvncf,vnumtX->dumctfX", Kc, w2)
+        return ops.contract("dumbe,dumctfX->bctefX", B, w1)
+
+    def orth_big(z):
+        g = ops.allreduce(ops.gram(z))
+        pz, _, _, _, deficient = ops.gram_factors(g)
+        if np.any(deficient):  # orthonormal completion needs global rows: gather, complete, re-slice
+            qf = ops.orth(ops.allgather(z, 2, T))
+            return ops.slice(qf, 2, t0, t1)
+        return ops.contract("bctefX,XY->bctefY", z, pz)
+
+    omega = ops.random_slice((b, c, T, e, f, probe), 2, t0, t1, seed)
+    pm = ops.orth(apply(omega))
+    for _ in range(power_iters):
+        qm = orth_big(adjoint(pm))
+        pm = ops.orth(apply(qm))
+    z = adjoint(pm)
+
+    # projected SVD of B = P^H A = Z^H (decomposition.cpp:293-306; Gram route)
+    g = ops.allreduce(ops.gram(z))
+    _, _, ut, lam, _ = ops.gram_factors(g)
+    s = np.sqrt(np.maximum(np.asarray(lam, dtype=float), 0.0))
+    tgt = max(1, min(target, probe))
+    if not (s[0] > 0.0 and s[tgt - 1] >= 1e-4 * s[0]):
+        ut, s = ops.projected_svd(ops.allgather(z, 2, T), target)
+    rank = min(retained_rank(list(s), max_rank, rel_cutoff), target)
+    s = np.asarray(s[:rank], dtype=float)
+    wl, wr = _absorb_weights(s, absorb)
+    wv = np.where(s > 0.0, wr / np.where(s > 0.0, s, 1.0), 0.0)
+    u_r = ops.slice(ut, 1, 0, rank)
+    t1 = ops.contract("apqX,XR->pqaR", pm, ops.scale_cols(u_r, wl))
+    t2 = ops.contract("bctefX,XR->Rbctef", ops.conj(z), ops.scale_cols(ops.conj(u_r), wv))
+    return t1, t2, s
+
+
+def sharded_two_layer_apply_row(ops, top: Sequence, top_phys: Sequence[Tuple[int, int]], bra_row: Sequence,
+                                ket_row: Sequence, row: int, max_rank: int, seed: int, power_iters: int = 2,
+                                oversample: int = -1, canonicalize: bool = True, seed_tag: int = 0x20,
+                                rel_cutoff: float = 1e-14):
+    """contraction.cpp:254-311 with every column einsumsvd sharded along the
+    boundary bond.  Inputs and outputs are replicated on every rank; returns
+    (sites, phys) of the new boundary."""
+    comm = ops.comm
+    n = len(bra_row)
+    absorb = (2 if row % 2 else 1) if canonicalize else 0
+    s0 = top[0]
+    sh = ops.shape(s0)
+    s0s = ops.reshape(s0, (top_phys[0][0], top_phys[0][1], sh[1], sh[2]))
+    v = ops.contract("uvls,dumbe,dvncf->bcsef", s0s, ops.conj(bra_row[0]), ket_row[0])
+    v = ops.reshape(v, (1,) + tuple(ops.shape(v)))
+    sharded, s_range = False, None
+    out: List = [None] * n
+    for col in range(1, n):
+        sc = top[col]
+        sh = ops.shape(sc)
+        S = ops.reshape(sc, (top_phys[col][0], top_phys[col][1], sh[1], sh[2]))
+        T = sh[2]
+        Bc = ops.conj(bra_row[col])
+        K = ket_row[col]
+        cseed = derive_seed(seed, seed_tag, row, col)
+        if T >= comm.world:
+            if not sharded:
+                s_ext = ops.shape(v)[3]
+                s_range = shard_range(s_ext, comm.world, comm.rank)
+                v = ops.slice(v, 3, *s_range)
+            t1, t2, _ = sharded_column_einsumsvd(ops, v, S, Bc, K, s_range, T, max_rank, rel_cutoff, absorb,
+                                                 power_iters, oversample, cseed)
+            v, sharded, s_range = t2, True, shard_range(T, comm.world, comm.rank)
+        else:
+            if sharded:
+                v = ops.allgather(v, 3, ops.shape(S)[2])
+                sharded = False
+            t1, t2, _ = ops.einsumsvd([v, S, Bc, K], ["apqsmn", "uvst", "dumbe", "dvncf"], "apq", "bctef",
+                                      max_rank, rel_cutoff, absorb, power_iters, oversample, cseed)
+            t1 = ops.contract("apqR->pqaR", t1)
+            v = t2
+        ts = ops.shape(t1)
+        out[col - 1] = ops.reshape(t1, (ts[0] * ts[1], ts[2], ts[3]))
+    if sharded:
+        v = ops.allgather(v, 3, ops.shape(top[n - 1])[2])
+    last = ops.contract("abcdef->bcadef", v)
+    ls = ops.shape(last)
+    out[n - 1] = ops.reshape(last, (ls[0] * ls[1], ls[2], ls[3] * ls[4] * ls[5]))
+    phys = [(ops.shape(bra_row[col])[3], ops.shape(ket_row[col])[3]) for col in range(n)]
+    return out, phys

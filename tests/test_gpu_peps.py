@@ -230,3 +230,49 @@ def test_ite_config4_shapes_and_speed(A):
     out = A.ite_tfim(st, 1.0, 3.0, 0.01, 5, 8)
     assert out.site(3, 3).shape == (2, 8, 8, 8, 8)
     assert out.site(0, 0).shape == (2, 1, 1, 8, 8)
+
+
+@pytest.mark.parametrize("canon,key", [(True, "row_site"), (False, "row_split_site")])
+def test_sharded_driver_on_device_matches_reference(faithful, golden, canon, key):
+    """The bond-sharded row absorb (paper_2006_15234_b200/sharded.py) on the
+    device backend (world size 1: every column runs the sharded schedule with
+    identity collectives) reproduces the reference golden row elementwise."""
+    from paper_2006_15234_b200 import sharded as SH
+    A = faithful
+    sites = I.random_peps(3, 5, 3, 71)
+    top, phys = I.random_boundary(5, (3, 3), 9, 72)
+    ops = SH.DeviceOps(SH.Comm())
+    row = [A.to_device(sites[1 * 5 + c]) for c in range(5)]
+    tops = [A.to_device(t) for t in top]
+    got, gphys = SH.sharded_two_layer_apply_row(ops, tops, phys, row, row, 1, 9, 5, 2, -1, canon, 0x20)
+    assert gphys == [(3, 3)] * 5
+    for i, s in enumerate(got):
+        g = golden[f"{key}{i}"]
+        assert s.shape == g.shape
+        assert rel(s.numpy(), g) < 1e-8
+
+
+def test_random_slice_and_building_blocks(A):
+    """random_slice == slice of random_tensor (bitwise); gram / gram_factors /
+    projected_svd / slice / conj / reshape against numpy."""
+    full = A.random_tensor((3, 4, 9, 2, 5), 99).numpy()
+    for a, b in [(0, 9), (2, 7), (8, 9)]:
+        sl = A.random_slice((3, 4, 9, 2, 5), 2, a, b - a, 99).numpy()
+        assert np.array_equal(sl, full[:, :, a:b])
+    z = O.random_tensor((50, 3, 7), 5)
+    g = A.gram(z).numpy()
+    zz = z.reshape(-1, 7)
+    assert rel(g, zz.conj().T @ zz) < 1e-13
+    p, r, x, lam, dfc = A.gram_factors(g)
+    w, xr = O.eigh(g)
+    assert np.allclose(lam, w, rtol=1e-12, atol=0) and not dfc.any()
+    assert rel(x.numpy(), xr) < 1e-10
+    assert rel((zz @ p.numpy()).conj().T @ (zz @ p.numpy()), np.eye(7)) < 1e-12
+    ut, s = A.projected_svd(z, 7)
+    uu, ss, _ = O.svd(np.moveaxis(z.conj(), -1, 0), 1)
+    assert np.allclose(s, ss, rtol=1e-10, atol=0)
+    assert rel(ut.numpy(), uu) < 1e-9
+    t = A.to_device(z)
+    assert np.array_equal(t.slice(1, 1, 3).numpy(), z[:, 1:3])
+    assert np.array_equal(t.conj().numpy(), z.conj())
+    assert np.array_equal(t.reshape(150, 7).numpy(), z.reshape(150, 7))

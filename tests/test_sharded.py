@@ -1,0 +1,186 @@
+"""Bond-sharded row absorb: the product driver
+paper_2006_15234_b200/sharded.py run on world-size-2 gloo groups on CPU with a
+numpy compute backend (test infrastructure: the oracle supplies the dense
+kernels), against the unsharded reference restatement of two_layer_apply_row
+(contraction.cpp:254-311).  Exercises even and uneven bond partitions, the
+replicated edge column (t = 1) and the all-reduce / all-gather schedule."""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+from oracle import peps_oracle as O
+from paper_2006_15234_b200 import sharded as SH
+
+
+class NumpyOps:
+    """Numpy backend with the DeviceOps interface (collectives over gloo)."""
+
+    def __init__(self, comm):
+        self.comm = comm
+        self.calls = {"allreduce": 0, "allgather": 0}
+
+    def shape(self, t):
+        return tuple(t.shape)
+
+    def reshape(self, t, shape):
+        return np.ascontiguousarray(t).reshape(shape)
+
+    def conj(self, t):
+        return np.conj(t)
+
+    def slice(self, t, axis, start, stop):
+        return np.take(t, np.arange(start, stop), axis=axis)
+
+    def contract(self, spec, *ts):
+        return np.einsum(spec, *ts, optimize="optimal")
+
+    def random_slice(self, shape, axis, start, stop, seed):
+        return np.take(O.random_tensor(tuple(shape), seed), np.arange(start, stop), axis=axis)
+
+    def scale_cols(self, m, w):
+        return m * np.asarray(w)[None, :]
+
+    def gram(self, z):
+        zz = z.reshape(-1, z.shape[-1])
+        return zz.conj().T @ zz
+
+    def gram_factors(self, g):
+        w, x = O.eigh(g)
+        lmax = w[0]
+        deficient = w < 1e-12 * lmax
+        lam = np.maximum(w, 1e-12 * lmax)
+        return x / np.sqrt(lam)[None, :], np.sqrt(lam)[:, None] * x.conj().T, x, w, deficient
+
+    def orth(self, y):
+        return O.gram_orthogonalize(y, y.ndim - 1)[0]
+
+    def projected_svd(self, z, target):
+        b = np.moveaxis(z.conj(), -1, 0)
+        uu, s, _ = O.svd(b, 1)
+        return uu, s
+
+    def einsumsvd(self, tensors, labels, rows, cols, max_rank, rel_cutoff, absorb, power_iters, oversample, seed):
+        op = O.ImplicitOperator(tensors, labels, rows, cols)
+        t1, t2, s, _ = O.einsumsvd(op, max_rank, rel_cutoff, "implicit_rsvd", ["split", "left", "right"][absorb],
+                                   power_iters, oversample, seed)
+        return t1, t2, s
+
+    def allreduce(self, t):
+        if self.comm.world == 1:
+            return t
+        import torch
+        self.calls["allreduce"] += 1
+        x = torch.from_numpy(np.ascontiguousarray(t).view(np.float64).copy())
+        self.comm.dist.all_reduce(x)
+        return x.numpy().view(np.complex128).reshape(t.shape)
+
+    def allgather(self, t, axis, extent):
+        if self.comm.world == 1:
+            return t
+        import torch
+        self.calls["allgather"] += 1
+        w = self.comm.world
+        sizes = [SH.shard_range(extent, w, r) for r in range(w)]
+        mx = max(b - a for a, b in sizes)
+        pad = list(t.shape)
+        pad[axis] = mx
+        buf = np.zeros(pad, dtype=np.complex128)
+        idx = [slice(None)] * t.ndim
+        idx[axis] = slice(0, t.shape[axis])
+        buf[tuple(idx)] = t
+        x = torch.from_numpy(buf.view(np.float64).copy())
+        parts = [torch.empty_like(x) for _ in range(w)]
+        self.comm.dist.all_gather(parts, x)
+        out = []
+        for p, (a, b) in zip(parts, sizes):
+            arr = p.numpy().view(np.complex128).reshape(pad)
+            idx[axis] = slice(0, b - a)
+            out.append(arr[tuple(idx)])
+        return np.concatenate(out, axis=axis)
+
+
+def _problem(r, rows=3, cols=4, seed=11):
+    sites = []
+    for i in range(rows):
+        for j in range(cols):
+            up = 1 if i == 0 else r
+            left = 1 if j == 0 else r
+            down = 1 if i == rows - 1 else r
+            right = 1 if j == cols - 1 else r
+            sites.append(O.random_tensor((2, up, left, down, right), O.derive_seed(seed, i, j)))
+    top, phys = O.two_layer_first_row(sites, rows, cols)
+    return sites, top, phys
+
+
+def _run_sharded(ops, r, m, row=1, rows=3, cols=4, oversample=-1):
+    sites, top, phys = _problem(r, rows, cols)
+    bra = [sites[row * cols + c] for c in range(cols)]
+    got, gphys = SH.sharded_two_layer_apply_row(ops, top, phys, bra, bra, row, m, 7, 2, oversample, True, 0x20)
+    ref, rphys = O.two_layer_apply_row(top, phys, sites, rows, cols, row, m, 7, 2, oversample, True, 0x20)
+    assert [tuple(p) for p in gphys] == [tuple(p) for p in rphys]
+    err = 0.0
+    for a, b in zip(got, ref):
+        assert a.shape == b.shape
+        err = max(err, float(np.abs(a - b).max() / np.abs(b).max()))
+    return err
+
+
+def test_shard_ranges_partition():
+    for extent in (1, 4, 9, 64):
+        for world in (1, 2, 3, 8):
+            rs = [SH.shard_range(extent, world, r) for r in range(world)]
+            assert rs[0][0] == 0 and rs[-1][1] == extent
+            assert all(rs[i][1] == rs[i + 1][0] for i in range(world - 1))
+            assert max(b - a for a, b in rs) - min(b - a for a, b in rs) <= 1
+
+
+def test_derive_seed_matches_reference_rng():
+    for parts in [(0x20, 1, 2), (0x21, 5, 9), (1,), ()]:
+        assert SH.derive_seed(123456789, *parts) == O.derive_seed(123456789, *parts)
+
+
+@pytest.mark.parametrize("r,m", [(2, 4), (3, 6)])
+def test_sharded_row_world1(r, m):
+    err = _run_sharded(NumpyOps(SH.Comm()), r, m)
+    assert err < 1e-9
+
+
+def _worker(rank, world, port, r, m, q):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        ops = NumpyOps(SH.Comm())
+        err = _run_sharded(ops, r, m)
+        q.put((rank, err, dict(ops.calls)))
+    finally:
+        dist.destroy_process_group()
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+@pytest.mark.parametrize("r,m", [(2, 4), (3, 6)])
+def test_sharded_row_world2_gloo(r, m):
+    """r = 2: bond t = 4 split 2 + 2; r = 3: t = 9 split 5 + 4 (uneven)."""
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(rk, 2, port, r, m, q)) for rk in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=300)
+    res = [q.get(timeout=5) for _ in procs]
+    for rank, err, calls in res:
+        assert err < 1e-9, (rank, err)
+        # two sharded columns (q = 2): per column 2 all-reduces per apply x 3 applies,
+        # 1 all-gather per adjoint x 3, Gram all-reduces, plus the v gather before the edge column
+        assert calls["allreduce"] >= 2 * (2 * 3 + 3) and calls["allgather"] >= 2 * 3 + 1
