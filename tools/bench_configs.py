@@ -1,0 +1,205 @@
+"""Per-config measurements of the einsumsvd path on one B200 (BASELINE configs 1, 3, 4, 5).
+
+bench.py's headline line is config 2 (the metric's TF/s quote).  This tool times
+the other BASELINE configs through the same public API and prints one JSON line
+per config; results are committed under profiles/ (rNN_configs.jsonl).
+
+  python tools/bench_configs.py [--configs 1,3,4,5] [--ref] [--zz all|centre]
+
+--ref also runs the compiled reference (oracle/_ref, all host threads) where it
+finishes in bounded time (config 1 norm; config 4 100-step ITE, compared
+elementwise), as the parity/CPU-baseline leg.  Configs 3 and 5 are far beyond a
+bounded CPU run (1511 s / ~16 h); their CPU numbers are the ones
+measured in SURVEY §6 / BASELINE.md, and their parity is pinned by the reduced
+size tests in tests/test_gpu_peps.py.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, HERE)
+
+import paper_2006_15234_b200.api as A  # noqa: E402
+from paper_2006_15234_b200 import costmodel, inputs  # noqa: E402
+
+Z = np.diag([1.0, -1.0]).astype(complex)
+
+
+def _sync(ctx):
+    ctx.sync()
+
+
+def zz_pieces():
+    """split_two_site of Z (x) Z (observables.cpp:284-295) via the device SVD."""
+    zz = np.einsum("ac,bd->abcd", Z, Z)
+    u, s, v = A.svd(zz.transpose(0, 2, 1, 3).copy(), 2)
+    s = np.asarray(s)
+    g = int((s >= 1e-14 * s[0]).sum())
+    w = np.sqrt(s[:g])
+    left = u.numpy()[..., :g] * w
+    right = (v.numpy()[:g] * w[:, None, None]).transpose(1, 2, 0)
+    return left, right
+
+
+def contract_flops(n, r, m, q, os_):
+    """Algorithmic real FP64 flops (4 x the reference's instr::flops) of contract_two_layer's
+    row absorbs on an n x n lattice whose boundary bonds are already m (true for configs 3
+    and 5: the first row's boundary bond r*r equals m)."""
+    return sum(4 * costmodel.two_layer_row_flops(n, r, m, q, os_, interior=row < n - 1) for row in range(1, n))
+
+
+def cfg1(args, ctx):
+    c = inputs.config1()
+    st = A.PepsState(4, 4, 2, c["sites"], ctx=ctx)
+    opt = A.ContractOption.two_layer_opt(4, c["seed"], 1, 4)
+    for _ in range(3):
+        v = A.contract_two_layer(st, st, opt)
+    n = 20
+    t0 = time.perf_counter()
+    for _ in range(n):
+        v = A.contract_two_layer(st, st, opt)
+    dt = (time.perf_counter() - t0) / n
+    exact = None
+    out = {"config": 1, "workload": "4x4 r=2 PEPS norm, two-layer IBMPS m=4 os=4 q=1", "s_per_norm": dt,
+           "norm": [v.real, v.imag]}
+    if args.ref:
+        from oracle import ref
+        ref.set_threads(os.cpu_count() or 1)
+        t0 = time.perf_counter()
+        for _ in range(n):
+            w, _ = ref.contract_two_layer(c["sites"], 4, 4, 4, c["seed"], 1, 4)
+        out["ref_s_per_norm"] = (time.perf_counter() - t0) / n
+        out["ref_norm"] = [w.real, w.imag]
+        out["rel_err_vs_ref"] = abs(v - w) / abs(w)
+        exact = ref.inner_exact(c["sites"], 4, 4)
+        out["exact"] = [exact.real, exact.imag]
+        out["truncation_rel_diff_vs_exact"] = abs(v - exact) / abs(exact)
+        out["cpu_cores"] = os.cpu_count()
+    return out
+
+
+def cfg3(args, ctx):
+    c = inputs.config3()
+    n = c["rows"]
+    st = A.PepsState(n, n, 2, c["sites"], ctx=ctx)
+    opt = A.ContractOption.two_layer_opt(c["m"], c["seed"], c["power_iters"], c["oversample"])
+    t0 = time.perf_counter()
+    nrm = A.contract_two_layer(st, st, opt)
+    t_norm = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    cache = A.build_row_cache(st, opt)
+    _sync(ctx)
+    t_cache = time.perf_counter() - t0
+    norm = A.chain_scalar(cache.tops[n - 1])
+    t0 = time.perf_counter()
+    zs = np.zeros((n, n))
+    for i in range(n):
+        top = cache.tops[i - 1] if i > 0 else None
+        bot = cache.bots[i + 1] if i + 1 < n else None
+        env = A.band_environment(top, st, st, i, i, bot)
+        for j in range(n):
+            val = A.band_splice(env, top, st, st, bot, [A.InsertionPiece((i, j), Z, [])], j, j) / norm
+            zs[i, j] = val.real
+    t_bands = time.perf_counter() - t0
+    return {"config": 3, "norm_alg_tflops": contract_flops(n, 6, 36, 2, 5) / t_norm / 1e12, "workload": "16x16 r=6 m=36 (k=41, q=2): norm + <Z_i> on all 256 sites via cached envs",
+            "s_per_norm": t_norm, "norm": [nrm.real, nrm.imag], "cache_s": t_cache,
+            "bands_256_Z_s": t_bands, "total_cached_s": t_cache + t_bands,
+            "cached_norm_bitwise_equal": bool(norm == nrm), "mean_Z": float(zs.mean()),
+            "Z_centre": float(zs[n // 2, n // 2]),
+            "ref_cpu_s_total_SURVEY": 1511.1, "ref_cpu_cores_SURVEY": 8}
+
+
+def cfg4(args, ctx):
+    steps = args.ite_steps
+    plus = [np.array([1, 1], dtype=complex).reshape(2, 1, 1, 1, 1) / np.sqrt(2) for _ in range(64)]
+    st = A.PepsState(8, 8, 2, plus, ctx=ctx)
+    A.ite_tfim(st, 1.0, 3.0, 0.01, 2, 8)  # warm-up
+    _sync(ctx)
+    t0 = time.perf_counter()
+    out = A.ite_tfim(st, 1.0, 3.0, 0.01, steps, 8)
+    _sync(ctx)
+    dt = time.perf_counter() - t0
+    res = {"config": 4, "workload": f"TFIM ITE 8x8 r=8 J=1 h=3 tau=0.01, {steps} steps, simple update "
+                                     "(bonds batched per colour)",
+           "s_total": dt, "s_per_step": dt / steps, "updates_per_s": steps * (64 + 112) / dt}
+    if args.ref:
+        from oracle import ref
+        ref.set_threads(os.cpu_count() or 1)
+        t0 = time.perf_counter()
+        want, _ = ref.ite_tfim(plus, 8, 8, 1.0, 3.0, 0.01, steps, 8)
+        rdt = time.perf_counter() - t0
+        got = [s.numpy() for s in out.sites]
+        shapes_equal = [g.shape for g in got] == [w.shape for w in want]
+        worst = max(float(np.abs(g - w).max() / max(np.abs(w).max(), 1e-300)) for g, w in zip(got, want)) \
+            if shapes_equal else None
+        res.update({"ref_s_total": rdt, "ref_s_per_step": rdt / steps, "cpu_cores": os.cpu_count(),
+                    "shapes_bit_exact": shapes_equal, "max_site_rel_err_vs_ref": worst})
+    return res
+
+
+def cfg5(args, ctx):
+    c = inputs.config5()
+    n = c["rows"]
+    st = A.PepsState(n, n, 2, c["sites"], ctx=ctx)
+    opt = A.ContractOption.two_layer_opt(c["m"], c["seed"], c["power_iters"], c["oversample"])
+    t0 = time.perf_counter()
+    nrm = A.contract_two_layer(st, st, opt)
+    t_norm = time.perf_counter() - t0
+    res = {"config": 5, "workload": "32x32 r=8 m=64 (k=72, q=2): norm by two-layer boundary contraction "
+                                    "+ nearest-neighbour ZZ via cached envs",
+           "s_per_norm": t_norm, "norm": [nrm.real, nrm.imag],
+           "norm_alg_flops_model": contract_flops(n, 8, 64, 2, 8),
+           "norm_alg_tflops": contract_flops(n, 8, 64, 2, 8) / t_norm / 1e12}
+    if args.zz == "none":
+        return res
+    t0 = time.perf_counter()
+    cache = A.build_row_cache(st, opt)
+    _sync(ctx)
+    res["cache_s"] = time.perf_counter() - t0
+    norm = A.chain_scalar(cache.tops[n - 1])
+    res["cached_norm_bitwise_equal"] = bool(norm == nrm)
+    left, right = zz_pieces()
+    i, j = n // 2, n // 2 - 1
+    t0 = time.perf_counter()
+    top, bot = cache.tops[i - 1], cache.bots[i + 1]
+    env = A.band_environment(top, st, st, i, i, bot)
+    pieces = [A.InsertionPiece((i, j), left, [0]), A.InsertionPiece((i, j + 1), right, [0])]
+    zz_h = A.band_splice(env, top, st, st, bot, pieces, j, j + 1) / norm
+    res["zz_centre_horizontal"] = [zz_h.real, zz_h.imag]
+    res["zz_centre_horizontal_s"] = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    top, bot = cache.tops[i - 1], cache.bots[i + 2]
+    env2 = A.band_environment(top, st, st, i, i + 1, bot)
+    pieces = [A.InsertionPiece((i, j), left, [0]), A.InsertionPiece((i + 1, j), right, [0])]
+    zz_v = A.band_splice(env2, top, st, st, bot, pieces, j, j) / norm
+    res["zz_centre_vertical"] = [zz_v.real, zz_v.imag]
+    res["zz_centre_vertical_s"] = time.perf_counter() - t0
+    return res
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--configs", default="1,3,4,5")
+    ap.add_argument("--ref", action="store_true")
+    ap.add_argument("--ite-steps", type=int, default=100)
+    ap.add_argument("--zz", choices=["none", "centre"], default="centre")
+    args = ap.parse_args()
+    ctx = A.default_context()
+    fns = {1: cfg1, 3: cfg3, 4: cfg4, 5: cfg5}
+    for k in [int(x) for x in args.configs.split(",")]:
+        t0 = time.perf_counter()
+        res = fns[k](args, ctx)
+        res["wall_s"] = time.perf_counter() - t0
+        res["launches"] = ctx.counters().get("launches")
+        print(json.dumps(res), flush=True)
+
+
+if __name__ == "__main__":
+    main()
