@@ -148,6 +148,68 @@ class DeviceOps:
                         A.Absorb(absorb), A.RsvdConfig(power_iters, oversample, seed))
         return r.t1, r.t2, r.s
 
+    def chain_scalar(self, sites):
+        """mps.cpp:102-110 on the device."""
+        t = self.A.to_device(np.ones(1, dtype=np.complex128), self.ctx)
+        for s in sites:
+            t = self.A.contract("l,plr->r", t, s, ctx=self.ctx)
+        return complex(t.numpy()[0])
+
+    # --- simple update (config 4)
+    def exp_gate(self, op, coeff, tau):
+        return self.A.hermitian_exp(op, coeff, tau, self.ctx)
+
+    def _state(self, sites, rows, cols):
+        return self.A.PepsState(rows, cols, 2, sites, ctx=self.ctx)
+
+    def apply_one_site(self, sites, rows, cols, gate):
+        out = self.A.apply_one_site(self._state(sites, rows, cols), gate,
+                                    [(r, c) for r in range(rows) for c in range(cols)])
+        return list(out.sites)
+
+    def apply_two_site(self, sites, rows, cols, gate, bonds, rank):
+        out = self.A.apply_two_site(self._state(sites, rows, cols), gate, bonds, self.A.TruncationPolicy(rank, 1e-14))
+        return {p: out.site(*p) for bd in bonds for p in ((bd[0], bd[1]), (bd[2], bd[3]))}
+
+    def exchange_sites(self, mine, owners):
+        """Every rank's updated sites to every rank: all-gather of the shapes,
+        then of the packed complex data (padded to the largest share)."""
+        if self.comm.world == 1:
+            return dict(mine)
+        import torch
+        dist, w, me = self.comm.dist, self.comm.world, self.comm.rank
+        nmax = max(len(o) for o in owners)
+        shp = torch.zeros(5 * max(1, nmax), dtype=torch.int64, device="cuda")
+        for i, p in enumerate(owners[me]):
+            shp[5 * i:5 * i + 5] = torch.tensor(mine[p].shape, dtype=torch.int64)
+        shps = [torch.empty_like(shp) for _ in range(w)]
+        dist.all_gather(shps, shp, group=self.comm.group)
+        host = [s.cpu().numpy() for s in shps]
+        sizes = [sum(int(np.prod(h[5 * i:5 * i + 5])) for i in range(len(owners[rk]))) for rk, h in enumerate(host)]
+        self.ctx.sync()
+        buf = torch.zeros(2 * max(1, max(sizes)), dtype=torch.float64, device="cuda")
+        off = 0
+        for p in owners[me]:
+            x = torch.view_as_real(torch.as_tensor(mine[p], device="cuda")).reshape(-1)
+            buf[off:off + x.numel()].copy_(x)
+            off += x.numel()
+        parts = [torch.empty_like(buf) for _ in range(w)]
+        dist.all_gather(parts, buf, group=self.comm.group)
+        torch.cuda.current_stream().synchronize()
+        out = dict(mine)
+        for rk in range(w):
+            if rk == me:
+                continue
+            off = 0
+            for i, p in enumerate(owners[rk]):
+                shape = tuple(int(v) for v in host[rk][5 * i:5 * i + 5])
+                n = 2 * int(np.prod(shape))
+                out[p] = self.A.from_device_ptr(parts[rk][off:off + n].data_ptr(), shape, self.ctx)
+                off += n
+            assert off == 2 * sizes[rk]
+        self.ctx.sync()
+        return out
+
     # --- collectives (in place on the library's buffer / new tensor)
     def _torch(self, t):
         import torch
@@ -315,3 +377,78 @@ def sharded_two_layer_apply_row(ops, top: Sequence, top_phys: Sequence[Tuple[int
     out[n - 1] = ops.reshape(last, (ls[0] * ls[1], ls[2], ls[3] * ls[4] * ls[5]))
     phys = [(ops.shape(bra_row[col])[3], ops.shape(ket_row[col])[3]) for col in range(n)]
     return out, phys
+
+
+# ----------------------------------------------------------------------------- full contraction
+
+def sharded_contract_two_layer(ops, bra_sites: Sequence, ket_sites: Sequence, rows: int, cols: int, max_rank: int,
+                               seed: int, power_iters: int = 2, oversample: int = -1, canonicalize: bool = True):
+    """<bra|ket> by two-layer boundary contraction (contraction.cpp:313-338:
+    two_layer_first_row, then two_layer_apply_row for rows 1..n-1 with tag
+    0x20, then chain_scalar mps.cpp:102-110) with every row absorb
+    bond-sharded across the ranks (config 5 on N GPUs).  Sites are replicated
+    (row-major list, PEPS axes (phys, up, left, down, right)); the scalar is
+    returned on every rank."""
+    top, phys = [], []
+    for c in range(cols):
+        b, k = bra_sites[c], ket_sites[c]
+        sb, sk = ops.shape(b), ops.shape(k)
+        t = ops.contract("dulbr,dULBR->bBlLrR", ops.conj(b), k)
+        top.append(ops.reshape(t, (sb[3] * sk[3], sb[2] * sk[2], sb[4] * sk[4])))
+        phys.append((sb[3], sk[3]))
+    for r in range(1, rows):
+        bra_row = [bra_sites[r * cols + c] for c in range(cols)]
+        ket_row = [ket_sites[r * cols + c] for c in range(cols)]
+        top, phys = sharded_two_layer_apply_row(ops, top, phys, bra_row, ket_row, r, max_rank, seed, power_iters,
+                                                oversample, canonicalize, 0x20)
+    return ops.chain_scalar(top)
+
+
+# ----------------------------------------------------------------------------- simple-update ITE
+
+def tfim_bond_colours(rows: int, cols: int) -> List[List[Tuple[int, int, int, int]]]:
+    """The four bond colours of the TFIM Trotter step in the order the driver
+    applies them (csrc/ite.cpp tfim_bond_colours): even / odd horizontal, then
+    even / odd vertical bonds; the bonds of one colour are disjoint."""
+    out: List[List[Tuple[int, int, int, int]]] = [[], [], [], []]
+    for par in range(2):
+        for r in range(rows):
+            for c in range(par, cols - 1, 2):
+                out[par].append((r, c, r, c + 1))
+    for par in range(2):
+        for r in range(par, rows - 1, 2):
+            for c in range(cols):
+                out[2 + par].append((r, c, r + 1, c))
+    return out
+
+
+def sharded_ite_tfim(ops, sites: Sequence, rows: int, cols: int, J: float, h: float, tau: float, steps: int,
+                     rank: int):
+    """TFIM imaginary-time evolution by simple update (the reference's
+    apply_ite_term loop, drivers.cpp:56-98, with apply_two_site qr_svd_gram,
+    state.cpp:161-204) with the bonds of every colour split across the ranks:
+    each rank updates its contiguous share of the colour's (disjoint) bonds in
+    one batch, then the updated site tensors are exchanged (one all-gather of
+    shapes + one of packed data per colour).  One-site field gates are applied
+    replicated.  Per-bond updates are independent and deterministic, so the
+    result equals the single-device / serial reference bond for bond."""
+    comm = ops.comm
+    x = np.array([[0, 1], [1, 0]], dtype=np.complex128)
+    zz = np.diag([1.0, -1.0, -1.0, 1.0]).astype(np.complex128)
+    gx = ops.exp_gate(x, -h, tau)
+    gzz = ops.reshape(ops.exp_gate(zz, -J, tau), (2, 2, 2, 2))
+    colours = tfim_bond_colours(rows, cols)
+    sites = list(sites)
+    for _ in range(steps):
+        sites = ops.apply_one_site(sites, rows, cols, gx)
+        for bonds in colours:
+            a, b = shard_range(len(bonds), comm.world, comm.rank)
+            mine = bonds[a:b]
+            new = ops.apply_two_site(sites, rows, cols, gzz, mine, rank) if mine else {}
+            owners = []
+            for rk in range(comm.world):
+                ra, rb = shard_range(len(bonds), comm.world, rk)
+                owners.append([p for bd in bonds[ra:rb] for p in ((bd[0], bd[1]), (bd[2], bd[3]))])
+            for (r, c), t in ops.exchange_sites(new, owners).items():
+                sites[r * cols + c] = t
+    return sites

@@ -252,6 +252,25 @@ def test_sharded_driver_on_device_matches_reference(faithful, golden, canon, key
         assert rel(s.numpy(), g) < 1e-8
 
 
+def test_sharded_contract_and_ite_on_device(A, refo):
+    """World-size-1 device runs of the sharded full contraction (config-5
+    driver) and the colour-sharded simple-update ITE (config-4 driver) against
+    the reference: norm to 1e-8, ITE sites elementwise to 1e-9."""
+    from paper_2006_15234_b200 import sharded as SH
+    ops = SH.DeviceOps(SH.Comm())
+    sites = I.random_peps(4, 3, 2, 23)
+    dev = [A.to_device(x) for x in sites]
+    got = SH.sharded_contract_two_layer(ops, dev, dev, 4, 3, 4, 5, 2, -1, True)
+    want, _ = refo.contract_two_layer(sites, 4, 3, 4, 5, 2, -1)
+    assert abs(got - want) / abs(want) < 1e-8
+    plus = [np.array([1, 1], dtype=complex).reshape(2, 1, 1, 1, 1) / np.sqrt(2) for _ in range(12)]
+    got = SH.sharded_ite_tfim(ops, [A.to_device(x) for x in plus], 3, 4, 1.0, 3.0, 0.05, 3, 3)
+    want, _ = refo.ite_tfim(plus, 3, 4, 1.0, 3.0, 0.05, 3, 3)
+    for g, w in zip(got, want):
+        assert g.shape == w.shape
+        assert rel(g.numpy(), w) < 1e-9
+
+
 def test_random_slice_and_building_blocks(A):
     """random_slice == slice of random_tensor (bitwise); gram / gram_factors /
     projected_svd / slice / conj / reshape against numpy."""
