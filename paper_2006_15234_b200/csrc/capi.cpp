@@ -187,6 +187,7 @@ int pepsb_ctx_set_option(pepsb_ctx* c, const char* key, int64_t value) {
     if (k == "orth_mode") c->ctx->orth_mode = static_cast<int>(value);
     else if (k == "eig_solver") set_eig_solver(static_cast<int>(value));
     else if (k == "gemm_algo") zgemm_set_algo(static_cast<int>(value));
+    else if (k == "gemm_ws") zgemm_set_ws(static_cast<int>(value));
     else throw Error(kConfigError, "unknown option '" + k + "'");
   });
 }

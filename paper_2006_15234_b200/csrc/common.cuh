@@ -9,6 +9,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 #include <stdexcept>
 #include <string>
 
@@ -38,7 +39,20 @@ inline void cuda_check(cudaError_t e, const char* what, const char* file, int li
   }
 }
 #define PEPSB_CUDA(x) ::pepsb::cuda_check((x), #x, __FILE__, __LINE__)
-#define PEPSB_LAUNCH() ::pepsb::cuda_check(cudaGetLastError(), "kernel launch", __FILE__, __LINE__)
+// Debug aid: PEPSB_SYNC_DEBUG=1 synchronises after every launch so a faulting
+// kernel is reported at its own launch site (file:line) instead of at a later sync.
+inline bool sync_debug() {
+  static const bool on = [] {
+    const char* e = std::getenv("PEPSB_SYNC_DEBUG");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+inline void launch_check(const char* file, int line) {
+  cuda_check(cudaGetLastError(), "kernel launch", file, line);
+  if (sync_debug()) cuda_check(cudaDeviceSynchronize(), "kernel execution (PEPSB_SYNC_DEBUG)", file, line);
+}
+#define PEPSB_LAUNCH() ::pepsb::launch_check(__FILE__, __LINE__)
 
 // ------------------------------------------------------------------ complex helpers
 __host__ __device__ __forceinline__ double2 cmul(double2 a, double2 b) {

@@ -5,6 +5,7 @@
 // per Jacobi rotation pair (round-robin ordering, all pairs of a round
 // disjoint, one __syncthreads per round).
 #include <atomic>
+#include <vector>
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
@@ -1602,6 +1603,16 @@ void gram_factors(const double2* G, int n, double2* P, double2* R, int* deficien
   static const int env_threads = getenv("PEPSB_EIG_THREADS") ? atoi(getenv("PEPSB_EIG_THREADS")) : 0;
   const int threads = env_threads >= 64 && env_threads <= kEigThreads ? env_threads : kEigThreads;
   const int use_jacobi = eig_solver() == kEigJacobi;
+  static const char* dump = getenv("PEPSB_DUMP_EIG");  // debug aid: last input matrix to a file
+  if (dump) {
+    std::vector<double2> h(static_cast<size_t>(n) * n);
+    PEPSB_CUDA(cudaMemcpyAsync(h.data(), G, h.size() * sizeof(double2), cudaMemcpyDeviceToHost, stream));
+    PEPSB_CUDA(cudaStreamSynchronize(stream));
+    if (FILE* f = fopen(dump, "wb")) {
+      fwrite(h.data(), sizeof(double2), h.size(), f);
+      fclose(f);
+    }
+  }
   gram_factors_kernel<<<1, threads, fits ? smem : 0, stream>>>(G, n, P, R, deficient, any_def, status,
                                                                 fits ? nullptr : work, use_jacobi, lam_out,
                                                                 vec_out);

@@ -318,6 +318,7 @@ int ctas_per_sm(int cfg) { return cfg <= 1 ? 2 : 1; }
 int ctas_per_sm3m(int cfg) { return cfg == 0 ? 2 : 1; }
 
 std::atomic<int> g_algo{-1};
+std::atomic<int> g_ws{-1};
 
 template <bool AK, bool BNC>
 void launch_any(const ZgemmParams& p, cudaStream_t stream) {
@@ -708,6 +709,18 @@ void zgemm_set_algo(int a) {
   g_algo.store(a);
 }
 
+bool zgemm_ws_enabled() {
+  int v = g_ws.load();
+  if (v < 0) {
+    const char* e = getenv("PEPSB_GEMM_WS");
+    v = (e && std::string(e) == "1") ? 1 : 0;
+    g_ws.store(v);
+  }
+  return v != 0;
+}
+
+void zgemm_set_ws(int on) { g_ws.store(on ? 1 : 0); }
+
 int64_t zgemm_plan_splits(ZgemmParams& p, int num_sms) {
   if (p.M > 64 && p.M <= 72 && p.N > 72) transpose_problem(p);
   p.cfg = choose_cfg(p.M, p.N);
@@ -717,11 +730,15 @@ int64_t zgemm_plan_splits(ZgemmParams& p, int num_sms) {
   // complex-fragment kernel's 64 x 64 tile (twice the 3M tile) wins there.
   if (p.algo == kGemm3M && p.cfg == 0 && p.K <= 64) p.algo = kGemm4C;
   const TileCfg tc = p.algo == kGemm3M ? kCfgs3m[p.cfg] : p.algo == kGemm4C ? kCfgs4c[p.cfg] : kCfgs[p.cfg];
-  const int64_t bm = tc.bm, bn = tc.bn;
+  int64_t bm = tc.bm, bn = tc.bn;
+  p.num_sms = num_sms;
+  p.ws = (zgemm_ws_enabled() && p.cfg == 0 && p.algo != kGemm4M && zgemm_ws_eligible(p)) ? 1 : 0;
+  if (p.ws) zgemm_ws_tile(p, bm, bn);
   const int64_t tiles = ((p.M + bm - 1) / bm) * ((p.N + bn - 1) / bn) * p.batch;
   // one full wave of resident CTAs (no partial second wave)
   const int64_t target =
-      static_cast<int64_t>(p.algo == kGemm4M ? ctas_per_sm(p.cfg) : ctas_per_sm3m(p.cfg)) * num_sms;
+      p.ws ? num_sms
+           : static_cast<int64_t>(p.algo == kGemm4M ? ctas_per_sm(p.cfg) : ctas_per_sm3m(p.cfg)) * num_sms;
   int64_t splits = 1;
   if (tiles < target && p.K > 4 * kBK) {
     splits = std::min<int64_t>(std::max<int64_t>(1, target / tiles), (p.K + 4 * kBK - 1) / (4 * kBK));
@@ -751,7 +768,9 @@ void zgemm_launch(ZgemmParams p, cudaStream_t stream) {
     // empty contraction: C = 0 (or unchanged when accumulating)
     p.splits = 1;
   }
-  if (p.algo == kGemm3M) {
+  if (p.ws && p.K > 0) {
+    zgemm_ws_launch(p, p.num_sms, stream);
+  } else if (p.algo == kGemm3M) {
     if (p.cfg == 4) p.cfg = 0;
     if (ak && bnc)
       launch_any3m<true, true>(p, stream);

@@ -43,6 +43,8 @@ struct ZgemmParams {
   int accumulate = 0;  // C += result instead of C = result
   int cfg = 0;         // tile configuration (set by zgemm_plan_splits)
   int algo = 0;        // kGemm4M / kGemm3M (set by zgemm_plan_splits)
+  int ws = 0;          // persistent warp-specialised kernel (zgemm_ws.cu)
+  int num_sms = 148;   // grid of the persistent kernel
 };
 
 // Complex product scheme (process-wide): kGemm4M = real embedding, 4 real MACs
@@ -56,6 +58,14 @@ inline double zgemm_exec_flops(const ZgemmParams& p) {
   return (p.algo == kGemm3M ? 6.0 : 8.0) * static_cast<double>(p.batch) * p.M * p.N * p.K;
 }
 void zgemm_set_algo(int a);
+// Persistent kernel with TMA tensor-map operand staging (zgemm_ws.cu): opt-in
+// (PEPSB_GEMM_WS=1 or option "gemm_ws" = 1); measured at config 2 it does not
+// beat the classic cp.async kernels, so they stay the default.
+bool zgemm_ws_enabled();
+void zgemm_set_ws(int on);
+bool zgemm_ws_eligible(const ZgemmParams& p);
+void zgemm_ws_tile(const ZgemmParams& p, int64_t& bm, int64_t& bn);
+void zgemm_ws_launch(const ZgemmParams& p, int num_sms, cudaStream_t stream);
 
 // Launches the GEMM (and the deterministic split-K reduction when needed).
 // `work` is allocated by the caller when splits > 1 (see zgemm_workspace).

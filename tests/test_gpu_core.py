@@ -263,13 +263,16 @@ def test_errors_mirror_reference(A):
                          A.TruncationPolicy(0, 1e-14))
 
 
-@pytest.mark.parametrize("algo", [0, 1, 2], ids=["4m_embed", "3m", "4m_cfrag"])
-def test_gemm_kernels_all_layouts(A, algo):
+@pytest.mark.parametrize("algo,ws", [(0, 0), (1, 0), (2, 0), (1, 1), (2, 1)],
+                         ids=["4m_embed", "3m", "4m_cfrag", "3m_ws", "4m_cfrag_ws"])
+def test_gemm_kernels_all_layouts(A, algo, ws):
     """Every complex GEMM kernel (real embedding, 3M/Gauss, 4M complex
-    fragments) on every tile configuration (64/72-wide, transposed problems,
-    ragged edges, split-K) and operand layout, against numpy at rounding level."""
+    fragments; classic and persistent warp-specialised bulk-copy variants) on
+    every tile configuration (64/72-wide, transposed problems, ragged edges,
+    split-K) and operand layout, against numpy at rounding level."""
     ctx = A.default_context()
     ctx.set_option("gemm_algo", algo)
+    ctx.set_option("gemm_ws", ws)
     try:
         shapes = [(70, 90, 300), (64, 64, 64), (72, 72, 72), (128, 300, 64), (65, 70, 17), (5, 7, 3),
                   (200, 72, 130), (72, 200, 33), (64, 72, 64), (72, 64, 48), (33, 65, 129), (1, 1, 1),
@@ -288,3 +291,38 @@ def test_gemm_kernels_all_layouts(A, algo):
             assert np.abs(got - a.conj() @ b).max() <= 1e-12 * np.abs(a.conj() @ b).max()
     finally:
         ctx.set_option("gemm_algo", 1)
+        ctx.set_option("gemm_ws", 0)
+
+
+@pytest.mark.parametrize("algo", [1, 2], ids=["3m", "4m_cfrag"])
+def test_gemm_ws_persistent_tiles_and_batches(A, algo):
+    """Persistent warp-specialised GEMM: several tiles per CTA (the producer
+    runs ahead across tile boundaries and reuses the offset tables), K tails,
+    batched contractions and scattered (permuted) outputs, against numpy."""
+    ctx = A.default_context()
+    ctx.set_option("gemm_algo", algo)
+    ctx.set_option("gemm_ws", 1)
+    try:
+        for (m, n, k) in [(128, 9000, 64), (64, 20000, 40), (200, 3000, 37), (96, 4100, 128)]:
+            a = O.random_tensor((m, k), m + 3 * k)
+            b = O.random_tensor((k, n), n + 5 * k)
+            ref = a @ b
+            got = A.contract("ik,kj->ij", a, b).numpy()
+            assert np.abs(got - ref).max() <= 1e-12 * np.abs(ref).max(), (algo, m, n, k)
+            got = A.contract("ik,kj->ji", a.conj(), b).numpy()
+            ref = (a.conj() @ b).T
+            assert np.abs(got - ref).max() <= 1e-12 * np.abs(ref).max(), (algo, m, n, k)
+        a = O.random_tensor((3, 70, 40), 91)
+        b = O.random_tensor((3, 40, 2100), 92)
+        got = A.contract("bik,bkj->ibj", a, b).numpy()
+        ref = np.einsum("bik,bkj->ibj", a, b)
+        assert np.abs(got - ref).max() <= 1e-12 * np.abs(ref).max()
+        # split into output axes (mixed-radix scatter of the epilogue)
+        a = O.random_tensor((8, 8, 24), 93)
+        b = O.random_tensor((24, 40, 50), 94)
+        got = A.contract("pqk,kst->sqtp", a, b).numpy()
+        ref = np.einsum("pqk,kst->sqtp", a, b)
+        assert np.abs(got - ref).max() <= 1e-12 * np.abs(ref).max()
+    finally:
+        ctx.set_option("gemm_algo", 1)
+        ctx.set_option("gemm_ws", 0)
