@@ -86,6 +86,11 @@ int pepsb_ctx_set_option(pepsb_ctx* ctx, const char* key, int64_t value);
  * CholeskyQR breakdowns redone on the Gram-eigh route, TSQR fallbacks */
 int pepsb_ctx_counters(pepsb_ctx* ctx, uint64_t* out6);
 int pepsb_ctx_reset_counters(pepsb_ctx* ctx);
+/* Named counter: "flops", "einsumsvd_flops", "peak_elements", "launches",
+ * "faithful_redos", "tsqr_fallbacks", "degenerate_truncations" (simple-update
+ * truncations whose cut falls inside a singular pair equal to 1e-10 relative:
+ * the kept subspace there is rounding-dependent). */
+int pepsb_ctx_get_counter(pepsb_ctx* ctx, const char* name, uint64_t* value);
 /* Per-launch CUDA-event timing of the library's kernels (off by default).
  * Report: 4 kinds (0 GEMM, 1 small factorizations, 2 gathers, 3 other) x
  * {launches, device ms, algorithmic real flops, algorithmic bytes}. */

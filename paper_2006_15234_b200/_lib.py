@@ -47,6 +47,7 @@ _SIGS = {
     "pepsb_ctx_sync": (C.c_int, [_VP]),
     "pepsb_ctx_set_option": (C.c_int, [_VP, C.c_char_p, C.c_int64]),
     "pepsb_ctx_counters": (C.c_int, [_VP, C.POINTER(C.c_uint64)]),
+    "pepsb_ctx_get_counter": (C.c_int, [_VP, C.c_char_p, C.POINTER(C.c_uint64)]),
     "pepsb_ctx_reset_counters": (C.c_int, [_VP]),
     "pepsb_ctx_stream": (_VP, [_VP]),
     "pepsb_ctx_debug_word": (C.c_int, [_VP, C.c_int, C.c_int]),

@@ -107,6 +107,11 @@ class Context:
         return dict(flops=int(a[0]), einsumsvd_flops=int(a[1]), peak_elements=int(a[2]), launches=int(a[3]),
                     faithful_redos=int(a[4]), tsqr_fallbacks=int(a[5]))
 
+    def counter(self, name: str) -> int:
+        v = C.c_uint64()
+        check(lib().pepsb_ctx_get_counter(self.h, name.encode(), C.byref(v)))
+        return int(v.value)
+
     def reset_counters(self):
         check(lib().pepsb_ctx_reset_counters(self.h))
 

@@ -1,3 +1,4 @@
+#include <algorithm>
 // extern "C" boundary (include/peps_b200.h): POD in, handles out, status codes.
 #include <cstring>
 #include <exception>
@@ -188,6 +189,7 @@ int pepsb_ctx_set_option(pepsb_ctx* c, const char* key, int64_t value) {
     else if (k == "eig_solver") set_eig_solver(static_cast<int>(value));
     else if (k == "gemm_algo") zgemm_set_algo(static_cast<int>(value));
     else if (k == "gemm_ws") zgemm_set_ws(static_cast<int>(value));
+    else if (k == "overlap") c->ctx->overlap = static_cast<int>(std::clamp<int64_t>(value, 0, 2));
     else throw Error(kConfigError, "unknown option '" + k + "'");
   });
 }
@@ -204,12 +206,34 @@ int pepsb_ctx_counters(pepsb_ctx* c, uint64_t* out) {
   });
 }
 
+int pepsb_ctx_get_counter(pepsb_ctx* c, const char* name, uint64_t* value) {
+  return guard([&] {
+    need(c, "ctx");
+    need(value, "value");
+    const std::string k = name ? name : "";
+    Ctx& x = *c->ctx;
+    if (k == "flops") *value = x.flops;
+    else if (k == "einsumsvd_flops") *value = x.einsumsvd_flops;
+    else if (k == "peak_elements") *value = x.peak_elements;
+    else if (k == "launches") *value = static_cast<uint64_t>(x.launches);
+    else if (k == "faithful_redos") *value = static_cast<uint64_t>(x.faithful_redos);
+    else if (k == "tsqr_fallbacks") *value = static_cast<uint64_t>(x.tsqr_fallbacks);
+    else if (k == "degenerate_truncations") {
+      unsigned long long v = 0;
+      PEPSB_CUDA(cudaMemcpyAsync(&v, x.d_degenerate, sizeof(v), cudaMemcpyDeviceToHost, x.stream));
+      x.sync();
+      *value = v;
+    } else throw Error(kConfigError, "unknown counter '" + k + "'");
+  });
+}
+
 int pepsb_ctx_reset_counters(pepsb_ctx* c) {
   return guard([&] {
     need(c, "ctx");
     c->ctx->flops = c->ctx->einsumsvd_flops = c->ctx->peak_elements = 0;
     c->ctx->launches = 0;
     c->ctx->faithful_redos = c->ctx->tsqr_fallbacks = 0;
+    PEPSB_CUDA(cudaMemsetAsync(c->ctx->d_degenerate, 0, sizeof(unsigned long long), c->ctx->stream));
   });
 }
 

@@ -42,6 +42,10 @@ void* Pool::alloc(size_t bytes, size_t* reserved) {
 }
 
 void Pool::release(void* p, size_t bytes) {
+  if (defer) {
+    parked.emplace_back(bytes, p);
+    return;
+  }
   free_blocks.emplace(bytes, p);
   cached_bytes += bytes;
 }
@@ -49,6 +53,10 @@ void Pool::release(void* p, size_t bytes) {
 void Pool::trim() {
   if (stream) cudaStreamSynchronize(stream);
   else cudaDeviceSynchronize();
+  if (!defer) {
+    for (auto& [sz, p] : parked) free_blocks.emplace(sz, p);
+    parked.clear();
+  }
   for (auto& [sz, p] : free_blocks) {
     cudaFree(p);
     reserved_bytes -= sz;
@@ -98,25 +106,61 @@ HostTimer::~HostTimer() {
 
 Ctx::Ctx(int dev) : device(dev) {
   trace = getenv("PEPSB_TRACE") != nullptr;
+  if (const char* e = getenv("PEPSB_OVERLAP")) overlap = e[0] == '0' ? 0 : e[0] == '2' ? 2 : 1;
   PEPSB_CUDA(cudaSetDevice(dev));
   PEPSB_CUDA(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev));
   PEPSB_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+  PEPSB_CUDA(cudaStreamCreateWithFlags(&side_stream, cudaStreamNonBlocking));
+  PEPSB_CUDA(cudaEventCreateWithFlags(&fork_event, cudaEventDisableTiming));
+  PEPSB_CUDA(cudaEventCreateWithFlags(&join_event, cudaEventDisableTiming));
+  main_stream = stream;
   pool = std::make_shared<Pool>();
   pool->stream = stream;
   PEPSB_CUDA(cudaMalloc(&d_status, 64 * sizeof(int)));
   PEPSB_CUDA(cudaMemset(d_status, 0, 64 * sizeof(int)));
   PEPSB_CUDA(cudaMallocHost(&h_status, 64 * sizeof(int)));
+  PEPSB_CUDA(cudaMalloc(&d_degenerate, sizeof(unsigned long long)));
+  PEPSB_CUDA(cudaMemset(d_degenerate, 0, sizeof(unsigned long long)));
 }
 
 Ctx::~Ctx() {
+  if (stream != main_stream) join();
+  if (side_stream) cudaStreamSynchronize(side_stream);
   if (stream) cudaStreamSynchronize(stream);
   pool->trim();
   pool->stream = nullptr;  // buffers that outlive the context release into a stream-less pool
   profile_clear();
   for (auto e : event_pool) cudaEventDestroy(e);
   if (d_status) cudaFree(d_status);
+  if (d_degenerate) cudaFree(d_degenerate);
   if (h_status) cudaFreeHost(h_status);
   if (stream) cudaStreamDestroy(stream);
+  if (side_stream) cudaStreamDestroy(side_stream);
+  if (fork_event) cudaEventDestroy(fork_event);
+  if (join_event) cudaEventDestroy(join_event);
+}
+
+void Ctx::fork() {
+  if (pool->defer) throw Error(kOtherError, "nested stream fork");
+  PEPSB_CUDA(cudaEventRecord(fork_event, main_stream));
+  pool->defer = true;
+}
+
+void Ctx::side() {
+  PEPSB_CUDA(cudaStreamWaitEvent(side_stream, fork_event, 0));
+  stream = side_stream;
+}
+
+void Ctx::join() {
+  PEPSB_CUDA(cudaEventRecord(join_event, side_stream));
+  stream = main_stream;
+  PEPSB_CUDA(cudaStreamWaitEvent(main_stream, join_event, 0));
+  pool->defer = false;
+  for (auto& [sz, p] : pool->parked) {
+    pool->free_blocks.emplace(sz, p);
+    pool->cached_bytes += sz;
+  }
+  pool->parked.clear();
 }
 
 BufPtr Ctx::alloc(int64_t n) {

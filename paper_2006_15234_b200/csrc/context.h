@@ -33,6 +33,11 @@ struct Pool {
   std::multimap<size_t, void*> free_blocks;
   size_t cached_bytes = 0, reserved_bytes = 0;
   cudaStream_t stream = nullptr;  // cleared when the owning context goes away
+  // Two-stream phases (Ctx::fork): blocks released while work runs on two
+  // streams are parked until the streams join -- stream order alone no longer
+  // protects them from reuse by the other stream.
+  bool defer = false;
+  std::vector<std::pair<size_t, void*>> parked;
   void* alloc(size_t bytes, size_t* reserved);
   void release(void* p, size_t bytes);
   void trim();  // synchronises, then returns every cached block to the driver
@@ -94,13 +99,27 @@ class Ctx {
   DTensor zeros(const std::vector<int64_t>& shape);
   void sync();
 
+  // Two-stream phase: fork() marks the fork point on the main stream (blocks
+  // released from here on are parked); work enqueued next stays on the main
+  // stream; side() switches `stream` to the side stream, which starts after
+  // the fork point, i.e. concurrently with the main-stream work enqueued since;
+  // join() makes the main stream wait for the side stream, switches back and
+  // unparks the blocks.
+  void fork();
+  void side();
+  void join();
+
   int device = 0;
   int num_sms = 148;
   cudaStream_t stream = nullptr;
+  cudaStream_t main_stream = nullptr, side_stream = nullptr;
+  cudaEvent_t fork_event = nullptr, join_event = nullptr;
   // Device status word shared by the small factorization kernels
   // (SmallStatus bits); read back at the einsumsvd sync points.
   int* d_status = nullptr;
   int* h_status = nullptr;  // pinned
+  // Simple-update truncations through a degenerate singular pair (device counter).
+  unsigned long long* d_degenerate = nullptr;
   // Launch accounting (for the bench's gpu_launches claim).
   int64_t launches = 0;
   // Host-side tracing (PEPSB_TRACE): seconds spent in allocation, free and sync.
@@ -125,6 +144,11 @@ class Ctx {
   // basis): identical within one row / one einsumsvd, but across rows it
   // differs from the reference by the sketch-dependent rSVD error.
   int orth_mode = 0;
+  // Hide the big-side k x k eigensolver of each power iteration behind the
+  // next operator application on a second stream (decomp.cpp
+  // apply_orth_speculative): option "overlap" / PEPSB_OVERLAP, 0 off, 1 when
+  // the column extent is >= 2^15 (default), 2 always.
+  int overlap = 1;
 
   // Optional per-launch device timing (CUDA events on `stream`), used by the
   // bench's roofline pass; off in timed runs.

@@ -191,6 +191,71 @@ LTensor orth(Ctx& ctx, const LTensor& Y) {
   return out;
 }
 
+// apply(orth(Z)) for the big-side orthogonalisation of a power iteration,
+// with the k x k eigensolver hidden behind the operator application: by
+// linearity A (Z P) = (A Z) P, so A Z runs on the side stream while the Gram
+// matrix and its eigendecomposition run on the main stream, and only the
+// small (rows_Y x k) product (A Z) P follows.  This also skips the big
+// Q = Z P product.  When the Gram matrix is deficient (columns clamped and
+// completed, decomposition.cpp:86-117) the completed basis is not of the form
+// Z P: the speculative A Z is discarded and A (orth(Z)) is formed as usual.
+// Rounding differs from A (Z P) at the level eps ||A|| ||Z|| ||P||.
+template <class ApplyFn>
+LTensor apply_orth_speculative(Ctx& ctx, const LTensor& Z, ApplyFn&& apply) {
+  const int64_t k = Z.ext.back();
+  const int64_t rows = Z.size() / k;
+  ctx.fork();
+  BufPtr G = ctx.alloc(k * k);
+  mm(ctx, G->p, Z.ptr, true, true, Z.ptr, false, false, k, k, rows);
+  BufPtr P = ctx.alloc(k * k), R = ctx.alloc(k * k), def = ctx.alloc((k + 2 + 1) / 2 + 1);
+  int* d_def = reinterpret_cast<int*>(def->p);
+  int* d_any = d_def + k;
+  BufPtr work;
+  if (2 * k * (k + 1) * 16 > 176 * 1024) work = ctx.alloc(2 * k * (k + 1));
+  {
+    ProfScope ps_(ctx, Ctx::kProfSmall);
+    gram_factors(G->p, static_cast<int>(k), P->p, R->p, d_def, d_any, ctx.d_status, work ? work->p : nullptr,
+                 ctx.stream);
+  }
+  ++ctx.launches;
+  PEPSB_CUDA(cudaMemcpyAsync(ctx.h_status + 16, d_any, sizeof(int), cudaMemcpyDeviceToHost, ctx.stream));
+  cudaEvent_t eig_done = ctx.take_event();
+  PEPSB_CUDA(cudaEventRecord(eig_done, ctx.stream));
+  ctx.side();
+  LTensor AZ = apply(Z);
+  ctx.join();
+  {
+    HostTimer ht(ctx.trace ? &ctx.t_sync : nullptr);
+    PEPSB_CUDA(cudaEventSynchronize(eig_done));
+  }
+  ctx.event_pool.push_back(eig_done);
+  if (ctx.h_status[16] == 0) {
+    const int64_t ry = AZ.size() / k;
+    BufPtr Y = ctx.alloc(ry * k);
+    mm(ctx, Y->p, AZ.ptr, false, AZ.conj, P->p, false, false, ry, k, k);
+    LTensor out = AZ;
+    out.buf = Y;
+    out.ptr = Y->p;
+    out.conj = false;
+    out.str = row_major_strides(out.ext);
+    return out;
+  }
+  // deficient Gram: the reference's completed basis, then the plain application
+  BufPtr Q = ctx.alloc(rows * k);
+  mm(ctx, Q->p, Z.ptr, false, Z.conj, P->p, false, false, rows, k, k);
+  {
+    ProfScope ps_(ctx, Ctx::kProfSmall);
+    complete_columns(Q->p, rows, static_cast<int>(k), d_def, d_any, ctx.d_status, ctx.stream);
+  }
+  ++ctx.launches;
+  LTensor q = Z;
+  q.buf = Q;
+  q.ptr = Q->p;
+  q.conj = false;
+  q.str = row_major_strides(q.ext);
+  return apply(q);
+}
+
 struct Projected {
   BufPtr Ut;  // k x k left singular vectors of B = P^H A (phase-fixed)
   std::vector<double> s;
@@ -388,8 +453,13 @@ EinsumsvdResultD rsvd_core(Ctx& ctx, const ImplicitOp& op, const Trunc& policy, 
   const double tr0 = trace ? now() : 0.0;
   LTensor p = orth(ctx, apply(q));
   for (int i = 0; i < cfg.power_iters; ++i) {
-    q = orth(ctx, adjoint(p));
-    p = orth(ctx, apply(q));
+    // (small problems: the host sync on the eigensolver would cost more than it hides)
+    if (ctx.orth_mode == 0 && (ctx.overlap == 2 || (ctx.overlap == 1 && op.col_extent() >= (1 << 15)))) {
+      p = orth(ctx, apply_orth_speculative(ctx, adjoint(p), apply));
+    } else {
+      q = orth(ctx, adjoint(p));
+      p = orth(ctx, apply(q));
+    }
   }
   LTensor z = adjoint(p);
   q = LTensor();

@@ -166,7 +166,7 @@ PepsStateD apply_two_site_batch(Ctx& ctx, const PepsStateD& s, const DTensor& ga
   int* status = ctx.d_status + 2;
   PEPSB_CUDA(cudaMemsetAsync(status, 0, sizeof(int), ctx.stream));
   su_reduce(reinterpret_cast<const SuSiteDesc*>(dsd->p), 2 * nb, smem_reduce, status, ctx.stream);
-  su_split(reinterpret_cast<const SuBondDesc*>(dbd->p), nb, smem_split, ranks, status, ctx.stream);
+  su_split(reinterpret_cast<const SuBondDesc*>(dbd->p), nb, smem_split, ranks, status, ctx.d_degenerate, ctx.stream);
   ctx.launches += 2;
   std::vector<int> hr(nb + 1);
   PEPSB_CUDA(cudaMemcpyAsync(hr.data(), ranks, nb * sizeof(int), cudaMemcpyDeviceToHost, ctx.stream));

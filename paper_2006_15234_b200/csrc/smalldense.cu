@@ -957,6 +957,20 @@ __device__ void gram_factors_dev(const double2* G, int n, double2* X, double2* V
   atomicMax(reinterpret_cast<unsigned long long*>(&hmax[1]), __double_as_longlong(scale));
   __syncthreads();
   if (threadIdx.x == 0 && hmax[0] > 1e-10 * fmax(1.0, hmax[1])) atomicOr(status, kSmallNotHermitian);
+  // Exact power-of-two scaling to max |A| in [1, 2): the solvers form squares of
+  // the entries (reflector norms, secular-equation terms), which overflow for
+  // the Gram matrices of unnormalised states (|G| ~ 1e171 after 100 ITE steps;
+  // zheevd scales the same way).  Scaling by 2^-e is exact, so eigenvectors are
+  // bitwise those of the unscaled problem wherever that one does not overflow.
+  const double gmax = hmax[1];
+  const int gexp = (gmax > 0.0 && isfinite(gmax)) ? ilogb(gmax) : 0;
+  if (gexp != 0) {
+    for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
+      double2& x = X[(e / n) * ld + e % n];
+      x = make_double2(scalbn(x.x, -gexp), scalbn(x.y, -gexp));
+    }
+    __syncthreads();
+  }
 
   double fro = 0.0;
   for (int e = threadIdx.x; e < n * n; e += blockDim.x) fro += cnorm2(X[(e / n) * ld + e % n]);
@@ -982,7 +996,7 @@ __device__ void gram_factors_dev(const double2* G, int n, double2* X, double2* V
     herm_jacobi(X, V, n, ld, neps, abs_skip, low_skip, 40, status);
   else
     herm_eig_tridiag(X, V, n, ld, status);
-  for (int j = threadIdx.x; j < n; j += blockDim.x) lam[j] = X[j * ld + j].x;
+  for (int j = threadIdx.x; j < n; j += blockDim.x) lam[j] = scalbn(X[j * ld + j].x, gexp);
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
   sort_desc(lam, order, n);
@@ -1416,7 +1430,8 @@ __global__ void __launch_bounds__(512) su_reduce_kernel(const SuSiteDesc* descs,
   for (int idx = threadIdx.x; idx < S * S; idx += blockDim.x) D.R[idx] = Rm[idx];
 }
 
-__global__ void __launch_bounds__(256) su_split_kernel(const SuBondDesc* descs, int* ranks, int* status) {
+__global__ void __launch_bounds__(256) su_split_kernel(const SuBondDesc* descs, int* ranks, int* status,
+                                                       unsigned long long* degenerate) {
   extern __shared__ __align__(16) unsigned char sm[];
   __shared__ int rank_sh;
   const SuBondDesc B = descs[blockIdx.x];
@@ -1450,6 +1465,9 @@ __global__ void __launch_bounds__(256) su_split_kernel(const SuBondDesc* descs, 
     if (B.cap > 0 && B.cap < r) r = B.cap;
     rank_sh = static_cast<int>(r < 1 ? 1 : r);
     ranks[blockIdx.x] = rank_sh;
+    // truncation through a (numerically) degenerate pair: the kept subspace is
+    // rounding-dependent -- counted and reported, not hidden
+    if (degenerate && r >= 1 && r < above && sv[r - 1] - sv[r] <= 1e-10 * sv[r - 1]) atomicAdd(degenerate, 1ull);
   }
   __syncthreads();
   const int rank = rank_sh;
@@ -1558,14 +1576,15 @@ void su_reduce(const SuSiteDesc* d, int n, size_t smem, int* status, cudaStream_
   PEPSB_LAUNCH();
 }
 
-void su_split(const SuBondDesc* d, int n, size_t smem, int* ranks, int* status, cudaStream_t st) {
+void su_split(const SuBondDesc* d, int n, size_t smem, int* ranks, int* status, unsigned long long* degenerate,
+              cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
     PEPSB_CUDA(cudaFuncSetAttribute(su_split_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     attr = true;
   }
   if (n == 0) return;
-  su_split_kernel<<<n, 256, smem, st>>>(d, ranks, status);
+  su_split_kernel<<<n, 256, smem, st>>>(d, ranks, status, degenerate);
   PEPSB_LAUNCH();
 }
 

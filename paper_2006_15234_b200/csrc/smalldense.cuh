@@ -105,7 +105,10 @@ struct SuOneSiteDesc {
   const double2* gate;
 };
 void su_reduce(const SuSiteDesc* d_descs, int n, size_t smem, int* status, cudaStream_t stream);
-void su_split(const SuBondDesc* d_descs, int n, size_t smem, int* ranks, int* status, cudaStream_t stream);
+// degenerate (optional): counts truncations whose cut falls inside a pair of
+// singular values equal to 1e-10 relative.
+void su_split(const SuBondDesc* d_descs, int n, size_t smem, int* ranks, int* status, unsigned long long* degenerate,
+              cudaStream_t stream);
 void su_restore(const SuRestoreDesc* d_descs, int n, const int* ranks, cudaStream_t stream);
 void su_one_site(const SuOneSiteDesc* d_descs, int n, cudaStream_t stream);
 // out = exp(-tau * coeff * H) for Hermitian n x n H (hermitian_function, linalg.cpp:297-314)

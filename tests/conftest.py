@@ -41,13 +41,17 @@ def rel(a, b):
     return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
 
 
-@pytest.fixture
-def faithful(A):
-    """Reference-faithful orthogonalisation basis (elementwise parity of t1/t2)."""
+@pytest.fixture(params=[1, 2], ids=["overlap_auto", "overlap_forced"])
+def faithful(A, request):
+    """Reference-faithful orthogonalisation basis (elementwise parity of t1/t2),
+    with the eigensolver/operator-application overlap (A (Z P) = (A Z) P on two
+    streams) at its default size threshold and forced on every einsumsvd."""
     ctx = A.default_context()
     ctx.set_option("orth_mode", 0)
+    ctx.set_option("overlap", request.param)
     yield A
     ctx.set_option("orth_mode", 0)
+    ctx.set_option("overlap", 1)
 
 
 @pytest.fixture

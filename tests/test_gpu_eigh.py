@@ -101,3 +101,23 @@ def test_eigh_rejects_non_hermitian(A, solver):
     m = O.random_tensor((6, 6), 3)
     with pytest.raises(PepsError):
         A.eigh(m)
+
+
+@pytest.mark.parametrize("solver", [0, 1], ids=["dc", "jacobi"])
+def test_eigh_scale_invariant_extreme_magnitudes(A, solver):
+    """Gram matrices of unnormalised states reach |G| ~ 1e171 (8x8 TFIM after
+    100 ITE steps); squares of such entries overflow.  The solver scales by an
+    exact power of two: eigenvectors are bitwise those of the unscaled matrix
+    and eigenvalues scale exactly, for 2^+560 and 2^-500."""
+    ctx = A.default_context()
+    ctx.set_option("eig_solver", solver)
+    try:
+        m = _herm(72, 5) @ _herm(72, 6)
+        m = m @ m.conj().T  # positive definite Gram-like
+        w0, v0 = A.eigh(m)
+        for e in (560, -500):
+            w, v = A.eigh(m * 2.0 ** e)
+            assert np.array_equal(v.numpy(), v0.numpy())
+            assert np.array_equal(np.asarray(w), np.asarray(w0) * 2.0 ** e)
+    finally:
+        ctx.set_option("eig_solver", 0)

@@ -55,6 +55,35 @@ def contract_flops(n, r, m, q, os_):
     return sum(4 * costmodel.two_layer_row_flops(n, r, m, q, os_, interior=row < n - 1) for row in range(1, n))
 
 
+def bond_spectra(sites, rows, cols, top=8):
+    """Gauge-invariant per-bond check: singular values of the two-site tensor
+    contracted over each bond and matricised (site-a legs) x (site-b legs) --
+    invariant under unitary gauge changes on every bond (the SVD phase and
+    degenerate-subspace freedom of simple update), normalised by the largest."""
+    out = []
+    for r in range(rows):
+        for c in range(cols):
+            a = sites[r * cols + c]
+            if c + 1 < cols:  # horizontal: a right (4) with b left (2)
+                b = sites[r * cols + c + 1]
+                m = np.tensordot(a, b, axes=([4], [2]))  # (pa, ua, la, da, pb, ub, db, rb)
+                m = m.reshape(int(np.prod(a.shape[:4])), -1)
+                s = np.linalg.svd(m, compute_uv=False)[:top]
+                out.append(s / s[0])
+            if r + 1 < rows:  # vertical: a down (3) with b up (1)
+                b = sites[(r + 1) * cols + c]
+                m = np.tensordot(a, b, axes=([3], [1]))
+                m = m.reshape(int(np.prod(a.shape[:3]) * a.shape[4]), -1)
+                s = np.linalg.svd(m, compute_uv=False)[:top]
+                out.append(s / s[0])
+    return out
+
+
+def spectra_err(got, want, rows, cols):
+    sg, sw = bond_spectra(got, rows, cols), bond_spectra(want, rows, cols)
+    return max(float(np.abs(x - y).max()) for x, y in zip(sg, sw))
+
+
 def cfg1(args, ctx):
     c = inputs.config1()
     st = A.PepsState(4, 4, 2, c["sites"], ctx=ctx)
@@ -122,13 +151,16 @@ def cfg4(args, ctx):
     st = A.PepsState(8, 8, 2, plus, ctx=ctx)
     A.ite_tfim(st, 1.0, 3.0, 0.01, 2, 8)  # warm-up
     _sync(ctx)
+    ctx.reset_counters()
     t0 = time.perf_counter()
     out = A.ite_tfim(st, 1.0, 3.0, 0.01, steps, 8)
     _sync(ctx)
     dt = time.perf_counter() - t0
+    degenerate = ctx.counter("degenerate_truncations")
     res = {"config": 4, "workload": f"TFIM ITE 8x8 r=8 J=1 h=3 tau=0.01, {steps} steps, simple update "
                                      "(bonds batched per colour)",
-           "s_total": dt, "s_per_step": dt / steps, "updates_per_s": steps * (64 + 112) / dt}
+           "s_total": dt, "s_per_step": dt / steps, "updates_per_s": steps * (64 + 112) / dt,
+           "degenerate_truncations": degenerate, "bond_updates": steps * 112}
     if args.ref:
         from oracle import ref
         ref.set_threads(os.cpu_count() or 1)
@@ -140,7 +172,61 @@ def cfg4(args, ctx):
         worst = max(float(np.abs(g - w).max() / max(np.abs(w).max(), 1e-300)) for g, w in zip(got, want)) \
             if shapes_equal else None
         res.update({"ref_s_total": rdt, "ref_s_per_step": rdt / steps, "cpu_cores": os.cpu_count(),
-                    "shapes_bit_exact": shapes_equal, "max_site_rel_err_vs_ref": worst})
+                    "shapes_bit_exact": shapes_equal, "max_site_rel_err_vs_ref": worst,
+                    "bond_spectra_max_err_vs_ref": spectra_err(got, want, 8, 8) if shapes_equal else None})
+        # Gauge-invariant comparison: the SVD gauge of degenerate bond spectra
+        # (exact at the |+> start) is arbitrary, so compare the STATES: norms and
+        # fidelity |<ref|gpu>|^2 / (<ref|ref><gpu|gpu>) by device boundary
+        # contraction (m=64, accurate for this weakly entangled state).
+        # The unnormalised states reach |<psi|psi>| ~ 1e300+ after 100 steps (the
+        # reference does not normalise either): scale every site by its max |entry|
+        # and carry the log of the scale factors.
+        mg = [float(np.abs(g).max()) for g in got]
+        mr = [float(np.abs(w).max()) for w in want]
+        sg = A.PepsState(8, 8, 2, [g / m for g, m in zip(got, mg)], ctx=ctx)
+        sr = A.PepsState(8, 8, 2, [w / m for w, m in zip(want, mr)], ctx=ctx)
+        opt = A.ContractOption.two_layer_opt(64, 7, 2, 8)
+        n_g = A.contract_two_layer(sg, sg, opt)
+        n_r = A.contract_two_layer(sr, sr, opt)
+        ov = A.contract_two_layer(sr, sg, opt)
+        ln_g = np.log(abs(n_g)) + 2 * np.log(mg).sum()
+        ln_r = np.log(abs(n_r)) + 2 * np.log(mr).sum()
+        res.update({"log_norm_gpu_state": ln_g, "log_norm_ref_state": ln_r,
+                    "log_norm_rel_diff": abs(ln_g - ln_r) / abs(ln_r),
+                    "norm_rel_diff": float(abs(np.expm1(ln_g - ln_r))),
+                    "one_minus_fidelity": 1.0 - abs(ov) ** 2 / (abs(n_g) * abs(n_r))})
+    return res
+
+
+def cfg4b(args, ctx):
+    """Config 4 from a random (symmetry-breaking) product state: the |+> start of
+    config 4 produces exactly degenerate bond spectra whose truncation subspace
+    is rounding-dependent, so bond-for-bond parity is checked here,
+    elementwise, on the full 8x8 r=8 100-step evolution."""
+    steps = args.ite_steps
+    rs = np.random.default_rng(44)
+    init = []
+    for _ in range(64):
+        v = rs.standard_normal(2) + 1j * rs.standard_normal(2)
+        init.append((v / np.linalg.norm(v)).reshape(2, 1, 1, 1, 1))
+    st = A.PepsState(8, 8, 2, init, ctx=ctx)
+    _sync(ctx)
+    t0 = time.perf_counter()
+    ctx.reset_counters()
+    out = A.ite_tfim(st, 1.0, 3.0, 0.01, steps, 8)
+    _sync(ctx)
+    dt = time.perf_counter() - t0
+    res = {"config": "4b", "degenerate_truncations": ctx.counter("degenerate_truncations"), "workload": f"as config 4 from a random product state, {steps} steps", "s_total": dt,
+           "s_per_step": dt / steps}
+    from oracle import ref
+    ref.set_threads(os.cpu_count() or 1)
+    want, _ = ref.ite_tfim(init, 8, 8, 1.0, 3.0, 0.01, steps, 8)
+    got = [s.numpy() for s in out.sites]
+    shapes_equal = [g.shape for g in got] == [w.shape for w in want]
+    res["shapes_bit_exact"] = shapes_equal
+    if shapes_equal:
+        res["max_site_rel_err_vs_ref"] = max(float(np.abs(g - w).max() / np.abs(w).max()) for g, w in zip(got, want))
+        res["bond_spectra_max_err_vs_ref"] = spectra_err(got, want, 8, 8)
     return res
 
 
@@ -192,8 +278,8 @@ def main():
     ap.add_argument("--zz", choices=["none", "centre"], default="centre")
     args = ap.parse_args()
     ctx = A.default_context()
-    fns = {1: cfg1, 3: cfg3, 4: cfg4, 5: cfg5}
-    for k in [int(x) for x in args.configs.split(",")]:
+    fns = {"1": cfg1, "3": cfg3, "4": cfg4, "4b": cfg4b, "5": cfg5}
+    for k in args.configs.split(","):
         t0 = time.perf_counter()
         res = fns[k](args, ctx)
         res["wall_s"] = time.perf_counter() - t0
