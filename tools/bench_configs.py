@@ -171,6 +171,11 @@ def cfg4(args, ctx):
         shapes_equal = [g.shape for g in got] == [w.shape for w in want]
         worst = max(float(np.abs(g - w).max() / max(np.abs(w).max(), 1e-300)) for g, w in zip(got, want)) \
             if shapes_equal else None
+        rs = np.random.default_rng(45)
+        pert = [x * (1.0 + 1e-14 * rs.standard_normal()) for x in plus]
+        want2, _ = ref.ite_tfim(pert, 8, 8, 1.0, 3.0, 0.01, steps, 8)
+        if [w.shape for w in want2] == [w.shape for w in want]:
+            res["ref_vs_ref_perturbed_1e-14_bond_spectra_err"] = spectra_err(want2, want, 8, 8)
         res.update({"ref_s_total": rdt, "ref_s_per_step": rdt / steps, "cpu_cores": os.cpu_count(),
                     "shapes_bit_exact": shapes_equal, "max_site_rel_err_vs_ref": worst,
                     "bond_spectra_max_err_vs_ref": spectra_err(got, want, 8, 8) if shapes_equal else None})
@@ -227,6 +232,13 @@ def cfg4b(args, ctx):
     if shapes_equal:
         res["max_site_rel_err_vs_ref"] = max(float(np.abs(g - w).max() / np.abs(w).max()) for g, w in zip(got, want))
         res["bond_spectra_max_err_vs_ref"] = spectra_err(got, want, 8, 8)
+    # intrinsic sensitivity: the reference against itself with the initial state
+    # perturbed at 1e-14 relative (the spread any two correct implementations
+    # with different rounding can show after 100 steps)
+    pert = [x * (1.0 + 1e-14 * rs.standard_normal()) for x in init]
+    want2, _ = ref.ite_tfim(pert, 8, 8, 1.0, 3.0, 0.01, steps, 8)
+    if [w.shape for w in want2] == [w.shape for w in want]:
+        res["ref_vs_ref_perturbed_1e-14_bond_spectra_err"] = spectra_err(want2, want, 8, 8)
     return res
 
 
