@@ -308,6 +308,8 @@ def run_b200(args, rank, world, local_rank):
             "e2e": {"value": world * flops / dt_e2e / 1e12, "unit": UNIT, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "s_per_step": dt_e2e},
             "roofline": roof}
+    if world == 1 and not args.no_norms:
+        line["s_per_norm"] = norm_timings(A, ctx)
     if world == 1 and not args.no_cpu_baseline:
         try:
             cores = os.cpu_count() or 1
@@ -320,6 +322,44 @@ def run_b200(args, rank, world, local_rank):
                                     "sample": f"unavailable: {e}"}
     print(json.dumps(line), flush=True)
     return 0
+
+
+def norm_timings(A, ctx):
+    """The metric's other half: seconds per <psi|psi> by two-layer boundary
+    contraction (contract_two_layer) on BASELINE configs 1, 3 and 5, and
+    seconds per ITE step of config 4, through the public API (wall clock around
+    synchronised calls; inputs resident).  Reference CPU figures for 3 and 5 are
+    SURVEY §6's (1511 s for config 3's cache + bands on 8 cores; ~16 h per
+    config-5 sweep); config 1's and 4's are timed by tools/bench_configs.py."""
+    out = {}
+    c1 = inputs.config1()
+    st = A.PepsState(4, 4, 2, c1["sites"], ctx=ctx)
+    o1 = A.ContractOption.two_layer_opt(4, c1["seed"], 1, 4)
+    A.contract_two_layer(st, st, o1)
+    t0 = time.perf_counter()
+    for _ in range(10):
+        A.contract_two_layer(st, st, o1)
+    out["config1_4x4_r2_m4"] = (time.perf_counter() - t0) / 10
+    for name, cfg, r, m, q, os_ in (("config3_16x16_r6_m36", inputs.config3(), 6, 36, 2, -1),
+                                    ("config5_32x32_r8_m64", inputs.config5(), 8, 64, 2, 8)):
+        n = cfg["rows"]
+        st = A.PepsState(n, n, 2, cfg["sites"], ctx=ctx)
+        opt = A.ContractOption.two_layer_opt(m, cfg["seed"], q, os_)
+        ctx.sync()
+        t0 = time.perf_counter()
+        A.contract_two_layer(st, st, opt)
+        out[name] = time.perf_counter() - t0
+        del st
+    plus = [np.array([1, 1], dtype=complex).reshape(2, 1, 1, 1, 1) / np.sqrt(2) for _ in range(64)]
+    st = A.PepsState(8, 8, 2, plus, ctx=ctx)
+    A.ite_tfim(st, 1.0, 3.0, 0.01, 2, 8)
+    ctx.sync()
+    t0 = time.perf_counter()
+    A.ite_tfim(st, 1.0, 3.0, 0.01, 20, 8)
+    ctx.sync()
+    out["config4_ite_8x8_r8_s_per_step"] = (time.perf_counter() - t0) / 20
+    out["note"] = "seconds per norm (config 4: per Trotter step); wall clock, synchronised, one B200"
+    return out
 
 
 def _from_pinned(ctx, pinned, shape):
@@ -439,6 +479,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-norms", action="store_true", help="skip the per-config s/norm timings (configs 1, 3, 5, 4)")
     ap.add_argument("--sharded", action="store_true",
                     help="N>1: split one row absorb across the ranks along the boundary bond (strong scaling) "
                          "instead of N independent replicas")

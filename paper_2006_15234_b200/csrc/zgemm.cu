@@ -550,14 +550,20 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32, MINB)
         bi[b] = flip(fb[buf][b].y, sgb);
         bs[b] = br[b] + bi[b];
       }
+      // pass-major: the P3 DMMAs, which wait on the DADD sums, come after
+      // 2 FM FN DMMAs that hide the DADD latency
 #pragma unroll
       for (int a = 0; a < FM; ++a)
 #pragma unroll
-        for (int b = 0; b < FN; ++b) {
-          dmma884(acc[a][b][0][0], acc[a][b][0][1], ar[a], br[b]);
-          dmma884(acc[a][b][1][0], acc[a][b][1][1], ai[a], bi[b]);
-          dmma884(acc[a][b][2][0], acc[a][b][2][1], as[a], bs[b]);
-        }
+        for (int b = 0; b < FN; ++b) dmma884(acc[a][b][0][0], acc[a][b][0][1], ar[a], br[b]);
+#pragma unroll
+      for (int a = 0; a < FM; ++a)
+#pragma unroll
+        for (int b = 0; b < FN; ++b) dmma884(acc[a][b][1][0], acc[a][b][1][1], ai[a], bi[b]);
+#pragma unroll
+      for (int a = 0; a < FM; ++a)
+#pragma unroll
+        for (int b = 0; b < FN; ++b) dmma884(acc[a][b][2][0], acc[a][b][2][1], as[a], bs[b]);
     } else {
       // Re += Ar Br - Ai Bi,  Im += Ar Bi + Ai Br
       double ai[FM], nai[FM], bi[FN];
@@ -709,17 +715,20 @@ void zgemm_set_algo(int a) {
   g_algo.store(a);
 }
 
-bool zgemm_ws_enabled() {
+int zgemm_ws_mode() {
   int v = g_ws.load();
   if (v < 0) {
     const char* e = getenv("PEPSB_GEMM_WS");
-    v = (e && std::string(e) == "1") ? 1 : 0;
+    v = e ? std::atoi(e) : 0;
+    if (v < 0 || v > 2) v = 0;
     g_ws.store(v);
   }
-  return v != 0;
+  return v;
 }
 
-void zgemm_set_ws(int on) { g_ws.store(on ? 1 : 0); }
+bool zgemm_ws_enabled() { return zgemm_ws_mode() != 0; }
+
+void zgemm_set_ws(int mode) { g_ws.store(mode >= 0 && mode <= 2 ? mode : 0); }
 
 int64_t zgemm_plan_splits(ZgemmParams& p, int num_sms) {
   if (p.M > 64 && p.M <= 72 && p.N > 72) transpose_problem(p);
@@ -737,7 +746,7 @@ int64_t zgemm_plan_splits(ZgemmParams& p, int num_sms) {
   const int64_t tiles = ((p.M + bm - 1) / bm) * ((p.N + bn - 1) / bn) * p.batch;
   // one full wave of resident CTAs (no partial second wave)
   const int64_t target =
-      p.ws ? num_sms
+      p.ws ? (zgemm_ws_mode() == 2 ? 2 * num_sms : num_sms)
            : static_cast<int64_t>(p.algo == kGemm4M ? ctas_per_sm(p.cfg) : ctas_per_sm3m(p.cfg)) * num_sms;
   int64_t splits = 1;
   if (tiles < target && p.K > 4 * kBK) {

@@ -61,8 +61,11 @@ void zgemm_set_algo(int a);
 // Persistent kernel with TMA tensor-map operand staging (zgemm_ws.cu): opt-in
 // (PEPSB_GEMM_WS=1 or option "gemm_ws" = 1); measured at config 2 it does not
 // beat the classic cp.async kernels, so they stay the default.
+// mode 0: classic cp.async kernels; 1: persistent TMA kernel; 2: one tile per
+// CTA with TMA staging (2 CTAs / SM).
+int zgemm_ws_mode();
 bool zgemm_ws_enabled();
-void zgemm_set_ws(int on);
+void zgemm_set_ws(int mode);
 bool zgemm_ws_eligible(const ZgemmParams& p);
 void zgemm_ws_tile(const ZgemmParams& p, int64_t& bm, int64_t& bn);
 void zgemm_ws_launch(const ZgemmParams& p, int num_sms, cudaStream_t stream);

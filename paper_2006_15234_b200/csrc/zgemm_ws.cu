@@ -344,11 +344,15 @@ __global__ void __launch_bounds__(kThreadsW, 1)
 #pragma unroll
       for (int a = 0; a < FM; ++a)
 #pragma unroll
-        for (int b = 0; b < FN; ++b) {
-          dmma(acc[a][b][0][0], acc[a][b][0][1], ar[a], br[b]);
-          dmma(acc[a][b][1][0], acc[a][b][1][1], ai[a], bi[b]);
-          dmma(acc[a][b][2][0], acc[a][b][2][1], as[a], bs[b]);
-        }
+        for (int b = 0; b < FN; ++b) dmma(acc[a][b][0][0], acc[a][b][0][1], ar[a], br[b]);
+#pragma unroll
+      for (int a = 0; a < FM; ++a)
+#pragma unroll
+        for (int b = 0; b < FN; ++b) dmma(acc[a][b][1][0], acc[a][b][1][1], ai[a], bi[b]);
+#pragma unroll
+      for (int a = 0; a < FM; ++a)
+#pragma unroll
+        for (int b = 0; b < FN; ++b) dmma(acc[a][b][2][0], acc[a][b][2][1], as[a], bs[b]);
     } else {
       double ai[FM], nai[FM], bi[FN];
 #pragma unroll
@@ -455,6 +459,231 @@ __global__ void __launch_bounds__(kThreadsW, 1)
   }
 }
 
+// Non-persistent TMA variant with the classic kernels' structure: one output
+// tile per CTA, 4 warps, 2 CTAs per SM (so one CTA's prologue / epilogue
+// overlaps the other's main loop), thread 0 issuing the tensor-map loads of
+// stage kt + STAGES - 1 right after the per-k-tile barrier that frees its
+// slot; consumers wait on the stage's full mbarrier.  No global address
+// arithmetic in the loop, K tails and ragged edges zero-filled by the TMA unit.
+template <int BM, int BN, int WM, int WN, int STAGES, bool AK, bool BNC, int ALG>
+__global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32, 2)
+    zgemm_tma_kernel(const __grid_constant__ WsArgs args, const __grid_constant__ CUtensorMap tmA,
+                     const __grid_constant__ CUtensorMap tmB) {
+  constexpr int NT = (BM / WM) * (BN / WN) * 32;
+  constexpr int FM = WM / 8, FN = WN / 8;
+  constexpr int NACC = ALG == 3 ? 3 : 2;
+  constexpr int KS = kBKw / 4;
+  constexpr int A_ELEMS = BM * kBKw, STAGE = A_ELEMS + kBKw * BN;  // double2
+  constexpr uint32_t STAGE_BYTES = STAGE * 16;
+  const ZgemmParams& p = args.p;
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  double2* ring = reinterpret_cast<double2*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(ring + STAGES * STAGE);
+  int64_t* rowoff = reinterpret_cast<int64_t*>(full + STAGES);
+  int64_t* coloff = rowoff + BM;
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t mtiles = (p.M + BM - 1) / BM;
+  const int64_t tile = blockIdx.x;
+  const int64_t m0 = (tile % mtiles) * BM, n0 = (tile / mtiles) * BN;
+  const int bz = static_cast<int>(blockIdx.y / p.splits), split = static_cast<int>(blockIdx.y % p.splits);
+  const int64_t kbeg = static_cast<int64_t>(split) * p.kchunk;
+  const int64_t kend = min(p.K, kbeg + p.kchunk);
+  const int nk = static_cast<int>((kend - kbeg + kBKw - 1) / kBKw);
+
+  int ca[5] = {0, 0, 0, 0, 0}, cb[5] = {0, 0, 0, 0, 0};
+  int64_t offC = 0;
+  {
+    int64_t idx = bz;
+    int bidx[4] = {0, 0, 0, 0};
+#pragma unroll
+    for (int a = 3; a >= 0; --a) {
+      if (a >= p.nb) continue;
+      const int64_t q = idx / p.bext[a];
+      bidx[a] = static_cast<int>(idx - q * p.bext[a]);
+      offC += bidx[a] * p.bsC[a];
+      idx = q;
+    }
+    auto sel = [&](int m) { return m == 0 ? bidx[0] : m == 1 ? bidx[1] : m == 2 ? bidx[2] : bidx[3]; };
+#pragma unroll
+    for (int u = 0; u < 3; ++u) {
+      if (u < args.oa.nbm) ca[2 + u] = sel(args.oa.bmode[u]);
+      if (u < args.ob.nbm) cb[2 + u] = sel(args.ob.bmode[u]);
+    }
+  }
+  auto issue = [&](int kt) {
+    const int slot = kt % STAGES;
+    double2* As = ring + slot * STAGE;
+    double2* Bs = As + A_ELEMS;
+    uint64_t* bar = &full[slot];
+    const int k0 = static_cast<int>(kbeg) + kt * kBKw;
+    mbar_arrive_tx(bar, STAGE_BYTES);
+    if (AK) {
+#pragma unroll
+      for (int j = 0; j < kBKw / 4; ++j) {
+        ca[0] = 2 * (k0 + 4 * j);
+        ca[1] = static_cast<int>(m0);
+        tma_load(As + j * BM * 4, &tmA, args.oa.rank, ca, bar);
+      }
+    } else {
+#pragma unroll
+      for (int c = 0; c < BM / 8; ++c) {
+        ca[0] = static_cast<int>(2 * (m0 + 8 * c));
+        ca[1] = k0;
+        tma_load(As + c * kBKw * 8, &tmA, args.oa.rank, ca, bar);
+      }
+    }
+    if (BNC) {
+#pragma unroll
+      for (int c = 0; c < BN / 8; ++c) {
+        cb[0] = static_cast<int>(2 * (n0 + 8 * c));
+        cb[1] = k0;
+        tma_load(Bs + c * kBKw * 8, &tmB, args.ob.rank, cb, bar);
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < kBKw / 4; ++j) {
+        cb[0] = 2 * (k0 + 4 * j);
+        cb[1] = static_cast<int>(n0);
+        tma_load(Bs + j * BN * 4, &tmB, args.ob.rank, cb, bar);
+      }
+    }
+  };
+  if (tid == 0) {
+    for (int s = 0; s < STAGES; ++s) mbar_init(&full[s], 1);
+    fence_mbar_init();
+    for (int kt = 0; kt < STAGES - 1 && kt < nk; ++kt) issue(kt);
+  }
+  if (p.splits == 1) {
+    for (int r = tid; r < BM; r += NT) rowoff[r] = m0 + r < p.M ? decode_off(m0 + r, p.nr, p.rext, p.rstr) : 0;
+    for (int c = tid; c < BN; c += NT) coloff[c] = n0 + c < p.N ? decode_off(n0 + c, p.nc, p.cext, p.cstr) : 0;
+  }
+  __syncthreads();
+
+  const int wm0 = (warp % (BM / WM)) * WM, wn0 = (warp / (BM / WM)) * WN;
+  const int kq = lane & 3, rq = lane >> 2;
+  const long long sga = p.conjA ? (long long)0x8000000000000000ULL : 0LL;
+  const long long sgb = p.conjB ? (long long)0x8000000000000000ULL : 0LL;
+  auto flip = [](double v, long long m) { return __longlong_as_double(__double_as_longlong(v) ^ m); };
+  const int abase = AK ? (wm0 + rq) * 4 + kq : (wm0 / 8) * kBKw * 8;
+  const int bbase = BNC ? A_ELEMS + (wn0 / 8) * kBKw * 8 : A_ELEMS + (wn0 + rq) * 4 + kq;
+  constexpr int ASTEP = AK ? 32 : kBKw * 8, BSTEP = BNC ? kBKw * 8 : 32;
+  const int pr = pi8(rq);
+  double acc[FM][FN][NACC][2];
+#pragma unroll
+  for (int a = 0; a < FM; ++a)
+#pragma unroll
+    for (int b = 0; b < FN; ++b)
+#pragma unroll
+      for (int q = 0; q < NACC; ++q) acc[a][b][q][0] = acc[a][b][q][1] = 0.0;
+  double2 fa[2][FM], fb[2][FN];
+  auto load_frags = [&](int buf, const double2* St, int ks) {
+    const int k = ks * 4 + kq;
+    const int sw = (pr ^ (k & 7));
+#pragma unroll
+    for (int a = 0; a < FM; ++a)
+      fa[buf][a] = AK ? St[abase + a * ASTEP + ks * BM * 4] : St[abase + a * ASTEP + k * 8 + sw];
+#pragma unroll
+    for (int b = 0; b < FN; ++b)
+      fb[buf][b] = BNC ? St[bbase + b * BSTEP + k * 8 + sw] : St[bbase + b * BSTEP + ks * BN * 4];
+  };
+  auto compute = [&](int buf) {
+    if constexpr (ALG == 3) {
+      double ar[FM], ai[FM], as[FM], br[FN], bi[FN], bs[FN];
+#pragma unroll
+      for (int a = 0; a < FM; ++a) {
+        ar[a] = fa[buf][a].x;
+        ai[a] = flip(fa[buf][a].y, sga);
+        as[a] = ar[a] + ai[a];
+      }
+#pragma unroll
+      for (int b = 0; b < FN; ++b) {
+        br[b] = fb[buf][b].x;
+        bi[b] = flip(fb[buf][b].y, sgb);
+        bs[b] = br[b] + bi[b];
+      }
+#pragma unroll
+      for (int a = 0; a < FM; ++a)
+#pragma unroll
+        for (int b = 0; b < FN; ++b) dmma(acc[a][b][0][0], acc[a][b][0][1], ar[a], br[b]);
+#pragma unroll
+      for (int a = 0; a < FM; ++a)
+#pragma unroll
+        for (int b = 0; b < FN; ++b) dmma(acc[a][b][1][0], acc[a][b][1][1], ai[a], bi[b]);
+#pragma unroll
+      for (int a = 0; a < FM; ++a)
+#pragma unroll
+        for (int b = 0; b < FN; ++b) dmma(acc[a][b][NACC - 1][0], acc[a][b][NACC - 1][1], as[a], bs[b]);
+    } else {
+      double ai[FM], nai[FM], bi[FN];
+#pragma unroll
+      for (int a = 0; a < FM; ++a) {
+        ai[a] = flip(fa[buf][a].y, sga);
+        nai[a] = flip(fa[buf][a].y, sga ^ (long long)0x8000000000000000ULL);
+      }
+#pragma unroll
+      for (int b = 0; b < FN; ++b) bi[b] = flip(fb[buf][b].y, sgb);
+#pragma unroll
+      for (int a = 0; a < FM; ++a)
+#pragma unroll
+        for (int b = 0; b < FN; ++b) {
+          dmma(acc[a][b][0][0], acc[a][b][0][1], fa[buf][a].x, fb[buf][b].x);
+          dmma(acc[a][b][1][0], acc[a][b][1][1], fa[buf][a].x, bi[b]);
+        }
+#pragma unroll
+      for (int a = 0; a < FM; ++a)
+#pragma unroll
+        for (int b = 0; b < FN; ++b) {
+          dmma(acc[a][b][0][0], acc[a][b][0][1], nai[a], bi[b]);
+          dmma(acc[a][b][1][0], acc[a][b][1][1], ai[a], fb[buf][b].x);
+        }
+    }
+  };
+
+  for (int kt = 0; kt < nk; ++kt) {
+    if (kt > 0) __syncthreads();  // every warp is done with slot (kt - 1) % STAGES
+    if (tid == 0 && kt + STAGES - 1 < nk) issue(kt + STAGES - 1);
+    mbar_wait(&full[kt % STAGES], static_cast<uint32_t>((kt / STAGES) & 1));
+    const double2* St = ring + (kt % STAGES) * STAGE;
+    load_frags(0, St, 0);
+#pragma unroll
+    for (int ks = 0; ks < KS; ks += 2) {
+      load_frags(1, St, ks + 1);
+      compute(0);
+      if (ks + 2 < KS) load_frags(0, St, ks + 2);
+      compute(1);
+    }
+  }
+
+#pragma unroll
+  for (int a = 0; a < FM; ++a) {
+    const int li = wm0 + a * 8 + (AK ? rq : pr);
+    if (m0 + li >= p.M) continue;
+#pragma unroll
+    for (int b = 0; b < FN; ++b)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int lj = wn0 + b * 8 + (BNC ? pi8(2 * kq + h) : 2 * kq + h);
+        if (n0 + lj >= p.N) continue;
+        double2 v;
+        if constexpr (ALG == 3) {
+          const double p1 = acc[a][b][0][h], p2 = acc[a][b][1][h], p3 = acc[a][b][NACC - 1][h];
+          v = make_double2(p1 - p2, p3 - p1 - p2);
+        } else {
+          v = make_double2(acc[a][b][0][h], acc[a][b][1][h]);
+        }
+        if (p.splits == 1) {
+          double2* dst = p.C + offC + rowoff[li] + coloff[lj];
+          if (p.accumulate) v = cadd(*dst, v);
+          *dst = v;
+        } else {
+          double2* W = p.work + ((static_cast<int64_t>(split) * p.batch + bz) * p.M) * p.N;
+          W[(m0 + li) * p.N + n0 + lj] = v;
+        }
+      }
+  }
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
     void* f = nullptr;
@@ -544,6 +773,35 @@ void launch_ws_any(const ZgemmParams& p, int num_sms, cudaStream_t stream) {
   }
 }
 
+template <int BM, int BN, int WM, int WN, int STAGES, bool AK, bool BNC, int ALG>
+void launch_tma(const ZgemmParams& p, cudaStream_t stream) {
+  constexpr int STAGE = (BM + BN) * kBKw;
+  constexpr int NT = (BM / WM) * (BN / WN) * 32;
+  const size_t smem = 1024 + static_cast<size_t>(STAGES) * STAGE * 16 + STAGES * 8 + (BM + BN) * 8;
+  auto kern = zgemm_tma_kernel<BM, BN, WM, WN, STAGES, AK, BNC, ALG>;
+  static bool attr_set = false;  // per instantiation
+  if (!attr_set) {
+    PEPSB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    attr_set = true;
+  }
+  WsArgs args;
+  args.p = p;
+  CUtensorMap ta, tb;
+  make_map(&ta, args.oa, p.A, p.M, p.K, p.sAi, p.sAk, AK, BM, p, p.bsA);
+  make_map(&tb, args.ob, p.B, p.N, p.K, p.sBj, p.sBk, !BNC, BN, p, p.bsB);
+  const int64_t tiles = ((p.M + BM - 1) / BM) * ((p.N + BN - 1) / BN);
+  args.nwork = tiles * p.batch * p.splits;
+  dim3 grid(static_cast<unsigned>(tiles), static_cast<unsigned>(p.batch * p.splits));
+  kern<<<grid, NT, smem, stream>>>(args, ta, tb);
+  PEPSB_LAUNCH();
+}
+
+template <bool AK, bool BNC>
+void launch_tma_any(const ZgemmParams& p, cudaStream_t stream) {
+  if (p.algo == kGemm3M) launch_tma<64, 32, 32, 16, 4, AK, BNC, 3>(p, stream);
+  else launch_tma<64, 64, 32, 32, 3, AK, BNC, 4>(p, stream);
+}
+
 }  // namespace
 
 bool zgemm_ws_eligible(const ZgemmParams& p) {
@@ -561,12 +819,24 @@ bool zgemm_ws_eligible(const ZgemmParams& p) {
 
 void zgemm_ws_tile(const ZgemmParams& p, int64_t& bm, int64_t& bn) {
   const bool wide = p.M <= 64;
+  if (zgemm_ws_mode() == 2) {  // non-persistent TMA kernel
+    bm = 64;
+    bn = p.algo == kGemm3M ? 32 : 64;
+    return;
+  }
   bm = wide ? 64 : 128;
   bn = p.algo == kGemm3M ? (wide ? 64 : 32) : (wide ? 128 : 64);
 }
 
 void zgemm_ws_launch(const ZgemmParams& p, int num_sms, cudaStream_t stream) {
   const bool ak = p.sAk == 1, bnc = p.sBj == 1;
+  if (zgemm_ws_mode() == 2) {
+    if (ak && bnc) launch_tma_any<true, true>(p, stream);
+    else if (ak) launch_tma_any<true, false>(p, stream);
+    else if (bnc) launch_tma_any<false, true>(p, stream);
+    else launch_tma_any<false, false>(p, stream);
+    return;
+  }
   if (ak && bnc) launch_ws_any<true, true>(p, num_sms, stream);
   else if (ak) launch_ws_any<true, false>(p, num_sms, stream);
   else if (bnc) launch_ws_any<false, true>(p, num_sms, stream);

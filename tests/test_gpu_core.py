@@ -263,8 +263,8 @@ def test_errors_mirror_reference(A):
                          A.TruncationPolicy(0, 1e-14))
 
 
-@pytest.mark.parametrize("algo,ws", [(0, 0), (1, 0), (2, 0), (1, 1), (2, 1)],
-                         ids=["4m_embed", "3m", "4m_cfrag", "3m_ws", "4m_cfrag_ws"])
+@pytest.mark.parametrize("algo,ws", [(0, 0), (1, 0), (2, 0), (1, 1), (2, 1), (1, 2), (2, 2)],
+                         ids=["4m_embed", "3m", "4m_cfrag", "3m_ws", "4m_cfrag_ws", "3m_tma", "4m_cfrag_tma"])
 def test_gemm_kernels_all_layouts(A, algo, ws):
     """Every complex GEMM kernel (real embedding, 3M/Gauss, 4M complex
     fragments; classic and persistent warp-specialised bulk-copy variants) on
@@ -294,14 +294,14 @@ def test_gemm_kernels_all_layouts(A, algo, ws):
         ctx.set_option("gemm_ws", 0)
 
 
-@pytest.mark.parametrize("algo", [1, 2], ids=["3m", "4m_cfrag"])
-def test_gemm_ws_persistent_tiles_and_batches(A, algo):
+@pytest.mark.parametrize("algo,ws", [(1, 1), (2, 1), (1, 2), (2, 2)], ids=["3m_ws", "4m_ws", "3m_tma", "4m_tma"])
+def test_gemm_ws_persistent_tiles_and_batches(A, algo, ws):
     """Persistent warp-specialised GEMM: several tiles per CTA (the producer
     runs ahead across tile boundaries and reuses the offset tables), K tails,
     batched contractions and scattered (permuted) outputs, against numpy."""
     ctx = A.default_context()
     ctx.set_option("gemm_algo", algo)
-    ctx.set_option("gemm_ws", 1)
+    ctx.set_option("gemm_ws", ws)
     try:
         for (m, n, k) in [(128, 9000, 64), (64, 20000, 40), (200, 3000, 37), (96, 4100, 128)]:
             a = O.random_tensor((m, k), m + 3 * k)
