@@ -87,7 +87,9 @@ int pepsb_ctx_set_option(pepsb_ctx* ctx, const char* key, int64_t value);
 int pepsb_ctx_counters(pepsb_ctx* ctx, uint64_t* out6);
 int pepsb_ctx_reset_counters(pepsb_ctx* ctx);
 /* Named counter: "flops", "einsumsvd_flops", "peak_elements", "launches",
- * "faithful_redos", "tsqr_fallbacks", "degenerate_truncations" (simple-update
+ * "faithful_redos", "tsqr_fallbacks", "lookahead_misses" (row-absorb
+ * lookaheads discarded because the next column's rank guess failed),
+ * "degenerate_truncations" (simple-update
  * truncations whose cut falls inside a singular pair equal to 1e-10 relative:
  * the kept subspace there is rounding-dependent). */
 int pepsb_ctx_get_counter(pepsb_ctx* ctx, const char* name, uint64_t* value);

@@ -218,6 +218,7 @@ int pepsb_ctx_get_counter(pepsb_ctx* c, const char* name, uint64_t* value) {
     else if (k == "launches") *value = static_cast<uint64_t>(x.launches);
     else if (k == "faithful_redos") *value = static_cast<uint64_t>(x.faithful_redos);
     else if (k == "tsqr_fallbacks") *value = static_cast<uint64_t>(x.tsqr_fallbacks);
+    else if (k == "lookahead_misses") *value = static_cast<uint64_t>(x.lookahead_misses);
     else if (k == "degenerate_truncations") {
       unsigned long long v = 0;
       PEPSB_CUDA(cudaMemcpyAsync(&v, x.d_degenerate, sizeof(v), cudaMemcpyDeviceToHost, x.stream));

@@ -125,6 +125,9 @@ Ctx::Ctx(int dev) : device(dev) {
 
 Ctx::~Ctx() {
   if (stream != main_stream) join();
+  join_pending();
+  prefetched.reset();
+  lookahead.reset();
   if (side_stream) cudaStreamSynchronize(side_stream);
   if (stream) cudaStreamSynchronize(stream);
   pool->trim();
@@ -141,6 +144,7 @@ Ctx::~Ctx() {
 }
 
 void Ctx::fork() {
+  join_pending();
   if (pool->defer) throw Error(kOtherError, "nested stream fork");
   PEPSB_CUDA(cudaEventRecord(fork_event, main_stream));
   pool->defer = true;
@@ -149,6 +153,24 @@ void Ctx::fork() {
 void Ctx::side() {
   PEPSB_CUDA(cudaStreamWaitEvent(side_stream, fork_event, 0));
   stream = side_stream;
+}
+
+void Ctx::back() {
+  PEPSB_CUDA(cudaEventRecord(join_event, side_stream));
+  stream = main_stream;
+  side_pending = true;
+}
+
+void Ctx::join_pending() {
+  if (!side_pending) return;
+  side_pending = false;
+  PEPSB_CUDA(cudaStreamWaitEvent(main_stream, join_event, 0));
+  pool->defer = false;
+  for (auto& [sz, p] : pool->parked) {
+    pool->free_blocks.emplace(sz, p);
+    pool->cached_bytes += sz;
+  }
+  pool->parked.clear();
 }
 
 void Ctx::join() {
@@ -191,7 +213,13 @@ DTensor Ctx::zeros(const std::vector<int64_t>& shape) {
 
 void Ctx::sync() {
   HostTimer ht(trace ? &t_sync : nullptr);
+  if (side_pending) PEPSB_CUDA(cudaStreamSynchronize(side_stream));
   PEPSB_CUDA(cudaStreamSynchronize(stream));
+}
+
+void Ctx::sync_main() {
+  HostTimer ht(trace ? &t_sync : nullptr);
+  PEPSB_CUDA(cudaStreamSynchronize(main_stream));
 }
 
 cudaEvent_t Ctx::take_event() {

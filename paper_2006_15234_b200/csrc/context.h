@@ -97,7 +97,8 @@ class Ctx {
   std::shared_ptr<struct Pool> pool;
   DTensor empty(const std::vector<int64_t>& shape);
   DTensor zeros(const std::vector<int64_t>& shape);
-  void sync();
+  void sync();       // every stream of the context
+  void sync_main();  // the main stream only (pending side-stream work keeps running)
 
   // Two-stream phase: fork() marks the fork point on the main stream (blocks
   // released from here on are parked); work enqueued next stays on the main
@@ -108,6 +109,14 @@ class Ctx {
   void fork();
   void side();
   void join();
+  // Leave the side stream without joining (work on it keeps running); a later
+  // join_pending() makes the main stream wait for it and unparks the blocks.
+  void back();
+  void join_pending();
+  bool side_pending = false;
+  // Row lookahead (decomp.cpp): the next column's operator to start on the
+  // side stream during this column's tail, and what was started for this one.
+  std::shared_ptr<void> lookahead, prefetched;
 
   int device = 0;
   int num_sms = 148;
@@ -127,6 +136,7 @@ class Ctx {
   double t_alloc = 0.0, t_free = 0.0, t_sync = 0.0;
   int64_t faithful_redos = 0;  // CholeskyQR breakdowns redone on the Gram-eigh route
   int64_t tsqr_fallbacks = 0;  // projected SVDs that needed the TSQR R factor
+  int64_t lookahead_misses = 0;  // row lookaheads discarded (the rank guess was wrong)
   // Cost counters (reference instr::flops definition: 2 per complex MAC,
   // proj/include/peps/instrument.hpp:19-65).
   uint64_t flops = 0;

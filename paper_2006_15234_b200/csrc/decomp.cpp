@@ -290,7 +290,7 @@ Projected projected_svd(Ctx& ctx, const LTensor& Z, int64_t target) {
     out.s.resize(k);
     PEPSB_CUDA(cudaMemcpyAsync(out.s.data(), d_s, k * sizeof(double), cudaMemcpyDeviceToHost, ctx.stream));
     read_status(ctx);
-    ctx.sync();
+    ctx.sync_main();
     return *ctx.h_status;
   };
   auto gram = [&](const double2* X) {
@@ -320,7 +320,7 @@ Projected projected_svd(Ctx& ctx, const LTensor& Z, int64_t target) {
     std::vector<double> lam(k);
     PEPSB_CUDA(cudaMemcpyAsync(lam.data(), d_s, k * sizeof(double), cudaMemcpyDeviceToHost, ctx.stream));
     read_status(ctx);
-    ctx.sync();
+    ctx.sync_main();
     const int st = *ctx.h_status & ~kSmallZeroGram;  // a zero Z is judged below
     raise_status(st, false);
     out.s.resize(k);
@@ -381,6 +381,104 @@ void absorb_weights(const std::vector<double>& s, int absorb, std::vector<double
   }
 }
 
+struct RsvdPlans {
+  std::shared_ptr<ContractionPlan> ap, adj;
+};
+
+// The apply / adjoint plans of an implicit operator with `probe` probe
+// columns under label X; each writes its output in the layout the other
+// consumes (decomposition.cpp:259-306 lowered).
+RsvdPlans build_plans(const ImplicitOp& op, int64_t probe, char X) {
+  const size_t nt = op.tensors.size();
+  std::vector<LeafMeta> meta_ap, meta_adj;
+  for (size_t i = 0; i < nt; ++i) {
+    meta_ap.push_back({op.labels[i], op.tensors[i].shape});
+    meta_adj.push_back({op.labels[i], op.tensors[i].shape});
+  }
+  std::vector<int64_t> qshape = op.col_shape(), pshape = op.row_shape();
+  qshape.push_back(probe);
+  pshape.push_back(probe);
+  meta_ap.push_back({op.cols + X, qshape});
+  meta_adj.push_back({op.rows + X, pshape});
+  RsvdPlans pl;
+  pl.ap = std::make_shared<ContractionPlan>(meta_ap, op.rows + X, static_cast<int>(nt), X);
+  pl.adj = std::make_shared<ContractionPlan>(meta_adj, op.cols + X, static_cast<int>(nt), X);
+  pl.ap->finalize(pl.adj->flexible_order());
+  pl.adj->finalize(pl.ap->flexible_order());
+  pl.ap->cache_static = pl.adj->cache_static = true;
+  return pl;
+}
+
+// Omega = random_tensor(col_shape + [probe], seed) (decomposition.cpp:267-270)
+// generated directly in the probe layout the apply plan wants.
+LTensor make_sketch(Ctx& ctx, const ImplicitOp& op, const ContractionPlan& plan_ap, int64_t probe, char X,
+                    uint64_t seed) {
+  std::vector<int64_t> qshape = op.col_shape();
+  qshape.push_back(probe);
+  const std::string qord = plan_ap.flexible_order();
+  std::vector<int64_t> pext, lstr;
+  const std::string logical = op.cols + X;
+  const std::vector<int64_t> lst = row_major_strides(qshape);
+  for (char c : qord) {
+    auto pos = logical.find(c);
+    pext.push_back(qshape[pos]);
+    lstr.push_back(lst[pos]);
+  }
+  BufPtr om = ctx.alloc(prod(qshape));
+  random_fill(om->p, static_cast<int>(qord.size()), pext.data(), lstr.data(), seed, 0, ctx.stream);
+  ++ctx.launches;
+  return wrap(om, qord, pext);
+}
+
+int64_t probe_count(const ImplicitOp& op, const Trunc& policy, const Rsvd& cfg) {
+  const int64_t mindim = std::min(op.row_extent(), op.col_extent());
+  const int64_t target = static_cast<int64_t>(std::min<uint64_t>(policy.max_rank, static_cast<uint64_t>(mindim)));
+  return std::min<int64_t>(target + static_cast<int64_t>(effective_oversample(cfg, target)), mindim);
+}
+
+// Work started for a column on the side stream by the previous column.
+struct Prefetched {
+  std::vector<std::vector<int64_t>> shapes;  // leaf shapes assumed (leaf 0: the guessed pending tensor)
+  std::vector<std::string> labels;
+  std::string rows, cols;
+  uint64_t seed = 0;
+  int64_t probe = 0;
+  RsvdPlans plans;
+  LTensor omega, prefix;
+  bool matches(const ImplicitOp& op, uint64_t sd, int64_t pr) const {
+    if (sd != seed || pr != probe || op.rows != rows || op.cols != cols || op.labels != labels) return false;
+    if (op.tensors.size() != shapes.size()) return false;
+    for (size_t i = 0; i < shapes.size(); ++i)
+      if (op.tensors[i].shape != shapes[i]) return false;
+    return true;
+  }
+};
+
+void launch_lookahead(Ctx& ctx, const Lookahead& la, const Trunc& policy, const Rsvd& cfg) {
+  const ImplicitOp& op = la.op;
+  Rsvd c2 = cfg;
+  c2.seed = la.seed;
+  const int64_t probe = probe_count(op, policy, c2);
+  const char X = op.fresh_label();
+  auto pf = std::make_shared<Prefetched>();
+  for (const auto& t : op.tensors) pf->shapes.push_back(t.shape);
+  pf->labels = op.labels;
+  pf->rows = op.rows;
+  pf->cols = op.cols;
+  pf->seed = la.seed;
+  pf->probe = probe;
+  pf->plans = build_plans(op, probe, X);
+  ctx.fork();
+  ctx.side();
+  pf->omega = make_sketch(ctx, op, *pf->plans.ap, probe, X, la.seed);
+  std::vector<LTensor> leaves;
+  for (size_t i = 0; i < op.tensors.size(); ++i) leaves.push_back(as_labelled(op.tensors[i], op.labels[i], op.conj[i]));
+  leaves.push_back(pf->omega);
+  pf->prefix = pf->plans.ap->run_prefix(ctx, leaves, 0);
+  ctx.back();
+  ctx.prefetched = pf;
+}
+
 // Core of randomized_svd / einsumsvd(implicit_rsvd).  Weights (absorb) are
 // applied when `absorb` >= 0, otherwise plain U, S, V are returned.
 EinsumsvdResultD rsvd_core(Ctx& ctx, const ImplicitOp& op, const Trunc& policy, const Rsvd& cfg, int absorb,
@@ -397,22 +495,17 @@ EinsumsvdResultD rsvd_core(Ctx& ctx, const ImplicitOp& op, const Trunc& policy, 
   const char RK = extra[0];
 
   const size_t nt = op.tensors.size();
-  std::vector<LeafMeta> meta_ap, meta_adj;
-  for (size_t i = 0; i < nt; ++i) {
-    meta_ap.push_back({op.labels[i], op.tensors[i].shape});
-    meta_adj.push_back({op.labels[i], op.tensors[i].shape});
-  }
-  std::vector<int64_t> qshape = op.col_shape(), pshape = op.row_shape();
-  qshape.push_back(probe);
-  pshape.push_back(probe);
-  meta_ap.push_back({op.cols + X, qshape});
-  meta_adj.push_back({op.rows + X, pshape});
-  ContractionPlan plan_ap(meta_ap, op.rows + X, static_cast<int>(nt), X);
-  ContractionPlan plan_adj(meta_adj, op.cols + X, static_cast<int>(nt), X);
-  plan_ap.finalize(plan_adj.flexible_order());
-  plan_adj.finalize(plan_ap.flexible_order());
-  plan_ap.cache_static = plan_adj.cache_static = true;
-
+  // Plans and sketch: built here, or taken over from the previous column of a
+  // row absorb, which started them (and the v-independent prefix of the first
+  // application) on the side stream during its own tail (row lookahead).
+  std::shared_ptr<Prefetched> pre = std::static_pointer_cast<Prefetched>(ctx.prefetched);
+  ctx.prefetched.reset();
+  ctx.join_pending();
+  const bool reuse = pre && pre->matches(op, cfg.seed, probe);
+  if (pre && !reuse) ++ctx.lookahead_misses;
+  RsvdPlans plans = reuse ? pre->plans : build_plans(op, probe, X);
+  ContractionPlan& plan_ap = *plans.ap;
+  ContractionPlan& plan_adj = *plans.adj;
   std::vector<LTensor> leaves_ap, leaves_adj;
   for (size_t i = 0; i < nt; ++i) {
     leaves_ap.push_back(as_labelled(op.tensors[i], op.labels[i], op.conj[i]));
@@ -420,23 +513,9 @@ EinsumsvdResultD rsvd_core(Ctx& ctx, const ImplicitOp& op, const Trunc& policy, 
   }
   leaves_ap.push_back(LTensor());
   leaves_adj.push_back(LTensor());
-
-  // Omega = random_tensor(col_shape + [probe], seed) generated in the probe layout.
-  const std::string qord = plan_ap.flexible_order();
-  std::vector<int64_t> pext, lstr;
-  {
-    const std::string logical = op.cols + X;
-    std::vector<int64_t> lst = row_major_strides(qshape);
-    for (char c : qord) {
-      auto pos = logical.find(c);
-      pext.push_back(qshape[pos]);
-      lstr.push_back(lst[pos]);
-    }
-  }
-  BufPtr om = ctx.alloc(prod(qshape));
-  random_fill(om->p, static_cast<int>(qord.size()), pext.data(), lstr.data(), cfg.seed, 0, ctx.stream);
-  ++ctx.launches;
-  LTensor q = wrap(om, qord, pext);
+  LTensor q = reuse ? pre->omega : make_sketch(ctx, op, plan_ap, probe, X, cfg.seed);
+  LTensor prefix = reuse ? pre->prefix : LTensor();
+  pre.reset();
   clear_all_status(ctx);
 
   auto apply = [&](const LTensor& qq) {
@@ -451,7 +530,14 @@ EinsumsvdResultD rsvd_core(Ctx& ctx, const ImplicitOp& op, const Trunc& policy, 
   static const bool trace = getenv("PEPSB_TRACE") != nullptr;
   auto now = [] { return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count(); };
   const double tr0 = trace ? now() : 0.0;
-  LTensor p = orth(ctx, apply(q));
+  LTensor p;
+  if (prefix.buf) {
+    leaves_ap.back() = q;
+    p = orth(ctx, plan_ap.execute_with_prefix(ctx, leaves_ap, 0, prefix));
+    prefix = LTensor();
+  } else {
+    p = orth(ctx, apply(q));
+  }
   for (int i = 0; i < cfg.power_iters; ++i) {
     // (small problems: the host sync on the eigensolver would cost more than it hides)
     if (ctx.orth_mode == 0 && (ctx.overlap == 2 || (ctx.overlap == 1 && op.col_extent() >= (1 << 15)))) {
@@ -463,6 +549,13 @@ EinsumsvdResultD rsvd_core(Ctx& ctx, const ImplicitOp& op, const Trunc& policy, 
   }
   LTensor z = adjoint(p);
   q = LTensor();
+  // Row lookahead: start the next column's sketch and the v-independent
+  // prefix of its first application on the side stream; they run during this
+  // column's projected SVD (a one-block eigensolver plus a host sync).
+  if (std::shared_ptr<Lookahead> la = std::static_pointer_cast<Lookahead>(ctx.lookahead)) {
+    ctx.lookahead.reset();
+    if (ctx.orth_mode == 0 && ctx.overlap != 0) launch_lookahead(ctx, *la, policy, cfg);
+  }
   const double tr1 = trace ? now() : 0.0;
   if (trace) {
     ctx.sync();

@@ -5,6 +5,7 @@
 // adjoint_apply / materialize; gram_orthogonalize; randomized_svd; einsumsvd.
 #pragma once
 
+#include <memory>
 #include <string>
 #include <utility>
 #include <vector>
@@ -48,6 +49,19 @@ class ImplicitOp {
  private:
   std::vector<int64_t> row_shape_, col_shape_;
 };
+
+// Row lookahead (two_layer_apply_row): the NEXT einsumsvd's operator -- its
+// leaf 0 (the pending tensor) only a shape guess without data -- and seed.
+// The current einsumsvd starts that operator's sketch and the v-independent
+// prefix of its first application on the side stream during its own tail; the
+// next einsumsvd reuses them when its real operator has the guessed shapes.
+struct Lookahead {
+  ImplicitOp op;
+  uint64_t seed = 0;
+};
+inline void set_lookahead(Ctx& ctx, ImplicitOp next, uint64_t seed) {
+  ctx.lookahead = std::make_shared<Lookahead>(Lookahead{std::move(next), seed});
+}
 
 DTensor implicit_apply(Ctx& ctx, const ImplicitOp& op, const DTensor& q, bool adjoint);
 DTensor implicit_materialize(Ctx& ctx, const ImplicitOp& op);

@@ -529,6 +529,7 @@ LTensor ContractionPlan::prepare_leaf(Ctx& ctx, int leaf, const LTensor& t, cons
 }
 
 LTensor ContractionPlan::run(Ctx& ctx, int ni, const std::vector<LTensor>& leaves) {
+  if (ni == subst_node_) return subst_;
   const Node& nd = nodes_[ni];
   if (nd.leaf >= 0) return leaves[nd.leaf];
   LTensor ops[2];
@@ -588,6 +589,43 @@ LTensor ContractionPlan::execute(Ctx& ctx, const std::vector<LTensor>& leaves) {
     out = run(ctx, root_, leaves);
   }
   flops_ = ctx.flops - f0;
+  return out;
+}
+
+int ContractionPlan::prefix_node(int excl) const {
+  if (root_ < 0) return -1;
+  const Node& r = nodes_[root_];
+  if (r.leaf >= 0) return -1;
+  int other = -1;
+  if (nodes_[r.a_child].leaf == excl) other = r.b_child;
+  else if (nodes_[r.b_child].leaf == excl) other = r.a_child;
+  if (other < 0 || nodes_[other].leaf >= 0) return -1;  // only an internal subtree is worth running ahead
+  return other;
+}
+
+LTensor ContractionPlan::run_prefix(Ctx& ctx, const std::vector<LTensor>& leaves, int excl) {
+  if (!finalized_) throw Error(kOtherError, "internal: plan not finalized");
+  const int node = prefix_node(excl);
+  if (node < 0) return LTensor();
+  return run(ctx, node, leaves);
+}
+
+LTensor ContractionPlan::execute_with_prefix(Ctx& ctx, const std::vector<LTensor>& leaves, int excl,
+                                             const LTensor& prefix) {
+  const int node = prefix_node(excl);
+  if (node < 0 || !prefix.buf) return execute(ctx, leaves);
+  subst_node_ = node;
+  subst_ = prefix;
+  LTensor out;
+  try {
+    out = execute(ctx, leaves);
+  } catch (...) {
+    subst_node_ = -1;
+    subst_ = LTensor();
+    throw;
+  }
+  subst_node_ = -1;
+  subst_ = LTensor();
   return out;
 }
 

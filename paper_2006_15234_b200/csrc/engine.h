@@ -41,6 +41,12 @@ class ContractionPlan {
   // leaf must be in flexible_order()).  Static leaves' re-layout copies are
   // cached when `cache_static` is set.
   LTensor execute(Ctx& ctx, const std::vector<LTensor>& leaves);
+  // Speculative prefix: when the root step is (leaf `excl`) x (rest), runs the
+  // `rest` subtree (never touching leaf `excl`) and returns its result; an
+  // empty tensor (buf == nullptr) otherwise.
+  LTensor run_prefix(Ctx& ctx, const std::vector<LTensor>& leaves, int excl);
+  // execute() with the `rest` subtree's result supplied by run_prefix.
+  LTensor execute_with_prefix(Ctx& ctx, const std::vector<LTensor>& leaves, int excl, const LTensor& prefix);
 
   bool cache_static = false;
   // Reference-convention flops of one execution (instr::flops definition).
@@ -74,6 +80,9 @@ class ContractionPlan {
   // leaf -> order wanted (empty: use as given)
   std::vector<std::string> leaf_want_;
   std::map<int, LTensor> leaf_cache_;
+  int prefix_node(int excl) const;
+  int subst_node_ = -1;  // run() returns subst_ for this node (execute_with_prefix)
+  LTensor subst_;
   uint64_t flops_ = 0, cmacs_ = 0;
 };
 

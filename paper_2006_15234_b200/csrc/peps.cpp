@@ -91,6 +91,7 @@ BoundaryD two_layer_apply_row(Ctx& ctx, const BoundaryD& top, const PepsStateD& 
   out.sites.resize(n);
   for (int c = 0; c < n; ++c) out.phys.emplace_back(bra.site(row, c).shape[3], ket.site(row, c).shape[3]);
   const int absorb = opt.canonicalize ? (row % 2 ? kRight : kLeft) : kSplit;
+  ctx.lookahead.reset();
 
   // pending v: (a, bra-down, ket-down, mps bond, bra-right, ket-right)
   const DTensor& s0 = top.sites[0];
@@ -109,14 +110,34 @@ BoundaryD two_layer_apply_row(Ctx& ctx, const BoundaryD& top, const PepsStateD& 
     Trunc policy = opt.trunc;
     if (policy.max_rank == 0) policy.max_rank = UINT64_MAX;
     Rsvd cfg = opt.rsvd;
-    cfg.seed = derive_seed1(derive_seed1(derive_seed1(opt.seed, seed_tag), static_cast<uint64_t>(row)),
-                            static_cast<uint64_t>(c));
+    auto col_seed = [&](int col) {
+      return derive_seed1(derive_seed1(derive_seed1(opt.seed, seed_tag), static_cast<uint64_t>(row)),
+                          static_cast<uint64_t>(col));
+    };
+    cfg.seed = col_seed(c);
+    if (c + 1 < n && opt.strategy == kImplicitRsvd) {
+      // next column's operator with its pending tensor guessed at full rank
+      // (this column's target); reused only if the guess holds
+      const int64_t mindim = std::min(net.row_extent(), net.col_extent());
+      const int64_t rho = static_cast<int64_t>(std::min<uint64_t>(policy.max_rank, static_cast<uint64_t>(mindim)));
+      const auto& bs = bra.site(row, c).shape;
+      const auto& ks = ket.site(row, c).shape;
+      DTensor vg;
+      vg.shape = {rho, bs[3], ks[3], sc.shape[2], bs[4], ks[4]};
+      const DTensor& sn = top.sites[c + 1];
+      DTensor sns = reshape(sn, {top.phys[c + 1].first, top.phys[c + 1].second, sn.shape[1], sn.shape[2]});
+      set_lookahead(ctx,
+                    ImplicitOp({vg, sns, bra.site(row, c + 1), ket.site(row, c + 1)},
+                               {"apqsmn", "uvst", "dumbe", "dvncf"}, "apq", "bctef", {false, false, true, false}),
+                    col_seed(c + 1));
+    }
     // t1 (a, pb, pk, rho) written directly as (pb, pk, a, rho)
     EinsumsvdResultD split = einsumsvd(ctx, net, policy, opt.strategy, absorb, cfg, {1, 2, 0, 3});
     const auto& t1 = split.t1.shape;
     out.sites[c - 1] = reshape(split.t1, {t1[0] * t1[1], t1[2], t1[3]});
     v = split.t2;  // (rho, b, c, t, e, f)
   }
+  ctx.lookahead.reset();
   // last = v.permute({1,2,0,3,4,5}) -> (pb*pk, rho, t*e*f)
   LTensor last = reduce_to(ctx, as_labelled(v, "abcdef"), "bcadef");
   DTensor lastd = materialize(ctx, last, last.labels);
