@@ -256,6 +256,83 @@ LTensor apply_orth_speculative(Ctx& ctx, const LTensor& Z, ApplyFn&& apply) {
   return apply(q);
 }
 
+// adjoint(orth(Y)) for the small-side orthogonalisation of a power
+// iteration, with the k x k eigensolver hidden behind the first pairwise step
+// of the adjoint chain: that step is linear in the probe, so it runs on Y
+// itself on the side stream while the Gram matrix and its eigendecomposition
+// run on the main stream, and its (small) result is then multiplied by the
+// k x k factor P = X Lambda^-1/2 before the rest of the chain continues.  The
+// explicit basis orth(Y) = Y P is returned in *p_out (cheap: rows_Y x k x k).
+// Deficient Gram matrices (completed columns) fall back to the plain route.
+LTensor adjoint_orth_speculative(Ctx& ctx, const LTensor& Y, ContractionPlan& plan_adj,
+                                 std::vector<LTensor>& leaves_adj, LTensor* p_out) {
+  const int64_t k = Y.ext.back();
+  const int64_t rows = Y.size() / k;
+  const int probe_leaf = static_cast<int>(leaves_adj.size()) - 1;
+  const int node = plan_adj.parent_of_leaf(probe_leaf);
+  auto plain = [&]() {
+    *p_out = orth(ctx, Y);
+    leaves_adj.back() = *p_out;
+    return plan_adj.execute(ctx, leaves_adj);
+  };
+  if (node < 0) return plain();
+  ctx.fork();
+  BufPtr G = ctx.alloc(k * k);
+  mm(ctx, G->p, Y.ptr, true, true, Y.ptr, false, false, k, k, rows);
+  BufPtr P = ctx.alloc(k * k), R = ctx.alloc(k * k), def = ctx.alloc((k + 2 + 1) / 2 + 1);
+  int* d_def = reinterpret_cast<int*>(def->p);
+  int* d_any = d_def + k;
+  BufPtr work;
+  if (2 * k * (k + 1) * 16 > 176 * 1024) work = ctx.alloc(2 * k * (k + 1));
+  {
+    ProfScope ps_(ctx, Ctx::kProfSmall);
+    gram_factors(G->p, static_cast<int>(k), P->p, R->p, d_def, d_any, ctx.d_status, work ? work->p : nullptr,
+                 ctx.stream);
+  }
+  ++ctx.launches;
+  PEPSB_CUDA(cudaMemcpyAsync(ctx.h_status + 17, d_any, sizeof(int), cudaMemcpyDeviceToHost, ctx.stream));
+  cudaEvent_t eig_done = ctx.take_event();
+  PEPSB_CUDA(cudaEventRecord(eig_done, ctx.stream));
+  ctx.side();
+  leaves_adj.back() = Y;
+  LTensor T1 = plan_adj.run_node(ctx, node, leaves_adj);
+  ctx.join();
+  {
+    HostTimer ht(ctx.trace ? &ctx.t_sync : nullptr);
+    PEPSB_CUDA(cudaEventSynchronize(eig_done));
+  }
+  ctx.event_pool.push_back(eig_done);
+  // explicit basis Q = Y P (+ the reference's completion when deficient)
+  BufPtr Q = ctx.alloc(rows * k);
+  mm(ctx, Q->p, Y.ptr, false, Y.conj, P->p, false, false, rows, k, k);
+  const bool deficient = ctx.h_status[17] != 0;
+  if (deficient) {
+    {
+      ProfScope ps_(ctx, Ctx::kProfSmall);
+      complete_columns(Q->p, rows, static_cast<int>(k), d_def, d_any, ctx.d_status, ctx.stream);
+    }
+    ++ctx.launches;
+  }
+  LTensor q = Y;
+  q.buf = Q;
+  q.ptr = Q->p;
+  q.conj = false;
+  q.str = row_major_strides(q.ext);
+  *p_out = q;
+  leaves_adj.back() = q;
+  if (deficient) return plan_adj.execute(ctx, leaves_adj);
+  // T1 (.., X, ..) x P(X, X') -> relabel X' as X
+  const char X = Y.labels.back();
+  std::string used = T1.labels;
+  for (const auto& l : leaves_adj) used += l.labels;
+  const char Xp = unused_labels(used, 1)[0];
+  std::string out_order = T1.labels;
+  std::replace(out_order.begin(), out_order.end(), X, Xp);
+  LTensor T1p = pairwise_gemm(ctx, T1, wrap(P, std::string{X, Xp}, {k, k}), "", std::string(1, X), out_order);
+  std::replace(T1p.labels.begin(), T1p.labels.end(), Xp, X);
+  return plan_adj.execute_subst(ctx, leaves_adj, node, T1p);
+}
+
 struct Projected {
   BufPtr Ut;  // k x k left singular vectors of B = P^H A (phase-fixed)
   std::vector<double> s;
@@ -530,24 +607,31 @@ EinsumsvdResultD rsvd_core(Ctx& ctx, const ImplicitOp& op, const Trunc& policy, 
   static const bool trace = getenv("PEPSB_TRACE") != nullptr;
   auto now = [] { return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count(); };
   const double tr0 = trace ? now() : 0.0;
-  LTensor p;
+  LTensor y;
   if (prefix.buf) {
     leaves_ap.back() = q;
-    p = orth(ctx, plan_ap.execute_with_prefix(ctx, leaves_ap, 0, prefix));
+    y = plan_ap.execute_with_prefix(ctx, leaves_ap, 0, prefix);
     prefix = LTensor();
   } else {
-    p = orth(ctx, apply(q));
+    y = apply(q);
   }
-  for (int i = 0; i < cfg.power_iters; ++i) {
-    // (small problems: the host sync on the eigensolver would cost more than it hides)
-    if (ctx.orth_mode == 0 && (ctx.overlap == 2 || (ctx.overlap == 1 && op.col_extent() >= (1 << 15)))) {
-      p = orth(ctx, apply_orth_speculative(ctx, adjoint(p), apply));
+  // (small problems: the host syncs on the eigensolver would cost more than they hide)
+  const bool overlap =
+      ctx.orth_mode == 0 && (ctx.overlap == 2 || (ctx.overlap == 1 && op.col_extent() >= (1 << 15)));
+  LTensor p, z;
+  for (int i = 0; i <= cfg.power_iters; ++i) {
+    // z = A^* orth(y), p = orth(y)
+    if (overlap) {
+      z = adjoint_orth_speculative(ctx, y, plan_adj, leaves_adj, &p);
     } else {
-      q = orth(ctx, adjoint(p));
-      p = orth(ctx, apply(q));
+      p = orth(ctx, y);
+      z = adjoint(p);
     }
+    if (i == cfg.power_iters) break;
+    // y = A orth(z)
+    y = overlap ? apply_orth_speculative(ctx, z, apply) : apply(orth(ctx, z));
   }
-  LTensor z = adjoint(p);
+  y = LTensor();
   q = LTensor();
   // Row lookahead: start the next column's sketch and the v-independent
   // prefix of its first application on the side stream; they run during this

@@ -610,12 +610,25 @@ LTensor ContractionPlan::run_prefix(Ctx& ctx, const std::vector<LTensor>& leaves
   return run(ctx, node, leaves);
 }
 
+int ContractionPlan::parent_of_leaf(int leaf) const {
+  for (size_t i = 0; i < nodes_.size(); ++i) {
+    const Node& nd = nodes_[i];
+    if (nd.leaf >= 0) continue;
+    if (nodes_[nd.a_child].leaf == leaf || nodes_[nd.b_child].leaf == leaf) return static_cast<int>(i);
+  }
+  return -1;
+}
+
 LTensor ContractionPlan::execute_with_prefix(Ctx& ctx, const std::vector<LTensor>& leaves, int excl,
                                              const LTensor& prefix) {
   const int node = prefix_node(excl);
   if (node < 0 || !prefix.buf) return execute(ctx, leaves);
+  return execute_subst(ctx, leaves, node, prefix);
+}
+
+LTensor ContractionPlan::execute_subst(Ctx& ctx, const std::vector<LTensor>& leaves, int node, const LTensor& result) {
   subst_node_ = node;
-  subst_ = prefix;
+  subst_ = result;
   LTensor out;
   try {
     out = execute(ctx, leaves);

@@ -47,6 +47,12 @@ class ContractionPlan {
   LTensor run_prefix(Ctx& ctx, const std::vector<LTensor>& leaves, int excl);
   // execute() with the `rest` subtree's result supplied by run_prefix.
   LTensor execute_with_prefix(Ctx& ctx, const std::vector<LTensor>& leaves, int excl, const LTensor& prefix);
+  // The pairwise step that consumes leaf `leaf` directly (-1 if the leaf is
+  // the root); run_node runs one subtree; execute_subst runs the plan with
+  // node `node`'s result supplied.
+  int parent_of_leaf(int leaf) const;
+  LTensor run_node(Ctx& ctx, int node, const std::vector<LTensor>& leaves) { return run(ctx, node, leaves); }
+  LTensor execute_subst(Ctx& ctx, const std::vector<LTensor>& leaves, int node, const LTensor& result);
 
   bool cache_static = false;
   // Reference-convention flops of one execution (instr::flops definition).
