@@ -189,6 +189,7 @@ int pepsb_ctx_set_option(pepsb_ctx* c, const char* key, int64_t value) {
     else if (k == "eig_solver") set_eig_solver(static_cast<int>(value));
     else if (k == "gemm_algo") zgemm_set_algo(static_cast<int>(value));
     else if (k == "gemm_ws") zgemm_set_ws(static_cast<int>(value));
+    else if (k == "gemm_real") zgemm_set_real(static_cast<int>(value));
     else if (k == "overlap") c->ctx->overlap = static_cast<int>(std::clamp<int64_t>(value, 0, 2));
     else throw Error(kConfigError, "unknown option '" + k + "'");
   });
@@ -292,12 +293,25 @@ int pepsb_ctx_debug_word(pepsb_ctx* c, int idx, int reset) {
 
 void* pepsb_ctx_stream(pepsb_ctx* c) { return c ? static_cast<void*>(c->ctx->stream) : nullptr; }
 
+// Exact-zero imaginary parts (checked on the device, one small reduction and a
+// flag read-back): such tensors run the complex x real GEMM kernels.
+void mark_real(Ctx& ctx, DTensor& t) {
+  int* flag = ctx.d_status + 40;
+  imag_nonzero(t.data(), t.size(), flag, ctx.stream);
+  ++ctx.launches;
+  PEPSB_CUDA(cudaMemcpyAsync(ctx.h_status + 40, flag, sizeof(int), cudaMemcpyDeviceToHost, ctx.stream));
+  ctx.sync_main();
+  t.buf->real = ctx.h_status[40] == 0;
+}
+
 int pepsb_tensor_from_host(pepsb_ctx* c, int ndim, const int64_t* shape, const double* data, pepsb_tensor** out) {
   return guard([&] {
     need(c, "ctx");
     DTensor t = c->ctx->empty(shape_of(ndim, shape));
-    if (t.size())
+    if (t.size()) {
       PEPSB_CUDA(cudaMemcpyAsync(t.data(), data, t.size() * sizeof(double2), cudaMemcpyHostToDevice, c->ctx->stream));
+      mark_real(*c->ctx, t);
+    }
     *out = wrap(t);
   });
 }
@@ -306,8 +320,10 @@ int pepsb_tensor_from_device(pepsb_ctx* c, int ndim, const int64_t* shape, const
   return guard([&] {
     need(c, "ctx");
     DTensor t = c->ctx->empty(shape_of(ndim, shape));
-    if (t.size())
+    if (t.size()) {
       PEPSB_CUDA(cudaMemcpyAsync(t.data(), dptr, t.size() * sizeof(double2), cudaMemcpyDeviceToDevice, c->ctx->stream));
+      mark_real(*c->ctx, t);
+    }
     *out = wrap(t);
   });
 }

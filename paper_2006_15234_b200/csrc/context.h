@@ -48,6 +48,11 @@ struct Buf {
   double2* p = nullptr;
   int64_t n = 0;
   size_t bytes = 0;  // size class actually reserved
+  // Every imaginary part is exactly zero (host data checked on upload; kept by
+  // copies and by products of real operands).  GEMMs with a real operand run
+  // the complex x real kernel: half the DMMAs of the 4M scheme, bitwise the
+  // same sums as complex arithmetic on zero imaginary parts.
+  bool real = false;
   std::shared_ptr<Pool> pool;
   ~Buf();
 };

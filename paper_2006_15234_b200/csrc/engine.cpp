@@ -124,6 +124,7 @@ LTensor reduce_to(Ctx& ctx, const LTensor& t, const std::string& out_order) {
   p.conj = t.conj ? 1 : 0;
   LTensor out;
   out.buf = ctx.alloc(kept);
+  out.buf->real = t.buf && t.buf->real;  // a gather / sum of real entries is real
   out.ptr = out.buf->p;
   out.labels = out_order;
   out.ext = oext;
@@ -172,6 +173,7 @@ LTensor pairwise_gemm(Ctx& ctx, const LTensor& A, const LTensor& B, const std::s
   int64_t total = 1;
   for (auto e : cext) total *= e;
   C.buf = ctx.alloc(total);
+  C.buf->real = A.buf && A.buf->real && B.buf && B.buf->real;
   C.ptr = C.buf->p;
   C.labels = out_order;
   C.ext = cext;
@@ -191,6 +193,8 @@ LTensor pairwise_gemm(Ctx& ctx, const LTensor& A, const LTensor& B, const std::s
   if (p.K == 1) p.sAk = p.sBk = 1;
   p.conjA = A.conj;
   p.conjB = B.conj;
+  p.realA = A.buf && A.buf->real;
+  p.realB = B.buf && B.buf->real;
   int64_t nbatch = 1;
   for (char c : batch) {
     int64_t e = A.extent_of(c);

@@ -88,6 +88,14 @@ __global__ void slice_scale_kernel(double2* dst, const double2* src, int64_t row
   }
 }
 
+__global__ void imag_nonzero_kernel(const double2* x, int64_t n, int* flag) {
+  int any = 0;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    any |= x[i].y != 0.0;
+  if (__any_sync(0xffffffffu, any) && (threadIdx.x & 31) == 0) atomicOr(flag, 1);
+}
+
 __global__ void fill_zero_kernel(double2* dst, int64_t n) {
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x)
@@ -130,6 +138,13 @@ void slice_scale_cols(double2* dst, const double2* src, int64_t rows, int64_t co
                       const double* w, int conj, cudaStream_t st) {
   if (rows * cols == 0) return;
   slice_scale_kernel<<<grid_for(rows * cols), kT, 0, st>>>(dst, src, rows, cols, lds, w, conj);
+  PEPSB_LAUNCH();
+}
+
+void imag_nonzero(const double2* x, int64_t n, int* flag, cudaStream_t st) {
+  PEPSB_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), st));
+  if (n == 0) return;
+  imag_nonzero_kernel<<<grid_for(n), kT, 0, st>>>(x, n, flag);
   PEPSB_LAUNCH();
 }
 

@@ -39,6 +39,8 @@ void scale_axis(double2* t, int64_t total, int64_t inner, int64_t ext, const dou
 void slice_scale_cols(double2* dst, const double2* src, int64_t rows, int64_t cols, int64_t lds,
                       const double* w, int conj, cudaStream_t st);
 
+// *flag = 1 if any element has a nonzero imaginary part, else 0.
+void imag_nonzero(const double2* x, int64_t n, int* flag, cudaStream_t st);
 void fill_zero(double2* dst, int64_t n, cudaStream_t st);
 
 }  // namespace pepsb

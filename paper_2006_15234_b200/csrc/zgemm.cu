@@ -305,6 +305,7 @@ void transpose_problem(ZgemmParams& p) {
   p.sBk = sAk;
   p.sBj = sAi;
   std::swap(p.conjA, p.conjB);
+  std::swap(p.realA, p.realB);
   std::swap(p.M, p.N);
   for (int a = 0; a < 4; ++a) std::swap(p.bsA[a], p.bsB[a]);
   std::swap(p.nr, p.nc);
@@ -352,11 +353,14 @@ struct Smem3 {
 template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool AK, bool BNC, int ALG, int MINB>
 __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32, MINB)
     zgemm_cx_kernel(const ZgemmParams p) {
-  constexpr int NACC = ALG == 3 ? 3 : 2;  // 3M: P1, P2, P3;  4M: Re, Im
+  // 3M: P1, P2, P3;  4M: Re, Im;  complex x real (ALG 1): one DMMA pair (re, im)
+  constexpr int NACC = ALG == 3 ? 3 : ALG == 1 ? 1 : 2;
   using S = Smem3<BM, BN, BK, AK, BNC>;
   constexpr int NT = (BM / WM) * (BN / WN) * 32;
   constexpr int FM = WM / 8;  // 8-row blocks per warp
-  constexpr int FN = WN / 8;  // 8-column blocks per warp
+  // 8-column blocks per warp; complex x real: a DMMA covers 8 interleaved
+  // doubles of B = 4 complex columns
+  constexpr int FN = ALG == 1 ? WN / 4 : WN / 8;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double2* smem = reinterpret_cast<double2*>(smem_raw);
   int64_t* rowoff = reinterpret_cast<int64_t*>(smem + STAGES * S::STAGE);
@@ -519,24 +523,46 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32, MINB)
   // before the DMMAs of step s; one barrier per k-tile (before the first
   // fragment load of the next slot, which also frees the current slot for the
   // prefetch of stage kt + STAGES).
-  double2 fa[2][FM], fb[2][FN];
+  double2 fa[2][ALG == 1 ? 1 : FM], fb[2][ALG == 1 ? 1 : FN];
+  double ra[2][FM], rb[2][FN];  // complex x real: A real parts, B interleaved doubles
+  const long long sgbr = (rq & 1) ? sgb : 0LL;  // complex x real: this lane's B double is an imaginary part
   auto load_frags = [&](int buf, int slot, int ks) {
     const double2* As = smem + slot * S::STAGE;
     const double2* Bs = As + S::A_ELEMS;
     const int kc = ks * 4 + kq;
+    if constexpr (ALG == 1) {
 #pragma unroll
-    for (int a = 0; a < FM; ++a) {
-      const int row = wm0 + a * 8 + rq;
-      fa[buf][a] = AK ? As[row * S::LDA + kc] : As[kc * S::LDA + row];
-    }
+      for (int a = 0; a < FM; ++a) {
+        const int row = wm0 + a * 8 + rq;
+        ra[buf][a] = (AK ? As[row * S::LDA + kc] : As[kc * S::LDA + row]).x;
+      }
 #pragma unroll
-    for (int b = 0; b < FN; ++b) {
-      const int col = wn0 + b * 8 + rq;
-      fb[buf][b] = BNC ? Bs[kc * S::LDB + col] : Bs[col * S::LDB + kc];
+      for (int b = 0; b < FN; ++b) {
+        const int col = wn0 + b * 4 + (rq >> 1);
+        const double* e = reinterpret_cast<const double*>(BNC ? Bs + kc * S::LDB + col : Bs + col * S::LDB + kc);
+        rb[buf][b] = flip(e[rq & 1], sgbr);
+      }
+      return;
+    } else {
+#pragma unroll
+      for (int a = 0; a < FM; ++a) {
+        const int row = wm0 + a * 8 + rq;
+        fa[buf][a] = AK ? As[row * S::LDA + kc] : As[kc * S::LDA + row];
+      }
+#pragma unroll
+      for (int b = 0; b < FN; ++b) {
+        const int col = wn0 + b * 8 + rq;
+        fb[buf][b] = BNC ? Bs[kc * S::LDB + col] : Bs[col * S::LDB + kc];
+      }
     }
   };
   auto compute = [&](int buf) {
-    if constexpr (ALG == 3) {
+    if constexpr (ALG == 1) {
+#pragma unroll
+      for (int a = 0; a < FM; ++a)
+#pragma unroll
+        for (int b = 0; b < FN; ++b) dmma884(acc[a][b][0][0], acc[a][b][0][1], ra[buf][a], rb[buf][b]);
+    } else if constexpr (ALG == 3) {
       double ar[FM], ai[FM], as[FM], br[FN], bi[FN], bs[FN];
 #pragma unroll
       for (int a = 0; a < FM; ++a) {
@@ -628,7 +654,8 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32, MINB)
   cp_async_wait<0>();
   __syncthreads();
 
-  // Epilogue: lane owns C[a*8 + lane>>2][b*8 + 2*(lane&3) + {0,1}] of every block.
+  // Epilogue: lane owns C[a*8 + lane>>2][b*8 + 2*(lane&3) + {0,1}] of every block
+  // (complex x real: the complex C[a*8 + lane>>2][b*4 + lane&3] = (c0, c1)).
 #pragma unroll
   for (int a = 0; a < FM; ++a) {
     const int li = wm0 + a * 8 + (lane >> 2);
@@ -636,11 +663,13 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32, MINB)
 #pragma unroll
     for (int b = 0; b < FN; ++b)
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int lj = wn0 + b * 8 + 2 * (lane & 3) + h;
+      for (int h = 0; h < (ALG == 1 ? 1 : 2); ++h) {
+        const int lj = ALG == 1 ? wn0 + b * 4 + (lane & 3) : wn0 + b * 8 + 2 * (lane & 3) + h;
         if (n0 + lj >= p.N) continue;
         double2 v;
-        if constexpr (ALG == 3) {
+        if constexpr (ALG == 1) {
+          v = make_double2(acc[a][b][0][0], acc[a][b][0][1]);
+        } else if constexpr (ALG == 3) {
           const double p1 = acc[a][b][0][h], p2 = acc[a][b][1][h], p3 = acc[a][b][NACC - 1][h];
           v = make_double2(p1 - p2, p3 - p1 - p2);
         } else {
@@ -685,6 +714,13 @@ void launch_any3m(const ZgemmParams& p, cudaStream_t stream) {
   }
 }
 
+// Complex x real (A real): 64 x 64 complex tiles, 4 warps of 32 x 32 (8 x 8
+// DMMA blocks of 8 rows x 4 complex columns), half the DMMAs of 4M.
+template <bool AK, bool BNC>
+void launch_cr(const ZgemmParams& p, cudaStream_t stream) {
+  launch_cx<64, 64, kBK, 32, 32, kStages, AK, BNC, 1, 2>(p, stream);
+}
+
 // 4M with complex fragments (one LDS.128 per fragment element, four DMMAs per
 // 8 x 8 complex block into Re / Im accumulators), the CUTLASS z884 scheme.
 template <bool AK, bool BNC>
@@ -715,6 +751,20 @@ void zgemm_set_algo(int a) {
   g_algo.store(a);
 }
 
+std::atomic<int> g_real{-1};
+
+bool zgemm_real_enabled() {
+  int v = g_real.load();
+  if (v < 0) {
+    const char* e = getenv("PEPSB_GEMM_REAL");
+    v = (e && e[0] == '0') ? 0 : 1;
+    g_real.store(v);
+  }
+  return v != 0;
+}
+
+void zgemm_set_real(int on) { g_real.store(on ? 1 : 0); }
+
 int zgemm_ws_mode() {
   int v = g_ws.load();
   if (v < 0) {
@@ -731,23 +781,32 @@ bool zgemm_ws_enabled() { return zgemm_ws_mode() != 0; }
 void zgemm_set_ws(int mode) { g_ws.store(mode >= 0 && mode <= 2 ? mode : 0); }
 
 int64_t zgemm_plan_splits(ZgemmParams& p, int num_sms) {
-  if (p.M > 64 && p.M <= 72 && p.N > 72) transpose_problem(p);
+  // a real operand goes first (complex x real kernel), unless that breaks the
+  // 64-wide tiling the kernel has
+  const bool cr_ok = zgemm_real_enabled() && (p.realA || p.realB);
+  if (cr_ok && !p.realA && !(p.N > 64 && p.N <= 72)) transpose_problem(p);
+  if (!(cr_ok && p.realA) && p.M > 64 && p.M <= 72 && p.N > 72) transpose_problem(p);
   p.cfg = choose_cfg(p.M, p.N);
   p.algo = zgemm_algo();
+  if (cr_ok && p.realA && p.cfg == 0 && p.algo != kGemm4M) p.algo = kGemmCR;
   if (p.algo != kGemm4M && p.cfg == 4) p.cfg = 0;
   // Short-K problems on the 64-wide tiles are epilogue-heavy: the 4M
   // complex-fragment kernel's 64 x 64 tile (twice the 3M tile) wins there.
   if (p.algo == kGemm3M && p.cfg == 0 && p.K <= 64) p.algo = kGemm4C;
-  const TileCfg tc = p.algo == kGemm3M ? kCfgs3m[p.cfg] : p.algo == kGemm4C ? kCfgs4c[p.cfg] : kCfgs[p.cfg];
+  const TileCfg tc = p.algo == kGemm3M   ? kCfgs3m[p.cfg]
+                    : p.algo == kGemmCR ? TileCfg{64, 64}
+                    : p.algo == kGemm4C ? kCfgs4c[p.cfg]
+                                        : kCfgs[p.cfg];
   int64_t bm = tc.bm, bn = tc.bn;
   p.num_sms = num_sms;
-  p.ws = (zgemm_ws_enabled() && p.cfg == 0 && p.algo != kGemm4M && zgemm_ws_eligible(p)) ? 1 : 0;
+  p.ws = (zgemm_ws_enabled() && p.cfg == 0 && p.algo != kGemm4M && p.algo != kGemmCR && zgemm_ws_eligible(p)) ? 1 : 0;
   if (p.ws) zgemm_ws_tile(p, bm, bn);
   const int64_t tiles = ((p.M + bm - 1) / bm) * ((p.N + bn - 1) / bn) * p.batch;
   // one full wave of resident CTAs (no partial second wave)
   const int64_t target =
       p.ws ? (zgemm_ws_mode() == 2 ? 2 * num_sms : num_sms)
-           : static_cast<int64_t>(p.algo == kGemm4M ? ctas_per_sm(p.cfg) : ctas_per_sm3m(p.cfg)) * num_sms;
+           : static_cast<int64_t>(p.algo == kGemm4M ? ctas_per_sm(p.cfg) : p.algo == kGemmCR ? 2 : ctas_per_sm3m(p.cfg)) *
+                 num_sms;
   int64_t splits = 1;
   if (tiles < target && p.K > 4 * kBK) {
     splits = std::min<int64_t>(std::max<int64_t>(1, target / tiles), (p.K + 4 * kBK - 1) / (4 * kBK));
@@ -777,7 +836,12 @@ void zgemm_launch(ZgemmParams p, cudaStream_t stream) {
     // empty contraction: C = 0 (or unchanged when accumulating)
     p.splits = 1;
   }
-  if (p.ws && p.K > 0) {
+  if (p.algo == kGemmCR) {
+    if (ak && bnc) launch_cr<true, true>(p, stream);
+    else if (ak && !bnc) launch_cr<true, false>(p, stream);
+    else if (!ak && bnc) launch_cr<false, true>(p, stream);
+    else launch_cr<false, false>(p, stream);
+  } else if (p.ws && p.K > 0) {
     zgemm_ws_launch(p, p.num_sms, stream);
   } else if (p.algo == kGemm3M) {
     if (p.cfg == 4) p.cfg = 0;

@@ -44,6 +44,7 @@ struct ZgemmParams {
   int cfg = 0;         // tile configuration (set by zgemm_plan_splits)
   int algo = 0;        // kGemm4M / kGemm3M (set by zgemm_plan_splits)
   int ws = 0;          // persistent warp-specialised kernel (zgemm_ws.cu)
+  int realA = 0, realB = 0;  // operand with exactly zero imaginary parts (Buf::real)
   int num_sms = 148;   // grid of the persistent kernel
 };
 
@@ -51,13 +52,20 @@ struct ZgemmParams {
 // per complex MAC (the zgemm arithmetic); kGemm3M = Gauss / zgemm3m, 3 real MACs
 // per complex MAC (Im C = (Ar+Ai)(Br+Bi) - ArBr - AiBi).  Default 3M;
 // PEPSB_GEMM=4m or option "gemm_algo" = 0 selects 4M.
-enum GemmAlgo { kGemm4M = 0, kGemm3M = 1, kGemm4C = 2 };
+// kGemmCR: A real (imaginary parts exactly zero), C = A B as the real GEMM
+// A (M x K) . B' (K x 2N) on B's interleaved (re, im) doubles -- 2 real MACs
+// per complex MAC (set by zgemm_plan_splits when an operand is real).
+enum GemmAlgo { kGemm4M = 0, kGemm3M = 1, kGemm4C = 2, kGemmCR = 3 };
 int zgemm_algo();
 // Real flops the DMMAs execute for a planned problem (8 per complex MAC, 6 for 3M).
 inline double zgemm_exec_flops(const ZgemmParams& p) {
-  return (p.algo == kGemm3M ? 6.0 : 8.0) * static_cast<double>(p.batch) * p.M * p.N * p.K;
+  return (p.algo == kGemm3M ? 6.0 : p.algo == kGemmCR ? 4.0 : 8.0) * static_cast<double>(p.batch) * p.M * p.N * p.K;
 }
 void zgemm_set_algo(int a);
+// Complex x real kernel for operands with exactly zero imaginary parts
+// (default on; PEPSB_GEMM_REAL=0 or option "gemm_real" = 0 disables it).
+bool zgemm_real_enabled();
+void zgemm_set_real(int on);
 // Persistent kernel with TMA tensor-map operand staging (zgemm_ws.cu): opt-in
 // (PEPSB_GEMM_WS=1 or option "gemm_ws" = 1); measured at config 2 it does not
 // beat the classic cp.async kernels, so they stay the default.

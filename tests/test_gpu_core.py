@@ -326,3 +326,35 @@ def test_gemm_ws_persistent_tiles_and_batches(A, algo, ws):
     finally:
         ctx.set_option("gemm_algo", 1)
         ctx.set_option("gemm_ws", 0)
+
+
+def test_gemm_complex_by_real_operands(A):
+    """Operands whose imaginary parts are exactly zero (checked on upload) run
+    the complex x real kernel (2 real MACs per complex MAC): real x complex,
+    complex x real (transposed onto the real-first kernel), real x real,
+    conjugated complex operand, ragged edges, split-K, batched, scattered
+    output; against numpy at rounding level."""
+    ctx = A.default_context()
+    rng = np.random.default_rng(5)
+
+    def real(shape):
+        return rng.standard_normal(shape).astype(np.complex128)
+
+    try:
+        for (m, n, k) in [(128, 9000, 64), (64, 7000, 128), (70, 90, 300), (5, 7, 3), (64, 64, 64), (100, 300, 4000)]:
+            ar, bc = real((m, k)), O.random_tensor((k, n), m + n)
+            for spec, a, b in [("ik,kj->ij", ar, bc), ("ik,kj->ji", ar, bc), ("ik,kj->ij", O.random_tensor((m, k), 3), real((k, n))),
+                               ("ik,kj->ij", ar, real((k, n))), ("ki,kj->ij", ar.T.copy(), bc), ("ik,jk->ij", ar, bc.T.copy())]:
+                ref = np.einsum(spec, a, b)
+                got = A.contract(spec, a, b).numpy()
+                assert np.abs(got - ref).max() <= 1e-12 * np.abs(ref).max(), (spec, m, n, k)
+            got = A.contract("ik,kj->ij", ar, A.to_device(bc).conj()).numpy()
+            ref = ar @ bc.conj()
+            assert np.abs(got - ref).max() <= 1e-12 * np.abs(ref).max()
+        a = real((3, 70, 40))
+        b = O.random_tensor((3, 40, 2100), 92)
+        got = A.contract("bik,bkj->ibj", a, b).numpy()
+        ref = np.einsum("bik,bkj->ibj", a, b)
+        assert np.abs(got - ref).max() <= 1e-12 * np.abs(ref).max()
+    finally:
+        ctx.set_option("gemm_real", 1)
