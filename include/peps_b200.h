@@ -223,6 +223,29 @@ int pepsb_band_value(pepsb_ctx* ctx, const pepsb_boundary* top, const pepsb_stat
                      const int* nbonds, const int* bond_ids, double* re, double* im);
 void pepsb_band_env_free(pepsb_band_env* e);
 
+/* expectation (observables.hpp:87-100, observables.cpp:335-422): sum of local
+ * terms over <psi|psi>.  Term i: coefficient (coeff[2i], coeff[2i+1]),
+ * nsites[i] in {1, 2} at rc[4i .. 4i+3] (row, col[, row, col]), operator
+ * ops[i] of shape (d, d) or (d, d, d, d) with outputs first.  Two-site terms are
+ * split by SVD (split_two_site, observables.cpp:284-295) and spliced into a
+ * band of one or two rows between the cached boundaries.  Errors as the
+ * reference: ValidationError for a non-Hermitian observable unless
+ * allow_complex, NumericalError for an imaginary part above 1e-8. */
+typedef struct {
+  pepsb_contract_opt contract;
+  int32_t use_cache;           /* default 1 */
+  int32_t shared_environments; /* default 0 */
+  int32_t allow_complex;       /* default 0 */
+} pepsb_expectation_opt;
+typedef struct {
+  double value, norm_sq;
+  double raw_sum[2], complex_value[2];
+  uint64_t full_sweeps, band_contractions, flops;
+} pepsb_expectation_result;
+int pepsb_expectation(pepsb_ctx* ctx, const pepsb_state* s, int nterms, const double* coeff, const int* nsites,
+                      const int* rc, pepsb_tensor* const* ops, const pepsb_expectation_opt* opt,
+                      pepsb_expectation_result* out);
+
 /* ---------------------------------------------------------------- simple update / ITE (state.hpp:64-76) */
 /* hermitian_function(coeff * op, exp(-tau x)) (linalg.hpp:44): the ITE gate rule of drivers.cpp:56-71 */
 int pepsb_hermitian_exp(pepsb_ctx* ctx, const pepsb_tensor* op, double coeff, double tau, pepsb_tensor** out);

@@ -232,6 +232,16 @@ def contract_two_layer(sites, rows, cols, m, seed, power_iters=2, oversample=-1,
     return complex(dd[0], dd[1]), dict(seconds=float(dd[2]), flops=float(dd[3]), peak=float(dd[4]))
 
 
+def contract_one_layer(sites, rows, cols, family, m=0, seed=0, power_iters=2, oversample=-1, canonicalize=True):
+    """contract_one_layer on an order-4 grid; family 0 exact, 1 bmps, 2 ibmps."""
+    tl = _TList(sites)
+    _, dd = _bag(_fn("ref_contract_one_layer")(int(rows), int(cols), tl.ndims, tl.shapes, tl.datas, int(family),
+                                               C.c_int64(m),
+                                               C.c_uint64(seed), int(power_iters), int(oversample),
+                                               int(canonicalize)))
+    return complex(dd[0], dd[1])
+
+
 def inner_exact(sites, rows, cols, d=2):
     tl, a = _state_args(sites, rows, cols, d)
     _, dd = _bag(_fn("ref_inner_exact")(*a))

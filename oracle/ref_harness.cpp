@@ -362,6 +362,23 @@ Bag* ref_contract_two_layer(int rows, int cols, int d, const int* ndims, const i
   });
 }
 
+// contract_one_layer (contraction.cpp:205-252) on an order-4 grid (up, left,
+// down, right): family 0 exact (contract_exact), 1 bmps, 2 ibmps.
+Bag* ref_contract_one_layer(int rows, int cols, const int* ndims, const int64_t* shapes,
+                            const double* const* datas, int family, int64_t m, uint64_t seed,
+                            int power_iters, int oversample, int canonicalize) {
+  return guarded([&](Bag& b) {
+    OneLayerGrid g(rows, cols, make_list(rows * cols, ndims, shapes, datas));
+    ContractOption opt = family == 0 ? ContractOption::exact_network()
+                         : family == 1 ? ContractOption::bmps_opt(static_cast<std::size_t>(m), seed)
+                                       : ContractOption::ibmps_opt(static_cast<std::size_t>(m), seed, power_iters);
+    opt.rsvd.oversample = oversample;
+    opt.canonicalize = canonicalize != 0;
+    cplx v = contract_one_layer(g, opt);
+    b.doubles = {v.real(), v.imag()};
+  });
+}
+
 // Exact <psi|psi> (ContractOption::exact_network, via the merged one-layer grid).
 Bag* ref_inner_exact(int rows, int cols, int d, const int* ndims, const int64_t* shapes,
                      const double* const* datas) {

@@ -38,6 +38,17 @@ class ContractOpt(C.Structure):
                 ("seed", C.c_uint64)]
 
 
+class ExpectationOpt(C.Structure):
+    _fields_ = [("contract", ContractOpt), ("use_cache", C.c_int32), ("shared_environments", C.c_int32),
+                ("allow_complex", C.c_int32)]
+
+
+class ExpectationResult(C.Structure):
+    _fields_ = [("value", C.c_double), ("norm_sq", C.c_double), ("raw_sum", C.c_double * 2),
+                ("complex_value", C.c_double * 2), ("full_sweeps", C.c_uint64), ("band_contractions", C.c_uint64),
+                ("flops", C.c_uint64)]
+
+
 _VP = C.c_void_p
 _SIGS = {
     "pepsb_last_error": (C.c_char_p, []),
@@ -114,6 +125,9 @@ _SIGS = {
                                    C.POINTER(_VP), C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_double),
                                    C.POINTER(C.c_double)]),
     "pepsb_band_env_free": (None, [_VP]),
+    "pepsb_expectation": (C.c_int, [_VP, _VP, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_int),
+                                    C.POINTER(C.c_int), C.POINTER(_VP), C.POINTER(ExpectationOpt),
+                                    C.POINTER(ExpectationResult)]),
     "pepsb_hermitian_exp": (C.c_int, [_VP, _VP, C.c_double, C.c_double, C.POINTER(_VP)]),
     "pepsb_apply_one_site": (C.c_int, [_VP, _VP, _VP, C.c_int, C.POINTER(C.c_int), C.POINTER(_VP)]),
     "pepsb_apply_two_site": (C.c_int, [_VP, _VP, _VP, C.c_int, C.POINTER(C.c_int), C.POINTER(Trunc),

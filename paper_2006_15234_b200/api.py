@@ -603,6 +603,75 @@ def band_value(top, bra: PepsState, ket: PepsState, r0: int, r1: int, bottom, pi
     return complex(re.value, im.value)
 
 
+@dataclass
+class LocalTerm:
+    """observables.hpp:16-20: coeff * op on one or two sites; 2-site op (d,d,d,d) outputs first."""
+    coeff: complex
+    sites: List[Tuple[int, int]]
+    op: object
+
+
+@dataclass
+class ExpectationOptions:
+    """observables.hpp:69-77."""
+    contract: ContractOption = field(default_factory=ContractOption)
+    use_cache: bool = True
+    shared_environments: bool = False
+    allow_complex: bool = False
+
+
+@dataclass
+class ExpectationResult:
+    """observables.hpp:79-85 (+ ExpectationStats :63-67)."""
+    value: float
+    raw_sum: complex
+    norm_sq: float
+    complex_value: complex
+    full_sweeps: int
+    band_contractions: int
+    flops: int
+
+
+def expectation(s: PepsState, terms: Sequence[LocalTerm], opt: ExpectationOptions = None) -> ExpectationResult:
+    """expectation(state, observable, options) (observables.cpp:335-422) on the device."""
+    from ._lib import ExpectationOpt, ExpectationResult as _R
+    opt = opt or ExpectationOptions()
+    n = len(terms)
+    cf = (C.c_double * max(1, 2 * n))(*[x for t in terms for x in (complex(t.coeff).real, complex(t.coeff).imag)])
+    ns = (C.c_int * max(1, n))(*[len(t.sites) for t in terms])
+    rc = []
+    for t in terms:
+        flat = [int(x) for p in t.sites for x in p]
+        rc += flat + [0] * (4 - len(flat))
+    rca = (C.c_int * max(1, 4 * n))(*rc)
+    ops = [to_device(t.op, s.ctx) for t in terms]
+    oa = (_VP * max(1, n))(*[o.h for o in ops])
+    o = ExpectationOpt(opt.contract.c(), int(opt.use_cache), int(opt.shared_environments), int(opt.allow_complex))
+    r = _R()
+    check(lib().pepsb_expectation(s.ctx.h, s.h, n, cf, ns, rca, oa, C.byref(o), C.byref(r)))
+    return ExpectationResult(r.value, complex(r.raw_sum[0], r.raw_sum[1]), r.norm_sq,
+                             complex(r.complex_value[0], r.complex_value[1]), int(r.full_sweeps),
+                             int(r.band_contractions), int(r.flops))
+
+
+def tfim_terms(rows: int, cols: int, J: float, h: float) -> List[LocalTerm]:
+    """H = -J sum_<ij> Z_i Z_j - h sum_i X_i in the colour order of the ITE driver
+    (fields; even / odd horizontal; even / odd vertical bonds)."""
+    x = np.array([[0, 1], [1, 0]], dtype=np.complex128)
+    z = np.diag([1.0, -1.0]).astype(np.complex128)
+    zz = np.einsum("ac,bd->abcd", z, z)
+    out = [LocalTerm(-h, [(r, c)], x) for r in range(rows) for c in range(cols)]
+    for par in range(2):
+        for r in range(rows):
+            for c in range(par, cols - 1, 2):
+                out.append(LocalTerm(-J, [(r, c), (r, c + 1)], zz))
+    for par in range(2):
+        for r in range(par, rows - 1, 2):
+            for c in range(cols):
+                out.append(LocalTerm(-J, [(r, c), (r + 1, c)], zz))
+    return out
+
+
 def _wrap_state(h, like: PepsState) -> PepsState:
     out = PepsState.__new__(PepsState)
     out.ctx, out.rows, out.cols, out.d, out.h = like.ctx, like.rows, like.cols, like.d, h

@@ -757,6 +757,45 @@ int pepsb_band_value(pepsb_ctx* c, const pepsb_boundary* top, const pepsb_state*
 
 void pepsb_band_env_free(pepsb_band_env* e) { delete e; }
 
+int pepsb_expectation(pepsb_ctx* c, const pepsb_state* s, int nterms, const double* coeff, const int* nsites,
+                      const int* rc, pepsb_tensor* const* ops, const pepsb_expectation_opt* opt,
+                      pepsb_expectation_result* out) {
+  return guard([&] {
+    need(c, "ctx");
+    need(s, "state");
+    need(opt, "options");
+    need(out, "result");
+    if (nterms < 0) throw Error(kValidationError, "negative term count");
+    std::vector<LocalTermD> terms(static_cast<size_t>(nterms));
+    for (int i = 0; i < nterms; ++i) {
+      need(ops[i], "term operator");
+      LocalTermD& t = terms[i];
+      t.coeff_re = coeff[2 * i];
+      t.coeff_im = coeff[2 * i + 1];
+      if (nsites[i] != 1 && nsites[i] != 2) throw Error(kValidationError, "terms act on one or two sites");
+      for (int k = 0; k < nsites[i]; ++k) t.sites.emplace_back(rc[4 * i + 2 * k], rc[4 * i + 2 * k + 1]);
+      t.op = ops[i]->t;
+      const size_t want = nsites[i] == 1 ? 2 : 4;
+      if (t.op.shape.size() != want) throw Error(kShapeError, "term operator must have 2 (1-site) or 4 (2-site) axes");
+    }
+    ExpectOptD o;
+    o.contract = opt_of(&opt->contract);
+    o.use_cache = opt->use_cache != 0;
+    o.shared_environments = opt->shared_environments != 0;
+    o.allow_complex = opt->allow_complex != 0;
+    ExpectResultD r = expectation(*c->ctx, s->s, terms, o);
+    out->value = r.value;
+    out->norm_sq = r.norm_sq;
+    out->raw_sum[0] = r.raw_re;
+    out->raw_sum[1] = r.raw_im;
+    out->complex_value[0] = r.cx_re;
+    out->complex_value[1] = r.cx_im;
+    out->full_sweeps = r.full_sweeps;
+    out->band_contractions = r.band_contractions;
+    out->flops = r.flops;
+  });
+}
+
 int pepsb_hermitian_exp(pepsb_ctx* c, const pepsb_tensor* op, double coeff, double tau, pepsb_tensor** out) {
   return guard([&] {
     need(c, "ctx");

@@ -6,6 +6,8 @@
 #include "peps.h"
 
 #include <algorithm>
+#include <cmath>
+#include <map>
 #include <cstdio>
 #include <cstring>
 
@@ -432,6 +434,179 @@ std::pair<double, double> band_splice(Ctx& ctx, const BandEnvD& env, const Bound
   const LTensor& r = env.right[c1 + 1];
   LTensor v = contract_network(ctx, {l, r}, "");
   return read_scalar(ctx, v);
+}
+
+// ---------------------------------------------------------------------------- expectation
+
+namespace {
+
+std::vector<double2> to_host(Ctx& ctx, const DTensor& t) {
+  std::vector<double2> h(static_cast<size_t>(t.size()));
+  if (!h.empty())
+    PEPSB_CUDA(cudaMemcpyAsync(h.data(), t.data(), h.size() * sizeof(double2), cudaMemcpyDeviceToHost, ctx.stream));
+  ctx.sync();
+  return h;
+}
+
+DTensor upload(Ctx& ctx, const std::vector<double2>& h, const std::vector<int64_t>& shape) {
+  DTensor t = ctx.empty(shape);
+  if (!h.empty())
+    PEPSB_CUDA(cudaMemcpyAsync(t.data(), h.data(), h.size() * sizeof(double2), cudaMemcpyHostToDevice, ctx.stream));
+  ctx.sync();  // h is a host temporary
+  return t;
+}
+
+// Observable::is_hermitian (observables.cpp:41-58), tol 1e-12.
+bool is_hermitian(Ctx& ctx, const std::vector<LocalTermD>& terms) {
+  for (const auto& t : terms) {
+    const std::vector<double2> m = to_host(ctx, t.op);
+    const int64_t n = static_cast<int64_t>(std::llround(std::sqrt(static_cast<double>(m.size()))));
+    const double2 cf = make_double2(t.coeff_re, t.coeff_im);
+    for (int64_t i = 0; i < n; ++i)
+      for (int64_t j = 0; j < n; ++j) {
+        const double2 a = cmul(cf, m[i * n + j]);
+        const double2 b = cconj(cmul(cf, m[j * n + i]));
+        if (std::hypot(a.x - b.x, a.y - b.y) > 1e-12) return false;
+      }
+  }
+  return true;
+}
+
+// split_two_site (observables.cpp:284-295): SVD of op.permute{0,2,1,3} split 2|2,
+// rank by retained_rank with cap d^2, sqrt(s) on both sides; pieces (o1,i1,g),
+// (o2,i2,g).
+std::pair<DTensor, DTensor> split_two_site(Ctx& ctx, const DTensor& op) {
+  const int64_t d = op.shape[0];
+  const std::vector<double2> h = to_host(ctx, op);
+  std::vector<double2> pm(h.size());
+  for (int64_t a = 0; a < d; ++a)
+    for (int64_t b = 0; b < d; ++b)
+      for (int64_t c = 0; c < d; ++c)
+        for (int64_t e = 0; e < d; ++e) pm[((a * d + c) * d + b) * d + e] = h[((a * d + b) * d + c) * d + e];
+  SvdD sv = svd(ctx, upload(ctx, pm, {d, d, d, d}), 2);
+  const size_t g = retained_rank(sv.s, Trunc{static_cast<uint64_t>(d * d), 1e-14});
+  const int64_t k = static_cast<int64_t>(sv.s.size()), G = static_cast<int64_t>(g);
+  const std::vector<double2> u = to_host(ctx, sv.u), v = to_host(ctx, sv.v);  // u (d,d,k), v (k,d,d)
+  std::vector<double2> left(static_cast<size_t>(d * d * G)), right(static_cast<size_t>(d * d * G));
+  for (int64_t x = 0; x < d * d; ++x)
+    for (int64_t j = 0; j < G; ++j) {
+      const double w = std::sqrt(sv.s[j]);
+      left[x * G + j] = cscale(u[x * k + j], w);      // (o1, i1, g)
+      right[x * G + j] = cscale(v[j * d * d + x], w);  // (g, o2, i2) -> (o2, i2, g)
+    }
+  return {upload(ctx, left, {d, d, G}), upload(ctx, right, {d, d, G})};
+}
+
+struct TermPiecesD {
+  std::vector<InsertionPieceD> pieces;
+  int r0 = 0, r1 = 0, c0 = 0, c1 = 0;
+};
+
+// observables.cpp:302-321
+TermPiecesD term_pieces(Ctx& ctx, const LocalTermD& t) {
+  TermPiecesD out;
+  if (t.sites.size() == 1) {
+    out.pieces.push_back({t.sites[0].first, t.sites[0].second, t.op, {}});
+    out.r0 = out.r1 = t.sites[0].first;
+    out.c0 = out.c1 = t.sites[0].second;
+    return out;
+  }
+  auto lr = split_two_site(ctx, t.op);
+  out.pieces.push_back({t.sites[0].first, t.sites[0].second, lr.first, {0}});
+  out.pieces.push_back({t.sites[1].first, t.sites[1].second, lr.second, {0}});
+  out.r0 = std::min(t.sites[0].first, t.sites[1].first);
+  out.r1 = std::max(t.sites[0].first, t.sites[1].first);
+  out.c0 = std::min(t.sites[0].second, t.sites[1].second);
+  out.c1 = std::max(t.sites[0].second, t.sites[1].second);
+  if (out.r1 - out.r0 > 1)
+    throw Error(kValidationError, "term spans more than two rows; only 1- and 2-site terms are supported");
+  return out;
+}
+
+}  // namespace
+
+// observables.cpp:335-422
+ExpectResultD expectation(Ctx& ctx, const PepsStateD& s, const std::vector<LocalTermD>& terms,
+                          const ExpectOptD& opt) {
+  s.validate();
+  for (const auto& t : terms) {
+    if (t.sites.empty() || t.sites.size() > 2) throw Error(kValidationError, "terms act on one or two sites");
+    for (auto [r, c] : t.sites)
+      if (r < 0 || c < 0 || r >= s.rows || c >= s.cols)
+        throw Error(kValidationError, "site (" + std::to_string(r) + "," + std::to_string(c) + ") outside the grid");
+  }
+  if (!opt.allow_complex && !is_hermitian(ctx, terms))
+    throw Error(kValidationError, "observable is not Hermitian; request a complex expectation explicitly");
+  ExpectResultD out;
+  const uint64_t f0 = ctx.flops;
+  const int n = s.rows;
+  RowCacheD cache;
+  if (opt.use_cache) {
+    cache = build_row_cache(ctx, s, opt.contract);
+    out.full_sweeps = 2;
+    out.norm_sq = chain_scalar(ctx, cache.tops[n - 1]).first;
+  } else {
+    std::vector<BoundaryD> tops;
+    tops.push_back(two_layer_first_row(ctx, s, s));
+    for (int r = 1; r < n; ++r) tops.push_back(two_layer_apply_row(ctx, tops.back(), s, s, r, opt.contract, kTagTop));
+    out.norm_sq = chain_scalar(ctx, tops[n - 1]).first;
+  }
+  std::map<std::pair<int, int>, BandEnvD> envs;  // shared environments per band
+  double sr = 0.0, si = 0.0;
+  for (const auto& term : terms) {
+    TermPiecesD tp = term_pieces(ctx, term);
+    const BoundaryD* top = nullptr;
+    const BoundaryD* bottom = nullptr;
+    std::vector<BoundaryD> local_top, local_bot;
+    if (opt.use_cache) {
+      if (tp.r0 > 0) top = &cache.tops[tp.r0 - 1];
+      if (tp.r1 + 1 < n) bottom = &cache.bots[tp.r1 + 1];
+    } else {
+      // recompute the needed boundaries with the same structural seeds
+      if (tp.r0 > 0) {
+        local_top.push_back(two_layer_first_row(ctx, s, s));
+        for (int r = 1; r < tp.r0; ++r)
+          local_top.push_back(two_layer_apply_row(ctx, local_top.back(), s, s, r, opt.contract, kTagTop));
+        top = &local_top.back();
+      }
+      if (tp.r1 + 1 < n) {
+        PepsStateD fl = flip_vertical(ctx, s);
+        local_bot.push_back(two_layer_first_row(ctx, fl, fl));
+        for (int r = 1; r < n - 1 - tp.r1; ++r)
+          local_bot.push_back(two_layer_apply_row(ctx, local_bot.back(), fl, fl, r, opt.contract, kTagBottom));
+        bottom = &local_bot.back();
+      }
+      out.full_sweeps += 1;
+    }
+    std::pair<double, double> v;
+    if (opt.shared_environments && opt.use_cache) {
+      const auto key = std::make_pair(tp.r0, tp.r1);
+      auto it = envs.find(key);
+      if (it == envs.end()) {
+        it = envs.emplace(key, band_environment(ctx, top, s, s, tp.r0, tp.r1, bottom)).first;
+        out.band_contractions += 1;
+      }
+      v = band_splice(ctx, it->second, top, s, s, bottom, tp.pieces, tp.c0, tp.c1);
+    } else {
+      v = band_value(ctx, top, s, s, tp.r0, tp.r1, bottom, tp.pieces);
+      out.band_contractions += opt.use_cache ? 1 : 0;
+    }
+    sr += term.coeff_re * v.first - term.coeff_im * v.second;
+    si += term.coeff_re * v.second + term.coeff_im * v.first;
+  }
+  out.raw_re = sr;
+  out.raw_im = si;
+  out.cx_re = sr / out.norm_sq;
+  out.cx_im = si / out.norm_sq;
+  out.flops = ctx.flops - f0;
+  if (!opt.allow_complex) {
+    const double scale = std::max(1.0, std::hypot(out.cx_re, out.cx_im));
+    if (std::fabs(out.cx_im) > 1e-8 * scale)
+      throw Error(kNumericalError, "expectation of a Hermitian observable has imaginary part " +
+                                       std::to_string(out.cx_im));
+  }
+  out.value = out.cx_re;
+  return out;
 }
 
 }  // namespace pepsb

@@ -75,4 +75,25 @@ std::pair<double, double> band_splice(Ctx& ctx, const BandEnvD& env, const Bound
                                       const PepsStateD& ket, const BoundaryD* bottom,
                                       const std::vector<InsertionPieceD>& pieces, int c0, int c1);
 
+// observables.hpp:16-20,63-85 and observables.cpp:284-422: local terms
+// (1- or 2-site operators, outputs first), options and result of expectation.
+struct LocalTermD {
+  double coeff_re = 1.0, coeff_im = 0.0;
+  std::vector<std::pair<int, int>> sites;  // 1 or 2 (row, col)
+  DTensor op;                              // (d, d) or (d, d, d, d)
+};
+struct ExpectOptD {
+  ContractOptD contract;
+  bool use_cache = true;
+  bool shared_environments = false;
+  bool allow_complex = false;
+};
+struct ExpectResultD {
+  double value = 0.0, norm_sq = 0.0;
+  double raw_re = 0.0, raw_im = 0.0, cx_re = 0.0, cx_im = 0.0;
+  uint64_t full_sweeps = 0, band_contractions = 0, flops = 0;
+};
+ExpectResultD expectation(Ctx& ctx, const PepsStateD& s, const std::vector<LocalTermD>& terms,
+                          const ExpectOptD& opt);
+
 }  // namespace pepsb

@@ -303,3 +303,43 @@ def test_random_slice_and_building_blocks(A):
     assert np.array_equal(t.slice(1, 1, 3).numpy(), z[:, 1:3])
     assert np.array_equal(t.conj().numpy(), z.conj())
     assert np.array_equal(t.reshape(150, 7).numpy(), z.reshape(150, 7))
+
+
+@pytest.mark.parametrize("shared", [False, True], ids=["band_value", "shared_envs"])
+def test_expectation_tfim_matches_reference(A, refo, shared):
+    """expectation(state, observable, options) (observables.cpp:335-422) for the
+    TFIM Hamiltonian on a random 4x4 r=2 PEPS against the compiled reference:
+    value, norm_sq and raw_sum to 1e-8; the cache-free route agrees.  At m = 4
+    the truncated environments leave an imaginary part of 1.2e-4 and both the
+    reference and the device raise NumericalError with the same value."""
+    sites = I.random_peps(4, 4, 2, 91, scale=1 / np.sqrt(8))
+    st = A.PepsState(4, 4, 2, sites)
+    opt4 = A.ExpectationOptions(A.ContractOption.two_layer_opt(4, 13, 2, -1), True, shared, False)
+    with pytest.raises(A.PepsError, match="NumericalError: expectation of a Hermitian observable has imaginary "
+                                          "part -0.000119"):
+        A.expectation(st, A.tfim_terms(4, 4, 1.0, 3.0), opt4)
+    with pytest.raises(Exception, match="imaginary part -0.000119"):
+        refo.tfim_energy(sites, 4, 4, 1.0, 3.0, 4, 13, 2, -1, shared)
+    opt = A.ExpectationOptions(A.ContractOption.two_layer_opt(12, 13, 2, -1), True, shared, False)
+    got = A.expectation(st, A.tfim_terms(4, 4, 1.0, 3.0), opt)
+    want = refo.tfim_energy(sites, 4, 4, 1.0, 3.0, 12, 13, 2, -1, shared)
+    assert abs(got.value - want["value"]) <= 1e-8 * abs(want["value"])
+    assert abs(got.norm_sq - want["norm_sq"]) <= 1e-8 * abs(want["norm_sq"])
+    assert abs(got.raw_sum - want["raw_sum"]) <= 1e-8 * abs(want["raw_sum"])
+    assert got.full_sweeps == 2
+    nc = A.expectation(st, A.tfim_terms(4, 4, 1.0, 3.0),
+                       A.ExpectationOptions(opt.contract, False, False, False))
+    assert abs(nc.value - got.value) <= 1e-10 * abs(got.value)
+
+
+def test_expectation_rejects_non_hermitian(A):
+    sites = I.random_peps(3, 3, 2, 5)
+    st = A.PepsState(3, 3, 2, sites)
+    y_like = np.array([[0, 1], [0, 0]], dtype=complex)  # not Hermitian
+    terms = [A.LocalTerm(1.0, [(1, 1)], y_like)]
+    opt = A.ExpectationOptions(A.ContractOption.two_layer_opt(4, 1, 2, -1))
+    with pytest.raises(A.PepsError, match="ValidationError"):
+        A.expectation(st, terms, opt)
+    opt.allow_complex = True
+    r = A.expectation(st, terms, opt)
+    assert np.isfinite(r.complex_value.real) and r.norm_sq > 0
