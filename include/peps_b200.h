@@ -180,6 +180,8 @@ int pepsb_einsumsvd(pepsb_ctx* ctx, int n, pepsb_tensor* const* ts, const char* 
 /* ---------------------------------------------------------------- PEPS (state.hpp:33-61) */
 int pepsb_state_create(pepsb_ctx* ctx, int rows, int cols, int d, pepsb_tensor* const* sites, pepsb_state** out);
 int pepsb_state_site(const pepsb_state* s, int row, int col, pepsb_tensor** out);
+/* grid size and physical dimension of a state */
+int pepsb_state_dims(const pepsb_state* s, int* rows, int* cols, int* d);
 void pepsb_state_free(pepsb_state* s);
 
 /* TwoLayerBoundary (contraction.hpp:77-80) */
@@ -222,6 +224,28 @@ int pepsb_band_value(pepsb_ctx* ctx, const pepsb_boundary* top, const pepsb_stat
                      int r1, const pepsb_boundary* bottom, int npieces, const int* rc, pepsb_tensor* const* ops,
                      const int* nbonds, const int* bond_ids, double* re, double* im);
 void pepsb_band_env_free(pepsb_band_env* e);
+
+/* PEPS container (save_peps / load_peps, state.hpp, state.cpp:240-299): the
+ * reference's binary format ("PEPS2D01", rows, cols, d, axis tag "pudlr", per
+ * site order + extents + complex128 data), so the device path reads and
+ * writes the reference's own files. */
+int pepsb_save_peps(pepsb_ctx* ctx, const pepsb_state* s, const char* path);
+int pepsb_load_peps(pepsb_ctx* ctx, const char* path, pepsb_state** out);
+
+/* ---------------------------------------------------------------- one-layer boundary MPS */
+/* approx_apply_mpo (mps.hpp / mps.cpp:44-84): zip-up of an MPO (sites (p, d,
+ * left, right)) into an MPS (sites (phys, left, right)) of length n with one
+ * einsumsvd per site (network {v(adso), s(pst), o(peoq)}, rows "ad", cols
+ * "etq", seed derive_seed(seed_base, i)); out_sites receives n new tensors. */
+int pepsb_approx_apply_mpo(pepsb_ctx* ctx, int n, pepsb_tensor* const* mps_sites, pepsb_tensor* const* mpo_sites,
+                           const pepsb_trunc* policy, int strategy, int absorb, const pepsb_rsvd* rsvd,
+                           uint64_t seed_base, pepsb_tensor** out_sites);
+/* contract_one_layer (contraction.hpp:67-75, contraction.cpp:178-252) on an
+ * order-4 grid (up, left, down, right), row-major sites: family 0 exact
+ * (contract_exact with the element budget; ResourceError above it), 1 bmps,
+ * 2 ibmps (contract_boundary: seeds derive_seed(seed, 0x10, r)). */
+int pepsb_contract_one_layer(pepsb_ctx* ctx, int rows, int cols, pepsb_tensor* const* sites, int family,
+                             const pepsb_contract_opt* opt, uint64_t memory_budget, double* re, double* im);
 
 /* expectation (observables.hpp:87-100, observables.cpp:335-422): sum of local
  * terms over <psi|psi>.  Term i: coefficient (coeff[2i], coeff[2i+1]),

@@ -232,6 +232,16 @@ def contract_two_layer(sites, rows, cols, m, seed, power_iters=2, oversample=-1,
     return complex(dd[0], dd[1]), dict(seconds=float(dd[2]), flops=float(dd[3]), peak=float(dd[4]))
 
 
+def save_peps(sites, rows, cols, path, d=2):
+    tl, a = _state_args(sites, rows, cols, d)
+    _bag(_fn("ref_save_peps")(*a, str(path).encode()))
+
+
+def load_peps(path):
+    t, dd = _bag(_fn("ref_load_peps")(str(path).encode()))
+    return t, int(dd[0]), int(dd[1]), int(dd[2])
+
+
 def contract_one_layer(sites, rows, cols, family, m=0, seed=0, power_iters=2, oversample=-1, canonicalize=True):
     """contract_one_layer on an order-4 grid; family 0 exact, 1 bmps, 2 ibmps."""
     tl = _TList(sites)

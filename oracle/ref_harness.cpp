@@ -362,6 +362,23 @@ Bag* ref_contract_two_layer(int rows, int cols, int d, const int* ndims, const i
   });
 }
 
+// save_peps / load_peps (state.cpp:240-299) through the reference's own code.
+Bag* ref_save_peps(int rows, int cols, int d, const int* ndims, const int64_t* shapes, const double* const* datas,
+                   const char* path) {
+  return guarded([&](Bag& b) {
+    save_peps(make_state(rows, cols, d, ndims, shapes, datas), path);
+    (void)b;
+  });
+}
+
+Bag* ref_load_peps(const char* path) {
+  return guarded([&](Bag& b) {
+    PepsState s = load_peps(path);
+    for (const auto& t : s.sites()) b.tensors.push_back(t);
+    b.doubles = {static_cast<double>(s.rows()), static_cast<double>(s.cols()), static_cast<double>(s.phys_dim())};
+  });
+}
+
 // contract_one_layer (contraction.cpp:205-252) on an order-4 grid (up, left,
 // down, right): family 0 exact (contract_exact), 1 bmps, 2 ibmps.
 Bag* ref_contract_one_layer(int rows, int cols, const int* ndims, const int64_t* shapes,

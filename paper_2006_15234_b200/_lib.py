@@ -125,6 +125,13 @@ _SIGS = {
                                    C.POINTER(_VP), C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_double),
                                    C.POINTER(C.c_double)]),
     "pepsb_band_env_free": (None, [_VP]),
+    "pepsb_save_peps": (C.c_int, [_VP, _VP, C.c_char_p]),
+    "pepsb_state_dims": (C.c_int, [_VP, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int)]),
+    "pepsb_load_peps": (C.c_int, [_VP, C.c_char_p, C.POINTER(_VP)]),
+    "pepsb_approx_apply_mpo": (C.c_int, [_VP, C.c_int, C.POINTER(_VP), C.POINTER(_VP), C.POINTER(Trunc), C.c_int,
+                                         C.c_int, C.POINTER(Rsvd), C.c_uint64, C.POINTER(_VP)]),
+    "pepsb_contract_one_layer": (C.c_int, [_VP, C.c_int, C.c_int, C.POINTER(_VP), C.c_int, C.POINTER(ContractOpt),
+                                           C.c_uint64, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
     "pepsb_expectation": (C.c_int, [_VP, _VP, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_int),
                                     C.POINTER(C.c_int), C.POINTER(_VP), C.POINTER(ExpectationOpt),
                                     C.POINTER(ExpectationResult)]),

@@ -603,6 +603,75 @@ def band_value(top, bra: PepsState, ket: PepsState, r0: int, r1: int, bottom, pi
     return complex(re.value, im.value)
 
 
+def save_peps(s: PepsState, path: str) -> None:
+    """save_peps (state.cpp:256-272): the reference's binary PEPS container."""
+    check(lib().pepsb_save_peps(s.ctx.h, s.h, str(path).encode()))
+
+
+def load_peps(path: str, ctx: Optional[Context] = None) -> PepsState:
+    """load_peps (state.cpp:273-299): reads the reference's container onto the device."""
+    ctx = ctx or default_context()
+    h = _VP()
+    check(lib().pepsb_load_peps(ctx.h, str(path).encode(), C.byref(h)))
+    rows, cols, d = C.c_int(), C.c_int(), C.c_int()
+    check(lib().pepsb_state_dims(h, C.byref(rows), C.byref(cols), C.byref(d)))
+    out = PepsState.__new__(PepsState)
+    out.ctx, out.rows, out.cols, out.d, out.h = ctx, rows.value, cols.value, d.value, h
+    out.sites = []
+    for r in range(out.rows):
+        for c in range(out.cols):
+            t = _VP()
+            check(lib().pepsb_state_site(h, r, c, C.byref(t)))
+            out.sites.append(DeviceTensor(t, ctx))
+    return out
+
+
+class ContractFamily(IntEnum):
+    """contraction.hpp:14 (one-layer families)."""
+    exact = 0
+    bmps = 1
+    ibmps = 2
+
+
+def bmps_opt(m: int, seed: int = 0) -> ContractOption:
+    """ContractOption::bmps_opt (contraction.cpp:36-43): exact SVD truncation."""
+    return ContractOption(TruncationPolicy(m, 1e-14), SvdStrategy.exact, RsvdConfig(), True, seed)
+
+
+def ibmps_opt(m: int, seed: int = 0, power_iters: int = 2, oversample: int = -1) -> ContractOption:
+    """ContractOption::ibmps_opt (contraction.cpp:45-53): implicit randomized SVD."""
+    return ContractOption(TruncationPolicy(m, 1e-14), SvdStrategy.implicit_rsvd, RsvdConfig(power_iters, oversample, 0),
+                          True, seed)
+
+
+def contract_one_layer(sites: Sequence, rows: int, cols: int, family: ContractFamily,
+                       opt: Optional[ContractOption] = None, memory_budget: int = 1 << 27,
+                       ctx: Optional[Context] = None) -> complex:
+    """contract_one_layer (contraction.cpp:178-252) on an order-4 grid (up, left, down, right)."""
+    ctx = ctx or default_context()
+    dts, arr = _handles(sites, ctx)
+    opt = opt or ContractOption()
+    re, im = C.c_double(), C.c_double()
+    o = opt.c()
+    check(lib().pepsb_contract_one_layer(ctx.h, int(rows), int(cols), arr, int(family), C.byref(o),
+                                         C.c_uint64(memory_budget), C.byref(re), C.byref(im)))
+    return complex(re.value, im.value)
+
+
+def approx_apply_mpo(mps: Sequence, mpo: Sequence, policy: TruncationPolicy, strategy: SvdStrategy, absorb: Absorb,
+                     rsvd: RsvdConfig, seed_base: int, ctx: Optional[Context] = None) -> List[DeviceTensor]:
+    """approx_apply_mpo (mps.cpp:44-84): MPS sites (phys, left, right), MPO sites (p, d, left, right)."""
+    ctx = ctx or default_context()
+    n = len(mps)
+    ds, sa = _handles(mps, ctx)
+    do, oa = _handles(mpo, ctx)
+    out = (_VP * n)()
+    pol, rs = policy.c(), rsvd.c()
+    check(lib().pepsb_approx_apply_mpo(ctx.h, n, sa, oa, C.byref(pol), int(strategy), int(absorb), C.byref(rs),
+                                       C.c_uint64(seed_base & 0xFFFFFFFFFFFFFFFF), out))
+    return [DeviceTensor(out[i], ctx) for i in range(n)]
+
+
 @dataclass
 class LocalTerm:
     """observables.hpp:16-20: coeff * op on one or two sites; 2-site op (d,d,d,d) outputs first."""

@@ -1,4 +1,6 @@
 #include <algorithm>
+#include <cstdio>
+#include <memory>
 // extern "C" boundary (include/peps_b200.h): POD in, handles out, status codes.
 #include <cstring>
 #include <exception>
@@ -8,8 +10,8 @@
 #include "ite.h"
 #include "peps.h"
 #include "smalldense.cuh"
-#include "zgemm.cuh"
 #include "tensor_ops.cuh"
+#include "zgemm.cuh"
 
 using namespace pepsb;
 
@@ -601,6 +603,103 @@ int pepsb_state_create(pepsb_ctx* c, int rows, int cols, int d, pepsb_tensor* co
   });
 }
 
+// ---- PEPS container (save_peps / load_peps, state.cpp:240-299): magic
+// "PEPS2D01", u64 rows / cols / d, u64 tag length + axis tag "pudlr", per site
+// u64 order, u64 extents, raw complex128 data (host byte order).
+namespace {
+constexpr char kPepsMagic[8] = {'P', 'E', 'P', 'S', '2', 'D', '0', '1'};
+constexpr char kPepsTag[] = "pudlr";
+}  // namespace
+
+int pepsb_save_peps(pepsb_ctx* c, const pepsb_state* s, const char* path) {
+  return guard([&] {
+    need(c, "ctx");
+    need(s, "state");
+    need(path, "path");
+    FILE* f = fopen(path, "wb");
+    if (!f) throw Error(kValidationError, std::string("cannot open '") + path + "' for writing");
+    bool ok = true;
+    auto u64 = [&](uint64_t v) { ok = ok && fwrite(&v, sizeof(v), 1, f) == 1; };
+    ok = fwrite(kPepsMagic, 1, 8, f) == 8;
+    u64(static_cast<uint64_t>(s->s.rows));
+    u64(static_cast<uint64_t>(s->s.cols));
+    u64(static_cast<uint64_t>(s->s.d));
+    u64(sizeof(kPepsTag) - 1);
+    ok = ok && fwrite(kPepsTag, 1, sizeof(kPepsTag) - 1, f) == sizeof(kPepsTag) - 1;
+    for (const DTensor& t : s->s.sites) {
+      u64(t.shape.size());
+      for (auto e : t.shape) u64(static_cast<uint64_t>(e));
+      std::vector<double2> h(static_cast<size_t>(t.size()));
+      if (!h.empty()) {
+        PEPSB_CUDA(cudaMemcpyAsync(h.data(), t.data(), h.size() * sizeof(double2), cudaMemcpyDeviceToHost,
+                                   c->ctx->stream));
+        c->ctx->sync();
+        ok = ok && fwrite(h.data(), sizeof(double2), h.size(), f) == h.size();
+      }
+    }
+    ok = (fclose(f) == 0) && ok;
+    if (!ok) throw Error(kValidationError, std::string("write failed for '") + path + "'");
+  });
+}
+
+int pepsb_load_peps(pepsb_ctx* c, const char* path, pepsb_state** out) {
+  return guard([&] {
+    need(c, "ctx");
+    need(path, "path");
+    FILE* f = fopen(path, "rb");
+    if (!f) throw Error(kValidationError, std::string("cannot open '") + path + "' for reading");
+    std::unique_ptr<FILE, int (*)(FILE*)> guard_f(f, fclose);
+    char magic[8];
+    if (fread(magic, 1, 8, f) != 8 || std::memcmp(magic, kPepsMagic, 8) != 0)
+      throw Error(kValidationError, std::string("'") + path + "' is not a PEPS container");
+    bool ok = true;
+    auto u64 = [&]() {
+      uint64_t v = 0;
+      ok = ok && fread(&v, sizeof(v), 1, f) == 1;
+      return v;
+    };
+    const uint64_t rows = u64(), cols = u64(), d = u64(), tl = u64();
+    if (!ok || tl > 64) throw Error(kValidationError, std::string("truncated PEPS container '") + path + "'");
+    std::string tag(tl, '\0');
+    if (tl && fread(tag.data(), 1, tl, f) != tl) ok = false;
+    if (tag != kPepsTag) throw Error(kValidationError, "unknown axis convention tag '" + tag + "'");
+    PepsStateD st;
+    st.rows = static_cast<int>(rows);
+    st.cols = static_cast<int>(cols);
+    st.d = static_cast<int>(d);
+    for (uint64_t i = 0; ok && i < rows * cols; ++i) {
+      const uint64_t order = u64();
+      if (!ok || order > kMaxModes) break;
+      std::vector<int64_t> shape(order);
+      for (auto& e : shape) e = static_cast<int64_t>(u64());
+      if (!ok) break;
+      DTensor t = c->ctx->empty(shape);
+      std::vector<double2> h(static_cast<size_t>(t.size()));
+      if (!h.empty() && fread(h.data(), sizeof(double2), h.size(), f) != h.size()) ok = false;
+      if (!ok) break;
+      if (!h.empty()) {
+        PEPSB_CUDA(cudaMemcpyAsync(t.data(), h.data(), h.size() * sizeof(double2), cudaMemcpyHostToDevice,
+                                   c->ctx->stream));
+        mark_real(*c->ctx, t);  // (syncs: h is a host temporary)
+      }
+      st.sites.push_back(t);
+    }
+    if (!ok || st.sites.size() != rows * cols)
+      throw Error(kValidationError, std::string("truncated PEPS container '") + path + "'");
+    st.validate();
+    *out = new pepsb_state{st};
+  });
+}
+
+int pepsb_state_dims(const pepsb_state* s, int* rows, int* cols, int* d) {
+  return guard([&] {
+    need(s, "state");
+    *rows = s->s.rows;
+    *cols = s->s.cols;
+    *d = s->s.d;
+  });
+}
+
 int pepsb_state_site(const pepsb_state* s, int row, int col, pepsb_tensor** out) {
   return guard([&] {
     need(s, "state");
@@ -756,6 +855,51 @@ int pepsb_band_value(pepsb_ctx* c, const pepsb_boundary* top, const pepsb_state*
 }
 
 void pepsb_band_env_free(pepsb_band_env* e) { delete e; }
+
+int pepsb_approx_apply_mpo(pepsb_ctx* c, int n, pepsb_tensor* const* mps_sites, pepsb_tensor* const* mpo_sites,
+                           const pepsb_trunc* policy, int strategy, int absorb, const pepsb_rsvd* rsvd,
+                           uint64_t seed_base, pepsb_tensor** out_sites) {
+  return guard([&] {
+    need(c, "ctx");
+    need(policy, "policy");
+    need(rsvd, "rsvd");
+    if (n < 1) throw Error(kShapeError, "empty MPS");
+    MpsD s;
+    MpoD o;
+    for (int i = 0; i < n; ++i) {
+      need(mps_sites[i], "MPS site");
+      need(mpo_sites[i], "MPO site");
+      s.sites.push_back(mps_sites[i]->t);
+      o.sites.push_back(mpo_sites[i]->t);
+    }
+    ApplyOptD ao;
+    ao.policy = Trunc{policy->max_rank, policy->rel_cutoff};
+    ao.strategy = strategy;
+    ao.absorb = absorb;
+    ao.rsvd = Rsvd{rsvd->power_iters, rsvd->oversample, rsvd->seed};
+    ao.seed_base = seed_base;
+    MpsD out = approx_apply_mpo(*c->ctx, s, o, ao);
+    for (int i = 0; i < n; ++i) out_sites[i] = wrap(out.sites[i]);
+  });
+}
+
+int pepsb_contract_one_layer(pepsb_ctx* c, int rows, int cols, pepsb_tensor* const* sites, int family,
+                             const pepsb_contract_opt* opt, uint64_t memory_budget, double* re, double* im) {
+  return guard([&] {
+    need(c, "ctx");
+    need(opt, "options");
+    GridD g;
+    g.rows = rows;
+    g.cols = cols;
+    for (int i = 0; i < rows * cols; ++i) {
+      need(sites[i], "grid site");
+      g.sites.push_back(sites[i]->t);
+    }
+    auto v = contract_one_layer(*c->ctx, g, family, opt_of(opt), memory_budget);
+    *re = v.first;
+    *im = v.second;
+  });
+}
 
 int pepsb_expectation(pepsb_ctx* c, const pepsb_state* s, int nterms, const double* coeff, const int* nsites,
                       const int* rc, pepsb_tensor* const* ops, const pepsb_expectation_opt* opt,

@@ -609,4 +609,169 @@ ExpectResultD expectation(Ctx& ctx, const PepsStateD& s, const std::vector<Local
   return out;
 }
 
+// ---------------------------------------------------------------------------- one-layer boundary MPS
+
+namespace {
+
+DTensor contract_to(Ctx& ctx, const std::vector<LTensor>& leaves, const std::string& out) {
+  LTensor t = contract_network(ctx, leaves, out);
+  return materialize(ctx, t, t.labels);
+}
+
+void check_mpo_pair(const MpsD& s, const MpoD& o) {
+  if (s.sites.empty()) throw Error(kShapeError, "empty MPS");
+  if (o.sites.size() != s.sites.size()) throw Error(kShapeError, "MPS/MPO length mismatch");
+  for (size_t i = 0; i < s.sites.size(); ++i) {
+    if (s.sites[i].shape.size() != 3 || o.sites[i].shape.size() != 4)
+      throw Error(kShapeError, "MPS sites are (phys, left, right), MPO sites (p, d, left, right)");
+    if (s.sites[i].shape[0] != o.sites[i].shape[0])
+      throw Error(kShapeError, "physical extent mismatch at site " + std::to_string(i));
+  }
+}
+
+}  // namespace
+
+void GridD::validate() const {
+  if (rows <= 0 || cols <= 0) throw Error(kValidationError, "grid must be non-empty");
+  if (static_cast<int>(sites.size()) != rows * cols) throw Error(kShapeError, "one-layer site count mismatch");
+  for (int r = 0; r < rows; ++r)
+    for (int c = 0; c < cols; ++c) {
+      const auto& t = site(r, c).shape;
+      if (t.size() != 4)
+        throw Error(kShapeError, "one-layer sites must be order 4 (up, left, down, right); physical indices must be "
+                                 "projected or merged first");
+      if (r == 0 && t[0] != 1) throw Error(kShapeError, "top boundary bond must be 1");
+      if (c == 0 && t[1] != 1) throw Error(kShapeError, "left boundary bond must be 1");
+      if (r == rows - 1 && t[2] != 1) throw Error(kShapeError, "bottom boundary bond must be 1");
+      if (c == cols - 1 && t[3] != 1) throw Error(kShapeError, "right boundary bond must be 1");
+      if (r + 1 < rows && t[2] != site(r + 1, c).shape[0])
+        throw Error(kShapeError, "vertical bond mismatch in one-layer grid");
+      if (c + 1 < cols && t[3] != site(r, c + 1).shape[1])
+        throw Error(kShapeError, "horizontal bond mismatch in one-layer grid");
+    }
+}
+
+MpsD approx_apply_mpo(Ctx& ctx, const MpsD& s, const MpoD& o, const ApplyOptD& opt) {
+  check_mpo_pair(s, o);
+  const size_t n = s.sites.size();
+  MpsD out;
+  out.sites.resize(n);
+  // v1 = sum_p s1(p, l, r) o1(p, d, L, R), (l, L) merged into a
+  const DTensor& s0 = s.sites[0];
+  const DTensor& o0 = o.sites[0];
+  DTensor v = contract_to(ctx, {as_labelled(s0, "plr"), as_labelled(o0, "pdLR")}, "lLdrR");
+  v = reshape(v, {s0.shape[1] * o0.shape[2], o0.shape[1], s0.shape[2], o0.shape[3]});
+  if (n == 1) {
+    DTensor t = contract_to(ctx, {as_labelled(v, "adso")}, "daso");
+    out.sites[0] = reshape(t, {v.shape[1], v.shape[0], v.shape[2] * v.shape[3]});
+    return out;
+  }
+  for (size_t i = 1; i < n; ++i) {
+    ImplicitOp net({v, s.sites[i], o.sites[i]}, {"adso", "pst", "peoq"}, "ad", "etq");
+    Rsvd cfg = opt.rsvd;
+    cfg.seed = derive_seed1(opt.seed_base, static_cast<uint64_t>(i));
+    // t1 (a, d, rho) written directly as (d, a, rho)
+    EinsumsvdResultD split = einsumsvd(ctx, net, opt.policy, opt.strategy, opt.absorb, cfg, {1, 0, 2});
+    out.sites[i - 1] = split.t1;
+    v = split.t2;  // (rho, e, t, q)
+  }
+  DTensor t = contract_to(ctx, {as_labelled(v, "adso")}, "daso");
+  out.sites[n - 1] = reshape(t, {v.shape[1], v.shape[0], v.shape[2] * v.shape[3]});
+  return out;
+}
+
+MpsD exact_apply_mpo(Ctx& ctx, const MpsD& s, const MpoD& o) {
+  check_mpo_pair(s, o);
+  MpsD out;
+  for (size_t i = 0; i < s.sites.size(); ++i) {
+    const DTensor& a = s.sites[i];
+    const DTensor& b = o.sites[i];
+    DTensor t = contract_to(ctx, {as_labelled(a, "plr"), as_labelled(b, "pdLR")}, "dlLrR");
+    out.sites.push_back(reshape(t, {b.shape[1], a.shape[1] * b.shape[2], a.shape[2] * b.shape[3]}));
+  }
+  return out;
+}
+
+std::pair<double, double> mps_glue(Ctx& ctx, const MpsD& top, const MpsD& bottom) {
+  if (top.sites.size() != bottom.sites.size()) throw Error(kShapeError, "MPS length mismatch in glue");
+  LTensor l = scalar_one(ctx);
+  l.labels = "ab";
+  l.ext = {1, 1};
+  l.str = {1, 1};
+  for (size_t i = 0; i < top.sites.size(); ++i) {
+    LTensor t = contract_network(ctx, {l, as_labelled(top.sites[i], "pac"), as_labelled(bottom.sites[i], "pbd")},
+                                 "cd");
+    l = t;
+    l.labels = "ab";
+  }
+  return read_scalar(ctx, l);
+}
+
+std::pair<double, double> contract_one_layer(Ctx& ctx, const GridD& g, int family, const ContractOptD& opt,
+                                             uint64_t memory_budget) {
+  g.validate();
+  // (u, l, d, r) -> (u*d [phys], l, r)  (contraction.cpp:136-146)
+  auto as_mps = [&](int r) {
+    MpsD m;
+    for (int c = 0; c < g.cols; ++c) {
+      const DTensor& t = g.site(r, c);
+      DTensor p = contract_to(ctx, {as_labelled(t, "uldr")}, "udlr");
+      m.sites.push_back(reshape(p, {t.shape[0] * t.shape[2], t.shape[1], t.shape[3]}));
+    }
+    return m;
+  };
+  // (u, l, d, r) -> (u, d, l, r); from below (d, u, l, r)  (contraction.cpp:148-158)
+  auto as_mpo = [&](int r, bool from_below) {
+    MpoD m;
+    for (int c = 0; c < g.cols; ++c)
+      m.sites.push_back(contract_to(ctx, {as_labelled(g.site(r, c), "uldr")}, from_below ? "dulr" : "udlr"));
+    return m;
+  };
+  auto budget = [&](uint64_t el, const char* what) {
+    if (el > memory_budget)
+      throw Error(kResourceError, std::string(what) + " needs " + std::to_string(el) + " elements, budget is " +
+                                      std::to_string(memory_budget));
+  };
+  auto apply_budget = [&](const MpsD& s, const MpoD& o) {
+    for (size_t c = 0; c < s.sites.size(); ++c)
+      budget(static_cast<uint64_t>(o.sites[c].shape[1] * s.sites[c].shape[1] * o.sites[c].shape[2] *
+                                   s.sites[c].shape[2] * o.sites[c].shape[3]),
+             "contract_exact");
+  };
+  const int n = g.rows;
+  if (family == kFamilyExact) {  // contraction.cpp:178-201
+    if (n == 1) return chain_scalar(ctx, BoundaryD{as_mps(0).sites, {}});
+    const int half = n / 2;
+    MpsD top = as_mps(0);
+    for (int r = 1; r < half; ++r) {
+      MpoD o = as_mpo(r, false);
+      apply_budget(top, o);
+      top = exact_apply_mpo(ctx, top, o);
+    }
+    MpsD bottom = as_mps(n - 1);
+    for (int r = n - 1; r-- > half;) {
+      MpoD o = as_mpo(r, true);
+      apply_budget(bottom, o);
+      bottom = exact_apply_mpo(ctx, bottom, o);
+    }
+    for (int c = 0; c < g.cols; ++c)
+      budget(static_cast<uint64_t>(top.sites[c].shape[0] * top.sites[c].shape[2] * bottom.sites[c].shape[2]),
+             "contract_exact");
+    return mps_glue(ctx, top, bottom);
+  }
+  if (family != kFamilyBmps && family != kFamilyIbmps) throw Error(kValidationError, "unknown one-layer family");
+  MpsD s = as_mps(0);  // contraction.cpp:205-221
+  for (int r = 1; r < n; ++r) {
+    ApplyOptD ao;
+    ao.policy = opt.trunc;
+    if (ao.policy.max_rank == 0) ao.policy.max_rank = UINT64_MAX;
+    ao.strategy = opt.strategy;
+    ao.rsvd = opt.rsvd;
+    ao.absorb = opt.canonicalize ? (r % 2 ? kRight : kLeft) : kSplit;
+    ao.seed_base = derive_seed1(derive_seed1(opt.seed, 0x10), static_cast<uint64_t>(r));
+    s = approx_apply_mpo(ctx, s, as_mpo(r, false), ao);
+  }
+  return chain_scalar(ctx, BoundaryD{s.sites, {}});
+}
+
 }  // namespace pepsb

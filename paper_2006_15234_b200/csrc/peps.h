@@ -75,6 +75,41 @@ std::pair<double, double> band_splice(Ctx& ctx, const BandEnvD& env, const Bound
                                       const PepsStateD& ket, const BoundaryD* bottom,
                                       const std::vector<InsertionPieceD>& pieces, int c0, int c1);
 
+// ---- one-layer boundary MPS (mps.hpp / contraction.hpp:47-75)
+struct MpsD {  // sites (phys, left, right)
+  std::vector<DTensor> sites;
+};
+struct MpoD {  // sites (p = input phys, d = output phys, left, right)
+  std::vector<DTensor> sites;
+};
+struct ApplyOptD {  // mps.hpp ApplyOption
+  Trunc policy{0, 1e-14};
+  int strategy = kImplicitRsvd;
+  int absorb = kSplit;
+  Rsvd rsvd;
+  uint64_t seed_base = 0;
+};
+// mps.cpp:44-84 (zip-up: einsumsvd of {v(adso), s(pst), o(peoq)} rows "ad" cols "etq")
+MpsD approx_apply_mpo(Ctx& ctx, const MpsD& s, const MpoD& o, const ApplyOptD& opt);
+// mps.cpp:86-100
+MpsD exact_apply_mpo(Ctx& ctx, const MpsD& s, const MpoD& o);
+// mps.cpp:121-128
+std::pair<double, double> mps_glue(Ctx& ctx, const MpsD& top, const MpsD& bottom);
+// contraction.cpp:77-99: order-4 grid (up, left, down, right), edge bonds 1
+struct GridD {
+  int rows = 0, cols = 0;
+  std::vector<DTensor> sites;
+  const DTensor& site(int r, int c) const { return sites[static_cast<size_t>(r) * cols + c]; }
+  void validate() const;
+};
+enum Family { kFamilyExact = 0, kFamilyBmps = 1, kFamilyIbmps = 2 };
+// contraction.cpp:178-252: contract_exact (untruncated absorption from both ends
+// + zipper, ResourceError above the element budget) or contract_boundary
+// (approx_apply_mpo per row, seeds derive_seed(seed, 0x10, r), absorb by row
+// parity) for the BMPS / IBMPS families.
+std::pair<double, double> contract_one_layer(Ctx& ctx, const GridD& g, int family, const ContractOptD& opt,
+                                             uint64_t memory_budget);
+
 // observables.hpp:16-20,63-85 and observables.cpp:284-422: local terms
 // (1- or 2-site operators, outputs first), options and result of expectation.
 struct LocalTermD {

@@ -343,3 +343,57 @@ def test_expectation_rejects_non_hermitian(A):
     opt.allow_complex = True
     r = A.expectation(st, terms, opt)
     assert np.isfinite(r.complex_value.real) and r.norm_sq > 0
+
+
+def _grid(rows, cols, bond, seed):
+    return [O.random_tensor((1 if r == 0 else bond, 1 if c == 0 else bond, 1 if r == rows - 1 else bond,
+                             1 if c == cols - 1 else bond), O.derive_seed(seed, r, c))
+            for r in range(rows) for c in range(cols)]
+
+
+@pytest.mark.parametrize("rows,cols,bond,m", [(4, 4, 3, 4), (5, 6, 3, 6), (3, 5, 2, 3)])
+def test_one_layer_contraction_matches_reference(A, refo, rows, cols, bond, m):
+    """One-layer grid contraction (contraction.cpp:178-252,
+    mps.cpp:44-128): exact (two-sided absorption + zipper), BMPS (exact SVD
+    truncation) and IBMPS (implicit rSVD zip-up) against the compiled
+    reference on the same grid and seeds."""
+    g = _grid(rows, cols, bond, 17 + bond)
+    ex = A.contract_one_layer(g, rows, cols, A.ContractFamily.exact)
+    want = refo.contract_one_layer(g, rows, cols, 0)
+    assert abs(ex - want) <= 1e-10 * abs(want)
+    got = A.contract_one_layer(g, rows, cols, A.ContractFamily.bmps, A.bmps_opt(m, 3))
+    want = refo.contract_one_layer(g, rows, cols, 1, m, 3)
+    assert abs(got - want) <= 1e-8 * abs(want), (got, want)
+    got = A.contract_one_layer(g, rows, cols, A.ContractFamily.ibmps, A.ibmps_opt(m, 3, 2))
+    want = refo.contract_one_layer(g, rows, cols, 2, m, 3, 2)
+    assert abs(got - want) <= 1e-8 * abs(want), (got, want)
+
+
+def test_one_layer_exact_budget_and_ibmps_limit(A):
+    g = _grid(4, 4, 3, 5)
+    with pytest.raises(A.PepsError, match="ResourceError"):
+        A.contract_one_layer(g, 4, 4, A.ContractFamily.exact, memory_budget=100)
+    ex = A.contract_one_layer(g, 4, 4, A.ContractFamily.exact)
+    big = A.contract_one_layer(g, 4, 4, A.ContractFamily.ibmps, A.ibmps_opt(81, 1, 2))  # m >= exact bond
+    assert abs(big - ex) <= 1e-9 * abs(ex)
+
+
+def test_peps_container_interchange_with_reference(A, refo, tmp_path):
+    """The device reads the reference's PEPS files and the reference reads the
+    device's (state.cpp:240-299 format), bit for bit; bad files are rejected."""
+    sites = I.random_peps(3, 4, 3, 12)
+    refo.save_peps(sites, 3, 4, tmp_path / "ref.peps")
+    st = A.load_peps(tmp_path / "ref.peps")
+    assert (st.rows, st.cols, st.d) == (3, 4, 2)
+    for a, b in zip(st.sites, sites):
+        assert np.array_equal(a.numpy(), b)
+    A.save_peps(st, tmp_path / "dev.peps")
+    assert (tmp_path / "dev.peps").read_bytes() == (tmp_path / "ref.peps").read_bytes()
+    back, rows, cols, d = refo.load_peps(tmp_path / "dev.peps")
+    assert all(np.array_equal(a, b) for a, b in zip(back, sites))
+    (tmp_path / "bad.peps").write_bytes(b"NOTPEPS!" + bytes(40))
+    with pytest.raises(A.PepsError, match="ValidationError"):
+        A.load_peps(tmp_path / "bad.peps")
+    (tmp_path / "short.peps").write_bytes((tmp_path / "ref.peps").read_bytes()[:200])
+    with pytest.raises(A.PepsError, match="truncated"):
+        A.load_peps(tmp_path / "short.peps")

@@ -78,3 +78,25 @@ def test_oracle_restatement_vs_live_reference(refo):
     a = O.contract_two_layer(c["sites"], 5, 5, 6, 9, 2, -1)
     b, _ = refo.contract_two_layer(c["sites"], 5, 5, 6, 9, 2, -1)
     assert abs(a - b) / abs(b) < 1e-10
+
+
+def test_reference_one_layer_families_consistent(refo):
+    """The compiled reference's one-layer families agree when the boundary bond
+    is not truncated (pins the harness entry used by the GPU parity tests)."""
+    from oracle import peps_oracle as O
+    g = [O.random_tensor((1 if r == 0 else 2, 1 if c == 0 else 2, 1 if r == 2 else 2, 1 if c == 2 else 2),
+                         O.derive_seed(9, r, c)) for r in range(3) for c in range(3)]
+    ex = refo.contract_one_layer(g, 3, 3, 0)
+    for fam in (1, 2):
+        v = refo.contract_one_layer(g, 3, 3, fam, 16, 1)
+        assert abs(v - ex) <= 1e-10 * abs(ex)
+
+
+def test_reference_peps_container_round_trip(refo, tmp_path):
+    """save_peps / load_peps of the compiled reference (state.cpp:240-299)."""
+    from paper_2006_15234_b200 import inputs as I
+    sites = I.random_peps(3, 2, 2, 4)
+    refo.save_peps(sites, 3, 2, tmp_path / "s.peps")
+    back, rows, cols, d = refo.load_peps(tmp_path / "s.peps")
+    assert (rows, cols, d) == (3, 2, 2)
+    assert all(np.array_equal(a, b) for a, b in zip(sites, back))
