@@ -304,6 +304,17 @@ def ite_tfim(sites, rows, cols, J, h, tau, steps, rank, d=2):
     return t, float(dd[0])
 
 
+def run_ite(rows, cols, J, h, tau, steps, evolution_rank, contraction_rank, rsvd_iters=1, energy_every=1,
+            initial="neel", seed=0):
+    """run_ite (drivers.cpp:75-98), TFIM in colour order: ([(step, energy)], final sites)."""
+    t, dd = _bag(_fn("ref_run_ite")(int(rows), int(cols), C.c_double(J), C.c_double(h), C.c_double(tau),
+                                    int(steps), C.c_uint64(evolution_rank), C.c_uint64(contraction_rank),
+                                    int(rsvd_iters), int(energy_every), int(initial == "neel"),
+                                    C.c_uint64(seed)))
+    e = [(int(dd[2 * i]), float(dd[2 * i + 1])) for i in range(len(dd) // 2)]
+    return e, t
+
+
 def plus_state(rows, cols):
     t, _ = _bag(_fn("ref_plus_state")(int(rows), int(cols)))
     return t

@@ -27,6 +27,7 @@
 #include "peps/instrument.hpp"
 #include "peps/linalg.hpp"
 #include "peps/mps.hpp"
+#include "peps/drivers.hpp"
 #include "peps/observables.hpp"
 #include "peps/rng.hpp"
 #include "peps/state.hpp"
@@ -528,6 +529,33 @@ Bag* ref_ite_tfim(int rows, int cols, int d, const int* ndims, const int64_t* sh
     double dt = now_s() - t0;
     for (const auto& t : s.sites()) b.tensors.push_back(t);
     b.doubles = {dt};
+  });
+}
+
+// run_ite (drivers.cpp:75-98) with the TFIM Hamiltonian in colour order:
+// energies (step, value) in doubles, final state in tensors.
+Bag* ref_run_ite(int rows, int cols, double J, double h, double tau, int steps, uint64_t evolution_rank,
+                 uint64_t contraction_rank, int rsvd_iters, int energy_every, int neel, uint64_t seed) {
+  return guarded([&](Bag& b) {
+    IteConfig cfg;
+    cfg.rows = rows;
+    cfg.cols = cols;
+    cfg.hamiltonian = tfim_colour_order(rows, cols, J, h);
+    cfg.tau = tau;
+    cfg.steps = static_cast<std::size_t>(steps);
+    cfg.evolution_rank = static_cast<std::size_t>(evolution_rank);
+    cfg.contraction_rank = static_cast<std::size_t>(contraction_rank);
+    cfg.family = ContractFamily::two_layer_ibmps;
+    cfg.rsvd_iters = rsvd_iters;
+    cfg.energy_every = static_cast<std::size_t>(energy_every);
+    cfg.initial = neel ? "neel" : "zeros";
+    cfg.seed = seed;
+    IteOutcome out = run_ite(cfg);
+    for (auto [st, e] : out.energies) {
+      b.doubles.push_back(static_cast<double>(st));
+      b.doubles.push_back(e);
+    }
+    for (const auto& t : out.state.sites()) b.tensors.push_back(t);
   });
 }
 

@@ -741,6 +741,83 @@ def tfim_terms(rows: int, cols: int, J: float, h: float) -> List[LocalTerm]:
     return out
 
 
+def computational_basis(rows: int, cols: int, bits: Sequence[int], d: int = 2,
+                        ctx: Optional[Context] = None) -> PepsState:
+    """PepsState::computational_basis (state.cpp:44-58): product state, bonds 1."""
+    sites = []
+    for b in bits:
+        v = np.zeros((d, 1, 1, 1, 1), dtype=np.complex128)
+        v[int(b), 0, 0, 0, 0] = 1.0
+        sites.append(v)
+    return PepsState(rows, cols, d, sites, ctx=ctx)
+
+
+def run_ite(rows: int, cols: int, terms: Sequence[LocalTerm], tau: float, steps: int, evolution_rank: int,
+            contraction_rank: int, rsvd_iters: int = 1, energy_every: int = 1, initial: str = "neel",
+            seed: int = 0, ctx: Optional[Context] = None):
+    """run_ite (drivers.cpp:75-98) on the device: per step every term in
+    Hamiltonian order as exp(-tau coeff op) (apply_ite_term, drivers.cpp:56-71;
+    adjacent two-site terms by the QR-reduced simple update with cap
+    evolution_rank), runs of consecutive disjoint terms with the same gate
+    applied in one batched call (they commute exactly); the energy
+    (state_energy: cached, shared environments, two-layer IBMPS with m =
+    contraction_rank, seed derive_seed(seed, 0xE, step)) every energy_every
+    steps and at the end.  Returns ([(step, energy)], final state)."""
+    from .inputs import derive_seed
+    if tau <= 0:
+        raise PepsError(5, "tau must be positive")
+    if evolution_rank < 1 or contraction_rank < 1:
+        raise PepsError(5, "ranks must be >= 1")
+    if initial not in ("neel", "zeros"):
+        raise PepsError(5, f"unknown initial state '{initial}' (use neel or zeros)")
+    ctx = ctx or default_context()
+    bits = [((r + c) % 2 if initial == "neel" else 0) for r in range(rows) for c in range(cols)]
+    st = computational_basis(rows, cols, bits, ctx=ctx)
+    d = 2
+    gates = []
+    for t in terms:
+        op = np.asarray(t.op, dtype=np.complex128)
+        if len(t.sites) == 1:
+            g = hermitian_exp(op, complex(t.coeff).real, tau, ctx)
+        else:
+            a, b = t.sites
+            if not ((a[0] == b[0] and abs(a[1] - b[1]) == 1) or (a[1] == b[1] and abs(a[0] - b[0]) == 1)):
+                raise PepsError(2, "run_ite: distant two-site terms (SWAP routing) are not supported")
+            g = hermitian_exp(op.reshape(d * d, d * d), complex(t.coeff).real, tau, ctx).reshape(d, d, d, d)
+        gates.append(g)
+    # batches of consecutive, site-disjoint terms sharing (op, coeff)
+    groups, cur, used = [], [], set()
+    key = None
+    for i, t in enumerate(terms):
+        k = (len(t.sites), complex(t.coeff), np.asarray(t.op).tobytes())
+        if complex(t.coeff).imag != 0.0:
+            raise PepsError(2, "run_ite: complex term coefficients are not supported")
+        sites = [tuple(p) for p in t.sites]
+        if cur and (k != key or any(p in used for p in sites)):
+            groups.append(cur)
+            cur, used = [], set()
+        cur.append(i)
+        used.update(sites)
+        key = k
+    if cur:
+        groups.append(cur)
+    energies = []
+    pol = TruncationPolicy(evolution_rank, 1e-14)
+    for step in range(1, steps + 1):
+        for grp in groups:
+            t0 = terms[grp[0]]
+            if len(t0.sites) == 1:
+                st = apply_one_site(st, gates[grp[0]], [tuple(terms[i].sites[0]) for i in grp])
+            else:
+                bonds = [tuple(terms[i].sites[0]) + tuple(terms[i].sites[1]) for i in grp]
+                st = apply_two_site(st, gates[grp[0]], bonds, pol)
+        if step % max(1, energy_every) == 0 or step == steps:
+            opt = ExpectationOptions(ContractOption.two_layer_opt(contraction_rank, derive_seed(seed, 0xE, step),
+                                                                  rsvd_iters), True, True, False)
+            energies.append((step, expectation(st, terms, opt).value))
+    return energies, st
+
+
 def _wrap_state(h, like: PepsState) -> PepsState:
     out = PepsState.__new__(PepsState)
     out.ctx, out.rows, out.cols, out.d, out.h = like.ctx, like.rows, like.cols, like.d, h

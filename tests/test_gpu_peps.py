@@ -397,3 +397,22 @@ def test_peps_container_interchange_with_reference(A, refo, tmp_path):
     (tmp_path / "short.peps").write_bytes((tmp_path / "ref.peps").read_bytes()[:200])
     with pytest.raises(A.PepsError, match="truncated"):
         A.load_peps(tmp_path / "short.peps")
+
+
+@pytest.mark.parametrize("initial", ["neel", "zeros"])
+def test_run_ite_energies_match_reference(A, refo, initial):
+    """run_ite (drivers.cpp:75-98) with the TFIM Hamiltonian:
+    per-step energies (cached, shared environments) against the reference's
+    driver to 1e-8; final states agree (norm and fidelity by exact contraction)."""
+    terms = A.tfim_terms(3, 3, 1.0, 3.0)
+    got_e, st = A.run_ite(3, 3, terms, 0.05, 4, 2, 4, 1, 2, initial, 7)
+    want_e, want = refo.run_ite(3, 3, 1.0, 3.0, 0.05, 4, 2, 4, 1, 2, initial, 7)
+    assert [s for s, _ in got_e] == [s for s, _ in want_e]
+    for (_, g), (_, w) in zip(got_e, want_e):
+        assert abs(g - w) <= 1e-8 * max(1.0, abs(w)), (g, w)
+    got = [s.numpy() for s in st.sites]
+    assert [g.shape for g in got] == [w.shape for w in want]
+    n_g, n_w = O.inner_exact(got, 3, 3), O.inner_exact(want, 3, 3)
+    assert abs(n_g - n_w) / abs(n_w) < 1e-8
+    mix = O.inner_exact_pair(want, got, 3, 3)
+    assert abs(abs(mix) / np.sqrt(abs(n_g) * abs(n_w)) - 1) < 1e-8
