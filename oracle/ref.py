@@ -315,6 +315,14 @@ def run_ite(rows, cols, J, h, tau, steps, evolution_rank, contraction_rank, rsvd
     return e, t
 
 
+def expectation_trotter(sites, rows, cols, J, h, tau, m, seed, power_iters=2, oversample=-1, growth_cap=0, d=2):
+    tl, a = _state_args(sites, rows, cols, d)
+    _, dd = _bag(_fn("ref_expectation_trotter")(*a, C.c_double(J), C.c_double(h), C.c_double(tau), C.c_int64(m),
+                                                C.c_uint64(seed), int(power_iters), int(oversample),
+                                                C.c_uint64(growth_cap)))
+    return float(dd[0])
+
+
 def plus_state(rows, cols):
     t, _ = _bag(_fn("ref_plus_state")(int(rows), int(cols)))
     return t

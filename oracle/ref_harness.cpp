@@ -559,6 +559,20 @@ Bag* ref_run_ite(int rows, int cols, double J, double h, double tau, int steps, 
   });
 }
 
+// expectation_trotter (observables.cpp:424-454) of the colour-ordered TFIM.
+Bag* ref_expectation_trotter(int rows, int cols, int d, const int* ndims, const int64_t* shapes,
+                             const double* const* datas, double J, double h, double tau, int64_t m, uint64_t seed,
+                             int power_iters, int oversample, uint64_t growth_cap) {
+  return guarded([&](Bag& b) {
+    PepsState s = make_state(rows, cols, d, ndims, shapes, datas);
+    ExpectationOptions eo;
+    eo.contract = make_opt(m, seed, power_iters, oversample, 1);
+    UpdateOption growth;
+    growth.policy = TruncationPolicy{static_cast<std::size_t>(growth_cap), 1e-14};
+    b.doubles = {expectation_trotter(s, tfim_colour_order(rows, cols, J, h), tau, eo, growth)};
+  });
+}
+
 // |+> on every site: computational_basis zeros then H (state.cpp:44-58,75-85).
 Bag* ref_plus_state(int rows, int cols) {
   return guarded([&](Bag& b) {

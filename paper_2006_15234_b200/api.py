@@ -818,6 +818,44 @@ def run_ite(rows: int, cols: int, terms: Sequence[LocalTerm], tau: float, steps:
     return energies, st
 
 
+def expectation_trotter(s: PepsState, terms: Sequence[LocalTerm], tau: float, opt: ExpectationOptions,
+                        growth: Optional[TruncationPolicy] = None) -> float:
+    """expectation_trotter (observables.cpp:424-454): <H> ~ (<psi|e^{tau H}|psi> -
+    <psi|psi>) / (tau <psi|psi>), e^{tau H} applied term by term as e^{tau coeff op}
+    (adjacent two-site terms by the QR-reduced simple update with the growth
+    policy, which must hold the exact application: cap 0 or >= d * max_bond)."""
+    if tau <= 0.0:
+        raise PepsError(2, "tau must be positive")
+    ctx = s.ctx
+    for t in terms:  # Hermiticity as Observable::is_hermitian
+        op = np.asarray(t.op, dtype=np.complex128)
+        m = op.reshape(int(round(np.sqrt(op.size))), -1)
+        cm = complex(t.coeff) * m
+        if np.abs(cm - cm.conj().T).max() > 1e-12:
+            raise PepsError(2, "Trotter expectation needs a Hermitian observable")
+    growth = growth or TruncationPolicy(0, 1e-14)
+    d = s.d
+    phi = s
+    for t in terms:
+        op = np.asarray(t.op, dtype=np.complex128)
+        if complex(t.coeff).imag != 0.0:
+            raise PepsError(2, "expectation_trotter: complex term coefficients are not supported")
+        if len(t.sites) == 1:
+            phi = apply_one_site(phi, hermitian_exp(op, -complex(t.coeff).real, tau, ctx), [tuple(t.sites[0])])
+        else:
+            a, b = (tuple(x) for x in t.sites)
+            if not ((a[0] == b[0] and abs(a[1] - b[1]) == 1) or (a[1] == b[1] and abs(a[0] - b[0]) == 1)):
+                raise PepsError(2, "expectation_trotter: distant two-site terms (SWAP routing) are not supported")
+            max_bond = max(max(x.shape[1:]) for x in phi.sites)
+            if growth.max_rank != 0 and growth.max_rank < d * max_bond:
+                raise PepsError(2, "bond-growth policy cannot hold an exact e^{tau H_j} application")
+            g = hermitian_exp(op.reshape(d * d, d * d), -complex(t.coeff).real, tau, ctx).reshape(d, d, d, d)
+            phi = apply_two_site(phi, g, [a + b], growth)
+    num = contract_two_layer(s, phi, opt.contract)
+    den = contract_two_layer(s, s, opt.contract)
+    return ((num - den) / (tau * den)).real
+
+
 def _wrap_state(h, like: PepsState) -> PepsState:
     out = PepsState.__new__(PepsState)
     out.ctx, out.rows, out.cols, out.d, out.h = like.ctx, like.rows, like.cols, like.d, h

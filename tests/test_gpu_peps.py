@@ -416,3 +416,14 @@ def test_run_ite_energies_match_reference(A, refo, initial):
     assert abs(n_g - n_w) / abs(n_w) < 1e-8
     mix = O.inner_exact_pair(want, got, 3, 3)
     assert abs(abs(mix) / np.sqrt(abs(n_g) * abs(n_w)) - 1) < 1e-8
+
+
+def test_expectation_trotter_matches_reference(A, refo):
+    """expectation_trotter (observables.cpp:424-454) for the
+    TFIM on a random 3x3 r=2 PEPS against the reference to 1e-8."""
+    sites = I.random_peps(3, 3, 2, 91, scale=1 / np.sqrt(8))
+    st = A.PepsState(3, 3, 2, sites)
+    opt = A.ExpectationOptions(A.ContractOption.two_layer_opt(16, 13, 2, -1))
+    got = A.expectation_trotter(st, A.tfim_terms(3, 3, 1.0, 3.0), 1e-3, opt)
+    want = refo.expectation_trotter(sites, 3, 3, 1.0, 3.0, 1e-3, 16, 13, 2, -1, 0)
+    assert abs(got - want) <= 1e-8 * abs(want), (got, want)
