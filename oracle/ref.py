@@ -315,6 +315,14 @@ def run_ite(rows, cols, J, h, tau, steps, evolution_rank, contraction_rank, rsvd
     return e, t
 
 
+def apply_distant(sites, rows, cols, gate, a, b, max_rank=0, d=2):
+    tl, args = _state_args(sites, rows, cols, d)
+    g = np.ascontiguousarray(gate, dtype=np.complex128)
+    t, _ = _bag(_fn("ref_apply_distant")(*args, C.c_void_p(g.ctypes.data), int(a[0]), int(a[1]), int(b[0]),
+                                         int(b[1]), C.c_uint64(max_rank)))
+    return t
+
+
 def expectation_trotter(sites, rows, cols, J, h, tau, m, seed, power_iters=2, oversample=-1, growth_cap=0, d=2):
     tl, a = _state_args(sites, rows, cols, d)
     _, dd = _bag(_fn("ref_expectation_trotter")(*a, C.c_double(J), C.c_double(h), C.c_double(tau), C.c_int64(m),

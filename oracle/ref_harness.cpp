@@ -559,6 +559,22 @@ Bag* ref_run_ite(int rows, int cols, double J, double h, double tau, int steps, 
   });
 }
 
+// apply_distant (state.cpp:206-236): SWAP-routed two-site gate.
+Bag* ref_apply_distant(int rows, int cols, int d, const int* ndims, const int64_t* shapes,
+                       const double* const* datas, const double* gate, int ar, int ac, int br, int bc,
+                       uint64_t max_rank) {
+  return guarded([&](Bag& b) {
+    PepsState s = make_state(rows, cols, d, ndims, shapes, datas);
+    int64_t gs[4] = {d, d, d, d};
+    UpdateOption uo;
+    uo.policy = TruncationPolicy{static_cast<std::size_t>(max_rank), 1e-14};
+    uo.strategy = UpdateStrategy::qr_svd_gram;
+    PepsState out = apply_distant(s, make_tensor(4, gs, gate), Coord{(std::size_t)ar, (std::size_t)ac},
+                                  Coord{(std::size_t)br, (std::size_t)bc}, uo);
+    for (const auto& t : out.sites()) b.tensors.push_back(t);
+  });
+}
+
 // expectation_trotter (observables.cpp:424-454) of the colour-ordered TFIM.
 Bag* ref_expectation_trotter(int rows, int cols, int d, const int* ndims, const int64_t* shapes,
                              const double* const* datas, double J, double h, double tau, int64_t m, uint64_t seed,

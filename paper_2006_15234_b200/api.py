@@ -758,7 +758,8 @@ def run_ite(rows: int, cols: int, terms: Sequence[LocalTerm], tau: float, steps:
     """run_ite (drivers.cpp:75-98) on the device: per step every term in
     Hamiltonian order as exp(-tau coeff op) (apply_ite_term, drivers.cpp:56-71;
     adjacent two-site terms by the QR-reduced simple update with cap
-    evolution_rank), runs of consecutive disjoint terms with the same gate
+    evolution_rank, distant ones by SWAP routing, apply_distant), runs of
+    consecutive disjoint adjacent terms with the same gate
     applied in one batched call (they commute exactly); the energy
     (state_energy: cached, shared environments, two-layer IBMPS with m =
     contraction_rank, seed derive_seed(seed, 0xE, step)) every energy_every
@@ -780,20 +781,18 @@ def run_ite(rows: int, cols: int, terms: Sequence[LocalTerm], tau: float, steps:
         if len(t.sites) == 1:
             g = hermitian_exp(op, complex(t.coeff).real, tau, ctx)
         else:
-            a, b = t.sites
-            if not ((a[0] == b[0] and abs(a[1] - b[1]) == 1) or (a[1] == b[1] and abs(a[0] - b[0]) == 1)):
-                raise PepsError(2, "run_ite: distant two-site terms (SWAP routing) are not supported")
             g = hermitian_exp(op.reshape(d * d, d * d), complex(t.coeff).real, tau, ctx).reshape(d, d, d, d)
         gates.append(g)
     # batches of consecutive, site-disjoint terms sharing (op, coeff)
     groups, cur, used = [], [], set()
     key = None
     for i, t in enumerate(terms):
-        k = (len(t.sites), complex(t.coeff), np.asarray(t.op).tobytes())
+        k = (len(t.sites), complex(t.coeff), np.asarray(t.op).tobytes(),
+             len(t.sites) == 1 or _adjacent(*t.sites))
         if complex(t.coeff).imag != 0.0:
             raise PepsError(2, "run_ite: complex term coefficients are not supported")
         sites = [tuple(p) for p in t.sites]
-        if cur and (k != key or any(p in used for p in sites)):
+        if cur and (k != key or any(p in used for p in sites) or not k[3]):
             groups.append(cur)
             cur, used = [], set()
         cur.append(i)
@@ -808,6 +807,8 @@ def run_ite(rows: int, cols: int, terms: Sequence[LocalTerm], tau: float, steps:
             t0 = terms[grp[0]]
             if len(t0.sites) == 1:
                 st = apply_one_site(st, gates[grp[0]], [tuple(terms[i].sites[0]) for i in grp])
+            elif not _adjacent(*t0.sites):  # distant: SWAP routing (one term per group)
+                st = apply_distant(st, gates[grp[0]], t0.sites[0], t0.sites[1], pol)
             else:
                 bonds = [tuple(terms[i].sites[0]) + tuple(terms[i].sites[1]) for i in grp]
                 st = apply_two_site(st, gates[grp[0]], bonds, pol)
@@ -816,6 +817,42 @@ def run_ite(rows: int, cols: int, terms: Sequence[LocalTerm], tau: float, steps:
                                                                   rsvd_iters), True, True, False)
             energies.append((step, expectation(st, terms, opt).value))
     return energies, st
+
+
+SWAP = np.einsum("ad,bc->abcd", np.eye(2), np.eye(2)).astype(np.complex128)  # gates::SWAP, outputs first
+
+
+def _adjacent(a, b) -> bool:
+    return (a[0] == b[0] and abs(a[1] - b[1]) == 1) or (a[1] == b[1] and abs(a[0] - b[0]) == 1)
+
+
+def apply_distant(s: PepsState, gate, a: Tuple[int, int], b: Tuple[int, int],
+                  policy: Optional[TruncationPolicy] = None) -> PepsState:
+    """apply_distant (state.cpp:206-236): route a along its row to b's column,
+    then along the column, with SWAP simple updates; apply the gate on the last
+    bond; route back.  Every step is the device QR-reduced simple update."""
+    a, b = tuple(a), tuple(b)
+    for (r, c) in (a, b):
+        if not (0 <= r < s.rows and 0 <= c < s.cols):
+            raise PepsError(2, f"site ({r},{c}) outside the grid")
+    if a == b:
+        raise PepsError(2, "distant gate needs two distinct sites")
+    path = [a]
+    cur = list(a)
+    while cur[1] != b[1]:
+        cur[1] += 1 if b[1] > cur[1] else -1
+        path.append(tuple(cur))
+    while cur[0] != b[0]:
+        cur[0] += 1 if b[0] > cur[0] else -1
+        path.append(tuple(cur))
+    st = s
+    for i in range(len(path) - 2):
+        st = apply_two_site(st, SWAP, [path[i] + path[i + 1]], policy)
+    moved = path[-2] if len(path) >= 2 else a
+    st = apply_two_site(st, gate, [moved + b], policy)
+    for i in range(len(path) - 3, -1, -1):
+        st = apply_two_site(st, SWAP, [path[i] + path[i + 1]], policy)
+    return st
 
 
 def expectation_trotter(s: PepsState, terms: Sequence[LocalTerm], tau: float, opt: ExpectationOptions,
@@ -844,13 +881,11 @@ def expectation_trotter(s: PepsState, terms: Sequence[LocalTerm], tau: float, op
             phi = apply_one_site(phi, hermitian_exp(op, -complex(t.coeff).real, tau, ctx), [tuple(t.sites[0])])
         else:
             a, b = (tuple(x) for x in t.sites)
-            if not ((a[0] == b[0] and abs(a[1] - b[1]) == 1) or (a[1] == b[1] and abs(a[0] - b[0]) == 1)):
-                raise PepsError(2, "expectation_trotter: distant two-site terms (SWAP routing) are not supported")
             max_bond = max(max(x.shape[1:]) for x in phi.sites)
             if growth.max_rank != 0 and growth.max_rank < d * max_bond:
                 raise PepsError(2, "bond-growth policy cannot hold an exact e^{tau H_j} application")
             g = hermitian_exp(op.reshape(d * d, d * d), -complex(t.coeff).real, tau, ctx).reshape(d, d, d, d)
-            phi = apply_two_site(phi, g, [a + b], growth)
+            phi = apply_two_site(phi, g, [a + b], growth) if _adjacent(a, b) else apply_distant(phi, g, a, b, growth)
     num = contract_two_layer(s, phi, opt.contract)
     den = contract_two_layer(s, s, opt.contract)
     return ((num - den) / (tau * den)).real

@@ -427,3 +427,26 @@ def test_expectation_trotter_matches_reference(A, refo):
     got = A.expectation_trotter(st, A.tfim_terms(3, 3, 1.0, 3.0), 1e-3, opt)
     want = refo.expectation_trotter(sites, 3, 3, 1.0, 3.0, 1e-3, 16, 13, 2, -1, 0)
     assert abs(got - want) <= 1e-8 * abs(want), (got, want)
+
+
+def test_apply_distant_matches_reference(A, refo):
+    """apply_distant (state.cpp:206-236): SWAP-routed two-site gates (J1-J2
+    diagonals and longer) on random r=2 sites, elementwise against the
+    reference: uncapped routes site for site (1e-9); capped routes (several
+    truncated updates in a row amplify rounding in the SVD gauge) by shapes and
+    the state (norm and fidelity by exact contraction, 1e-8)."""
+    sites = I.random_peps(3, 3, 2, 77)
+    g = O.random_tensor((2, 2, 2, 2), 78)
+    st = A.PepsState(3, 3, 2, sites)
+    for a, b, cap in [((0, 0), (1, 1), 0), ((0, 0), (1, 2), 4), ((2, 1), (0, 0), 0), ((1, 2), (1, 0), 3)]:
+        out = A.apply_distant(st, g, a, b, A.TruncationPolicy(cap, 1e-14))
+        want = refo.apply_distant(sites, 3, 3, g, a, b, cap)
+        got = [s_.numpy() for s_ in out.sites]
+        assert [x.shape for x in got] == [w.shape for w in want], (a, b, cap)
+        if cap == 0:
+            for i, (x, w) in enumerate(zip(got, want)):
+                assert rel(x, w) < 1e-9, (a, b, cap, i)
+        n_g, n_w = O.inner_exact(got, 3, 3), O.inner_exact(want, 3, 3)
+        assert abs(n_g - n_w) / abs(n_w) < 1e-8, (a, b, cap)
+        mix = O.inner_exact_pair(want, got, 3, 3)
+        assert abs(abs(mix) / np.sqrt(abs(n_g) * abs(n_w)) - 1) < 1e-8, (a, b, cap)
