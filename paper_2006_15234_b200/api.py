@@ -658,6 +658,53 @@ def contract_one_layer(sites: Sequence, rows: int, cols: int, family: ContractFa
     return complex(re.value, im.value)
 
 
+def merge_two_layer(bra: PepsState, ket: PepsState) -> List[DeviceTensor]:
+    """merge_two_layer (contraction.cpp:673-688): order-4 grid of bra* x ket sites."""
+    if (bra.rows, bra.cols, bra.d) != (ket.rows, ket.cols, ket.d):
+        raise PepsError(2, "merge needs matching grids")
+    out = []
+    for b, k in zip(bra.sites, ket.sites):
+        m = contract("dulbr,dULBR->uUlLbBrR", b.conj(), k, ctx=bra.ctx)
+        out.append(m.reshape(b.shape[1] * k.shape[1], b.shape[2] * k.shape[2], b.shape[3] * k.shape[3],
+                             b.shape[4] * k.shape[4]))
+    return out
+
+
+def project_to_one_layer(s: PepsState, bits: Sequence[int]) -> List[DeviceTensor]:
+    """project_to_one_layer (contraction.cpp:654-671): <bits| applied on every site."""
+    if len(bits) != s.rows * s.cols:
+        raise PepsError(2, "bit string length must equal site count")
+    out = []
+    for b, t in zip(bits, s.sites):
+        if not 0 <= int(b) < s.d:
+            raise PepsError(2, "bit value out of range")
+        e = np.zeros(s.d, dtype=np.complex128)
+        e[int(b)] = 1.0
+        out.append(contract("p,puldr->uldr", e, t, ctx=s.ctx))
+    return out
+
+
+def amplitude(s: PepsState, bits: Sequence[int], family: ContractFamily, opt: Optional[ContractOption] = None) -> complex:
+    """amplitude (contraction.cpp:690-694)."""
+    return contract_one_layer(project_to_one_layer(s, bits), s.rows, s.cols, family, opt, ctx=s.ctx)
+
+
+def inner_product(bra: PepsState, ket: PepsState, opt: ContractOption,
+                  family: Optional[ContractFamily] = None) -> complex:
+    """inner_product (contraction.cpp:696-705): the two-layer IBMPS route unless a
+    one-layer family (exact / bmps / ibmps) is given, which contracts the merged grid."""
+    if (bra.rows, bra.cols, bra.d) != (ket.rows, ket.cols, ket.d):
+        raise PepsError(2, "inner product needs matching grids")
+    if family is None:
+        return contract_two_layer(bra, ket, opt)
+    return contract_one_layer(merge_two_layer(bra, ket), bra.rows, bra.cols, family, opt, ctx=bra.ctx)
+
+
+def norm(s: PepsState, opt: ContractOption, family: Optional[ContractFamily] = None) -> float:
+    """norm (contraction.cpp:707-710): sqrt(max(0, Re <s|s>))."""
+    return float(np.sqrt(max(0.0, inner_product(s, s, opt, family).real)))
+
+
 def approx_apply_mpo(mps: Sequence, mpo: Sequence, policy: TruncationPolicy, strategy: SvdStrategy, absorb: Absorb,
                      rsvd: RsvdConfig, seed_base: int, ctx: Optional[Context] = None) -> List[DeviceTensor]:
     """approx_apply_mpo (mps.cpp:44-84): MPS sites (phys, left, right), MPO sites (p, d, left, right)."""

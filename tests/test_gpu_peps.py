@@ -450,3 +450,24 @@ def test_apply_distant_matches_reference(A, refo):
         assert abs(n_g - n_w) / abs(n_w) < 1e-8, (a, b, cap)
         mix = O.inner_exact_pair(want, got, 3, 3)
         assert abs(abs(mix) / np.sqrt(abs(n_g) * abs(n_w)) - 1) < 1e-8, (a, b, cap)
+
+
+def test_inner_product_families_and_amplitude(A, refo):
+    """inner_product / norm through the merged one-layer grid (exact, BMPS,
+    IBMPS families; contraction.cpp:654-710) against the reference's exact
+    inner product and the two-layer route; amplitude of a basis state."""
+    sites = I.random_peps(3, 3, 2, 31)
+    st = A.PepsState(3, 3, 2, sites)
+    want = refo.inner_exact(sites, 3, 3)
+    ex = A.inner_product(st, st, A.ContractOption(), A.ContractFamily.exact)
+    assert abs(ex - want) <= 1e-10 * abs(want)
+    for fam, opt in [(A.ContractFamily.bmps, A.bmps_opt(16, 2)), (A.ContractFamily.ibmps, A.ibmps_opt(16, 2))]:
+        v = A.inner_product(st, st, opt, fam)
+        assert abs(v - want) <= 1e-9 * abs(want)
+    two = A.inner_product(st, st, A.ContractOption.two_layer_opt(16, 2))
+    assert abs(two - want) <= 1e-9 * abs(want)
+    assert abs(A.norm(st, A.ContractOption(), A.ContractFamily.exact) - np.sqrt(want.real)) <= 1e-10 * np.sqrt(want.real)
+    bits = [0, 1, 1, 0, 0, 1, 0, 1, 1]
+    amp = A.amplitude(st, bits, A.ContractFamily.exact)
+    grid = [np.einsum("p,puldr->uldr", np.eye(2)[b], t) for b, t in zip(bits, sites)]
+    assert abs(amp - refo.contract_one_layer(grid, 3, 3, 0)) <= 1e-10 * abs(amp)
