@@ -282,6 +282,36 @@ def cfg5(args, ctx):
     return res
 
 
+def cfg_sens(args, ctx):
+    """Rounding sensitivity of truncated boundary contractions.  Reduced size
+    (8x8 r=4 m=16 q=2 os=4, within the reference's reach): device vs
+    reference, and reference vs itself after a 1e-14 relative perturbation of
+    every site; full config 5: device with two rounding-different schedules
+    (eigensolver/apply overlap on vs off)."""
+    from oracle import ref
+    ref.set_threads(os.cpu_count() or 1)
+    out = {"config": "sensitivity"}
+    sites = inputs.random_peps(8, 8, 4, 51, scale=1 / np.sqrt(32))
+    st = A.PepsState(8, 8, 2, sites, ctx=ctx)
+    opt = A.ContractOption.two_layer_opt(16, 9, 2, 4)
+    dev = A.contract_two_layer(st, st, opt)
+    w, _ = ref.contract_two_layer(sites, 8, 8, 16, 9, 2, 4)
+    rs = np.random.default_rng(3)
+    pert = [x * (1.0 + 1e-14 * rs.standard_normal()) for x in sites]
+    w2, _ = ref.contract_two_layer(pert, 8, 8, 16, 9, 2, 4)
+    out.update({"reduced_8x8_r4_m16_device_vs_ref": abs(dev - w) / abs(w),
+                "reduced_8x8_r4_m16_ref_vs_ref_perturbed_1e-14": abs(w2 - w) / abs(w)})
+    c = inputs.config5()
+    st = A.PepsState(32, 32, 2, c["sites"], ctx=ctx)
+    opt = A.ContractOption.two_layer_opt(64, c["seed"], 2, 8)
+    a = A.contract_two_layer(st, st, opt)
+    ctx.set_option("overlap", 0)
+    b = A.contract_two_layer(st, st, opt)
+    ctx.set_option("overlap", 1)
+    out["config5_overlap_on_vs_off"] = abs(a - b) / abs(b)
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--configs", default="1,3,4,5")
@@ -290,7 +320,7 @@ def main():
     ap.add_argument("--zz", choices=["none", "centre"], default="centre")
     args = ap.parse_args()
     ctx = A.default_context()
-    fns = {"1": cfg1, "3": cfg3, "4": cfg4, "4b": cfg4b, "5": cfg5}
+    fns = {"1": cfg1, "3": cfg3, "4": cfg4, "4b": cfg4b, "5": cfg5, "sens": cfg_sens}
     for k in args.configs.split(","):
         t0 = time.perf_counter()
         res = fns[k](args, ctx)
