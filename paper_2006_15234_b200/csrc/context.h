@@ -164,6 +164,10 @@ class Ctx {
   // apply_orth_speculative): option "overlap" / PEPSB_OVERLAP, 0 off, 1 when
   // the column extent is >= 2^15 (default), 2 always.
   int overlap = 1;
+  // build_row_cache: run the bottom sweep on a helper context from a second
+  // host thread, concurrently with the top sweep (option "concurrent_sweeps").
+  int concurrent_sweeps = 1;
+  std::unique_ptr<Ctx> helper;  // lazily created, same device
 
   // Optional per-launch device timing (CUDA events on `stream`), used by the
   // bench's roofline pass; off in timed runs.

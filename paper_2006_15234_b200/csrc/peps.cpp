@@ -6,6 +6,9 @@
 #include "peps.h"
 
 #include <algorithm>
+#include <exception>
+#include <memory>
+#include <thread>
 #include <cmath>
 #include <map>
 #include <cstdio>
@@ -195,16 +198,66 @@ PepsStateD flip_vertical(Ctx& ctx, const PepsStateD& s) {
   return f;
 }
 
-// observables.cpp:272-281,325-333
+namespace {
+// sweep_boundaries (observables.cpp:272-281)
+std::vector<BoundaryD> sweep_boundaries(Ctx& ctx, const PepsStateD& s, const ContractOptD& opt, uint64_t tag) {
+  std::vector<BoundaryD> out;
+  out.push_back(two_layer_first_row(ctx, s, s));
+  for (int r = 1; r < s.rows; ++r) out.push_back(two_layer_apply_row(ctx, out.back(), s, s, r, opt, tag));
+  return out;
+}
+}  // namespace
+
+// observables.cpp:325-333.  The two sweeps are independent: the
+// bottom one (flipped state, tag 0x21) runs on a helper context driven by a
+// second host thread, so the latency-bound stretches of one sweep (one-block
+// eigensolvers, host syncs) overlap the other's GEMMs.  Each sweep is the same
+// sequence of kernels either way, so the cache is bitwise unchanged.
 RowCacheD build_row_cache(Ctx& ctx, const PepsStateD& s, const ContractOptD& opt) {
   RowCacheD cache;
-  cache.tops.push_back(two_layer_first_row(ctx, s, s));
-  for (int r = 1; r < s.rows; ++r)
-    cache.tops.push_back(two_layer_apply_row(ctx, cache.tops.back(), s, s, r, opt, kTagTop));
-  PepsStateD fl = flip_vertical(ctx, s);
   std::vector<BoundaryD> fb;
-  fb.push_back(two_layer_first_row(ctx, fl, fl));
-  for (int r = 1; r < s.rows; ++r) fb.push_back(two_layer_apply_row(ctx, fb.back(), fl, fl, r, opt, kTagBottom));
+  if (ctx.concurrent_sweeps && s.rows > 1) {
+    if (!ctx.helper) {
+      ctx.helper = std::make_unique<Ctx>(ctx.device);
+      ctx.helper->concurrent_sweeps = 0;
+    }
+    Ctx& c2 = *ctx.helper;
+    c2.overlap = ctx.overlap;
+    c2.orth_mode = ctx.orth_mode;
+    // the helper's work starts after everything enqueued on ctx so far (the
+    // state's uploads, earlier users of blocks the helper's pool may reuse)
+    cudaEvent_t ev = ctx.take_event();
+    PEPSB_CUDA(cudaEventRecord(ev, ctx.stream));
+    PEPSB_CUDA(cudaStreamWaitEvent(c2.stream, ev, 0));
+    const uint64_t f0 = c2.flops, l0 = static_cast<uint64_t>(c2.launches);
+    std::exception_ptr err;
+    std::thread bottom([&] {
+      try {
+        PEPSB_CUDA(cudaSetDevice(c2.device));
+        PepsStateD fl = flip_vertical(c2, s);
+        fb = sweep_boundaries(c2, fl, opt, kTagBottom);
+        c2.sync();
+      } catch (...) {
+        err = std::current_exception();
+      }
+    });
+    try {
+      cache.tops = sweep_boundaries(ctx, s, opt, kTagTop);
+    } catch (...) {
+      bottom.join();
+      ctx.event_pool.push_back(ev);
+      throw;
+    }
+    bottom.join();
+    ctx.event_pool.push_back(ev);
+    if (err) std::rethrow_exception(err);
+    ctx.flops += c2.flops - f0;
+    ctx.launches += static_cast<int64_t>(static_cast<uint64_t>(c2.launches) - l0);
+  } else {
+    cache.tops = sweep_boundaries(ctx, s, opt, kTagTop);
+    PepsStateD fl = flip_vertical(ctx, s);
+    fb = sweep_boundaries(ctx, fl, opt, kTagBottom);
+  }
   cache.bots.resize(s.rows);
   for (int k = 0; k < s.rows; ++k) cache.bots[k] = fb[s.rows - 1 - k];
   return cache;
