@@ -13,6 +13,7 @@ Buf::~Buf() {
 }
 
 void* Pool::alloc(size_t bytes, size_t* reserved) {
+  std::lock_guard<std::mutex> lock(mu);
   // size classes: 512 B granules below 1 MiB, 2 MiB granules above
   const size_t g = bytes <= (1u << 20) ? 512 : (2u << 20);
   const size_t want = ((bytes + g - 1) / g) * g;
@@ -28,7 +29,7 @@ void* Pool::alloc(size_t bytes, size_t* reserved) {
   cudaError_t e = cudaMalloc(&p, want);
   if (e != cudaSuccess) {  // release the cache and retry once
     cudaGetLastError();
-    trim();
+    trim_locked();
     e = cudaMalloc(&p, want);
     if (e != cudaSuccess) {
       cudaGetLastError();
@@ -42,6 +43,7 @@ void* Pool::alloc(size_t bytes, size_t* reserved) {
 }
 
 void Pool::release(void* p, size_t bytes) {
+  std::lock_guard<std::mutex> g(mu);
   if (defer) {
     parked.emplace_back(bytes, p);
     return;
@@ -51,6 +53,11 @@ void Pool::release(void* p, size_t bytes) {
 }
 
 void Pool::trim() {
+  std::lock_guard<std::mutex> g(mu);
+  trim_locked();
+}
+
+void Pool::trim_locked() {
   if (stream) cudaStreamSynchronize(stream);
   else cudaDeviceSynchronize();
   if (!defer) {
@@ -108,6 +115,7 @@ Ctx::Ctx(int dev) : device(dev) {
   trace = getenv("PEPSB_TRACE") != nullptr;
   if (const char* e = getenv("PEPSB_OVERLAP")) overlap = e[0] == '0' ? 0 : e[0] == '2' ? 2 : 1;
   if (const char* e = getenv("PEPSB_CONCURRENT_SWEEPS")) concurrent_sweeps = e[0] != '0';
+  if (const char* e = getenv("PEPSB_PIPELINE_ROWS")) pipeline_rows = e[0] != '0';
   PEPSB_CUDA(cudaSetDevice(dev));
   PEPSB_CUDA(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev));
   PEPSB_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
@@ -149,6 +157,7 @@ void Ctx::fork() {
   join_pending();
   if (pool->defer) throw Error(kOtherError, "nested stream fork");
   PEPSB_CUDA(cudaEventRecord(fork_event, main_stream));
+  std::lock_guard<std::mutex> g(pool->mu);
   pool->defer = true;
 }
 
@@ -167,6 +176,7 @@ void Ctx::join_pending() {
   if (!side_pending) return;
   side_pending = false;
   PEPSB_CUDA(cudaStreamWaitEvent(main_stream, join_event, 0));
+  std::lock_guard<std::mutex> g(pool->mu);
   pool->defer = false;
   for (auto& [sz, p] : pool->parked) {
     pool->free_blocks.emplace(sz, p);
@@ -179,6 +189,7 @@ void Ctx::join() {
   PEPSB_CUDA(cudaEventRecord(join_event, side_stream));
   stream = main_stream;
   PEPSB_CUDA(cudaStreamWaitEvent(main_stream, join_event, 0));
+  std::lock_guard<std::mutex> g(pool->mu);
   pool->defer = false;
   for (auto& [sz, p] : pool->parked) {
     pool->free_blocks.emplace(sz, p);

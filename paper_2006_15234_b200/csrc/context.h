@@ -5,6 +5,7 @@
 
 #include <cstdint>
 #include <map>
+#include <mutex>
 #include <memory>
 #include <string>
 #include <vector>
@@ -38,9 +39,13 @@ struct Pool {
   // protects them from reuse by the other stream.
   bool defer = false;
   std::vector<std::pair<size_t, void*>> parked;
+  // Buffers may be released from another host thread (the row pipeline and
+  // the concurrent cache sweeps hand tensors between contexts).
+  std::mutex mu;
   void* alloc(size_t bytes, size_t* reserved);
   void release(void* p, size_t bytes);
   void trim();  // synchronises, then returns every cached block to the driver
+  void trim_locked();
   ~Pool() { trim(); }
 };
 
@@ -167,6 +172,9 @@ class Ctx {
   // build_row_cache: run the bottom sweep on a helper context from a second
   // host thread, concurrently with the top sweep (option "concurrent_sweeps").
   int concurrent_sweeps = 1;
+  // contract_two_layer: consecutive rows on two contexts, a few columns apart
+  // (option "pipeline_rows").
+  int pipeline_rows = 1;
   std::unique_ptr<Ctx> helper;  // lazily created, same device
 
   // Optional per-launch device timing (CUDA events on `stream`), used by the

@@ -8,6 +8,8 @@
 #include <algorithm>
 #include <exception>
 #include <memory>
+#include <condition_variable>
+#include <mutex>
 #include <thread>
 #include <cmath>
 #include <map>
@@ -88,19 +90,73 @@ BoundaryD two_layer_first_row(Ctx& ctx, const PepsStateD& bra, const PepsStateD&
   return out;
 }
 
-// contraction.cpp:269-311
-BoundaryD two_layer_apply_row(Ctx& ctx, const BoundaryD& top, const PepsStateD& bra, const PepsStateD& ket, int row,
-                              const ContractOptD& opt, uint64_t seed_tag) {
+namespace {
+
+// A boundary row produced on one context and read on another (the row
+// pipeline of contract_two_layer): site c is published, with an event on the
+// producer's stream, as soon as its computation is enqueued; the consumer
+// waits for the host flag and makes its own stream wait for the event.
+struct Handoff {
+  explicit Handoff(int n) : sites(n), ev(n, nullptr), ready(n, 0) {}
+  ~Handoff() {
+    for (auto e : ev)
+      if (e) cudaEventDestroy(e);
+  }
+  std::vector<DTensor> sites;
+  std::vector<std::pair<int64_t, int64_t>> phys;
+  std::vector<cudaEvent_t> ev;
+  std::vector<char> ready;
+  std::mutex m;
+  std::condition_variable cv;
+  bool failed = false;
+  void publish(Ctx& ctx, int c, const DTensor& t) {
+    cudaEvent_t e;
+    PEPSB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    PEPSB_CUDA(cudaEventRecord(e, ctx.stream));
+    {
+      std::lock_guard<std::mutex> g(m);
+      sites[c] = t;
+      ev[c] = e;
+      ready[c] = 1;
+    }
+    cv.notify_all();
+  }
+  const DTensor& acquire(Ctx& ctx, int c) {
+    std::unique_lock<std::mutex> g(m);
+    cv.wait(g, [&] { return ready[c] || failed; });
+    if (!ready[c]) throw Error(kOtherError, "row pipeline: producer failed");
+    PEPSB_CUDA(cudaStreamWaitEvent(ctx.stream, ev[c], 0));
+    return sites[c];
+  }
+  void fail() {
+    {
+      std::lock_guard<std::mutex> g(m);
+      failed = true;
+    }
+    cv.notify_all();
+  }
+};
+
+// contraction.cpp:269-311, reading the top boundary from `top` or (pipeline)
+// from the handoff `tin`, and publishing the emitted sites into `hout`.
+BoundaryD apply_row_impl(Ctx& ctx, const BoundaryD* top, Handoff* tin, const PepsStateD& bra, const PepsStateD& ket,
+                         int row, const ContractOptD& opt, uint64_t seed_tag, Handoff* hout) {
   const int n = bra.cols;
   BoundaryD out;
   out.sites.resize(n);
   for (int c = 0; c < n; ++c) out.phys.emplace_back(bra.site(row, c).shape[3], ket.site(row, c).shape[3]);
   const int absorb = opt.canonicalize ? (row % 2 ? kRight : kLeft) : kSplit;
   ctx.lookahead.reset();
+  auto top_site = [&](int c) -> const DTensor& { return tin ? tin->acquire(ctx, c) : top->sites[c]; };
+  const auto& tphys = tin ? tin->phys : top->phys;
+  auto emit = [&](int c, const DTensor& t) {
+    out.sites[c] = t;
+    if (hout) hout->publish(ctx, c, t);
+  };
 
   // pending v: (a, bra-down, ket-down, mps bond, bra-right, ket-right)
-  const DTensor& s0 = top.sites[0];
-  DTensor s0s = reshape(s0, {top.phys[0].first, top.phys[0].second, s0.shape[1], s0.shape[2]});
+  const DTensor& s0 = top_site(0);
+  DTensor s0s = reshape(s0, {tphys[0].first, tphys[0].second, s0.shape[1], s0.shape[2]});
   LTensor v0 = contract_network(
       ctx, {as_labelled(s0s, "uvls"), as_labelled(bra.site(row, 0), "dumbe", true), as_labelled(ket.site(row, 0), "dvncf")},
       "bcsef");
@@ -108,8 +164,8 @@ BoundaryD two_layer_apply_row(Ctx& ctx, const BoundaryD& top, const PepsStateD& 
   v = reshape(v, {1, v.shape[0], v.shape[1], v.shape[2], v.shape[3], v.shape[4]});
 
   for (int c = 1; c < n; ++c) {
-    const DTensor& sc = top.sites[c];
-    DTensor scs = reshape(sc, {top.phys[c].first, top.phys[c].second, sc.shape[1], sc.shape[2]});
+    const DTensor& sc = top_site(c);
+    DTensor scs = reshape(sc, {tphys[c].first, tphys[c].second, sc.shape[1], sc.shape[2]});
     ImplicitOp net({v, scs, bra.site(row, c), ket.site(row, c)}, {"apqsmn", "uvst", "dumbe", "dvncf"}, "apq", "bctef",
                    {false, false, true, false});
     Trunc policy = opt.trunc;
@@ -129,8 +185,8 @@ BoundaryD two_layer_apply_row(Ctx& ctx, const BoundaryD& top, const PepsStateD& 
       const auto& ks = ket.site(row, c).shape;
       DTensor vg;
       vg.shape = {rho, bs[3], ks[3], sc.shape[2], bs[4], ks[4]};
-      const DTensor& sn = top.sites[c + 1];
-      DTensor sns = reshape(sn, {top.phys[c + 1].first, top.phys[c + 1].second, sn.shape[1], sn.shape[2]});
+      const DTensor& sn = top_site(c + 1);
+      DTensor sns = reshape(sn, {tphys[c + 1].first, tphys[c + 1].second, sn.shape[1], sn.shape[2]});
       set_lookahead(ctx,
                     ImplicitOp({vg, sns, bra.site(row, c + 1), ket.site(row, c + 1)},
                                {"apqsmn", "uvst", "dumbe", "dvncf"}, "apq", "bctef", {false, false, true, false}),
@@ -139,7 +195,7 @@ BoundaryD two_layer_apply_row(Ctx& ctx, const BoundaryD& top, const PepsStateD& 
     // t1 (a, pb, pk, rho) written directly as (pb, pk, a, rho)
     EinsumsvdResultD split = einsumsvd(ctx, net, policy, opt.strategy, absorb, cfg, {1, 2, 0, 3});
     const auto& t1 = split.t1.shape;
-    out.sites[c - 1] = reshape(split.t1, {t1[0] * t1[1], t1[2], t1[3]});
+    emit(c - 1, reshape(split.t1, {t1[0] * t1[1], t1[2], t1[3]}));
     v = split.t2;  // (rho, b, c, t, e, f)
   }
   ctx.lookahead.reset();
@@ -147,13 +203,21 @@ BoundaryD two_layer_apply_row(Ctx& ctx, const BoundaryD& top, const PepsStateD& 
   LTensor last = reduce_to(ctx, as_labelled(v, "abcdef"), "bcadef");
   DTensor lastd = materialize(ctx, last, last.labels);
   const auto& ls = lastd.shape;
-  out.sites[n - 1] = reshape(lastd, {ls[0] * ls[1], ls[2], ls[3] * ls[4] * ls[5]});
+  emit(n - 1, reshape(lastd, {ls[0] * ls[1], ls[2], ls[3] * ls[4] * ls[5]}));
   out.validate();
   if (ctx.trace) {
     fprintf(stderr, "[pepsb] row %d: host alloc %.2f ms, free %.2f ms, sync-wait %.2f ms (cumulative)\n", row,
             ctx.t_alloc * 1e3, ctx.t_free * 1e3, ctx.t_sync * 1e3);
   }
   return out;
+}
+
+}  // namespace
+
+// contraction.cpp:269-311
+BoundaryD two_layer_apply_row(Ctx& ctx, const BoundaryD& top, const PepsStateD& bra, const PepsStateD& ket, int row,
+                              const ContractOptD& opt, uint64_t seed_tag) {
+  return apply_row_impl(ctx, &top, nullptr, bra, ket, row, opt, seed_tag, nullptr);
 }
 
 std::pair<double, double> chain_scalar(Ctx& ctx, const BoundaryD& b) {
@@ -174,13 +238,73 @@ std::pair<double, double> chain_scalar(Ctx& ctx, const BoundaryD& b) {
   return read_scalar(ctx, t);
 }
 
+// contraction.cpp:313-338.  Row pipeline: row r's column c needs only the
+// top site c (+1 for the lookahead), which row r-1 emits at its column c+1, so
+// consecutive rows run concurrently, a few columns apart, on two contexts
+// driven by two host threads (odd rows here, even rows on the helper); each
+// row is the same kernel sequence with the same seeds, so the result is
+// bitwise that of the sequential sweep.
 std::pair<double, double> contract_two_layer(Ctx& ctx, const PepsStateD& bra, const PepsStateD& ket,
                                              const ContractOptD& opt) {
   if (bra.rows != ket.rows || bra.cols != ket.cols || bra.d != ket.d)
     throw Error(kValidationError, "two-layer contraction needs matching grids");
   BoundaryD s = two_layer_first_row(ctx, bra, ket);
-  for (int r = 1; r < bra.rows; ++r) s = two_layer_apply_row(ctx, s, bra, ket, r, opt, kTagTop);
-  return chain_scalar(ctx, s);
+  const int rows = bra.rows, n = bra.cols;
+  // (tiny lattices: the second thread and context cost more than they hide)
+  if (!ctx.pipeline_rows || rows < 3 || rows * n < 64) {
+    for (int r = 1; r < rows; ++r) s = two_layer_apply_row(ctx, s, bra, ket, r, opt, kTagTop);
+    return chain_scalar(ctx, s);
+  }
+  if (!ctx.helper) {
+    ctx.helper = std::make_unique<Ctx>(ctx.device);
+    ctx.helper->concurrent_sweeps = 0;
+  }
+  Ctx& c2 = *ctx.helper;
+  c2.overlap = ctx.overlap;
+  c2.orth_mode = ctx.orth_mode;
+  c2.pipeline_rows = 0;
+  std::vector<std::unique_ptr<Handoff>> H(rows);
+  for (int r = 0; r < rows; ++r) {
+    H[r] = std::make_unique<Handoff>(n);
+    for (int c = 0; c < n; ++c)
+      H[r]->phys.emplace_back(r == 0 ? std::make_pair(bra.site(0, c).shape[3], ket.site(0, c).shape[3])
+                                     : std::make_pair(bra.site(r, c).shape[3], ket.site(r, c).shape[3]));
+  }
+  for (int c = 0; c < n; ++c) H[0]->publish(ctx, c, s.sites[c]);
+  const uint64_t f0 = c2.flops, l0 = static_cast<uint64_t>(c2.launches);
+  auto work = [&](Ctx& cx, int parity) {
+    for (int r = 1; r < rows; ++r) {
+      if (r % 2 != parity) continue;
+      apply_row_impl(cx, nullptr, H[r - 1].get(), bra, ket, r, opt, kTagTop, H[r].get());
+      cx.sync();  // row r - 1 is no longer read: its blocks may return to their pool
+      H[r - 1]->sites.assign(n, DTensor());
+    }
+  };
+  std::exception_ptr err;
+  std::thread even([&] {
+    try {
+      PEPSB_CUDA(cudaSetDevice(c2.device));
+      work(c2, 0);
+    } catch (...) {
+      err = std::current_exception();
+      for (auto& h : H) h->fail();
+    }
+  });
+  try {
+    work(ctx, 1);
+  } catch (...) {
+    for (auto& h : H) h->fail();
+    even.join();
+    throw;
+  }
+  even.join();
+  if (err) std::rethrow_exception(err);
+  ctx.flops += c2.flops - f0;
+  ctx.launches += static_cast<int64_t>(static_cast<uint64_t>(c2.launches) - l0);
+  BoundaryD last;
+  last.phys = H[rows - 1]->phys;
+  for (int c = 0; c < n; ++c) last.sites.push_back(H[rows - 1]->acquire(ctx, c));
+  return chain_scalar(ctx, last);
 }
 
 // observables.cpp:261-270: reverse rows, swap up/down.
