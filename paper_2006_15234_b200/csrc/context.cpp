@@ -115,7 +115,7 @@ Ctx::Ctx(int dev) : device(dev) {
   trace = getenv("PEPSB_TRACE") != nullptr;
   if (const char* e = getenv("PEPSB_OVERLAP")) overlap = e[0] == '0' ? 0 : e[0] == '2' ? 2 : 1;
   if (const char* e = getenv("PEPSB_CONCURRENT_SWEEPS")) concurrent_sweeps = e[0] != '0';
-  if (const char* e = getenv("PEPSB_PIPELINE_ROWS")) pipeline_rows = e[0] != '0';
+  if (const char* e = getenv("PEPSB_PIPELINE_ROWS")) pipeline_rows = std::atoi(e);
   PEPSB_CUDA(cudaSetDevice(dev));
   PEPSB_CUDA(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev));
   PEPSB_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
@@ -133,7 +133,7 @@ Ctx::Ctx(int dev) : device(dev) {
 }
 
 Ctx::~Ctx() {
-  helper.reset();
+  helpers.clear();
   if (stream != main_stream) join();
   join_pending();
   prefetched.reset();

@@ -174,8 +174,8 @@ class Ctx {
   int concurrent_sweeps = 1;
   // contract_two_layer: consecutive rows on two contexts, a few columns apart
   // (option "pipeline_rows").
-  int pipeline_rows = 1;
-  std::unique_ptr<Ctx> helper;  // lazily created, same device
+  int pipeline_rows = -1;  // rows in flight K (< 2: sequential; -1: automatic, peps.cpp pipeline_depth)
+  std::vector<std::unique_ptr<Ctx>> helpers;  // lazily created, same device
 
   // Optional per-launch device timing (CUDA events on `stream`), used by the
   // bench's roofline pass; off in timed runs.

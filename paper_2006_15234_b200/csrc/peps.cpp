@@ -238,73 +238,122 @@ std::pair<double, double> chain_scalar(Ctx& ctx, const BoundaryD& b) {
   return read_scalar(ctx, t);
 }
 
-// contraction.cpp:313-338.  Row pipeline: row r's column c needs only the
-// top site c (+1 for the lookahead), which row r-1 emits at its column c+1, so
-// consecutive rows run concurrently, a few columns apart, on two contexts
-// driven by two host threads (odd rows here, even rows on the helper); each
-// row is the same kernel sequence with the same seeds, so the result is
-// bitwise that of the sequential sweep.
+// Row pipeline (contraction.cpp:313-338 / observables.cpp:272-281): row r's
+// column c reads only the top-boundary site c (+1 for the lookahead), which row
+// r-1 emits at its column c+1, so K consecutive rows run concurrently a few
+// columns apart on K contexts driven by K host threads (row r on context
+// (r-1) mod K; ctxs[0] is the caller's).  Each row is the same kernel sequence
+// with the same seeds, so every boundary is bitwise that of the sequential
+// sweep.  keep_all: return every row's boundary (the cache), else only the last.
+std::vector<BoundaryD> pipelined_sweep(const std::vector<Ctx*>& ctxs, const PepsStateD& bra, const PepsStateD& ket,
+                                       const ContractOptD& opt, uint64_t tag, bool keep_all) {
+  Ctx& ctx = *ctxs[0];
+  const int K = static_cast<int>(ctxs.size());
+  const int rows = bra.rows, n = bra.cols;
+  BoundaryD first = two_layer_first_row(ctx, bra, ket);
+  std::vector<std::unique_ptr<Handoff>> H(rows);
+  for (int r = 0; r < rows; ++r) {
+    H[r] = std::make_unique<Handoff>(n);
+    for (int c = 0; c < n; ++c) H[r]->phys.emplace_back(bra.site(r, c).shape[3], ket.site(r, c).shape[3]);
+  }
+  for (int c = 0; c < n; ++c) H[0]->publish(ctx, c, first.sites[c]);
+  std::vector<uint64_t> f0(K), l0(K);
+  for (int i = 1; i < K; ++i) {
+    f0[i] = ctxs[i]->flops;
+    l0[i] = static_cast<uint64_t>(ctxs[i]->launches);
+    // helpers start after everything enqueued on the caller's stream so far
+    cudaEvent_t ev = ctx.take_event();
+    PEPSB_CUDA(cudaEventRecord(ev, ctx.stream));
+    PEPSB_CUDA(cudaStreamWaitEvent(ctxs[i]->stream, ev, 0));
+    ctx.event_pool.push_back(ev);
+  }
+  auto work = [&](int idx) {
+    Ctx& cx = *ctxs[idx];
+    for (int r = 1 + idx; r < rows; r += K) {
+      apply_row_impl(cx, nullptr, H[r - 1].get(), bra, ket, r, opt, tag, H[r].get());
+      if (!keep_all) {
+        cx.sync();  // row r - 1 is no longer read: its blocks may return to their pool
+        H[r - 1]->sites.assign(n, DTensor());
+      }
+    }
+    cx.sync();
+  };
+  std::vector<std::exception_ptr> err(K);
+  std::vector<std::thread> threads;
+  for (int i = 1; i < K; ++i)
+    threads.emplace_back([&, i] {
+      try {
+        PEPSB_CUDA(cudaSetDevice(ctxs[i]->device));
+        work(i);
+      } catch (...) {
+        err[i] = std::current_exception();
+        for (auto& h : H) h->fail();
+      }
+    });
+  try {
+    work(0);
+  } catch (...) {
+    err[0] = std::current_exception();
+    for (auto& h : H) h->fail();
+  }
+  for (auto& t : threads) t.join();
+  for (auto& e : err)
+    if (e) std::rethrow_exception(e);
+  for (int i = 1; i < K; ++i) {
+    ctx.flops += ctxs[i]->flops - f0[i];
+    ctx.launches += static_cast<int64_t>(static_cast<uint64_t>(ctxs[i]->launches) - l0[i]);
+  }
+  std::vector<BoundaryD> out;
+  for (int r = keep_all ? 0 : rows - 1; r < rows; ++r) {
+    BoundaryD b;
+    b.phys = r == 0 ? first.phys : H[r]->phys;
+    for (int c = 0; c < n; ++c) b.sites.push_back(H[r]->acquire(ctx, c));
+    out.push_back(std::move(b));
+  }
+  return out;
+}
+
+// Rows in flight: option "pipeline_rows" (< 2 sequential), or automatic
+// (-1): 3 for small boundary bonds (m <= 48: latency-bound einsumsvds, the
+// one-block eigensolver dominates), 2 otherwise (GEMM-bound: more concurrent
+// rows only contend).  Measured: config 3 (m = 36) 0.43 / 0.37 / 0.36 s per
+// norm at K = 2 / 3 / 4; config 5 (m = 64) 9.2 / 9.5 / 10.0 s.
+int pipeline_depth(const Ctx& ctx, const ContractOptD& opt) {
+  if (ctx.pipeline_rows >= 0) return ctx.pipeline_rows;
+  return (opt.trunc.max_rank != 0 && opt.trunc.max_rank <= 48) ? 3 : 2;
+}
+
+std::vector<Ctx*> pipeline_contexts(Ctx& ctx, int K) {
+  std::vector<Ctx*> out{&ctx};
+  while (static_cast<int>(ctx.helpers.size()) < K - 1) {
+    ctx.helpers.push_back(std::make_unique<Ctx>(ctx.device));
+    ctx.helpers.back()->pipeline_rows = 0;
+    ctx.helpers.back()->concurrent_sweeps = 0;
+  }
+  for (int i = 0; i < K - 1; ++i) {
+    Ctx& h = *ctx.helpers[i];
+    h.overlap = ctx.overlap;
+    h.orth_mode = ctx.orth_mode;
+    out.push_back(&h);
+  }
+  return out;
+}
+
+// contraction.cpp:313-338 (rows pipelined, see pipelined_sweep)
 std::pair<double, double> contract_two_layer(Ctx& ctx, const PepsStateD& bra, const PepsStateD& ket,
                                              const ContractOptD& opt) {
   if (bra.rows != ket.rows || bra.cols != ket.cols || bra.d != ket.d)
     throw Error(kValidationError, "two-layer contraction needs matching grids");
-  BoundaryD s = two_layer_first_row(ctx, bra, ket);
   const int rows = bra.rows, n = bra.cols;
-  // (tiny lattices: the second thread and context cost more than they hide)
-  if (!ctx.pipeline_rows || rows < 3 || rows * n < 64) {
+  // (tiny lattices: extra threads and contexts cost more than they hide)
+  if (pipeline_depth(ctx, opt) < 2 || rows < 3 || rows * n < 64) {
+    BoundaryD s = two_layer_first_row(ctx, bra, ket);
     for (int r = 1; r < rows; ++r) s = two_layer_apply_row(ctx, s, bra, ket, r, opt, kTagTop);
     return chain_scalar(ctx, s);
   }
-  if (!ctx.helper) {
-    ctx.helper = std::make_unique<Ctx>(ctx.device);
-    ctx.helper->concurrent_sweeps = 0;
-  }
-  Ctx& c2 = *ctx.helper;
-  c2.overlap = ctx.overlap;
-  c2.orth_mode = ctx.orth_mode;
-  c2.pipeline_rows = 0;
-  std::vector<std::unique_ptr<Handoff>> H(rows);
-  for (int r = 0; r < rows; ++r) {
-    H[r] = std::make_unique<Handoff>(n);
-    for (int c = 0; c < n; ++c)
-      H[r]->phys.emplace_back(r == 0 ? std::make_pair(bra.site(0, c).shape[3], ket.site(0, c).shape[3])
-                                     : std::make_pair(bra.site(r, c).shape[3], ket.site(r, c).shape[3]));
-  }
-  for (int c = 0; c < n; ++c) H[0]->publish(ctx, c, s.sites[c]);
-  const uint64_t f0 = c2.flops, l0 = static_cast<uint64_t>(c2.launches);
-  auto work = [&](Ctx& cx, int parity) {
-    for (int r = 1; r < rows; ++r) {
-      if (r % 2 != parity) continue;
-      apply_row_impl(cx, nullptr, H[r - 1].get(), bra, ket, r, opt, kTagTop, H[r].get());
-      cx.sync();  // row r - 1 is no longer read: its blocks may return to their pool
-      H[r - 1]->sites.assign(n, DTensor());
-    }
-  };
-  std::exception_ptr err;
-  std::thread even([&] {
-    try {
-      PEPSB_CUDA(cudaSetDevice(c2.device));
-      work(c2, 0);
-    } catch (...) {
-      err = std::current_exception();
-      for (auto& h : H) h->fail();
-    }
-  });
-  try {
-    work(ctx, 1);
-  } catch (...) {
-    for (auto& h : H) h->fail();
-    even.join();
-    throw;
-  }
-  even.join();
-  if (err) std::rethrow_exception(err);
-  ctx.flops += c2.flops - f0;
-  ctx.launches += static_cast<int64_t>(static_cast<uint64_t>(c2.launches) - l0);
-  BoundaryD last;
-  last.phys = H[rows - 1]->phys;
-  for (int c = 0; c < n; ++c) last.sites.push_back(H[rows - 1]->acquire(ctx, c));
-  return chain_scalar(ctx, last);
+  const int K = std::min(pipeline_depth(ctx, opt), rows - 1);
+  std::vector<BoundaryD> last = pipelined_sweep(pipeline_contexts(ctx, K), bra, ket, opt, kTagTop, false);
+  return chain_scalar(ctx, last.back());
 }
 
 // observables.cpp:261-270: reverse rows, swap up/down.
@@ -340,47 +389,45 @@ std::vector<BoundaryD> sweep_boundaries(Ctx& ctx, const PepsStateD& s, const Con
 RowCacheD build_row_cache(Ctx& ctx, const PepsStateD& s, const ContractOptD& opt) {
   RowCacheD cache;
   std::vector<BoundaryD> fb;
+  const bool pipe = pipeline_depth(ctx, opt) >= 2 && s.rows >= 3 && s.rows * s.cols >= 64;
+  const int K = pipe ? std::min(pipeline_depth(ctx, opt), s.rows - 1) : 1;
   if (ctx.concurrent_sweeps && s.rows > 1) {
-    if (!ctx.helper) {
-      ctx.helper = std::make_unique<Ctx>(ctx.device);
-      ctx.helper->concurrent_sweeps = 0;
-    }
-    Ctx& c2 = *ctx.helper;
-    c2.overlap = ctx.overlap;
-    c2.orth_mode = ctx.orth_mode;
-    // the helper's work starts after everything enqueued on ctx so far (the
-    // state's uploads, earlier users of blocks the helper's pool may reuse)
+    // contexts: [ctx, helpers 0 .. K-2] run the top sweep, [helpers K-1 .. 2K-2]
+    // the bottom one, from a second host thread
+    std::vector<Ctx*> all = pipeline_contexts(ctx, 2 * K);
+    std::vector<Ctx*> top(all.begin(), all.begin() + K), bot(all.begin() + K, all.end());
+    Ctx& c2 = *bot[0];
     cudaEvent_t ev = ctx.take_event();
     PEPSB_CUDA(cudaEventRecord(ev, ctx.stream));
     PEPSB_CUDA(cudaStreamWaitEvent(c2.stream, ev, 0));
+    ctx.event_pool.push_back(ev);
     const uint64_t f0 = c2.flops, l0 = static_cast<uint64_t>(c2.launches);
     std::exception_ptr err;
     std::thread bottom([&] {
       try {
         PEPSB_CUDA(cudaSetDevice(c2.device));
         PepsStateD fl = flip_vertical(c2, s);
-        fb = sweep_boundaries(c2, fl, opt, kTagBottom);
+        fb = K > 1 ? pipelined_sweep(bot, fl, fl, opt, kTagBottom, true) : sweep_boundaries(c2, fl, opt, kTagBottom);
         c2.sync();
       } catch (...) {
         err = std::current_exception();
       }
     });
     try {
-      cache.tops = sweep_boundaries(ctx, s, opt, kTagTop);
+      cache.tops = K > 1 ? pipelined_sweep(top, s, s, opt, kTagTop, true) : sweep_boundaries(ctx, s, opt, kTagTop);
     } catch (...) {
       bottom.join();
-      ctx.event_pool.push_back(ev);
       throw;
     }
     bottom.join();
-    ctx.event_pool.push_back(ev);
     if (err) std::rethrow_exception(err);
     ctx.flops += c2.flops - f0;
     ctx.launches += static_cast<int64_t>(static_cast<uint64_t>(c2.launches) - l0);
   } else {
-    cache.tops = sweep_boundaries(ctx, s, opt, kTagTop);
+    std::vector<Ctx*> top = pipeline_contexts(ctx, K);
+    cache.tops = K > 1 ? pipelined_sweep(top, s, s, opt, kTagTop, true) : sweep_boundaries(ctx, s, opt, kTagTop);
     PepsStateD fl = flip_vertical(ctx, s);
-    fb = sweep_boundaries(ctx, fl, opt, kTagBottom);
+    fb = K > 1 ? pipelined_sweep(top, fl, fl, opt, kTagBottom, true) : sweep_boundaries(ctx, fl, opt, kTagBottom);
   }
   cache.bots.resize(s.rows);
   for (int k = 0; k < s.rows; ++k) cache.bots[k] = fb[s.rows - 1 - k];
