@@ -161,29 +161,40 @@ __device__ double2 column_phase(const double2* colp, int rows) {
 // termination they form a block whose eigenvalues are bounded by its trace, which
 // the caller sizes below its deficiency cut, so only the (discarded) basis of
 // that numerically-null block is left unresolved (0 disables).
-__device__ void herm_jacobi(double2* A, double2* V, int n, int ld, double tol, double abs_skip, double low_skip,
-                            int max_sweeps, int* status) {
-  __shared__ double jc[128], js[128];
-  __shared__ double2 je[128];
-  __shared__ int jp[128], jq[128];
-  __shared__ int rotated, flag[3];
-  for (int e = threadIdx.x; e < n * n; e += blockDim.x)
+// rotation scratch, shared by both instantiations (a block runs one of them)
+__shared__ double jc[128], js[128];
+__shared__ double2 je[128];
+__shared__ int jp[128], jq[128];
+__shared__ int rotated, flag[3];
+
+// WARP: run by warp 0 alone, __syncwarp instead of block barriers, the 2x2
+// blocks of pairs and the V rows flattened over the 32 lanes -- the
+// latency-optimal solver for the small k of the latency-bound configs.
+template <bool WARP>
+__device__ void herm_jacobi_t(double2* A, double2* V, int n, int ld, double tol, double abs_skip, double low_skip,
+                              int max_sweeps, int* status) {
+  const int tid = WARP ? static_cast<int>(threadIdx.x & 31) : static_cast<int>(threadIdx.x);
+  const int nthr = WARP ? 32 : static_cast<int>(blockDim.x);
+  auto sync = [] {
+    if constexpr (WARP) __syncwarp();
+    else __syncthreads();
+  };
+  for (int e = tid; e < n * n; e += nthr)
     V[(e / n) * ld + e % n] = make_double2((e / n) == (e % n) ? 1.0 : 0.0, 0.0);
-  if (threadIdx.x < 3) flag[threadIdx.x] = 0;
-  __syncthreads();
+  if (tid < 3) flag[tid] = 0;
+  sync();
   if (n < 2) return;
   const int npad = n + (n & 1);
   const int pairs = npad / 2;
-  const int nblk = pairs * pairs;
   const double tol2 = tol * tol, skip2 = abs_skip * abs_skip;
   int sweep = 0, round = 0;
   for (; sweep < max_sweeps; ++sweep) {
-    if (threadIdx.x == 0) rotated = 0;
-    __syncthreads();
+    if (tid == 0) rotated = 0;
+    sync();
     for (int r = 0; r < npad - 1; ++r, ++round) {
       // phase 1: rotation parameters of the round's disjoint pairs (reads A only)
-      if (threadIdx.x == 0) flag[(round + 1) % 3] = 0;  // last read two rounds ago
-      for (int pi = threadIdx.x; pi < pairs; pi += blockDim.x) {
+      if (tid == 0) flag[(round + 1) % 3] = 0;  // last read two rounds ago
+      for (int pi = tid; pi < pairs; pi += nthr) {
         int p = rr_pos(pi, r, npad), q = rr_pos(npad - 1 - pi, r, npad);
         if (p > q) { int t = p; p = q; q = t; }
         double c = 1.0, s = 0.0;
@@ -210,18 +221,31 @@ __device__ void herm_jacobi(double2* A, double2* V, int n, int ld, double tol, d
         js[pi] = s;
         je[pi] = e;
       }
-      __syncthreads();
+      sync();
       if (!flag[round % 3]) continue;  // nothing rotated: no writes, no second barrier
       // phase 2: A <- J^H A J per 2x2 block of pairs (i <= j, the mirror block is
       // its conjugate transpose), J = [[c, s], [-s conj(e), c conj(e)]]; V <- V J.
       {
-        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-        for (int i = warp; i < pairs; i += nw) {
+        const int lane = tid & 31, warp = tid >> 5, nw = nthr >> 5;
+        // WARP: lane -> block (i, j), i <= j, flattened; else warp -> i, lane -> j
+        const int nblk2 = pairs * (pairs + 1) / 2;
+        for (int bi = WARP ? lane : warp; bi < (WARP ? nblk2 : pairs); bi += WARP ? 32 : nw) {
+          int i = bi, j0 = i + lane, jstep = 32;
+          if constexpr (WARP) {  // unrank bi over the upper triangle of pairs
+            i = 0;
+            int rem = bi;
+            while (rem >= pairs - i) {
+              rem -= pairs - i;
+              ++i;
+            }
+            j0 = i + rem;
+            jstep = pairs;  // one block per lane
+          }
           const double sI = js[i], cI = jc[i];
           const double2 eI = je[i];
           const int ri0 = jp[i], ri1 = jq[i];
           const bool v0 = ri1 < n;
-          for (int j = i + lane; j < pairs; j += 32) {
+          for (int j = j0; j < pairs; j += jstep) {
             const double sJ = js[j];
             if (sI == 0.0 && sJ == 0.0) continue;
             const double cJ = jc[j];
@@ -258,8 +282,9 @@ __device__ void herm_jacobi(double2* A, double2* V, int n, int ld, double tol, d
             }
           }
         }
-        for (int k = warp; k < n; k += nw)
-          for (int j = lane; j < pairs; j += 32) {
+        for (int kk = WARP ? lane : warp; kk < (WARP ? n * pairs : n); kk += WARP ? 32 : nw)
+          for (int j = WARP ? kk % pairs : lane; j < pairs; j += WARP ? pairs : 32) {
+            const int k = WARP ? kk / pairs : kk;
             const double sj = js[j];
             const int q = jq[j];
             if (q >= n || sj == 0.0) continue;
@@ -270,14 +295,19 @@ __device__ void herm_jacobi(double2* A, double2* V, int n, int ld, double tol, d
             V[q * ld + k] = cadd(cscale(vkp, sj), cscale(vkq, cjv));
           }
       }
-      __syncthreads();
+      sync();
     }
     const int any = rotated;
-    __syncthreads();
+    sync();
     if (!any) break;
   }
-  if (sweep == max_sweeps && threadIdx.x == 0) atomicOr(status, kSmallNoConverge);
-  if (threadIdx.x == 0) atomicAdd(status + 7, sweep + 1);  // diagnostics: total sweeps
+  if (sweep == max_sweeps && tid == 0) atomicOr(status, kSmallNoConverge);
+  if (tid == 0) atomicAdd(status + 7, sweep + 1);  // diagnostics: total sweeps
+}
+
+__device__ void herm_jacobi(double2* A, double2* V, int n, int ld, double tol, double abs_skip, double low_skip,
+                            int max_sweeps, int* status) {
+  herm_jacobi_t<false>(A, V, n, ld, tol, abs_skip, low_skip, max_sweeps, status);
 }
 
 // ------------------------------------------------------------------ tridiagonal divide and conquer
@@ -933,9 +963,13 @@ __device__ void herm_eig_tridiag(double2* A, double2* V, int n, int ld, int* sta
 
 // Block-level gram_factors; X, V: n*n complex scratch each (column-major).
 // Outputs (P, R, deficient, any_def) are complete after the trailing barrier.
+// Largest k solved by the one-warp Jacobi under kEigAuto (divide and conquer
+// above; measured: k = 4 25 us vs 38 us, k = 8 66 us vs 58 us).
+constexpr int kWarpJacobiMax = 6;
+
 __device__ void gram_factors_dev(const double2* G, int n, double2* X, double2* V, double2* P, double2* R,
                                  int* deficient, int* any_def, int* status, double* lam_out = nullptr,
-                                 double2* vec_out = nullptr, bool use_jacobi = false) {
+                                 double2* vec_out = nullptr, int solver = 0) {
   __shared__ double lam[256];
   __shared__ int order[256];
   __shared__ double hmax[2];
@@ -992,10 +1026,14 @@ __device__ void gram_factors_dev(const double2* G, int n, double2* X, double2* V
   atomicMax(reinterpret_cast<unsigned long long*>(&sh_dmax), __double_as_longlong(dmax));
   __syncthreads();
   const double low_skip = vec_out ? 0.0 : 1e-12 * sh_dmax / n;
-  if (use_jacobi)
+  if (solver == kEigJacobi) {
     herm_jacobi(X, V, n, ld, neps, abs_skip, low_skip, 40, status);
-  else
+  } else if (solver == kEigAuto && n <= kWarpJacobiMax) {
+    if (threadIdx.x < 32) herm_jacobi_t<true>(X, V, n, ld, neps, abs_skip, low_skip, 40, status);
+    __syncthreads();
+  } else {
     herm_eig_tridiag(X, V, n, ld, status);
+  }
   for (int j = threadIdx.x; j < n; j += blockDim.x) lam[j] = scalbn(X[j * ld + j].x, gexp);
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
@@ -1043,7 +1081,7 @@ __global__ void __launch_bounds__(kEigThreads) gram_factors_kernel(const double2
                                                                 double2* vec_out) {
   extern __shared__ __align__(16) unsigned char sm[];
   double2* X = work ? work : reinterpret_cast<double2*>(sm);  // column-major n x (n+1)
-  gram_factors_dev(G, n, X, X + n * (n + 1), P, R, deficient, any_def, status, lam_out, vec_out, use_jacobi != 0);
+  gram_factors_dev(G, n, X, X + n * (n + 1), P, R, deficient, any_def, status, lam_out, vec_out, use_jacobi);
 }
 
 // ------------------------------------------------------------------ Cholesky
@@ -1418,7 +1456,7 @@ __global__ void __launch_bounds__(512) su_reduce_kernel(const SuSiteDesc* descs,
   }
   __syncthreads();
   // gram_orthogonalize(site as (env, d*s)) — decomposition.cpp:160-193
-  gram_factors_dev(G, S, X, V, P, Rm, def, &anyd, status);
+  gram_factors_dev(G, S, X, V, P, Rm, def, &anyd, status, nullptr, nullptr, kEigDivideConquer);
   for (int idx = threadIdx.x; idx < E * S; idx += blockDim.x) {
     const int j = idx / E, e = idx % E;
     double2 acc = make_double2(0.0, 0.0);
@@ -1621,7 +1659,7 @@ void gram_factors(const double2* G, int n, double2* P, double2* R, int* deficien
   }
   static const int env_threads = getenv("PEPSB_EIG_THREADS") ? atoi(getenv("PEPSB_EIG_THREADS")) : 0;
   const int threads = env_threads >= 64 && env_threads <= kEigThreads ? env_threads : kEigThreads;
-  const int use_jacobi = eig_solver() == kEigJacobi;
+  const int use_jacobi = eig_solver();
   static const char* dump = getenv("PEPSB_DUMP_EIG");  // debug aid: last input matrix to a file
   if (dump) {
     std::vector<double2> h(static_cast<size_t>(n) * n);
@@ -1646,14 +1684,15 @@ int eig_solver() {
   int v = g_eig_solver.load();
   if (v < 0) {  // PEPSB_EIG=jacobi selects the Jacobi solver before any option is set
     const char* e = getenv("PEPSB_EIG");
-    v = (e && std::string(e) == "jacobi") ? kEigJacobi : kEigDivideConquer;
+    v = (e && std::string(e) == "jacobi") ? kEigJacobi : (e && std::string(e) == "dc") ? kEigDivideConquer : kEigAuto;
     g_eig_solver.store(v);
   }
   return v;
 }
 
 void set_eig_solver(int s) {
-  if (s != kEigJacobi && s != kEigDivideConquer) throw Error(kValidationError, "eig_solver must be 0 or 1");
+  if (s != kEigAuto && s != kEigJacobi && s != kEigDivideConquer)
+    throw Error(kValidationError, "eig_solver must be 0 (auto), 1 (Jacobi) or 2 (divide and conquer)");
   g_eig_solver.store(s);
 }
 

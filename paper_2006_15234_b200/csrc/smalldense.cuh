@@ -31,9 +31,10 @@ void gram_factors(const double2* G, int n, double2* P, double2* R, int* deficien
                   double2* vec_out = nullptr);
 
 // Hermitian k x k eigensolver used by gram_factors / eigh_dense (process-wide):
+// kEigAuto = one-warp cyclic Jacobi for k <= 6 (latency-bound sizes), else
 // kEigDivideConquer = Householder tridiagonalisation + divide and conquer (the
-// zheevd route), kEigJacobi = two-sided cyclic Jacobi.
-enum EigSolver { kEigDivideConquer = 0, kEigJacobi = 1 };
+// zheevd route); kEigJacobi = block two-sided cyclic Jacobi for every k.
+enum EigSolver { kEigAuto = 0, kEigJacobi = 1, kEigDivideConquer = 2 };
 int eig_solver();
 void set_eig_solver(int s);
 

@@ -257,6 +257,53 @@ __global__ void zgemm_splitk_reduce(const ZgemmParams p) {
   }
 }
 
+// Small problems (the k x k products, scalars and thin chains of the
+// latency-bound configs): one thread per output element, a plain FMA loop over
+// K straight from global memory (L1/L2 resident).  The tiled DMMA kernels pay
+// ~2k instructions of pipeline prologue, index setup and epilogue per warp --
+// 8-14 us for a 4 x 16 x 4 product -- where this kernel finishes in ~2 us.
+__global__ void __launch_bounds__(128) zgemm_small_kernel(const ZgemmParams p) {
+  const int64_t MN = p.M * p.N;
+  for (int64_t bz = blockIdx.y; bz < p.batch; bz += gridDim.y) {
+    int64_t offA = 0, offB = 0, offC = 0, idx = bz;
+    for (int a = p.nb - 1; a >= 0; --a) {
+      const int64_t q = idx / p.bext[a], r = idx - q * p.bext[a];
+      offA += r * p.bsA[a];
+      offB += r * p.bsB[a];
+      offC += r * p.bsC[a];
+      idx = q;
+    }
+    const double sa = p.conjA ? -1.0 : 1.0, sb = p.conjB ? -1.0 : 1.0;
+    for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < MN;
+         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+      const int64_t i = e / p.N, j = e - (e / p.N) * p.N;
+      const double2* a = p.A + offA + i * p.sAi;
+      const double2* b = p.B + offB + j * p.sBj;
+      double re = 0.0, im = 0.0;
+#pragma unroll 4
+      for (int64_t k = 0; k < p.K; ++k) {
+        const double2 x = __ldg(a + k * p.sAk), y = __ldg(b + k * p.sBk);
+        const double xi = sa * x.y, yi = sb * y.y;
+        re = fma(x.x, y.x, re);
+        re = fma(-xi, yi, re);
+        im = fma(x.x, yi, im);
+        im = fma(xi, y.x, im);
+      }
+      double2* dst = p.C + offC + decode_offset(i, p.nr, p.rext, p.rstr) + decode_offset(j, p.nc, p.cext, p.cstr);
+      double2 v = make_double2(re, im);
+      if (p.accumulate) v = cadd(*dst, v);
+      *dst = v;
+    }
+  }
+}
+
+void launch_small(const ZgemmParams& p, cudaStream_t stream) {
+  const int64_t blocks = std::min<int64_t>((p.M * p.N + 127) / 128, 1024);
+  dim3 grid(static_cast<unsigned>(std::max<int64_t>(blocks, 1)), static_cast<unsigned>(std::min<int64_t>(p.batch, 65535)));
+  zgemm_small_kernel<<<grid, 128, 0, stream>>>(p);
+  PEPSB_LAUNCH();
+}
+
 template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool AK, bool BNC>
 void launch_cfg(const ZgemmParams& p, cudaStream_t stream) {
   using S = Smem<BM, BN, BK, AK, BNC>;
@@ -765,6 +812,24 @@ bool zgemm_real_enabled() {
 
 void zgemm_set_real(int on) { g_real.store(on ? 1 : 0); }
 
+std::atomic<int> g_small{-1};
+
+bool zgemm_small_enabled() {
+  int v = g_small.load();
+  if (v < 0) {
+    const char* e = getenv("PEPSB_GEMM_SMALL");
+    v = (e && e[0] == '0') ? 0 : 1;
+    g_small.store(v);
+  }
+  return v != 0;
+}
+
+void zgemm_set_small(int on) { g_small.store(on ? 1 : 0); }
+
+bool zgemm_is_small(const ZgemmParams& p) {
+  return zgemm_small_enabled() && p.K <= kSmallMaxK && p.M * p.N * p.batch * std::max<int64_t>(p.K, 1) <= kSmallMaxMacs;
+}
+
 int zgemm_ws_mode() {
   int v = g_ws.load();
   if (v < 0) {
@@ -781,6 +846,15 @@ bool zgemm_ws_enabled() { return zgemm_ws_mode() != 0; }
 void zgemm_set_ws(int mode) { g_ws.store(mode >= 0 && mode <= 2 ? mode : 0); }
 
 int64_t zgemm_plan_splits(ZgemmParams& p, int num_sms) {
+  p.num_sms = num_sms;
+  if (zgemm_is_small(p)) {
+    p.algo = kGemmSmall;
+    p.cfg = 0;
+    p.ws = 0;
+    p.splits = 1;
+    p.kchunk = std::max<int64_t>(p.K, 1);
+    return 0;
+  }
   // a real operand goes first (complex x real kernel), unless that breaks the
   // 64-wide tiling the kernel has
   const bool cr_ok = zgemm_real_enabled() && (p.realA || p.realB);
@@ -836,7 +910,9 @@ void zgemm_launch(ZgemmParams p, cudaStream_t stream) {
     // empty contraction: C = 0 (or unchanged when accumulating)
     p.splits = 1;
   }
-  if (p.algo == kGemmCR) {
+  if (p.algo == kGemmSmall) {
+    launch_small(p, stream);
+  } else if (p.algo == kGemmCR) {
     if (ak && bnc) launch_cr<true, true>(p, stream);
     else if (ak && !bnc) launch_cr<true, false>(p, stream);
     else if (!ak && bnc) launch_cr<false, true>(p, stream);

@@ -55,7 +55,14 @@ struct ZgemmParams {
 // kGemmCR: A real (imaginary parts exactly zero), C = A B as the real GEMM
 // A (M x K) . B' (K x 2N) on B's interleaved (re, im) doubles -- 2 real MACs
 // per complex MAC (set by zgemm_plan_splits when an operand is real).
-enum GemmAlgo { kGemm4M = 0, kGemm3M = 1, kGemm4C = 2, kGemmCR = 3 };
+// kGemmSmall: CUDA-core FMA kernel for problems below kSmallMaxMacs complex
+// MACs with K <= kSmallMaxK (set by zgemm_plan_splits; option "gemm_small").
+enum GemmAlgo { kGemm4M = 0, kGemm3M = 1, kGemm4C = 2, kGemmCR = 3, kGemmSmall = 4 };
+constexpr int64_t kSmallMaxK = 128;
+constexpr int64_t kSmallMaxMacs = int64_t{1} << 13;
+bool zgemm_small_enabled();
+void zgemm_set_small(int on);
+bool zgemm_is_small(const ZgemmParams& p);
 int zgemm_algo();
 // Real flops the DMMAs execute for a planned problem (8 per complex MAC, 6 for 3M).
 inline double zgemm_exec_flops(const ZgemmParams& p) {

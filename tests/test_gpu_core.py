@@ -273,6 +273,7 @@ def test_gemm_kernels_all_layouts(A, algo, ws):
     ctx = A.default_context()
     ctx.set_option("gemm_algo", algo)
     ctx.set_option("gemm_ws", ws)
+    ctx.set_option("gemm_small", 0)  # the tiled kernels on the tiny shapes too
     try:
         shapes = [(70, 90, 300), (64, 64, 64), (72, 72, 72), (128, 300, 64), (65, 70, 17), (5, 7, 3),
                   (200, 72, 130), (72, 200, 33), (64, 72, 64), (72, 64, 48), (33, 65, 129), (1, 1, 1),
@@ -292,6 +293,7 @@ def test_gemm_kernels_all_layouts(A, algo, ws):
     finally:
         ctx.set_option("gemm_algo", 1)
         ctx.set_option("gemm_ws", 0)
+        ctx.set_option("gemm_small", 1)
 
 
 @pytest.mark.parametrize("algo,ws", [(1, 1), (2, 1), (1, 2), (2, 2)], ids=["3m_ws", "4m_ws", "3m_tma", "4m_tma"])
@@ -340,6 +342,7 @@ def test_gemm_complex_by_real_operands(A):
     def real(shape):
         return rng.standard_normal(shape).astype(np.complex128)
 
+    ctx.set_option("gemm_small", 0)
     try:
         for (m, n, k) in [(128, 9000, 64), (64, 7000, 128), (70, 90, 300), (5, 7, 3), (64, 64, 64), (100, 300, 4000)]:
             ar, bc = real((m, k)), O.random_tensor((k, n), m + n)
@@ -358,3 +361,32 @@ def test_gemm_complex_by_real_operands(A):
         assert np.abs(got - ref).max() <= 1e-12 * np.abs(ref).max()
     finally:
         ctx.set_option("gemm_real", 1)
+        ctx.set_option("gemm_small", 1)
+
+
+def test_gemm_small_problem_kernel(A):
+    """Problems of at most 2^13 complex MACs (K <= 128) run the CUDA-core FMA
+    kernel: every operand layout, conjugation, batched and scattered outputs,
+    scalars and matrix-vector products, against numpy at rounding level."""
+    ctx = A.default_context()
+    ctx.set_option("gemm_small", 1)
+    for (m, n, k) in [(1, 1, 1), (4, 16, 4), (5, 7, 3), (8, 128, 4), (8, 8, 64), (4, 16, 128), (1, 300, 7), (72, 5, 20)]:
+        for sp in ["ik,kj->ij", "ki,kj->ij", "ik,jk->ij", "ki,jk->ij", "ik,kj->ji"]:
+            a = O.random_tensor((m, k) if sp[:2] == "ik" else (k, m), m * 7 + k)
+            b = O.random_tensor((k, n) if sp[3:5] == "kj" else (n, k), n * 5 + k)
+            got = A.contract(sp, a, b).numpy()
+            ref = np.einsum(sp, a, b)
+            assert np.abs(got - ref).max() <= 1e-13 * np.abs(ref).max(), (sp, m, n, k)
+        a = O.random_tensor((m, k), m + k)
+        b = O.random_tensor((k, n), n + k)
+        got = A.contract("ik,kj->ij", A.to_device(a).conj(), A.to_device(b).conj()).numpy()
+        ref = a.conj() @ b.conj()
+        assert np.abs(got - ref).max() <= 1e-13 * np.abs(ref).max()
+    a = O.random_tensor((3, 7, 4, 5), 91)
+    b = O.random_tensor((5, 3, 6, 2), 92)
+    got = A.contract("bipk,kbqj->qjbpi", a, b).numpy()
+    ref = np.einsum("bipk,kbqj->qjbpi", a, b)
+    assert np.abs(got - ref).max() <= 1e-13 * np.abs(ref).max()
+    ref = np.einsum("ab,b->a", a[0, :, 0, :4], b[0, 0, :4, 0])
+    got = A.contract("ab,b->a", a[0, :, 0, :4].copy(), b[0, 0, :4, 0].copy()).numpy()
+    assert np.abs(got - ref).max() <= 1e-13 * np.abs(ref).max()

@@ -54,7 +54,7 @@ def _cases():
 CASES = _cases()
 
 
-@pytest.fixture(params=[0, 1], ids=["dc", "jacobi"])
+@pytest.fixture(params=[0, 1, 2], ids=["auto", "jacobi", "dc"])
 def solver(A, request):
     ctx = A.default_context()
     ctx.set_option("eig_solver", request.param)
@@ -103,7 +103,7 @@ def test_eigh_rejects_non_hermitian(A, solver):
         A.eigh(m)
 
 
-@pytest.mark.parametrize("solver", [0, 1], ids=["dc", "jacobi"])
+@pytest.mark.parametrize("solver", [0, 1, 2], ids=["auto", "jacobi", "dc"])
 def test_eigh_scale_invariant_extreme_magnitudes(A, solver):
     """Gram matrices of unnormalised states reach |G| ~ 1e171 (8x8 TFIM after
     100 ITE steps); squares of such entries overflow.  The solver scales by an

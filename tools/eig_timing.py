@@ -9,7 +9,7 @@ for n in (4, 8, 12, 16, 24, 32, 41, 48, 64, 72):
     a = O.random_tensor((3 * n, n), n)
     g = a.conj().T @ a  # Gram-like, positive definite
     res = []
-    for solver in (0, 1):
+    for solver in (0, 2, 1):
         ctx.set_option("eig_solver", solver)
         for _ in range(3):
             A.gram_factors(g)
@@ -19,5 +19,5 @@ for n in (4, 8, 12, 16, 24, 32, 41, 48, 64, 72):
         rep = ctx.profile_report()
         ctx.profile(False)
         res.append(rep["small"]["ms"] / max(1, rep["small"]["launches"]))
-    print(n, "dc %.4f ms  jacobi %.4f ms" % tuple(res), flush=True)
+    print(n, "auto %.4f ms  dc %.4f ms  jacobi %.4f ms" % tuple(res), flush=True)
 ctx.set_option("eig_solver", 0)
