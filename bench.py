@@ -345,10 +345,16 @@ def norm_timings(A, ctx):
         n = cfg["rows"]
         st = A.PepsState(n, n, 2, cfg["sites"], ctx=ctx)
         opt = A.ContractOption.two_layer_opt(m, cfg["seed"], q, os_)
-        ctx.sync()
-        t0 = time.perf_counter()
-        A.contract_two_layer(st, st, opt)
-        out[name] = time.perf_counter() - t0
+        reps = 3 if n <= 16 else 1  # config 3: warm-up + median of 3 (0.4 s each); config 5: one cold-ish shot
+        if reps > 1:
+            A.contract_two_layer(st, st, opt)
+        ts = []
+        for _ in range(reps):
+            ctx.sync()
+            t0 = time.perf_counter()
+            A.contract_two_layer(st, st, opt)
+            ts.append(time.perf_counter() - t0)
+        out[name] = sorted(ts)[len(ts) // 2]
         del st
     plus = [np.array([1, 1], dtype=complex).reshape(2, 1, 1, 1, 1) / np.sqrt(2) for _ in range(64)]
     st = A.PepsState(8, 8, 2, plus, ctx=ctx)
