@@ -194,7 +194,7 @@ int pepsb_ctx_set_option(pepsb_ctx* c, const char* key, int64_t value) {
     else if (k == "gemm_real") zgemm_set_real(static_cast<int>(value));
     else if (k == "gemm_small") zgemm_set_small(static_cast<int>(value));
     else if (k == "overlap") c->ctx->overlap = static_cast<int>(std::clamp<int64_t>(value, 0, 2));
-    else if (k == "concurrent_sweeps") c->ctx->concurrent_sweeps = value != 0 ? 1 : 0;
+    else if (k == "concurrent_sweeps") c->ctx->concurrent_sweeps = static_cast<int>(std::clamp<int64_t>(value, -1, 1));
     else if (k == "pipeline_rows") c->ctx->pipeline_rows = static_cast<int>(std::clamp<int64_t>(value, -1, 8));
     else throw Error(kConfigError, "unknown option '" + k + "'");
   });

@@ -114,7 +114,7 @@ HostTimer::~HostTimer() {
 Ctx::Ctx(int dev) : device(dev) {
   trace = getenv("PEPSB_TRACE") != nullptr;
   if (const char* e = getenv("PEPSB_OVERLAP")) overlap = e[0] == '0' ? 0 : e[0] == '2' ? 2 : 1;
-  if (const char* e = getenv("PEPSB_CONCURRENT_SWEEPS")) concurrent_sweeps = e[0] != '0';
+  if (const char* e = getenv("PEPSB_CONCURRENT_SWEEPS")) concurrent_sweeps = std::atoi(e);
   if (const char* e = getenv("PEPSB_PIPELINE_ROWS")) pipeline_rows = std::atoi(e);
   PEPSB_CUDA(cudaSetDevice(dev));
   PEPSB_CUDA(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev));

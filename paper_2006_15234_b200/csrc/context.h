@@ -170,8 +170,11 @@ class Ctx {
   // the column extent is >= 2^15 (default), 2 always.
   int overlap = 1;
   // build_row_cache: run the bottom sweep on a helper context from a second
-  // host thread, concurrently with the top sweep (option "concurrent_sweeps").
-  int concurrent_sweeps = 1;
+  // host thread, concurrently with the top sweep (option "concurrent_sweeps":
+  // -1 auto = when max_rank <= 48, where the sweeps are latency-bound; at
+  // config 5's m = 64 one sweep already fills the GPU and two contend: 26.0 s
+  // concurrent vs 22.3 s sequential; 0 off; 1 on).
+  int concurrent_sweeps = -1;
   // contract_two_layer: consecutive rows on two contexts, a few columns apart
   // (option "pipeline_rows").
   int pipeline_rows = -1;  // rows in flight K (< 2: sequential; -1: automatic, peps.cpp pipeline_depth)

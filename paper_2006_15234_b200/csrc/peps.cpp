@@ -391,7 +391,9 @@ RowCacheD build_row_cache(Ctx& ctx, const PepsStateD& s, const ContractOptD& opt
   std::vector<BoundaryD> fb;
   const bool pipe = pipeline_depth(ctx, opt) >= 2 && s.rows >= 3 && s.rows * s.cols >= 64;
   const int K = pipe ? std::min(pipeline_depth(ctx, opt), s.rows - 1) : 1;
-  if (ctx.concurrent_sweeps && s.rows > 1) {
+  const bool concurrent = ctx.concurrent_sweeps > 0 ||
+                          (ctx.concurrent_sweeps < 0 && opt.trunc.max_rank != 0 && opt.trunc.max_rank <= 48);
+  if (concurrent && s.rows > 1) {
     // contexts: [ctx, helpers 0 .. K-2] run the top sweep, [helpers K-1 .. 2K-2]
     // the bottom one, from a second host thread
     std::vector<Ctx*> all = pipeline_contexts(ctx, 2 * K);

@@ -120,6 +120,36 @@ def test_flip_vertical_and_bottom_sweep(A, refo):
     assert abs(v - w) / abs(w) < 1e-2
 
 
+def test_row_cache_scheduling_is_bitwise_invariant(A):
+    """build_row_cache / contract_two_layer under every host schedule -- the
+    K-deep row pipeline (pipeline_rows 0, 2, 3) and the concurrent top/bottom
+    sweeps (concurrent_sweeps 0, 1) -- run the same kernel sequence per
+    boundary, so every cached boundary is bitwise identical (8 x 8 lattice:
+    64 sites, where the pipeline engages)."""
+    ctx = A.default_context()
+    sites = I.random_peps(8, 8, 2, 17, scale=1 / np.sqrt(8))
+    st = A.PepsState(8, 8, 2, sites)
+    opt = A.ContractOption.two_layer_opt(8, 5, 1, -1)
+    runs = []
+    try:
+        for pr, cs in [(0, 0), (2, 0), (3, 1), (2, 1)]:
+            ctx.set_option("pipeline_rows", pr)
+            ctx.set_option("concurrent_sweeps", cs)
+            cache = A.build_row_cache(st, opt)
+            runs.append(([[s.numpy() for s in t.sites] for t in cache.tops],
+                         [[s.numpy() for s in b.sites] for b in cache.bots],
+                         A.contract_two_layer(st, st, opt)))
+    finally:
+        ctx.set_option("pipeline_rows", -1)
+        ctx.set_option("concurrent_sweeps", -1)
+    tops0, bots0, norm0 = runs[0]
+    for tops, bots, norm in runs[1:]:
+        assert norm == norm0
+        for a, b in zip(tops + bots, tops0 + bots0):
+            assert all(np.array_equal(x, y) for x, y in zip(a, b))
+    assert A.chain_scalar(A.build_row_cache(st, opt).tops[7]) == norm0
+
+
 def test_row_cache_and_bands_match_reference(A, golden):
     sites = I.random_peps(4, 4, 2, 91, scale=1 / np.sqrt(8))
     st = A.PepsState(4, 4, 2, sites)
