@@ -118,8 +118,17 @@ Ctx::Ctx(int dev) : device(dev) {
   if (const char* e = getenv("PEPSB_PIPELINE_ROWS")) pipeline_rows = std::atoi(e);
   PEPSB_CUDA(cudaSetDevice(dev));
   PEPSB_CUDA(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev));
-  PEPSB_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
-  PEPSB_CUDA(cudaStreamCreateWithFlags(&side_stream, cudaStreamNonBlocking));
+  // The main stream carries the latency chain (Gram -> one-block eigensolver ->
+  // small factors) while the side stream runs the overlapped operator
+  // applications, whose CTAs fill every SM; with the main stream at the
+  // higher priority the eigensolver's block is dispatched to the first SM
+  // that drains instead of queueing behind the whole GEMM grid.
+  // PEPSB_STREAM_PRIORITY=0 creates both at the default priority.
+  int least = 0, greatest = 0;
+  const char* pe = getenv("PEPSB_STREAM_PRIORITY");
+  if (!(pe && pe[0] == '0')) PEPSB_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+  PEPSB_CUDA(cudaStreamCreateWithPriority(&stream, cudaStreamNonBlocking, greatest));
+  PEPSB_CUDA(cudaStreamCreateWithPriority(&side_stream, cudaStreamNonBlocking, least));
   PEPSB_CUDA(cudaEventCreateWithFlags(&fork_event, cudaEventDisableTiming));
   PEPSB_CUDA(cudaEventCreateWithFlags(&join_event, cudaEventDisableTiming));
   main_stream = stream;

@@ -191,6 +191,20 @@ LTensor orth(Ctx& ctx, const LTensor& Y) {
   return out;
 }
 
+// Fork the side stream after the Gram GEMM rather than before it: the side
+// stream's operator application then becomes ready together with the
+// eigensolver, and the main stream's higher priority dispatches the
+// eigensolver's block first instead of behind the whole application grid
+// (its 214 KB of shared memory cannot co-reside with a GEMM CTA).
+// PEPSB_FORK_AFTER_GRAM=0 forks before the Gram GEMM.
+bool fork_after_gram() {
+  static const bool v = [] {
+    const char* e = getenv("PEPSB_FORK_AFTER_GRAM");
+    return !(e && e[0] == '0');
+  }();
+  return v;
+}
+
 // apply(orth(Z)) for the big-side orthogonalisation of a power iteration,
 // with the k x k eigensolver hidden behind the operator application: by
 // linearity A (Z P) = (A Z) P, so A Z runs on the side stream while the Gram
@@ -204,9 +218,11 @@ template <class ApplyFn>
 LTensor apply_orth_speculative(Ctx& ctx, const LTensor& Z, ApplyFn&& apply) {
   const int64_t k = Z.ext.back();
   const int64_t rows = Z.size() / k;
-  ctx.fork();
+  const bool late = fork_after_gram();
+  if (!late) ctx.fork();
   BufPtr G = ctx.alloc(k * k);
   mm(ctx, G->p, Z.ptr, true, true, Z.ptr, false, false, k, k, rows);
+  if (late) ctx.fork();
   BufPtr P = ctx.alloc(k * k), R = ctx.alloc(k * k), def = ctx.alloc((k + 2 + 1) / 2 + 1);
   int* d_def = reinterpret_cast<int*>(def->p);
   int* d_any = d_def + k;
@@ -276,9 +292,11 @@ LTensor adjoint_orth_speculative(Ctx& ctx, const LTensor& Y, ContractionPlan& pl
     return plan_adj.execute(ctx, leaves_adj);
   };
   if (node < 0) return plain();
-  ctx.fork();
+  const bool late = fork_after_gram();
+  if (!late) ctx.fork();
   BufPtr G = ctx.alloc(k * k);
   mm(ctx, G->p, Y.ptr, true, true, Y.ptr, false, false, k, k, rows);
+  if (late) ctx.fork();
   BufPtr P = ctx.alloc(k * k), R = ctx.alloc(k * k), def = ctx.alloc((k + 2 + 1) / 2 + 1);
   int* d_def = reinterpret_cast<int*>(def->p);
   int* d_any = d_def + k;
