@@ -1074,13 +1074,18 @@ __device__ void gram_factors_dev(const double2* G, int n, double2* X, double2* V
   __syncthreads();
 }
 
+// SMEM: the two n x (n+1) work matrices live in dynamic shared memory and the
+// pointers derive from the __shared__ array, so the inlined solvers use
+// LDS/STS instead of generic loads (which the profile showed waiting on the
+// long scoreboard); otherwise they live in the global `work` buffer.
+template <bool SMEM>
 __global__ void __launch_bounds__(kEigThreads) gram_factors_kernel(const double2* G, int n, double2* P,
                                                                 double2* R, int* deficient,
                                                                 int* any_def, int* status,
                                                                 double2* work, int use_jacobi, double* lam_out,
                                                                 double2* vec_out) {
   extern __shared__ __align__(16) unsigned char sm[];
-  double2* X = work ? work : reinterpret_cast<double2*>(sm);  // column-major n x (n+1)
+  double2* X = SMEM ? reinterpret_cast<double2*>(sm) : work;  // column-major n x (n+1)
   gram_factors_dev(G, n, X, X + n * (n + 1), P, R, deficient, any_def, status, lam_out, vec_out, use_jacobi);
 }
 
@@ -1653,7 +1658,7 @@ void gram_factors(const double2* G, int n, double2* P, double2* R, int* deficien
   if (!fits && !work) throw Error(kOtherError, "gram_factors: workspace required");
   static bool attr = false;
   if (!attr) {
-    PEPSB_CUDA(cudaFuncSetAttribute(gram_factors_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    PEPSB_CUDA(cudaFuncSetAttribute(gram_factors_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     static_cast<int>(kCap)));
     attr = true;
   }
@@ -1670,9 +1675,12 @@ void gram_factors(const double2* G, int n, double2* P, double2* R, int* deficien
       fclose(f);
     }
   }
-  gram_factors_kernel<<<1, threads, fits ? smem : 0, stream>>>(G, n, P, R, deficient, any_def, status,
-                                                                fits ? nullptr : work, use_jacobi, lam_out,
-                                                                vec_out);
+  if (fits)
+    gram_factors_kernel<true><<<1, threads, smem, stream>>>(G, n, P, R, deficient, any_def, status, nullptr,
+                                                            use_jacobi, lam_out, vec_out);
+  else
+    gram_factors_kernel<false><<<1, threads, 0, stream>>>(G, n, P, R, deficient, any_def, status, work,
+                                                          use_jacobi, lam_out, vec_out);
   PEPSB_LAUNCH();
 }
 
