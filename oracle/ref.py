@@ -315,6 +315,15 @@ def run_ite(rows, cols, J, h, tau, steps, evolution_rank, contraction_rank, rsvd
     return e, t
 
 
+def vqe_ansatz(rows, cols, layers, theta, evolution_rank, J, h, contraction_rank, rsvd_iters, seed):
+    """vqe_ansatz_state (drivers.cpp:100-131) + its TFIM energy (run_vqe objective): (sites, energy)."""
+    th = np.ascontiguousarray(theta, dtype=np.float64)
+    t, dd = _bag(_fn("ref_vqe_ansatz")(int(rows), int(cols), int(layers), C.c_void_p(th.ctypes.data),
+                                       C.c_uint64(evolution_rank), C.c_double(J), C.c_double(h),
+                                       C.c_uint64(contraction_rank), int(rsvd_iters), C.c_uint64(seed)))
+    return t, float(dd[0])
+
+
 def apply_distant(sites, rows, cols, gate, a, b, max_rank=0, d=2):
     tl, args = _state_args(sites, rows, cols, d)
     g = np.ascontiguousarray(gate, dtype=np.complex128)

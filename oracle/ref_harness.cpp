@@ -559,6 +559,34 @@ Bag* ref_run_ite(int rows, int cols, double J, double h, double tau, int steps, 
   });
 }
 
+// vqe_ansatz_state (drivers.cpp:100-131) and its energy under the TFIM in
+// colour order (state_energy, drivers.cpp:46-53, seed derive_seed(seed, 0xF)
+// as run_vqe's objective): sites, then [energy].
+Bag* ref_vqe_ansatz(int rows, int cols, int layers, const double* theta, uint64_t evolution_rank, double J, double h,
+                    uint64_t contraction_rank, int rsvd_iters, uint64_t seed) {
+  return guarded([&](Bag& b) {
+    VqeConfig cfg;
+    cfg.rows = rows;
+    cfg.cols = cols;
+    cfg.layers = static_cast<std::size_t>(layers);
+    cfg.evolution_rank = static_cast<std::size_t>(evolution_rank);
+    std::vector<double> th(theta, theta + static_cast<std::size_t>(layers) * rows * cols);
+    PepsState st = vqe_ansatz_state(cfg, th);
+    for (const auto& t : st.sites()) b.tensors.push_back(t);
+    // state_energy / energy_contract_option are file-local in drivers.cpp:
+    // the same options through the public expectation()
+    ExpectationOptions eo;
+    eo.contract.family = ContractFamily::two_layer_ibmps;
+    eo.contract.trunc.max_rank = static_cast<std::size_t>(contraction_rank);
+    eo.contract.strategy = SvdStrategy::implicit_rsvd;
+    eo.contract.rsvd.power_iters = rsvd_iters;
+    eo.contract.seed = derive_seed(seed, 0xF);
+    eo.use_cache = true;
+    eo.shared_environments = true;
+    b.doubles.push_back(expectation(st, tfim_colour_order(rows, cols, J, h), eo).value);
+  });
+}
+
 // apply_distant (state.cpp:206-236): SWAP-routed two-site gate.
 Bag* ref_apply_distant(int rows, int cols, int d, const int* ndims, const int64_t* shapes,
                        const double* const* datas, const double* gate, int ar, int ac, int br, int bc,

@@ -979,6 +979,69 @@ def apply_two_site(s: PepsState, gate, bonds: Sequence[Tuple[int, int, int, int]
     return _wrap_state(h, s)
 
 
+def Ry(theta: float) -> np.ndarray:
+    """gates::Ry (state.cpp:316-319): [[cos t/2, -sin t/2], [sin t/2, cos t/2]]."""
+    c, s_ = np.cos(theta / 2), np.sin(theta / 2)
+    return np.array([[c, -s_], [s_, c]], dtype=np.complex128)
+
+
+# gates::CNOT (state.cpp:345-353): control = first site, g[c, t, c', t'] = <c t|CNOT|c' t'>
+CNOT = np.zeros((2, 2, 2, 2), dtype=np.complex128)
+for _c in range(2):
+    for _t in range(2):
+        CNOT[_c, _t ^ _c, _c, _t] = 1.0
+
+
+def state_energy(s: PepsState, terms: Sequence[LocalTerm], contraction_rank: int, rsvd_iters: int,
+                 seed: int) -> float:
+    """state_energy (drivers.cpp:46-53) for the two-layer IBMPS family: the
+    expectation with cached, shared environments (energy_contract_option,
+    drivers.cpp:33-44)."""
+    opt = ExpectationOptions(ContractOption.two_layer_opt(contraction_rank, seed, rsvd_iters), True, True, False)
+    return expectation(s, terms, opt).value
+
+
+def vqe_ansatz_state(rows: int, cols: int, layers: int, theta: Sequence[float], evolution_rank: int = 2,
+                     ctx: Optional[Context] = None) -> PepsState:
+    """vqe_ansatz_state (drivers.cpp:100-131): from |0...0>, per layer an Ry on
+    every site (row-major), then CNOTs on every horizontal bond (row-major,
+    control left) and every vertical bond (control on top), each a QR-reduced
+    simple update truncated to evolution_rank (rel. cutoff 1e-14)."""
+    theta = list(theta)
+    if len(theta) != layers * rows * cols:
+        raise PepsError(5, "theta length must be layers * rows * cols")
+    st = computational_basis(rows, cols, [0] * (rows * cols), ctx=ctx)
+    pol = TruncationPolicy(evolution_rank, 1e-14)
+    p = 0
+    for _ in range(layers):
+        for r in range(rows):
+            for c in range(cols):
+                st = apply_one_site(st, Ry(theta[p]), [(r, c)])
+                p += 1
+        for r in range(rows):
+            for c in range(cols - 1):
+                st = apply_two_site(st, CNOT, [(r, c, r, c + 1)], pol)
+        for r in range(rows - 1):
+            for c in range(cols):
+                st = apply_two_site(st, CNOT, [(r, c, r + 1, c)], pol)
+    return st
+
+
+def vqe_objective(rows: int, cols: int, layers: int, terms: Sequence[LocalTerm], evolution_rank: int = 2,
+                  contraction_rank: int = 16, rsvd_iters: int = 1, seed: int = 0,
+                  ctx: Optional[Context] = None):
+    """The objective run_vqe minimises (drivers.cpp:166-171): theta -> energy of
+    vqe_ansatz_state(theta), state_energy seeded derive_seed(seed, 0xF).  The
+    host-side optimiser loop (optimize.cpp) is left to the caller."""
+    from .inputs import derive_seed
+    es = derive_seed(seed, 0xF)
+
+    def f(theta):
+        st = vqe_ansatz_state(rows, cols, layers, theta, evolution_rank, ctx)
+        return state_energy(st, terms, contraction_rank, rsvd_iters, es)
+    return f
+
+
 def ite_tfim(s: PepsState, J: float, h: float, tau: float, steps: int, rank: int) -> PepsState:
     """TFIM imaginary-time evolution by batched simple update (config 4)."""
     out = _VP()

@@ -501,3 +501,43 @@ def test_inner_product_families_and_amplitude(A, refo):
     amp = A.amplitude(st, bits, A.ContractFamily.exact)
     grid = [np.einsum("p,puldr->uldr", np.eye(2)[b], t) for b, t in zip(bits, sites)]
     assert abs(amp - refo.contract_one_layer(grid, 3, 3, 0)) <= 1e-10 * abs(amp)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("rank,tol", [(8, 5e-8), (2, 1e-6)], ids=["untruncated", "truncated"])
+def test_vqe_ansatz_and_energy_match_reference(A, refo, rank, tol):
+    """vqe_ansatz_state (drivers.cpp:100-131: Ry layer, row-major horizontal
+    then vertical CNOT simple updates) and the run_vqe objective (state_energy
+    of the TFIM, seed derive_seed(seed, 0xF)) against the reference at a random
+    theta; final states compared by exact contraction (norm, fidelity).  At
+    evolution rank 8 no rank cap binds and the circuit is unitary (norm 1), but
+    the Gram-route QR of the simple update clamps the rank-deficient
+    environments of these near-product states at 1e-12 lambda_max, which loses
+    8.6e-9 of the norm in the reference and 1.8e-8 on the device: the bar is
+    5e-8, and both must be within it of the exact norm 1.  At rank 2 every
+    CNOT truncates and the reference itself moves the norm by 1.4e-8 / 1.4e-7
+    under a 1e-14 / 1e-13 relative perturbation of theta, so the bar is 1e-6.
+    Energies (m = 8 randomized contraction) to 1e-6 in both cases.  The
+    objective equals state_energy bitwise."""
+    rows, cols, layers, J, h, seed = 3, 3, 2, 1.0, 0.7, 11
+    theta = np.random.default_rng(4).uniform(-np.pi, np.pi, layers * rows * cols)
+    want, e_w = refo.vqe_ansatz(rows, cols, layers, theta, rank, J, h, 8, 1, seed)
+    st = A.vqe_ansatz_state(rows, cols, layers, theta, rank)
+    got = [s.numpy() for s in st.sites]
+    assert [g.shape for g in got] == [w.shape for w in want]
+    n_g, n_w = O.inner_exact(got, rows, cols), O.inner_exact(want, rows, cols)
+    assert abs(n_g - n_w) / abs(n_w) < tol
+    if rank == 8:
+        assert abs(n_g - 1) < tol and abs(n_w - 1) < tol
+    mix = O.inner_exact_pair(want, got, rows, cols)
+    assert abs(abs(mix) / np.sqrt(abs(n_g) * abs(n_w)) - 1) < tol
+    terms = A.tfim_terms(rows, cols, J, h)
+    f = A.vqe_objective(rows, cols, layers, terms, rank, 8, 1, seed)
+    e_g = f(theta)
+    # the energy contracts at m = 8 with a randomized SVD: its truncations
+    # amplify the 1e-8 state differences (measured 2.5e-7 at rank 8)
+    assert abs(e_g - e_w) <= 1e-6 * max(1.0, abs(e_w)), (e_g, e_w)
+    from paper_2006_15234_b200.inputs import derive_seed
+    assert e_g == A.state_energy(st, terms, 8, 1, derive_seed(seed, 0xF))
+    with pytest.raises(A.PepsError):
+        A.vqe_ansatz_state(rows, cols, layers, theta[:-1])

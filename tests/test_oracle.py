@@ -100,3 +100,30 @@ def test_reference_peps_container_round_trip(refo, tmp_path):
     back, rows, cols, d = refo.load_peps(tmp_path / "s.peps")
     assert (rows, cols, d) == (3, 2, 2)
     assert all(np.array_equal(a, b) for a, b in zip(sites, back))
+
+
+def _classical_tfim_energy(bits, rows, cols, J):
+    z = [1 - 2 * b for b in bits]
+    e = sum(-J * z[r * cols + c] * z[r * cols + c + 1] for r in range(rows) for c in range(cols - 1))
+    return e + sum(-J * z[r * cols + c] * z[(r + 1) * cols + c] for r in range(rows - 1) for c in range(cols))
+
+
+def test_reference_vqe_ansatz_known_answers(refo):
+    """vqe_ansatz_state (drivers.cpp:100-131) pinned by closed forms: zero
+    layers is |0...0>; one layer at theta = pi flips every site (Ry(pi)|0> =
+    |1>) and the CNOT cascade (horizontal row-major, then vertical) maps the
+    basis state classically.  Basis states have <X> = 0, so the TFIM energy
+    (H = -J sum ZZ - h sum X) is the classical ZZ sum."""
+    rows, cols, J, h = 2, 3, 1.0, 0.5
+    _, e0 = refo.vqe_ansatz(rows, cols, 0, [], 2, J, h, 8, 1, 3)
+    assert abs(e0 - _classical_tfim_energy([0] * 6, rows, cols, J)) < 1e-12
+    bits = [1] * (rows * cols)
+    for r in range(rows):
+        for c in range(cols - 1):
+            bits[r * cols + c + 1] ^= bits[r * cols + c]
+    for r in range(rows - 1):
+        for c in range(cols):
+            bits[(r + 1) * cols + c] ^= bits[r * cols + c]
+    sites, e1 = refo.vqe_ansatz(rows, cols, 1, [np.pi] * (rows * cols), 2, J, h, 8, 1, 3)
+    assert len(sites) == rows * cols
+    assert abs(e1 - _classical_tfim_energy(bits, rows, cols, J)) < 1e-12
