@@ -79,7 +79,12 @@ int pepsb_last_error_kind(void);
 int pepsb_ctx_create(int device, pepsb_ctx** out);
 int pepsb_ctx_destroy(pepsb_ctx* ctx);
 int pepsb_ctx_sync(pepsb_ctx* ctx);
-/* keys: "orth_mode" (0 reference Gram-eigh, 1 CholeskyQR2) */
+/* keys: "orth_mode" (0 reference Gram-eigh, 1 CholeskyQR2),
+ * "eig_solver" (0 auto, 1 Jacobi, 2 divide and conquer; process-wide),
+ * "gemm_algo" (0 4M real embedding, 1 3M, 2 4M complex fragments), "gemm_real",
+ * "gemm_small", "gemm_ws" (process-wide GEMM kernel choices), "overlap" (0..2),
+ * "pipeline_rows" (-1 auto, 0..8), "concurrent_sweeps" (-1 auto, 0, 1).
+ * Unknown keys fail with ConfigError. */
 int pepsb_ctx_set_option(pepsb_ctx* ctx, const char* key, int64_t value);
 /* out[0..5] = flops (instr::flops convention, instrument.hpp:19-65),
  * einsumsvd_flops, peak_elements, kernel launches issued by the library,
@@ -159,7 +164,8 @@ int pepsb_projected_svd(pepsb_ctx* ctx, const pepsb_tensor* z, int64_t target, p
 
 /* eigh(Tensor) (linalg.hpp:41, linalg.cpp:256-295): values descending (capacity cap),
  * vectors n x n with column j the phase-fixed eigenvector j.  n <= 256.  The
- * solver is process-wide option "eig_solver" (0 divide and conquer, 1 Jacobi). */
+ * solver is process-wide option "eig_solver" (0 auto: one-warp Jacobi for n <= 6,
+ * else divide and conquer; 1 Jacobi; 2 divide and conquer). */
 int pepsb_eigh(pepsb_ctx* ctx, const pepsb_tensor* a, double* values, int64_t cap, pepsb_tensor** vectors);
 
 /* svd(Tensor, split) (linalg.hpp:21-22); s has capacity s_cap, *k = min extent */
