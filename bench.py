@@ -8,14 +8,27 @@ N(0,1)), truncated back to m = 64 by implicit randomized SVD with oversample 8
 (k = 72) and 2 power iterations; sketch seeded as the reference does
 (derive_seed(seed, 0x20, row, col)).  One step = one row absorb = 7 einsumsvd.
 
-metric/unit: BASELINE.json's metric, reported as einsumsvd FP64 TFLOP/s =
-4 x (the reference's own instr::flops count of the row absorb, reproduced
-exactly by paper_2006_15234_b200/costmodel.py and pinned against the oracle in
-tests/test_costmodel.py) / time.  ms_per_step is the seconds-per-row-absorb
-figure.  Inputs (611 MB of intermediates per apply) exceed the 126 MB L2, so no
-explicit flush is needed between steps.
+metric/unit: BASELINE.json's metric as einsumsvd FP64 TFLOP/s = the row's
+ALGORITHMIC real FP64 flops / time, counted the SURVEY §8(d) real-aware way:
+the reference's own contraction order and instr::flops terms
+(paper_2006_15234_b200/costmodel.py, pinned against the reference counter in
+tests/test_costmodel.py), 8 real flops per complex multiply-add, 4 where one
+operand is a real PEPS site (the BASELINE PEPS are real).  2.067e12 flops per
+config-2 row.  The reference-counter rate (4 x instr::flops = 2.750e12 per row,
+every product counted complex) is reported beside it as
+``value_reference_counter``.  ms_per_step is the seconds-per-row-absorb figure.
+Inputs (611 MB of intermediates per apply) exceed the 126 MB L2, so no explicit
+flush is needed between steps.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+--impl reference: the compiled reference (oracle/_ref: the unmodified
+reference sources + OpenBLAS, all host threads) on rank 0; each step is one
+ImplicitOperator::apply + adjoint_apply (implicit.cpp:66-100) at the config-2
+interior-column size (the operator applications are 84 % of an einsumsvd's
+flops; a whole column takes ~27 s on 16 cores, so K = 20 columns would not fit
+"a few minutes"); rate = the same real-aware flop count of those two calls /
+their time.
 
 N > 1 (torchrun): the row-absorb chain is sequential, so ranks run
 independent replicas (scaling "weak"); value = sum of all ranks' work / max
@@ -42,21 +55,41 @@ from paper_2006_15234_b200 import costmodel, inputs  # noqa: E402
 METRIC = "PEPS boundary-contraction s/norm; einsumsvd FP64 TFLOP/s & % of DMMA peak"
 UNIT = "TFLOP/s"
 L, R, M, Q, OS = 8, 8, 64, 2, 8
+COLUMN_LABELS = ["apqsmn", "uvst", "dumbe", "dvncf"]
+COLUMN_SHAPES = [(M, R, R, M, R, R), (R, R, M, M), (2, R, R, R, R), (2, R, R, R, R)]
+COLUMN_REAL = [False, False, True, True]  # pending v, top site S complex; bra/ket real
 
 
-def workload_config(extra=None):
-    cfg = {"workload": "config2: two_layer_apply_row, boundary L=8 m=64, PEPS row r=8 d=2, implicit rSVD k=72 q=2",
-           "length": L, "bond_r": R, "boundary_m": M, "oversample": OS, "power_iters": Q, "probe_k": M + OS,
-           "data_layout": "complex128 row-major (reference Tensor layout)",
-           "l2": "inputs+intermediates (>600 MB per apply) exceed the 126 MB L2; no flush needed",
-           "parallelism": "replicas"}
-    if extra:
-        cfg.update(extra)
-    return cfg
+def workload_config(world=1):
+    """Identical in both arms (the driver compares them)."""
+    return {"workload": "config2: two_layer_apply_row, boundary L=8 m=64, PEPS row r=8 d=2, implicit rSVD k=72 q=2",
+            "length": L, "bond_r": R, "boundary_m": M, "oversample": OS, "power_iters": Q, "probe_k": M + OS,
+            "data_layout": "complex128 row-major (reference Tensor layout)",
+            "l2": "inputs+intermediates (>600 MB per apply) exceed the 126 MB L2; no flush needed",
+            "flop_count": "real-aware algorithmic (SURVEY 8(d)): 8 real flops per complex MAC, 4 with a real "
+                          "PEPS-site operand; reference contraction order",
+            "parallelism": f"replicas x{world}"}
 
 
 def alg_flops_row():
+    """Real-aware algorithmic real flops of one config-2 row absorb (2.067e12)."""
+    return 4 * costmodel.two_layer_row_flops(L, R, M, Q, OS, real_sites=True)
+
+
+def refcounter_flops_row():
+    """4 x the reference's instr::flops of one config-2 row absorb (2.750e12)."""
     return 4 * costmodel.two_layer_row_flops(L, R, M, Q, OS)
+
+
+def apply_pair_flops():
+    """Real-aware real flops of one apply + one adjoint_apply at the config-2 column size."""
+    k = M + OS
+    cols = [R, R, M, R, R]  # b c t e f
+    rows = [M, R, R]  # a p q
+    rf = COLUMN_REAL + [False]
+    ap = costmodel.network_flops(COLUMN_SHAPES + [cols + [k]], COLUMN_LABELS + ["bctefX"], "apqX", rf)
+    ad = costmodel.network_flops(COLUMN_SHAPES + [rows + [k]], COLUMN_LABELS + ["apqX"], "bctefX", rf)
+    return 4 * (ap + ad)
 
 
 # ----------------------------------------------------------------------------- clocks
@@ -117,70 +150,105 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-# ----------------------------------------------------------------------------- reference CPU sample
+# ----------------------------------------------------------------------------- reference CPU samples
 
-def cpu_sample(threads: int, seed: int = 42):
-    """One interior-column einsumsvd of config 2 on the compiled reference (oracle/_ref).
-
-    Pending tensor v (a,p,q,s,m,n) = (64,8,8,64,8,8), top site (8,8,64,64), bra/ket
-    (2,8,8,8,8): exactly the interior-column network of two_layer_apply_row
-    (contraction.cpp:293-299), N(0,1) entries.  Returns (seconds, algorithmic real flops).
-    """
-    from oracle import ref  # bench's CPU-baseline leg only
-    ref.set_threads(threads)
-    v = inputs.gaussian((M, R, R, M, R, R), seed)
-    s = inputs.gaussian((R, R, M, M), seed + 1)
-    b = inputs.gaussian((2, R, R, R, R), seed + 2)
-    ts = [v, s, b.conj(), b]
-    labels = ["apqsmn", "uvst", "dumbe", "dvncf"]
-    t0 = time.perf_counter()
-    ref.einsumsvd(ts, labels, "apq", "bctef", M, 1e-14, "implicit_rsvd", "right", Q, OS,
-                  inputs.derive_seed(seed, 0x20, 1, 3))
-    dt = time.perf_counter() - t0
-    fl = 4 * costmodel.rsvd_flops([t.shape for t in ts], labels, "apq", "bctef", M, Q, OS)
-    return dt, fl
+def _column_inputs(seed):
+    """One interior column of config 2 (contraction.cpp:293-299), N(0,1) entries."""
+    v = inputs.gaussian(COLUMN_SHAPES[0], seed)
+    s = inputs.gaussian(COLUMN_SHAPES[1], seed + 1)
+    b = inputs.gaussian(COLUMN_SHAPES[2], seed + 2)
+    return [v, s, b.conj(), b]
 
 
-def cpu_sample_small(threads: int):
+class ApplyPairSample:
+    """The reference arm's step: ImplicitOperator::apply(Omega) + adjoint_apply(P)
+    (implicit.cpp:66-100) of one config-2 interior column on oracle/_ref, timed
+    inside the reference (operator construction / marshalling excluded)."""
+
+    def __init__(self, threads, seed=42):
+        from oracle import ref  # bench's CPU-baseline leg only
+        self.ref = ref
+        ref.set_threads(threads)
+        self.ts = _column_inputs(seed)
+        k = M + OS
+        self.omega = ref.random_tensor((R, R, M, R, R, k), inputs.derive_seed(seed, 0x20, 1, 3))
+        self.p = ref.random_tensor((M, R, R, k), seed + 7)
+        self.flops = apply_pair_flops()
+
+    def step(self):
+        _, ta = self.ref.implicit_apply(self.ts, COLUMN_LABELS, "apq", "bctef", self.omega, timed=True)
+        _, tb = self.ref.implicit_apply(self.ts, COLUMN_LABELS, "apq", "bctef", self.p, adjoint=True, timed=True)
+        return ta + tb
+
+
+APPLY_PAIR_NOTE = ("one ImplicitOperator::apply + adjoint_apply of a config-2 interior column (v 64x8x8x64x8x8, "
+                   "probe k=72) per step on oracle/_ref (unmodified reference sources, OpenBLAS 0.3.15), timed "
+                   "inside the reference; the same real-aware flop count as the GPU arm")
+
+
+def cpu_config_baselines(cores):
+    """Per-config reference CPU timings on this box's host cores (bounded samples).
+
+    config 1: mean of 10 full norms; config 3: one interior row absorb at the
+    config-3 shapes (L=16, r=6, m=36, k=41), x15 rows for a norm; config 4: 10
+    ITE steps from |+>; config 5: one interior column einsumsvd at m=64 r=8
+    (the config-5 column), x31 columns x31 rows for a norm."""
     from oracle import ref
-    ref.set_threads(threads)
-    v = inputs.gaussian((16, 4, 4, 16, 4, 4), 1)
-    s = inputs.gaussian((4, 4, 16, 16), 2)
-    b = inputs.gaussian((2, 4, 4, 4, 4), 3)
-    ref.einsumsvd([v, s, b.conj(), b], ["apqsmn", "uvst", "dumbe", "dvncf"], "apq", "bctef", 16, 1e-14,
-                  "implicit_rsvd", "right", Q, OS, 7)
+    ref.set_threads(cores)
+    out = {"cores": cores, "kind": "reference"}
+    c1 = inputs.config1()
+    ref.contract_two_layer(c1["sites"], 4, 4, 4, c1["seed"], 1, 4)
+    t0 = time.perf_counter()
+    for _ in range(10):
+        ref.contract_two_layer(c1["sites"], 4, 4, 4, c1["seed"], 1, 4)
+    out["config1_s_per_norm"] = (time.perf_counter() - t0) / 10
+    sites3, top3, phys3 = _row_inputs(16, 6, 36, 3)
+    t0 = time.perf_counter()
+    ref.two_layer_apply_row(top3, phys3, sites3, 3, 16, 1, 36, 3, 2, -1, True, 0x20)
+    row3 = time.perf_counter() - t0
+    out["config3_s_per_row_absorb"] = row3
+    out["config3_s_per_norm_extrapolated"] = 15 * row3
+    plus = [np.array([1, 1], dtype=complex).reshape(2, 1, 1, 1, 1) / np.sqrt(2) for _ in range(64)]
+    _, dt4 = ref.ite_tfim(plus, 8, 8, 1.0, 3.0, 0.01, 10, 8)
+    out["config4_s_per_step"] = dt4 / 10
+    ts = _column_inputs(42)
+    r5 = ref.einsumsvd(ts, COLUMN_LABELS, "apq", "bctef", M, 1e-14, "implicit_rsvd", "right", Q, OS,
+                       inputs.derive_seed(42, 0x20, 1, 3))
+    out["config5_s_per_column"] = r5["seconds"]
+    out["config5_s_per_norm_extrapolated"] = 31 * 31 * r5["seconds"]
+    out["sample"] = ("config 1: mean of 10 norms; config 3: one interior row absorb (L=16 r=6 m=36) x 15 rows; "
+                     "config 4: 10 ITE steps; config 5: one interior m=64 r=8 column einsumsvd x 31 x 31")
+    return out
+
+
+def _row_inputs(length, bond, m, seed):
+    """A 3-row PEPS with the config's entry scaling and a Gaussian top boundary
+    (bonds m): the inputs of one interior row absorb at that config's shapes."""
+    scale = 1.0 / np.sqrt(bond * bond * 2)
+    sites = inputs.random_peps(3, length, bond, seed, scale=scale)
+    top, phys = inputs.random_boundary(length, (bond, bond), m, inputs.derive_seed(seed, 0x70), scale=0.1)
+    return sites, top, phys
 
 
 def run_reference(args, rank, world):
     if rank != 0:
         return 0
     cores = os.cpu_count() or 1
+    sample = ApplyPairSample(cores)
     for _ in range(max(0, args.warmup)):
-        cpu_sample_small(cores)
-    budget = float(os.environ.get("PEPSB_REF_BUDGET_S", "150"))
-    times, flops = [], 0.0
-    t_start = time.perf_counter()
-    for i in range(args.steps):
-        dt, fl = cpu_sample(cores, seed=42 + i)
-        times.append(dt)
-        flops = fl
-        if time.perf_counter() - t_start > budget:
-            break
+        sample.step()
+    times = [sample.step() for _ in range(args.steps)]
     per = statistics.median(times)
-    value = flops / per / 1e12
-    sample = ("one interior-column einsumsvd of config 2 (v 64x8x8x64x8x8, k=72, q=2) per step on "
-              "oracle/_ref (unmodified reference sources, OpenBLAS 0.3.15); warm-up steps use an "
-              "m=16 r=4 column")
+    value = sample.flops / per / 1e12
     line = {"metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
             "steps": len(times), "warmup": args.warmup, "ms_per_step": per * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128",
             "data": "synthetic (seeded N(0,1) Box-Muller over SplitMix64)",
-            "config": workload_config({"sample": "interior-column einsumsvd"}),
+            "config": workload_config(world),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference",
-                             "sample": sample},
-            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    if len(times) < args.steps:
-        line["steps_note"] = f"timed {len(times)} of {args.steps} requested steps within the {budget:.0f} s budget"
+                             "sample": APPLY_PAIR_NOTE},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "sample_flops_per_step": sample.flops, "mean_ms_per_step": 1e3 * sum(times) / len(times)}
     print(json.dumps(line), flush=True)
     return 0
 
@@ -276,6 +344,10 @@ def run_b200(args, rank, world, local_rank):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         dt, dt_e2e = float(t[0]), float(t[1])
 
+    extra_roofs = {}
+    if world == 1 and not args.no_norms:
+        extra_roofs = config_rooflines(A, ctx)
+
     if rank != 0:
         return 0
     flops = alg_flops_row()
@@ -283,54 +355,99 @@ def run_b200(args, rank, world, local_rank):
     peak = _fp64_peak()
     g = rep["gemm"]
     # achieved = real flops the DMMAs execute (3M launches: 6 per complex MAC,
-    # 4M launches: 8) / device time -- the tensor-pipe roofline; the algorithmic
-    # rate (8 per complex MAC, the reference's count) is reported beside it.
+    # 4M launches: 8, complex x real: 4) / device time of the GEMM launches --
+    # the tensor-pipe roofline (a hardware fraction, <= 1).
     achieved = g["exec_flops"] / (g["ms"] / 1e3) / 1e12 if g["ms"] > 0 else None
     achieved_alg = g["flops"] / (g["ms"] / 1e3) / 1e12 if g["ms"] > 0 else None
     total_ms = sum(v["ms"] for v in rep.values())
     roof = {"bound": "tensor", "achieved": achieved, "peak": peak["tflops"], "unit": "TFLOP/s",
             "frac": achieved / peak["tflops"] if achieved else None, "traffic": _ncu_traffic(),
-            "kernel": "zgemm_cx_kernel (complex FP64 GEMM on DMMA.8x8x4: 3M/Gauss and 4M complex-fragment "
-                      "instantiations, all launches of the step)",
-            "achieved_algorithmic": achieved_alg,
+            "kernel": "zgemm_cx_kernel (complex FP64 GEMM on DMMA.8x8x4: 3M/Gauss, 4M complex-fragment and "
+                      "complex x real instantiations, all launches of the step)",
+            "achieved_unit_note": "executed DMMA real flops / GEMM device time (serialised profile pass)",
+            "achieved_reference_counter": achieved_alg,
             "kernel_share_of_step": g["ms"] / total_ms if total_ms else None,
+            "eigensolver_share_of_step": rep["small"]["ms"] / total_ms if total_ms else None,
             "profile_pass": "serialised (overlap off); the timed step overlaps the k x k eigensolver with GEMMs",
             "launches_per_step": g["launches"], "avg_launch_ms": g["ms"] / max(1, g["launches"]),
-            "algorithmic_flops_per_step": g["flops"], "executed_flops_per_step": g["exec_flops"],
+            "reference_counter_flops_per_step": g["flops"], "executed_flops_per_step": g["exec_flops"],
             "peak_source": peak["source"],
-            "whole_step_frac": (flops / dt / 1e12) / peak["tflops"],
+            "whole_step_executed_frac": (g["exec_flops"] / dt / 1e12) / peak["tflops"],
+            "whole_step_value_frac": value / world / peak["tflops"],
             "breakdown_ms": {k: round(v["ms"], 3) for k, v in rep.items()}}
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "c128", "data": "synthetic (seeded N(0,1) Box-Muller over SplitMix64)",
-            "config": workload_config({"parallelism": f"replicas x{world}", "s_per_row_absorb": dt}),
+            "config": workload_config(world), "s_per_row_absorb": dt,
+            "value_reference_counter": world * refcounter_flops_row() / dt / 1e12,
             "clocks": clk.summary(), "gpu_launches": launches,
             "e2e": {"value": world * flops / dt_e2e / 1e12, "unit": UNIT, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "s_per_step": dt_e2e},
             "roofline": roof}
+    if extra_roofs:
+        line["roofline_configs"] = extra_roofs
     if world == 1 and not args.no_norms:
         line["s_per_norm"] = norm_timings(A, ctx)
     if world == 1 and not args.no_cpu_baseline:
+        cores = os.cpu_count() or 1
         try:
-            cores = os.cpu_count() or 1
-            cdt, cfl = cpu_sample(cores)
-            line["cpu_baseline"] = {"value": cfl / cdt / 1e12, "unit": UNIT, "cores": cores, "kind": "reference",
-                                    "sample": "one interior-column einsumsvd of config 2 on oracle/_ref "
-                                              f"({cdt:.1f} s)"}
+            sample = ApplyPairSample(cores)
+            sample.step()  # warm
+            ts = [sample.step() for _ in range(2)]
+            cv = sample.flops / min(ts) / 1e12
+            line["cpu_baseline"] = {"value": cv, "unit": UNIT, "cores": cores, "kind": "reference",
+                                    "sample": APPLY_PAIR_NOTE + f" (best of 2: {min(ts):.2f} s)"}
+            if not args.no_norms:
+                line["cpu_baseline_configs"] = cpu_config_baselines(cores)
         except Exception as e:  # oracle missing on this box
-            line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "reference",
+            line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": cores, "kind": "reference",
                                     "sample": f"unavailable: {e}"}
     print(json.dumps(line), flush=True)
     return 0
 
 
+def config_rooflines(A, ctx):
+    """Roofline of one interior row absorb at the config-3 and config-5 shapes
+    (serialised profile pass, overlap off): executed DMMA flops / GEMM device
+    time against the FP64 peak, and the k x k eigensolver's share of the
+    serialised kernel time (the latency chain of the row)."""
+    peak = _fp64_peak()["tflops"]
+    out = {}
+    for name, (length, bond, m, os_) in {"config3_row_L16_r6_m36": (16, 6, 36, -1),
+                                         "config5_row_L32_r8_m64": (32, 8, 64, 8)}.items():
+        sites, top, phys = _row_inputs(length, bond, m, 11)
+        st = A.PepsState(3, length, 2, sites, ctx=ctx)
+        tb = A.TwoLayerBoundary.from_sites(top, phys, ctx=ctx)
+        opt = A.ContractOption.two_layer_opt(m, 11, 2, os_)
+        A.two_layer_apply_row(tb, st, st, 1, opt, 0x20)  # warm the plans / pools
+        ctx.sync()
+        t0 = time.perf_counter()
+        A.two_layer_apply_row(tb, st, st, 1, opt, 0x20)
+        ctx.sync()
+        wall = time.perf_counter() - t0
+        ctx.set_option("overlap", 0)
+        ctx.profile(True)
+        A.two_layer_apply_row(tb, st, st, 1, opt, 0x20)
+        rep = ctx.profile_report()
+        ctx.profile(False)
+        ctx.set_option("overlap", 1)
+        g = rep["gemm"]
+        total = sum(v["ms"] for v in rep.values())
+        ach = g["exec_flops"] / (g["ms"] / 1e3) / 1e12 if g["ms"] > 0 else None
+        out[name] = {"bound": "tensor", "achieved": ach, "peak": peak, "unit": "TFLOP/s",
+                     "frac": ach / peak if ach else None, "s_per_row_absorb": wall,
+                     "gemm_share": g["ms"] / total if total else None,
+                     "eigensolver_share": rep["small"]["ms"] / total if total else None,
+                     "breakdown_ms": {k: round(v["ms"], 3) for k, v in rep.items()}}
+    return out
+
+
 def norm_timings(A, ctx):
     """The metric's other half: seconds per <psi|psi> by two-layer boundary
-    contraction (contract_two_layer) on BASELINE configs 1, 3 and 5, and
-    seconds per ITE step of config 4, through the public API (wall clock around
-    synchronised calls; inputs resident).  Reference CPU figures for 3 and 5 are
-    SURVEY §6's (1511 s for config 3's cache + bands on 8 cores; ~16 h per
-    config-5 sweep); config 1's and 4's are timed by tools/bench_configs.py."""
+    contraction (contract_two_layer) on BASELINE configs 1, 3 and 5 and seconds
+    per ITE step of config 4, through the public API (wall clock around
+    synchronised calls; inputs resident).  Config 1: mean of 10 after a warm-up;
+    configs 3 and 5: median of 3 after a warm-up; config 4: 20 steps."""
     out = {}
     c1 = inputs.config1()
     st = A.PepsState(4, 4, 2, c1["sites"], ctx=ctx)
@@ -340,21 +457,20 @@ def norm_timings(A, ctx):
     for _ in range(10):
         A.contract_two_layer(st, st, o1)
     out["config1_4x4_r2_m4"] = (time.perf_counter() - t0) / 10
-    for name, cfg, r, m, q, os_ in (("config3_16x16_r6_m36", inputs.config3(), 6, 36, 2, -1),
-                                    ("config5_32x32_r8_m64", inputs.config5(), 8, 64, 2, 8)):
+    for name, cfg, m, q, os_ in (("config3_16x16_r6_m36", inputs.config3(), 36, 2, -1),
+                                 ("config5_32x32_r8_m64", inputs.config5(), 64, 2, 8)):
         n = cfg["rows"]
         st = A.PepsState(n, n, 2, cfg["sites"], ctx=ctx)
         opt = A.ContractOption.two_layer_opt(m, cfg["seed"], q, os_)
-        reps = 3 if n <= 16 else 1  # config 3: warm-up + median of 3 (0.4 s each); config 5: one cold-ish shot
-        if reps > 1:
-            A.contract_two_layer(st, st, opt)
+        A.contract_two_layer(st, st, opt)
         ts = []
-        for _ in range(reps):
+        for _ in range(3):
             ctx.sync()
             t0 = time.perf_counter()
             A.contract_two_layer(st, st, opt)
             ts.append(time.perf_counter() - t0)
-        out[name] = sorted(ts)[len(ts) // 2]
+        out[name] = statistics.median(ts)
+        out[name + "_all"] = ts
         del st
     plus = [np.array([1, 1], dtype=complex).reshape(2, 1, 1, 1, 1) / np.sqrt(2) for _ in range(64)]
     st = A.PepsState(8, 8, 2, plus, ctx=ctx)
@@ -469,8 +585,8 @@ def run_sharded(args, rank, world, local_rank):
     line = {"metric": METRIC, "value": flops / dt / 1e12, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "c128", "data": "synthetic (seeded N(0,1) Box-Muller over SplitMix64)",
-            "config": workload_config({"parallelism": f"bond-sharded x{world} (t / s of the boundary bond)",
-                                       "s_per_row_absorb": dt}),
+            "config": dict(workload_config(world), parallelism=f"bond-sharded x{world} (t / s of the boundary bond)"),
+            "s_per_row_absorb": dt,
             "clocks": clk.summary(), "gpu_launches": launches,
             "e2e": {"value": flops / dt_e2e / 1e12, "unit": UNIT, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "s_per_step": dt_e2e}}

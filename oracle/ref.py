@@ -140,12 +140,15 @@ def _net(tensors, labels, rows, cols):
     return tl, ",".join(labels).encode(), rows.encode(), cols.encode()
 
 
-def implicit_apply(tensors, labels, rows, cols, probe, adjoint=False):
+def implicit_apply(tensors, labels, rows, cols, probe, adjoint=False, timed=False):
+    """ImplicitOperator::apply / adjoint_apply (implicit.cpp:66-100); with
+    timed=True also the seconds the reference spent inside the call (operator
+    construction and host marshalling excluded)."""
     tl, lab, r, c = _net(tensors, labels, rows, cols)
     p = np.ascontiguousarray(probe, dtype=np.complex128)
-    t, _ = _bag(_fn("ref_implicit")(1 if adjoint else 0, *tl.args(), lab, r, c, p.ndim,
+    t, d = _bag(_fn("ref_implicit")(1 if adjoint else 0, *tl.args(), lab, r, c, p.ndim,
                                     _i64(p.shape), C.c_void_p(p.ctypes.data)))
-    return t[0]
+    return (t[0], float(d[0])) if timed else t[0]
 
 
 def materialize(tensors, labels, rows, cols):

@@ -32,12 +32,19 @@ def _result_of(mask: int, labels: Sequence[str], ext: Sequence[Dict[str, int]], 
     return res
 
 
-def network_flops(shapes: Sequence[Sequence[int]], labels: Sequence[str], output: str) -> int:
-    """instr::flops added by detail::contract_network (einsum.cpp:340-406)."""
+def network_flops(shapes: Sequence[Sequence[int]], labels: Sequence[str], output: str,
+                  real: Sequence[bool] | None = None):
+    """instr::flops added by detail::contract_network (einsum.cpp:340-406).
+
+    With ``real`` (one flag per tensor) the count is real-aware:
+    a pairwise product with one real operand costs half the complex one (2 real
+    flops per MAC instead of 4 x 2), with two real operands a quarter; the
+    contraction order is the reference's either way.  Returns a float then."""
     n = len(labels)
     ext = [dict(zip(l, s)) for l, s in zip(labels, shapes)]
     if n == 1:
-        return _reduce_flops(ext[0], labels[0], output)
+        f = _reduce_flops(ext[0], labels[0], output)
+        return f * (0.5 if real and real[0] else 1.0) if real is not None else f
     if n > 10:
         raise NotImplementedError("greedy fallback not modelled")
     sub = [None] * (1 << n)
@@ -73,31 +80,32 @@ def network_flops(shapes: Sequence[Sequence[int]], labels: Sequence[str], output
 
     # walk the tree adding the leaf pre-reductions the reference performs
     total = 0
+    flags = list(real) if real is not None else [False] * n
 
-    def walk(mask) -> Tuple[str, Dict[str, int]]:
+    def walk(mask) -> Tuple[str, Dict[str, int], bool]:
         nonlocal total
         if bin(mask).count("1") == 1:
             t = mask.bit_length() - 1
-            return labels[t], ext[t]
+            return labels[t], ext[t], flags[t]
         _, _, l, r = best[mask]
-        ll, le = walk(l)
-        rl, re_ = walk(r)
+        ll, le, lr = walk(l)
+        rl, re_, rr = walk(r)
         keep = output + "".join(labels[t] for t in range(n) if not mask & (1 << t))
         # pre-reduce labels present on one side only and not kept (einsum.cpp:182-194)
         wa = {c: le[c] for c in le if c in rl or c in keep}
         wb = {c: re_[c] for c in re_ if c in ll or c in keep}
         if len(wa) != len(set(ll)):
-            total += _sum_flops(le, wa)
+            total += _sum_flops(le, wa) * (0.5 if lr else 1)
         if len(wb) != len(set(rl)):
-            total += _sum_flops(re_, wb)
+            total += _sum_flops(re_, wb) * (0.5 if rr else 1)
         uni = dict(wa)
         uni.update(wb)
-        total += 2 * math.prod(uni.values())
+        total += 2 * math.prod(uni.values()) * (0.5 if lr else 1) * (0.5 if rr else 1)
         res = {c: e for c, e in uni.items() if c in sub[mask]}
-        return "".join(res), res
+        return "".join(res), res, lr and rr
 
     walk((1 << n) - 1)
-    return total
+    return total if real is not None else int(total)
 
 
 def _sum_flops(ext: Dict[str, int], kept: Dict[str, int]) -> int:
@@ -125,8 +133,10 @@ def effective_oversample(oversample: int, target: int) -> int:
     return oversample if oversample >= 0 else max(5, math.ceil(0.1 * target))
 
 
-def rsvd_flops(shapes, labels, rows: str, cols: str, max_rank: int, power_iters: int, oversample: int) -> int:
-    """randomized_svd (decomposition.cpp:259-306) with the reference's counters."""
+def rsvd_flops(shapes, labels, rows: str, cols: str, max_rank: int, power_iters: int, oversample: int,
+               real: Sequence[bool] | None = None):
+    """randomized_svd (decomposition.cpp:259-306) with the reference's counters
+    (real-aware for the operator applications when ``real`` flags are given)."""
     ext = {}
     for l, s in zip(labels, shapes):
         ext.update(dict(zip(l, s)))
@@ -137,8 +147,9 @@ def rsvd_flops(shapes, labels, rows: str, cols: str, max_rank: int, power_iters:
     k = min(target + effective_oversample(oversample, target), mindim)
     free = next(c for c in "ABCDEFGHIJKLMNOPQRSTUVWXYZabcdefghijklmnopqrstuvwxyz"
                 if c not in rows + cols + "".join(labels))
-    ap = network_flops(list(shapes) + [[ext[c] for c in cols] + [k]], list(labels) + [cols + free], rows + free)
-    ad = network_flops(list(shapes) + [[ext[c] for c in rows] + [k]], list(labels) + [rows + free], cols + free)
+    rf = list(real) + [False] if real is not None else None  # the probe is complex
+    ap = network_flops(list(shapes) + [[ext[c] for c in cols] + [k]], list(labels) + [cols + free], rows + free, rf)
+    ad = network_flops(list(shapes) + [[ext[c] for c in rows] + [k]], list(labels) + [rows + free], cols + free, rf)
     total = (power_iters + 1) * ap + (power_iters + 1) * ad
     total += (power_iters + 1) * gram_orth_flops(R, k) + power_iters * gram_orth_flops(Cx, k)
     total += svd_flops(k, Cx) + 2 * R * k * k
@@ -146,22 +157,29 @@ def rsvd_flops(shapes, labels, rows: str, cols: str, max_rank: int, power_iters:
 
 
 def two_layer_row_flops(length: int, bond: int, m: int, power_iters: int, oversample: int, d: int = 2,
-                        top_bonds: Sequence[int] | None = None, interior: bool = True) -> int:
+                        top_bonds: Sequence[int] | None = None, interior: bool = True,
+                        real_sites: bool = False):
     """instr::flops of one two_layer_apply_row (contraction.cpp:269-311) on an
     interior row whose top boundary has bonds `m` (edges 1) and whose pending
-    bond saturates at min(m, ...) as the reference's truncation dictates."""
+    bond saturates at min(m, ...) as the reference's truncation dictates.
+
+    ``real_sites``: the real-aware count of SURVEY §8(d) -- the bra/ket PEPS
+    sites of the BASELINE configs are real, so their products are counted at 2
+    real flops per MAC (the top boundary and pending tensor stay complex)."""
     r = bond
     dn = r if interior else 1
     tb = list(top_bonds) if top_bonds is not None else [1] + [m] * (length - 1) + [1]
     # column 0: contract_network({s0s (u,v,l,s), bra (d,u,m,b,e), ket (d,v,n,c,f)}) -> bcsef
+    rl = [False, True, True] if real_sites else None
     total = network_flops([[r, r, 1, tb[1]], [d, r, 1, dn, r], [d, r, 1, dn, r]], ["uvls", "dumbe", "dvncf"],
-                          "bcsef")
+                          "bcsef", rl)
     a = 1
     for c in range(1, length):
         right = r if c < length - 1 else 1
         shapes = [[a, dn, dn, tb[c], r, r], [r, r, tb[c], tb[c + 1]], [d, r, r, dn, right], [d, r, r, dn, right]]
         labels = ["apqsmn", "uvst", "dumbe", "dvncf"]
-        total += rsvd_flops(shapes, labels, "apq", "bctef", m, power_iters, oversample)
+        total += rsvd_flops(shapes, labels, "apq", "bctef", m, power_iters, oversample,
+                            [False, False, True, True] if real_sites else None)
         R = a * dn * dn
         Cx = right * right * tb[c + 1] * dn * dn
         k_max = min(R, Cx)

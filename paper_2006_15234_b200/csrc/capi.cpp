@@ -621,6 +621,7 @@ int pepsb_save_peps(pepsb_ctx* c, const pepsb_state* s, const char* path) {
     need(path, "path");
     FILE* f = fopen(path, "wb");
     if (!f) throw Error(kValidationError, std::string("cannot open '") + path + "' for writing");
+    std::unique_ptr<FILE, int (*)(FILE*)> guard_f(f, fclose);  // closes on a mid-write throw
     bool ok = true;
     auto u64 = [&](uint64_t v) { ok = ok && fwrite(&v, sizeof(v), 1, f) == 1; };
     ok = fwrite(kPepsMagic, 1, 8, f) == 8;
@@ -640,7 +641,7 @@ int pepsb_save_peps(pepsb_ctx* c, const pepsb_state* s, const char* path) {
         ok = ok && fwrite(h.data(), sizeof(double2), h.size(), f) == h.size();
       }
     }
-    ok = (fclose(f) == 0) && ok;
+    ok = (fclose(guard_f.release()) == 0) && ok;
     if (!ok) throw Error(kValidationError, std::string("write failed for '") + path + "'");
   });
 }
@@ -663,6 +664,15 @@ int pepsb_load_peps(pepsb_ctx* c, const char* path, pepsb_state** out) {
     };
     const uint64_t rows = u64(), cols = u64(), d = u64(), tl = u64();
     if (!ok || tl > 64) throw Error(kValidationError, std::string("truncated PEPS container '") + path + "'");
+    // Every count below is untrusted: bound it by the file size before allocating.
+    const long here = ftell(f);
+    if (here < 0 || fseek(f, 0, SEEK_END) != 0) throw Error(kValidationError, "cannot size PEPS container");
+    const uint64_t file_bytes = static_cast<uint64_t>(ftell(f));
+    if (fseek(f, here, SEEK_SET) != 0) throw Error(kValidationError, "cannot size PEPS container");
+    constexpr uint64_t kMaxExtent = uint64_t{1} << 31;
+    if (rows < 1 || cols < 1 || rows >= kMaxExtent || cols >= kMaxExtent || d < 1 || d >= kMaxExtent ||
+        rows * cols > file_bytes / 16)
+      throw Error(kValidationError, std::string("corrupt PEPS container header in '") + path + "'");
     std::string tag(tl, '\0');
     if (tl && fread(tag.data(), 1, tl, f) != tl) ok = false;
     if (tag != kPepsTag) throw Error(kValidationError, "unknown axis convention tag '" + tag + "'");
@@ -672,9 +682,19 @@ int pepsb_load_peps(pepsb_ctx* c, const char* path, pepsb_state** out) {
     st.d = static_cast<int>(d);
     for (uint64_t i = 0; ok && i < rows * cols; ++i) {
       const uint64_t order = u64();
-      if (!ok || order > kMaxModes) break;
+      if (!ok) break;
+      if (order != 5) throw Error(kValidationError, std::string("corrupt PEPS site order in '") + path + "'");
       std::vector<int64_t> shape(order);
-      for (auto& e : shape) e = static_cast<int64_t>(u64());
+      uint64_t elems = 1;
+      for (auto& e : shape) {
+        const uint64_t v = u64();
+        if (ok && (v < 1 || v >= kMaxExtent))
+          throw Error(kValidationError, std::string("corrupt PEPS site extent in '") + path + "'");
+        e = static_cast<int64_t>(v);
+        elems = (elems > file_bytes / v) ? file_bytes + 1 : elems * v;  // saturates, no overflow
+      }
+      if (!ok) break;
+      if (elems > file_bytes / 16) ok = false;  // more data than the file holds: truncated
       if (!ok) break;
       DTensor t = c->ctx->empty(shape);
       std::vector<double2> h(static_cast<size_t>(t.size()));

@@ -27,9 +27,10 @@ void* Pool::alloc(size_t bytes, size_t* reserved) {
   }
   void* p = nullptr;
   cudaError_t e = cudaMalloc(&p, want);
-  if (e != cudaSuccess) {  // release the cache and retry once
+  if (e != cudaSuccess) {  // release this cache, then the siblings', and retry once
     cudaGetLastError();
     trim_locked();
+    trim_siblings(this);
     e = cudaMalloc(&p, want);
     if (e != cudaSuccess) {
       cudaGetLastError();
@@ -40,6 +41,38 @@ void* Pool::alloc(size_t bytes, size_t* reserved) {
   reserved_bytes += want;
   *reserved = want;
   return p;
+}
+
+namespace {
+std::mutex g_pools_mu;
+std::vector<Pool*> g_pools;
+}  // namespace
+
+Pool::Pool(int dev) : device(dev) {
+  std::lock_guard<std::mutex> g(g_pools_mu);
+  g_pools.push_back(this);
+}
+
+Pool::~Pool() {
+  {
+    std::lock_guard<std::mutex> g(g_pools_mu);
+    for (auto it = g_pools.begin(); it != g_pools.end(); ++it)
+      if (*it == this) {
+        g_pools.erase(it);
+        break;
+      }
+  }
+  trim();
+}
+
+void Pool::trim_siblings(const Pool* self) {
+  std::lock_guard<std::mutex> g(g_pools_mu);
+  for (Pool* other : g_pools) {
+    if (other == self || other->device != self->device) continue;
+    // try_lock: two pools failing at once must not wait on each other
+    std::unique_lock<std::mutex> l(other->mu, std::try_to_lock);
+    if (l.owns_lock()) other->trim_locked();
+  }
 }
 
 void Pool::release(void* p, size_t bytes) {
@@ -132,7 +165,7 @@ Ctx::Ctx(int dev) : device(dev) {
   PEPSB_CUDA(cudaEventCreateWithFlags(&fork_event, cudaEventDisableTiming));
   PEPSB_CUDA(cudaEventCreateWithFlags(&join_event, cudaEventDisableTiming));
   main_stream = stream;
-  pool = std::make_shared<Pool>();
+  pool = std::make_shared<Pool>(dev);
   pool->stream = stream;
   PEPSB_CUDA(cudaMalloc(&d_status, 64 * sizeof(int)));
   PEPSB_CUDA(cudaMemset(d_status, 0, 64 * sizeof(int)));

@@ -46,7 +46,13 @@ struct Pool {
   void release(void* p, size_t bytes);
   void trim();  // synchronises, then returns every cached block to the driver
   void trim_locked();
-  ~Pool() { trim(); }
+  // Every live pool of a device is registered so that an allocation failing
+  // in one pool can reclaim blocks cached by its siblings (the helper contexts
+  // of the row pipeline and the concurrent sweeps each own a pool).
+  int device = 0;
+  explicit Pool(int dev);
+  ~Pool();
+  static void trim_siblings(const Pool* self);
 };
 
 struct Buf {

@@ -150,19 +150,39 @@ DTensor materialize(Ctx& ctx, const LTensor& t, const std::string& order) {
 
 // ---------------------------------------------------------------------------- pairwise GEMM
 
-LTensor pairwise_gemm(Ctx& ctx, const LTensor& A, const LTensor& B, const std::string& batch,
+LTensor pairwise_gemm(Ctx& ctx, const LTensor& A_in, const LTensor& B_in, const std::string& batch,
                       const std::string& con, const std::string& out_order, uint64_t* cmacs) {
   std::string freeA, freeB;
-  for (char c : A.labels)
+  for (char c : A_in.labels)
     if (!has(batch, c) && !has(con, c)) freeA += c;
-  for (char c : B.labels)
+  for (char c : B_in.labels)
     if (!has(batch, c) && !has(con, c)) freeB += c;
+  // An operand whose free or contracted group is not one uniform-stride block
+  // (e.g. a probe label between row labels of an intermediate laid out for
+  // another consumer) is re-laid out once as [batch][free][con] / [batch][con][free].
+  auto usable = [&](const LTensor& t, const std::string& fr) {
+    const std::string fp = physical_order(t, fr);
+    if (!flattenable(t, con) || !flattenable(t, fp)) return false;
+    return group_stride(t, con) == 1 || group_stride(t, fp) == 1 || group_size(t, con) * group_size(t, fr) == 1;
+  };
+  const bool relayA = !usable(A_in, freeA), relayB = !usable(B_in, freeB);
+  const LTensor A = relayA ? reduce_to(ctx, A_in, batch + freeA + con) : A_in;
+  const LTensor B = relayB ? reduce_to(ctx, B_in, batch + con + freeB) : B_in;
   // physical orders of the free groups (extent-1 labels dropped)
   const std::string fa = physical_order(A, freeA), fb = physical_order(B, freeB);
+  auto describe = [&]() {
+    auto one = [](const LTensor& t) {
+      std::string d = t.labels + "[";
+      for (size_t a = 0; a < t.ext.size(); ++a)
+        d += (a ? "," : "") + std::to_string(t.ext[a]) + ":" + std::to_string(t.str[a]);
+      return d + "]";
+    };
+    return " (A " + one(A) + " B " + one(B) + " batch '" + batch + "' con '" + con + "' out '" + out_order + "')";
+  };
   if (!flattenable(A, con) || !flattenable(B, con) || drop_unit(A, con) != drop_unit(B, con))
-    throw Error(kOtherError, "internal: contracted labels not flattenable in the same order");
+    throw Error(kOtherError, "internal: contracted labels not flattenable in the same order" + describe());
   if (!flattenable(A, fa) || !flattenable(B, fb))
-    throw Error(kOtherError, "internal: free labels not flattenable");
+    throw Error(kOtherError, "internal: free labels not flattenable" + describe());
 
   LTensor C;
   std::vector<int64_t> cext;

@@ -128,8 +128,13 @@ PepsStateD apply_two_site_batch(Ctx& ctx, const PepsStateD& s, const DTensor& ga
       if (D.reduced) smem_reduce = std::max<size_t>(smem_reduce, (E * S + 5 * S * S + 2 * S) * 16 + S * 4 + 64);
       else smem_reduce = std::max<size_t>(smem_reduce, E * S * 16);
     }
-  if (smem_reduce > 176 * 1024)  // + the eigensolver's static shared memory throw Error(kShapeError, "simple update: site too large for the batched kernel");
-  if (sd[0].s != sd[1].s) throw Error(kShapeError, "shared bond mismatch");
+  // The ImplicitOperator ctor rejects a label extent mismatch with ShapeError
+  // (implicit.cpp:10-49); here the shared label is "s" of {Ra, Rb}.
+  for (int i = 0; i < nb; ++i)
+    if (sd[2 * i].s != sd[2 * i + 1].s) throw Error(kShapeError, "shared bond mismatch");
+  // 176 KB: the su_reduce attribute, leaving room for the eigensolver's static shared memory.
+  if (smem_reduce > 176 * 1024)
+    throw Error(kShapeError, "simple update: site too large for the batched kernel");
 
   // ---- exact einsumsvd of {g, Ra, Rb} (state.cpp:186-194)
   std::vector<SuBondDesc> bd(nb);

@@ -92,6 +92,27 @@ BoundaryD two_layer_first_row(Ctx& ctx, const PepsStateD& bra, const PepsStateD&
 
 namespace {
 
+// Thrown by a consumer whose producer failed: never the root cause, so the
+// pipeline rethrows the producer's own error instead when there is one.
+struct PipelineAborted : Error {
+  PipelineAborted() : Error(kOtherError, "row pipeline: producer failed") {}
+};
+
+void rethrow_root_cause(const std::vector<std::exception_ptr>& errs) {
+  std::exception_ptr sentinel;
+  for (auto& e : errs) {
+    if (!e) continue;
+    try {
+      std::rethrow_exception(e);
+    } catch (const PipelineAborted&) {
+      sentinel = e;
+    } catch (...) {
+      throw;
+    }
+  }
+  if (sentinel) std::rethrow_exception(sentinel);
+}
+
 // A boundary row produced on one context and read on another (the row
 // pipeline of contract_two_layer): site c is published, with an event on the
 // producer's stream, as soon as its computation is enqueued; the consumer
@@ -124,7 +145,7 @@ struct Handoff {
   const DTensor& acquire(Ctx& ctx, int c) {
     std::unique_lock<std::mutex> g(m);
     cv.wait(g, [&] { return ready[c] || failed; });
-    if (!ready[c]) throw Error(kOtherError, "row pipeline: producer failed");
+    if (!ready[c]) throw PipelineAborted();
     PEPSB_CUDA(cudaStreamWaitEvent(ctx.stream, ev[c], 0));
     return sites[c];
   }
@@ -297,8 +318,7 @@ std::vector<BoundaryD> pipelined_sweep(const std::vector<Ctx*>& ctxs, const Peps
     for (auto& h : H) h->fail();
   }
   for (auto& t : threads) t.join();
-  for (auto& e : err)
-    if (e) std::rethrow_exception(e);
+  rethrow_root_cause(err);
   for (int i = 1; i < K; ++i) {
     ctx.flops += ctxs[i]->flops - f0[i];
     ctx.launches += static_cast<int64_t>(static_cast<uint64_t>(ctxs[i]->launches) - l0[i]);

@@ -1092,9 +1092,12 @@ __global__ void __launch_bounds__(kEigThreads) gram_factors_kernel(const double2
 // ------------------------------------------------------------------ Cholesky
 
 __global__ void __launch_bounds__(kThreads) chol_kernel(const double2* G, int n, double shift_rel,
-                                                        double2* Rout, double2* Rinv, int* status) {
+                                                        double2* Rout, double2* Rinv, int* status,
+                                                        bool in_place) {
   extern __shared__ __align__(16) unsigned char sm[];
-  double2* A = reinterpret_cast<double2*>(sm);  // row-major n x n
+  // row-major n x n working copy: shared memory, or Rout itself when n x n
+  // complex does not fit (k > 113; every access below is then global)
+  double2* A = in_place ? Rout : reinterpret_cast<double2*>(sm);
   __shared__ double tr;
   __shared__ int bad;
   if (threadIdx.x == 0) { tr = 0.0; bad = 0; }
@@ -1143,6 +1146,7 @@ __global__ void __launch_bounds__(kThreads) chol_kernel(const double2* G, int n,
     int i = e / n, j = e % n;
     Rout[e] = j >= i ? A[e] : make_double2(0.0, 0.0);
   }
+  __syncthreads();
   // Rinv column c by back substitution (one thread per column).
   for (int c = threadIdx.x; c < n; c += blockDim.x) {
     for (int i = n - 1; i > c; --i) Rinv[i * n + c] = make_double2(0.0, 0.0);
@@ -1710,15 +1714,16 @@ void eigh_dense(const double2* G, int n, double* w, double2* vec, int* status, d
 
 void chol_factors(const double2* G, int n, double shift_rel, double2* R, double2* Rinv, int* status,
                   cudaStream_t stream) {
+  if (n > 256) throw Error(kShapeError, "chol_factors: k > 256 not supported");
   const size_t smem = static_cast<size_t>(n) * n * sizeof(double2);
-  if (smem > kSmemCap) throw Error(kShapeError, "chol_factors: k too large");
+  const bool in_place = smem > kSmemCap;
   static bool attr = false;
   if (!attr) {
     PEPSB_CUDA(cudaFuncSetAttribute(chol_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     static_cast<int>(kSmemCap)));
     attr = true;
   }
-  chol_kernel<<<1, kThreads, smem, stream>>>(G, n, shift_rel, R, Rinv, status);
+  chol_kernel<<<1, kThreads, in_place ? 0 : smem, stream>>>(G, n, shift_rel, R, Rinv, status, in_place);
   PEPSB_LAUNCH();
 }
 

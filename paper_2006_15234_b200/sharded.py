@@ -220,10 +220,14 @@ class DeviceOps:
         if self.comm.world == 1:
             return t
         import torch
-        x = self._torch(t)
+        x = self._torch(t).clone()
         self.comm.dist.all_reduce(x, group=self.comm.group)
         torch.cuda.current_stream().synchronize()
-        return t
+        # A fresh library tensor: its realness flag is recomputed on the summed
+        # data (an in-place write would keep a stale "real" flag on `t`).
+        out = self.A.from_device_ptr(x.data_ptr(), tuple(x.shape), self.ctx)
+        self.ctx.sync()
+        return out
 
     def allgather(self, t, axis, extent):
         if self.comm.world == 1:
