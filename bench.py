@@ -30,9 +30,10 @@ flops; a whole column takes ~27 s on 16 cores, so K = 20 columns would not fit
 "a few minutes"); rate = the same real-aware flop count of those two calls /
 their time.
 
-N > 1 (torchrun): the row-absorb chain is sequential, so ranks run
-independent replicas (scaling "weak"); value = sum of all ranks' work / max
-over ranks of the device time.
+N > 1 (torchrun): ONE config-2 row absorb split across the N ranks along the
+boundary bond by the C++ bond-sharded driver behind the C ABI (NCCL on the
+library stream), scaling "strong", value = the row's flops / the
+max over ranks of the device time; --replicas runs N independent rows instead.
 """
 from __future__ import annotations
 
@@ -521,28 +522,30 @@ def _ncu_traffic():
 
 
 def run_sharded(args, rank, world, local_rank):
-    """--sharded: ONE config-2 row absorb split across the N ranks along the
-    boundary bond (paper_2006_15234_b200/sharded.py, NCCL collectives);
-    scaling "strong", value = the row's algorithmic flops / max-over-ranks time."""
+    """N > 1 (default) or --sharded: ONE config-2 row absorb split across the N
+    ranks along the boundary bond by the C++ driver behind the C ABI
+    (pepsb_two_layer_apply_row_sharded, csrc/sharded.cpp: NCCL all-reduce /
+    all-gather on the library stream); scaling "strong", value = the row's
+    algorithmic flops / max-over-ranks device time.  Also times one sharded
+    config-5 norm (32x32, r=8, m=64)."""
     import torch
     import torch.distributed as dist
     import paper_2006_15234_b200.api as A
-    from paper_2006_15234_b200 import sharded as SH
 
     torch.cuda.set_device(local_rank)
     ctx = A.Context(local_rank)
+    if world > 1:
+        A.comm_init_from_torch(ctx)
+    else:
+        A.comm_init(ctx, A.comm_unique_id(), 0, 1)
     stream = torch.cuda.ExternalStream(ctx.stream, device=torch.device("cuda", local_rank))
-    ops = SH.DeviceOps(SH.Comm(), ctx)
     c2 = inputs.config2(seed=2)
-    row = [A.to_device(c2["sites"][1 * L + c], ctx) for c in range(L)]
-    tops = [A.to_device(t, ctx) for t in c2["top"]]
+    st = A.PepsState(3, L, 2, c2["sites"], ctx=ctx)
+    top = A.TwoLayerBoundary.from_sites(c2["top"], c2["phys"], ctx=ctx)
     opt = A.ContractOption.two_layer_opt(M, c2["seed"], Q, OS)
 
-    def step(tp, rw):
-        return SH.sharded_two_layer_apply_row(ops, tp, c2["phys"], rw, rw, 1, M, opt.seed, Q, OS, True, 0x20)
-
     for _ in range(max(args.warmup, 0)):
-        out = step(tops, row)
+        out = A.two_layer_apply_row_sharded(top, st, st, 1, opt, 0x20)
     ctx.sync()
     if world > 1:
         dist.barrier()
@@ -553,43 +556,74 @@ def run_sharded(args, rank, world, local_rank):
     with ClockSampler(local_rank) as clk:
         e0.record(stream)
         for _ in range(args.steps):
-            out = step(tops, row)
+            out = A.two_layer_apply_row_sharded(top, st, st, 1, opt, 0x20)
         e1.record(stream)
         ctx.sync()
         torch.cuda.synchronize()
     dt = e0.elapsed_time(e1) / 1e3 / args.steps
     launches = ctx.counters()["launches"]
+    del out
+
     # e2e: inputs from pinned host memory, boundary copied back every step
-    pinned_in = [torch.from_numpy(np.ascontiguousarray(x).view(np.float64)).pin_memory()
-                 for x in [c2["sites"][1 * L + c] for c in range(L)] + list(c2["top"])]
-    shapes = [c2["sites"][1 * L + c].shape for c in range(L)] + [t.shape for t in c2["top"]]
-    h2d = sum(p.numel() * 8 for p in pinned_in)
-    d2h = 0
+    host_sites, host_top = c2["sites"], c2["top"]
+    pinned_sites = [torch.from_numpy(x.view(np.float64)).pin_memory() for x in host_sites]
+    pinned_top = [torch.from_numpy(x.view(np.float64)).pin_memory() for x in host_top]
+    h2d = sum(x.nbytes for x in host_sites) + sum(x.nbytes for x in host_top)
+    out_shapes = [(R * R, 1 if c == 0 else M, 1 if c == L - 1 else M) for c in range(L)]
+    pinned_out = [torch.empty(int(np.prod(x)) * 2, dtype=torch.float64).pin_memory() for x in out_shapes]
+    d2h = sum(p.numel() * 8 for p in pinned_out)
+
+    def e2e_step():
+        sites = [A.DeviceTensor(_from_pinned(ctx, p, x.shape), ctx) for p, x in zip(pinned_sites, host_sites)]
+        tops = [A.DeviceTensor(_from_pinned(ctx, p, x.shape), ctx) for p, x in zip(pinned_top, host_top)]
+        s2 = A.PepsState(3, L, 2, sites, ctx=ctx)
+        t2 = A.TwoLayerBoundary.from_sites(tops, c2["phys"], ctx=ctx)
+        o = A.two_layer_apply_row_sharded(t2, s2, s2, 1, opt, 0x20)
+        for i, site in enumerate(o.sites):
+            _to_pinned(ctx, site, pinned_out[i])
+        ctx.sync()
+
+    e2e_step()
     if world > 1:
         dist.barrier()
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        dev = [A.DeviceTensor(_from_pinned(ctx, p, sh), ctx) for p, sh in zip(pinned_in, shapes)]
-        o, _ = step(dev[L:], dev[:L])
-        host = [x.numpy() for x in o]
-        d2h = sum(h.nbytes for h in host)
-    ctx.sync()
+        e2e_step()
     dt_e2e = (time.perf_counter() - t0) / args.steps
+
+    norm5 = None
+    if not args.no_norms:
+        c5 = inputs.config5()
+        st5 = A.PepsState(32, 32, 2, c5["sites"], ctx=ctx)
+        opt5 = A.ContractOption.two_layer_opt(64, c5["seed"], 2, 8)
+        if world > 1:
+            dist.barrier()
+        ctx.sync()
+        t0 = time.perf_counter()
+        A.contract_two_layer_sharded(st5, st5, opt5)
+        ctx.sync()
+        norm5 = time.perf_counter() - t0
     if world > 1:
-        t = torch.tensor([dt, dt_e2e], dtype=torch.float64, device="cuda")
+        t = torch.tensor([dt, dt_e2e, norm5 or 0.0], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        dt, dt_e2e = float(t[0]), float(t[1])
+        dt, dt_e2e, norm5 = float(t[0]), float(t[1]), (float(t[2]) if norm5 is not None else None)
+    A.comm_destroy(ctx)
     if rank != 0:
         return 0
     flops = alg_flops_row()
     line = {"metric": METRIC, "value": flops / dt / 1e12, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "c128", "data": "synthetic (seeded N(0,1) Box-Muller over SplitMix64)",
-            "config": dict(workload_config(world), parallelism=f"bond-sharded x{world} (t / s of the boundary bond)"),
+            "config": dict(workload_config(world),
+                           parallelism=f"bond-sharded x{world} (t / s of the boundary bond, NCCL)"),
             "s_per_row_absorb": dt,
+            "value_reference_counter": refcounter_flops_row() / dt / 1e12,
             "clocks": clk.summary(), "gpu_launches": launches,
             "e2e": {"value": flops / dt_e2e / 1e12, "unit": UNIT, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "s_per_step": dt_e2e}}
+    if norm5 is not None:
+        line["s_per_norm"] = {"config5_32x32_r8_m64_sharded": norm5,
+                              "note": "one bond-sharded contract_two_layer on all ranks (max over ranks)"}
     print(json.dumps(line), flush=True)
     return 0
 
@@ -603,8 +637,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-norms", action="store_true", help="skip the per-config s/norm timings (configs 1, 3, 5, 4)")
     ap.add_argument("--sharded", action="store_true",
-                    help="N>1: split one row absorb across the ranks along the boundary bond (strong scaling) "
-                         "instead of N independent replicas")
+                    help="run the bond-sharded C++ driver even at N=1 (N>1 always does)")
+    ap.add_argument("--replicas", action="store_true",
+                    help="N>1: N independent single-GPU replicas (weak scaling) instead of the sharded row")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -617,7 +652,7 @@ def main():
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl")
     try:
-        if args.sharded:
+        if args.sharded or (world > 1 and not args.replicas):
             return run_sharded(args, rank, world, local_rank)
         return run_b200(args, rank, world, local_rank)
     finally:

@@ -2,7 +2,7 @@
  * peps_b200.h — C ABI of the B200-native einsumsvd library.
  *
  * The reference (arxiv/paper_2006_15234, /root/reference/proj) has no FFI: its
- * drop-in interface is the public C++ API in proj/include/peps/*.hpp, and
+ * drop-in interface is the public C++ API in the proj/include/peps headers, and
  * proj/include/peps/backend.hpp:7-10 states that another engine "would slot in
  * behind the same kernel signatures".  Each entry point below replaces one of
  * those signatures (cited per function); a reference-side C++ shim that binds
@@ -205,6 +205,26 @@ int pepsb_two_layer_apply_row(pepsb_ctx* ctx, const pepsb_boundary* top, const p
                               pepsb_boundary** out);
 int pepsb_contract_two_layer(pepsb_ctx* ctx, const pepsb_state* bra, const pepsb_state* ket,
                              const pepsb_contract_opt* opt, double* re, double* im);
+
+/* ---- multi-GPU: one process per GPU, an NCCL communicator per
+ * context, the bond-sharded row absorb.  NCCL is loaded at run time
+ * (libnccl.so.2).  The reference is single-process; these entry
+ * points replace contract_two_layer / two_layer_apply_row (contraction.hpp:83-90)
+ * for a caller that owns N GPUs.  Collectives run on the library stream. */
+/* ncclGetUniqueId: rank 0 calls it and sends the 128 bytes to every rank */
+int pepsb_comm_unique_id(unsigned char* id128);
+/* ncclCommInitRank on the context's device (collective over the world) */
+int pepsb_comm_init(pepsb_ctx* ctx, const unsigned char* id128, int rank, int world);
+int pepsb_comm_destroy(pepsb_ctx* ctx);
+/* two_layer_apply_row with every column einsumsvd split along the boundary bond
+ * across the communicator's ranks; inputs and the emitted boundary replicated */
+int pepsb_two_layer_apply_row_sharded(pepsb_ctx* ctx, const pepsb_boundary* top, const pepsb_state* bra,
+                                      const pepsb_state* ket, int row, const pepsb_contract_opt* opt,
+                                      uint64_t seed_tag, pepsb_boundary** out);
+/* contract_two_layer with every row absorb bond-sharded; the scalar on every rank */
+int pepsb_contract_two_layer_sharded(pepsb_ctx* ctx, const pepsb_state* bra, const pepsb_state* ket,
+                                     const pepsb_contract_opt* opt, double* re, double* im);
+
 /* chain_scalar (mps.hpp:52) */
 int pepsb_chain_scalar(pepsb_ctx* ctx, const pepsb_boundary* b, double* re, double* im);
 

@@ -331,3 +331,136 @@ def inner_exact_pair(bra, ket, rows, cols) -> complex:
             tens.append(m)
             specs.append(lab)
     return complex(np.einsum(",".join(specs) + "->", *tens, optimize="greedy"))
+
+
+# ----------------------------------------------------------------------------- observables.cpp:261-333
+
+def flip_vertical(sites, rows, cols):
+    """observables.cpp:261-270: rows reversed, (phys, up, left, down, right) -> up/down swapped."""
+    return [sites[r * cols + c].transpose(0, 3, 2, 1, 4) for r in range(rows - 1, -1, -1) for c in range(cols)]
+
+
+def sweep_boundaries(sites, rows, cols, m, seed, power_iters=2, oversample=-1, tag=0x20):
+    """observables.cpp:272-281: boundaries after rows 0..k, k = 0..rows-1."""
+    top, phys = two_layer_first_row(sites, rows, cols)
+    out = [(top, phys)]
+    for r in range(1, rows):
+        top, phys = two_layer_apply_row(top, phys, sites, rows, cols, r, m, seed, power_iters, oversample, True, tag)
+        out.append((top, phys))
+    return out
+
+
+def build_row_cache(sites, rows, cols, m, seed, power_iters=2, oversample=-1):
+    """observables.cpp:325-333: tops (tag 0x20) and bots (flipped state, tag 0x21, bots[k] = fb[n-1-k])."""
+    tops = sweep_boundaries(sites, rows, cols, m, seed, power_iters, oversample, 0x20)
+    fb = sweep_boundaries(flip_vertical(sites, rows, cols), rows, cols, m, seed, power_iters, oversample, 0x21)
+    return tops, [fb[rows - 1 - k] for k in range(rows)]
+
+
+# ----------------------------------------------------------------------------- contraction.cpp:345-650 (band zipper)
+
+def band_value(top, bra, ket, rows, cols, r0, r1, bottom, pieces):
+    """Exact contraction of band rows r0..r1 between the boundary `top` (sites,
+    phys) and `bottom` (or None at the lattice edge) with insertion pieces
+    [(row, col, op, bond_ids)], column by column as band_column / band_step
+    build it (contraction.cpp:368-474, 545-560): carried roles [top][bra, ket per
+    band row][bottom] plus the gate bonds crossing the cut."""
+    if r1 < r0 or r1 - r0 > 1:
+        raise ValueError("band must span one or two rows")
+    IN, OUT = "ABCDEFGHIJ", "MNOPQRSTUV"
+    nrows = r1 - r0 + 1
+    has_top, has_bot = top is not None, bottom is not None
+    roles = int(has_top) + 2 * nrows + int(has_bot)
+
+    def partner_cols(p):
+        out = {}
+        for bid in p[3]:
+            for q in pieces:
+                if q is not p and bid in q[3]:
+                    out[bid] = q[1]
+        return out
+
+    def active(c):
+        ids = set()
+        for p in pieces:
+            for bid, pc in partner_cols(p).items():
+                lo, hi = min(p[1], pc), max(p[1], pc)
+                if lo <= c < hi:
+                    ids.add(bid)
+        return sorted(ids)
+
+    env, env_lab, in_bonds = np.ones((), dtype=np.complex128), "", []
+    for c in range(cols):
+        out_bonds = active(c)
+        dummies = iter("abcdefhmnopqrst")
+        h_in = lambda role: next(dummies) if c == 0 else IN[role]
+        h_out = lambda role: next(dummies) if c + 1 == cols else OUT[role]
+        ts, labs = [env], [env_lab]
+        if has_top:
+            t, ph = top[0][c], top[1][c]
+            ts.append(t.reshape(ph[0], ph[1], t.shape[1], t.shape[2]))
+            labs.append("uv" + h_in(0) + h_out(0))
+        for br in range(nrows):
+            row = r0 + br
+            up_b = ("u" if has_top else next(dummies)) if br == 0 else "y"
+            up_k = ("v" if has_top else next(dummies)) if br == 0 else "z"
+            last = br + 1 == nrows
+            dn_b = ("k" if has_bot else next(dummies)) if last else "y"
+            dn_k = ("l" if has_bot else next(dummies)) if last else "z"
+            piece = [p for p in pieces if p[0] == row and p[1] == c]
+            piece = piece[0] if piece else None
+            phys_b = "w" if br == 0 else "i"
+            phys_k = ("x" if br == 0 else "j") if piece else phys_b
+            rb, rk = int(has_top) + 2 * br, int(has_top) + 2 * br + 1
+            ts.append(bra[row * cols + c].conj())
+            labs.append(phys_b + up_b + h_in(rb) + dn_b + h_out(rb))
+            ts.append(ket[row * cols + c])
+            labs.append(phys_k + up_k + h_in(rk) + dn_k + h_out(rk))
+            if piece:
+                pl = phys_b + phys_k
+                pc = partner_cols(piece)
+                for bid in piece[3]:
+                    if pc[bid] == c:
+                        pl += "g"
+                    elif pc[bid] > c:
+                        pl += OUT[roles + out_bonds.index(bid)]
+                    else:
+                        pl += IN[roles + in_bonds.index(bid)]
+                ts.append(np.asarray(piece[2], dtype=np.complex128))
+                labs.append(pl)
+        if has_bot:
+            t, ph = bottom[0][c], bottom[1][c]
+            ts.append(t.reshape(ph[0], ph[1], t.shape[1], t.shape[2]))
+            labs.append("kl" + h_in(roles - 1) + h_out(roles - 1))
+        out_lab = (OUT[:roles] if c + 1 < cols else "") + "".join(OUT[roles + i] for i in range(len(out_bonds)))
+        env = np.einsum(",".join(labs) + "->" + out_lab, *ts, optimize="optimal")
+        env_lab = "".join(IN[OUT.index(ch)] for ch in out_lab)
+        in_bonds = out_bonds
+    return complex(env)
+
+
+def zz_pieces():
+    """split_two_site(Z (x) Z) (observables.cpp:284-295): SVD of op.permute{0,2,1,3}
+    split 2|2, rank by retained_rank (cap d^2), sqrt(s) on both sides."""
+    z = np.diag([1.0, -1.0]).astype(np.complex128)
+    zz = np.einsum("ac,bd->abcd", z, z)
+    u, s, vt = svd(zz.transpose(0, 2, 1, 3).copy(), 2)
+    g = retained_rank(s, 4, 1e-14)
+    w = np.sqrt(s[:g])
+    return z, u[..., :g] * w, (vt[:g] * w[:, None, None]).transpose(1, 2, 0)
+
+
+def local_expectations(sites, rows, cols, cache, terms):
+    """<Z_i> / <Z_iZ_j> terms (kind, r0, c0, r1, c1) from a row cache (tops, bots),
+    each band value divided by the cached norm (observables.cpp:335-422)."""
+    tops, bots = cache
+    norm = chain_scalar(tops[rows - 1][0])
+    z, left, right = zz_pieces()
+    vals = []
+    for kind, r0, c0, r1, c1 in terms:
+        br0, br1 = min(r0, r1), max(r0, r1)
+        top = tops[br0 - 1] if br0 > 0 else None
+        bot = bots[br1 + 1] if br1 + 1 < rows else None
+        pieces = [(r0, c0, z, [])] if kind == 0 else [(r0, c0, left, [0]), (r1, c1, right, [0])]
+        vals.append(band_value(top, sites, sites, rows, cols, br0, br1, bot, pieces) / norm)
+    return norm, np.array(vals)

@@ -110,6 +110,13 @@ _SIGS = {
     "pepsb_two_layer_first_row": (C.c_int, [_VP, _VP, _VP, C.POINTER(_VP)]),
     "pepsb_two_layer_apply_row": (C.c_int, [_VP, _VP, _VP, _VP, C.c_int, C.POINTER(ContractOpt), C.c_uint64,
                                             C.POINTER(_VP)]),
+    "pepsb_comm_unique_id": (C.c_int, [C.c_char_p]),
+    "pepsb_comm_init": (C.c_int, [_VP, C.c_char_p, C.c_int, C.c_int]),
+    "pepsb_comm_destroy": (C.c_int, [_VP]),
+    "pepsb_two_layer_apply_row_sharded": (C.c_int, [_VP, _VP, _VP, _VP, C.c_int, C.POINTER(ContractOpt),
+                                                    C.c_uint64, C.POINTER(_VP)]),
+    "pepsb_contract_two_layer_sharded": (C.c_int, [_VP, _VP, _VP, C.POINTER(ContractOpt), C.POINTER(C.c_double),
+                                                   C.POINTER(C.c_double)]),
     "pepsb_contract_two_layer": (C.c_int, [_VP, _VP, _VP, C.POINTER(ContractOpt), C.POINTER(C.c_double),
                                            C.POINTER(C.c_double)]),
     "pepsb_chain_scalar": (C.c_int, [_VP, _VP, C.POINTER(C.c_double), C.POINTER(C.c_double)]),

@@ -501,6 +501,56 @@ def contract_two_layer(bra: PepsState, ket: PepsState, opt: ContractOption) -> c
     return complex(re.value, im.value)
 
 
+# ---- multi-GPU: NCCL communicator per context, bond-sharded row absorb
+
+def comm_unique_id() -> bytes:
+    """ncclGetUniqueId (rank 0); broadcast the 128 bytes to the other ranks."""
+    buf = C.create_string_buffer(128)
+    check(lib().pepsb_comm_unique_id(buf))
+    return buf.raw
+
+
+def comm_init(ctx: "Context", unique_id: bytes, rank: int, world: int) -> None:
+    """ncclCommInitRank on the context's device (collective over the world)."""
+    if len(unique_id) != 128:
+        raise ValueError("unique id must be 128 bytes")
+    check(lib().pepsb_comm_init(ctx.h, unique_id, int(rank), int(world)))
+
+
+def comm_init_from_torch(ctx: "Context", group=None) -> None:
+    """Rank 0 draws the NCCL unique id and broadcasts it over an initialised
+    torch.distributed group (any backend); every rank then joins."""
+    import torch
+    import torch.distributed as dist
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    obj = [comm_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0, group=group)
+    comm_init(ctx, obj[0], rank, world)
+
+
+def comm_destroy(ctx: "Context") -> None:
+    check(lib().pepsb_comm_destroy(ctx.h))
+
+
+def two_layer_apply_row_sharded(top: TwoLayerBoundary, bra: PepsState, ket: PepsState, row: int,
+                                opt: ContractOption, seed_tag: int = 0x20) -> TwoLayerBoundary:
+    """two_layer_apply_row (contraction.cpp:269-311) split along the boundary
+    bond across the context's communicator (C++ driver, NCCL on the library stream)."""
+    h = _VP()
+    o = opt.c()
+    check(lib().pepsb_two_layer_apply_row_sharded(bra.ctx.h, top.h, bra.h, ket.h, int(row), C.byref(o),
+                                                  C.c_uint64(seed_tag), C.byref(h)))
+    return TwoLayerBoundary(h, bra.ctx)
+
+
+def contract_two_layer_sharded(bra: PepsState, ket: PepsState, opt: ContractOption) -> complex:
+    """contract_two_layer (contraction.cpp:313-338) with every row absorb bond-sharded."""
+    re, im = C.c_double(), C.c_double()
+    o = opt.c()
+    check(lib().pepsb_contract_two_layer_sharded(bra.ctx.h, bra.h, ket.h, C.byref(o), C.byref(re), C.byref(im)))
+    return complex(re.value, im.value)
+
+
 def chain_scalar(b: TwoLayerBoundary) -> complex:
     re, im = C.c_double(), C.c_double()
     check(lib().pepsb_chain_scalar(b.ctx.h, b.h, C.byref(re), C.byref(im)))

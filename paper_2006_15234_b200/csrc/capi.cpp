@@ -9,6 +9,7 @@
 #include "../../include/peps_b200.h"
 #include "ite.h"
 #include "peps.h"
+#include "sharded.h"
 #include "smalldense.cuh"
 #include "tensor_ops.cuh"
 #include "zgemm.cuh"
@@ -798,6 +799,53 @@ int pepsb_contract_two_layer(pepsb_ctx* c, const pepsb_state* bra, const pepsb_s
   return guard([&] {
     need(c, "ctx");
     auto v = contract_two_layer(*c->ctx, bra->s, ket->s, opt_of(opt));
+    *re = v.first;
+    *im = v.second;
+  });
+}
+
+int pepsb_comm_unique_id(unsigned char* id128) {
+  return guard([&] {
+    need(id128, "id");
+    comm_unique_id(id128);
+  });
+}
+
+int pepsb_comm_init(pepsb_ctx* c, const unsigned char* id128, int rank, int world) {
+  return guard([&] {
+    need(c, "ctx");
+    need(id128, "id");
+    comm_init(*c->ctx, id128, rank, world);
+  });
+}
+
+int pepsb_comm_destroy(pepsb_ctx* c) {
+  return guard([&] {
+    need(c, "ctx");
+    comm_destroy(*c->ctx);
+  });
+}
+
+int pepsb_two_layer_apply_row_sharded(pepsb_ctx* c, const pepsb_boundary* top, const pepsb_state* bra,
+                                      const pepsb_state* ket, int row, const pepsb_contract_opt* opt,
+                                      uint64_t tag, pepsb_boundary** out) {
+  return guard([&] {
+    need(c, "ctx");
+    need(top, "top");
+    need(bra, "bra");
+    need(ket, "ket");
+    if (row < 0 || row >= bra->s.rows) throw Error(kValidationError, "row outside the grid");
+    *out = new pepsb_boundary{two_layer_apply_row_sharded(*c->ctx, top->b, bra->s, ket->s, row, opt_of(opt), tag)};
+  });
+}
+
+int pepsb_contract_two_layer_sharded(pepsb_ctx* c, const pepsb_state* bra, const pepsb_state* ket,
+                                     const pepsb_contract_opt* opt, double* re, double* im) {
+  return guard([&] {
+    need(c, "ctx");
+    need(bra, "bra");
+    need(ket, "ket");
+    auto v = contract_two_layer_sharded(*c->ctx, bra->s, ket->s, opt_of(opt));
     *re = v.first;
     *im = v.second;
   });

@@ -15,6 +15,7 @@
 namespace pepsb {
 
 class Ctx;
+struct NcclComm;  // sharded.cpp
 
 // Accumulates host wall time into *acc (no-op when acc is null).
 struct HostTimer {
@@ -185,6 +186,8 @@ class Ctx {
   // (option "pipeline_rows").
   int pipeline_rows = -1;  // rows in flight K (< 2: sequential; -1: automatic, peps.cpp pipeline_depth)
   std::vector<std::unique_ptr<Ctx>> helpers;  // lazily created, same device
+  // NCCL communicator of the bond-sharded row absorb (pepsb_comm_init; sharded.cpp)
+  std::shared_ptr<NcclComm> comm;
 
   // Optional per-launch device timing (CUDA events on `stream`), used by the
   // bench's roofline pass; off in timed runs.

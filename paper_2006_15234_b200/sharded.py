@@ -210,6 +210,60 @@ class DeviceOps:
         self.ctx.sync()
         return out
 
+    # --- cached environments across groups
+    def new_group(self, ranks):
+        return self.comm.dist.new_group(ranks)
+
+    def broadcast_boundaries(self, bounds, src):
+        """Boundaries [(sites, phys)] from global rank `src` to every rank of the
+        world: shapes as objects, data as NCCL broadcasts of device buffers."""
+        import torch
+        dist = self.comm.dist
+        meta = [None if bounds is None else [([tuple(t.shape) for t in b[0]], list(b[1])) for b in bounds]]
+        dist.broadcast_object_list(meta, src=src, group=self.comm.group)
+        self.ctx.sync()
+        out = []
+        for k, (shapes, phys) in enumerate(meta[0]):
+            sites = []
+            for i, shp in enumerate(shapes):
+                if bounds is not None:
+                    x = torch.as_tensor(bounds[k][0][i], device="cuda").clone()
+                else:
+                    x = torch.empty(shp, dtype=torch.complex128, device="cuda")
+                dist.broadcast(x, src=src, group=self.comm.group)
+                torch.cuda.current_stream().synchronize()
+                sites.append(self.A.from_device_ptr(x.data_ptr(), shp, self.ctx))
+                self.ctx.sync()  # copied before x returns to torch's allocator
+            out.append((sites, [tuple(p) for p in phys]))
+        return out
+
+    def allgather_obj(self, obj):
+        out = [None] * self.comm.world
+        self.comm.dist.all_gather_object(out, obj, group=self.comm.group)
+        return out
+
+    def zz_pieces(self):
+        """split_two_site(Z (x) Z) (observables.cpp:284-295) with the device SVD."""
+        z = np.diag([1.0, -1.0]).astype(np.complex128)
+        zz = np.einsum("ac,bd->abcd", z, z)
+        u, sv, v = self.A.svd(zz.transpose(0, 2, 1, 3).copy(), 2, self.ctx)
+        g = retained_rank(list(sv), 4, 1e-14)
+        w = np.sqrt(np.asarray(sv[:g]))
+        return z, u.numpy()[..., :g] * w, (v.numpy()[:g] * w[:, None, None]).transpose(1, 2, 0)
+
+    def band_values(self, top, bot, sites, rows, cols, r0, r1, splices):
+        """One band environment (contraction.cpp:572-624) and a splice per term (:626-650)."""
+        A = self.A
+        st = A.PepsState(rows, cols, 2, sites, ctx=self.ctx)
+        tb = A.TwoLayerBoundary.from_sites(top[0], top[1], ctx=self.ctx) if top is not None else None
+        bb = A.TwoLayerBoundary.from_sites(bot[0], bot[1], ctx=self.ctx) if bot is not None else None
+        env = A.band_environment(tb, st, st, r0, r1, bb)
+        out = []
+        for pieces, c0, c1 in splices:
+            ps = [A.InsertionPiece((r, c), op, list(ids)) for r, c, op, ids in pieces]
+            out.append(A.band_splice(env, tb, st, st, bb, ps, c0, c1))
+        return out
+
     # --- collectives (in place on the library's buffer / new tensor)
     def _torch(self, t):
         import torch
@@ -406,6 +460,107 @@ def sharded_contract_two_layer(ops, bra_sites: Sequence, ket_sites: Sequence, ro
         top, phys = sharded_two_layer_apply_row(ops, top, phys, bra_row, ket_row, r, max_rank, seed, power_iters,
                                                 oversample, canonicalize, 0x20)
     return ops.chain_scalar(top)
+
+
+# ----------------------------------------------------------------------------- cached environments
+
+def _first_row(ops, bra_sites, ket_sites, cols):
+    """two_layer_first_row (contraction.cpp:254-267), replicated."""
+    top, phys = [], []
+    for c in range(cols):
+        b, k = bra_sites[c], ket_sites[c]
+        sb, sk = ops.shape(b), ops.shape(k)
+        t = ops.contract("dulbr,dULBR->bBlLrR", ops.conj(b), k)
+        top.append(ops.reshape(t, (sb[3] * sk[3], sb[2] * sk[2], sb[4] * sk[4])))
+        phys.append((sb[3], sk[3]))
+    return top, phys
+
+
+def sharded_sweep(ops, sites, rows, cols, max_rank, seed, power_iters, oversample, tag):
+    """sweep_boundaries (observables.cpp:272-281) with every row absorb
+    bond-sharded over ops.comm: [(sites, phys)] after rows 0..k, replicated."""
+    top, phys = _first_row(ops, sites, sites, cols)
+    out = [(top, phys)]
+    for r in range(1, rows):
+        row = [sites[r * cols + c] for c in range(cols)]
+        top, phys = sharded_two_layer_apply_row(ops, top, phys, row, row, r, max_rank, seed, power_iters,
+                                                oversample, True, tag)
+        out.append((top, phys))
+    return out
+
+
+def band_groups(terms, rows):
+    """Terms (kind, r0, c0, r1, c1) grouped by band (min row, max row), in band order."""
+    groups = {}
+    for i, (kind, r0, c0, r1, c1) in enumerate(terms):
+        key = (min(r0, r1), max(r0, r1))
+        if key[1] - key[0] > 1 or key[1] >= rows:
+            raise ValueError("terms must lie within one row or two adjacent rows")
+        groups.setdefault(key, []).append(i)
+    return sorted(groups.items())
+
+
+def distributed_local_expectations(ops, make_ops, sites, rows, cols, max_rank, seed, power_iters=2, oversample=-1,
+                                   terms=()):
+    """Cached-environment expectation values across GPU groups (SURVEY §8(e) row 2;
+    build_row_cache observables.cpp:325-333, bands contraction.cpp:572-650).
+
+    The world splits in two groups: the first ceil(W/2) ranks run the top sweep
+    (tag 0x20), the others the bottom sweep on the vertically flipped state (tag
+    0x21, bots[k] = fb[n-1-k]), each bond-sharded inside its group.  Each
+    group's leader broadcasts its boundaries; the bands are then distributed by
+    band row (band i on rank i mod W, one band environment + a splice per term)
+    and the scalars all-gathered.  With W = 1 both sweeps run on rank 0.
+
+    ops: the world's backend; make_ops(comm) builds one on a sub-communicator.
+    terms: (kind, r0, c0, r1, c1), kind 0 = Z_i, 1 = Z_iZ_j.  Returns (norm,
+    values) on every rank, values divided by the cached norm like the
+    reference's expectation()."""
+    comm = ops.comm
+    W, me = comm.world, comm.rank
+    flipped = [ops.contract("puldr->pdlur", sites[r * cols + c]) for r in range(rows - 1, -1, -1)
+               for c in range(cols)]
+    if W == 1:
+        tops = sharded_sweep(ops, sites, rows, cols, max_rank, seed, power_iters, oversample, 0x20)
+        fb = sharded_sweep(ops, flipped, rows, cols, max_rank, seed, power_iters, oversample, 0x21)
+    else:
+        n_top = (W + 1) // 2
+        top_ranks, bot_ranks = list(range(n_top)), list(range(n_top, W))
+        g_top, g_bot = ops.new_group(top_ranks), ops.new_group(bot_ranks)
+        mine = g_top if me < n_top else g_bot
+        sub = make_ops(Comm(mine))
+        if me < n_top:
+            tops = sharded_sweep(sub, sites, rows, cols, max_rank, seed, power_iters, oversample, 0x20)
+            fb = None
+        else:
+            fb = sharded_sweep(sub, flipped, rows, cols, max_rank, seed, power_iters, oversample, 0x21)
+            tops = None
+        tops = ops.broadcast_boundaries(tops, 0)
+        fb = ops.broadcast_boundaries(fb, n_top)
+    bots = [fb[rows - 1 - k] for k in range(rows)]
+    norm = ops.chain_scalar(tops[rows - 1][0])
+    z, left, right = ops.zz_pieces()
+    values = {}
+    for bi, ((br0, br1), idx) in enumerate(band_groups(terms, rows)):
+        if bi % W != me:
+            continue
+        top = tops[br0 - 1] if br0 > 0 else None
+        bot = bots[br1 + 1] if br1 + 1 < rows else None
+        splices = []
+        for i in idx:
+            kind, r0, c0, r1, c1 = terms[i]
+            if kind == 0:
+                splices.append(([(r0, c0, z, [])], c0, c0))
+            else:
+                splices.append(([(r0, c0, left, [0]), (r1, c1, right, [0])], min(c0, c1), max(c0, c1)))
+        for i, v in zip(idx, ops.band_values(top, bot, sites, rows, cols, br0, br1, splices)):
+            values[i] = v / norm
+    if W > 1:
+        merged = {}
+        for part in ops.allgather_obj(values):
+            merged.update(part)
+        values = merged
+    return norm, np.array([values[i] for i in range(len(terms))])
 
 
 # ----------------------------------------------------------------------------- simple-update ITE

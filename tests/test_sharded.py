@@ -11,6 +11,7 @@ import numpy as np
 import pytest
 
 from oracle import peps_oracle as O
+from paper_2006_15234_b200 import inputs as I
 from paper_2006_15234_b200 import sharded as SH
 
 
@@ -126,7 +127,7 @@ class NumpyOps:
         import torch
         self.calls["allreduce"] += 1
         x = torch.from_numpy(np.ascontiguousarray(t).view(np.float64).copy())
-        self.comm.dist.all_reduce(x)
+        self.comm.dist.all_reduce(x, group=self.comm.group)
         return x.numpy().view(np.complex128).reshape(t.shape)
 
     def allgather(self, t, axis, extent):
@@ -145,13 +146,35 @@ class NumpyOps:
         buf[tuple(idx)] = t
         x = torch.from_numpy(buf.view(np.float64).copy())
         parts = [torch.empty_like(x) for _ in range(w)]
-        self.comm.dist.all_gather(parts, x)
+        self.comm.dist.all_gather(parts, x, group=self.comm.group)
         out = []
         for p, (a, b) in zip(parts, sizes):
             arr = p.numpy().view(np.complex128).reshape(pad)
             idx[axis] = slice(0, b - a)
             out.append(arr[tuple(idx)])
         return np.concatenate(out, axis=axis)
+
+
+    # --- cached environments across groups
+    def new_group(self, ranks):
+        return self.comm.dist.new_group(ranks)
+
+    def broadcast_boundaries(self, bounds, src):
+        self.calls["broadcast"] = self.calls.get("broadcast", 0) + 1
+        obj = [bounds]
+        self.comm.dist.broadcast_object_list(obj, src=src, group=self.comm.group)
+        return obj[0]
+
+    def allgather_obj(self, obj):
+        out = [None] * self.comm.world
+        self.comm.dist.all_gather_object(out, obj, group=self.comm.group)
+        return out
+
+    def zz_pieces(self):
+        return O.zz_pieces()
+
+    def band_values(self, top, bot, sites, rows, cols, r0, r1, splices):
+        return [O.band_value(top, sites, sites, rows, cols, r0, r1, bot, pieces) for pieces, _, _ in splices]
 
 
 def _problem(r, rows=3, cols=4, seed=11):
@@ -302,3 +325,82 @@ def test_sharded_contract_and_ite_world2_gloo(refo):
         assert e1 < 1e-9, (rank, e1)
         assert e2 < 1e-12, (rank, e2)  # per-bond updates are the reference's own code
         assert calls["exchange"] == 3 * 4  # one exchange per colour per step
+
+
+# ----------------------------------------------------------------------------- cached environments across groups
+
+def _cache_terms(rows, cols):
+    terms = [(0, i // cols, i % cols, i // cols, i % cols) for i in range(rows * cols)]
+    terms += [(1, 1, 1, 1, 2), (1, 0, 2, 1, 2), (1, 2, 3, 3, 3), (1, 3, 0, 3, 1)]
+    return terms
+
+
+def _cache_case(ops, make_ops):
+    """Config-3/5 style: <Z_i> on every site + horizontal / vertical ZZ from the
+    distributed cached environments, against the reference's own values
+    (tests/golden/golden.npz: bands_*, generated by oracle/_ref) and the serial
+    numpy restatement."""
+    import numpy as _np
+    sites = I.random_peps(4, 4, 2, 91, scale=1 / _np.sqrt(8))
+    terms = _cache_terms(4, 4)
+    norm, vals = SH.distributed_local_expectations(ops, make_ops, sites, 4, 4, 4, 13, 2, -1, terms)
+    g = dict(_np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "golden.npz")))
+    assert [tuple(t) for t in g["bands_terms"]] == terms
+    return abs(norm - g["bands_norm"][0]) / abs(g["bands_norm"][0]), float(_np.abs(vals - g["bands_values"]).max())
+
+
+def test_numpy_band_restatement_matches_reference_golden(golden):
+    sites = I.random_peps(4, 4, 2, 91, scale=1 / np.sqrt(8))
+    cache = O.build_row_cache(sites, 4, 4, 4, 13, 2, -1)
+    norm, vals = O.local_expectations(sites, 4, 4, cache, [tuple(t) for t in golden["bands_terms"]])
+    assert abs(norm - golden["bands_norm"][0]) <= 1e-12 * abs(golden["bands_norm"][0])
+    assert np.abs(vals - golden["bands_values"]).max() < 1e-12
+
+
+def test_distributed_cache_world1():
+    en, ev = _cache_case(NumpyOps(SH.Comm()), NumpyOps)
+    assert en < 1e-10 and ev < 1e-10
+
+
+def _worker3(rank, world, port, q):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        ops = NumpyOps(SH.Comm())
+        made = []
+
+        def make_ops(comm):
+            made.append(NumpyOps(comm))
+            return made[-1]
+
+        en, ev = _cache_case(ops, make_ops)
+        sub = made[0].calls if made else {}
+        q.put((rank, en, ev, dict(ops.calls), dict(sub), made[0].comm.world if made else 0))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_distributed_cache_gloo(world):
+    """SURVEY §8(e) row 2 on world-size-2 and -3 gloo groups: the top and bottom
+    sweeps on separate rank groups (bond-sharded inside a group of 2 at world
+    3), boundaries broadcast, bands distributed by row, scalars gathered; norm
+    and all 20 values match the reference to 1e-10 on every rank."""
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker3, args=(rk, world, port, q)) for rk in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=600)
+    res = [q.get(timeout=5) for _ in procs]
+    for rank, en, ev, calls, sub, sub_world in res:
+        assert en < 1e-10 and ev < 1e-10, (rank, en, ev)
+        assert calls["broadcast"] == 2  # tops from rank 0, bots from the bottom group's leader
+        assert sub_world == (((world + 1) // 2) if rank < (world + 1) // 2 else world // 2)
+        if sub_world > 1:  # the sweep inside a group is itself bond-sharded
+            assert sub["allreduce"] > 0 and sub["allgather"] > 0
