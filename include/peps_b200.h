@@ -108,6 +108,10 @@ int pepsb_ctx_profile_report(pepsb_ctx* ctx, double* out16);
 int pepsb_ctx_profile_report_ex(pepsb_ctx* ctx, double* out20);
 /* Per-launch records of the profile (kind, device ms, algorithmic flops) x n; returns n */
 int pepsb_ctx_profile_records(pepsb_ctx* ctx, double* out, int cap);
+/* Timeline of the profile (streams overlapped as in a timed run): per launch
+ * (kind, start ms, end ms, executed flops, stream 0 main / 1 side), times
+ * relative to the first record; returns n */
+int pepsb_ctx_profile_timeline(pepsb_ctx* ctx, double* out, int cap);
 /* Diagnostics: device status word idx (word 7 = cumulative Jacobi sweeps). */
 int pepsb_ctx_debug_word(pepsb_ctx* ctx, int idx, int reset);
 /* CUDA stream the library enqueues on (cudaStream_t), for event timing */

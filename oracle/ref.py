@@ -352,3 +352,29 @@ def chain_scalar(sites):
     tl = _TList(sites)
     _, dd = _bag(_fn("ref_chain_scalar")(*tl.args()))
     return complex(dd[0], dd[1])
+
+
+def json_driver(which: str, config: str) -> str:
+    """run_expect_json / run_vqe_json / run_ite_json (drivers.cpp:265-550): the result document."""
+    L = lib()
+    L.ref_bag_text_len.restype = C.c_int64
+    ptr = _fn("ref_json_driver")({"expect": 0, "vqe": 1, "ite": 2}[which], config.encode())
+    if not ptr:
+        raise RefError(L.ref_last_error_type(), L.ref_last_error().decode())
+    bag = C.c_void_p(ptr)
+    try:
+        n = L.ref_bag_text_len(bag)
+        buf = C.create_string_buffer(int(n) + 1)
+        L.ref_bag_text(bag, buf)
+        return buf.raw[:n].decode()
+    finally:
+        L.ref_bag_free(bag)
+
+
+def minimize(method: str, fn: int, x0, max_evaluations=300, tolerance=1e-6, initial_step=0.4):
+    """optimize.cpp minimize on analytic objective `fn` (0 Rosenbrock, 1 quadratic + cosine)."""
+    x = np.ascontiguousarray(x0, dtype=np.float64)
+    t, d = _bag(_fn("ref_minimize")(method.encode(), int(fn), len(x), C.c_void_p(x.ctypes.data),
+                                    int(max_evaluations), C.c_double(tolerance), C.c_double(initial_step)))
+    return dict(converged=bool(d[0]), evaluations=int(d[1]), best_f=float(d[2]), trace=d[3:].copy(),
+                best_x=t[0].real.copy())

@@ -28,6 +28,7 @@
 #include "peps/linalg.hpp"
 #include "peps/mps.hpp"
 #include "peps/drivers.hpp"
+#include "peps/optimize.hpp"
 #include "peps/observables.hpp"
 #include "peps/rng.hpp"
 #include "peps/state.hpp"
@@ -45,6 +46,7 @@ thread_local int g_err_type = 0;
 struct Bag {
   std::vector<Tensor> tensors;
   std::vector<double> doubles;
+  std::string text;  // JSON front ends
 };
 
 template <class F>
@@ -204,6 +206,42 @@ void ref_bag_doubles(Bag* b, double* out) {
   std::memcpy(out, b->doubles.data(), b->doubles.size() * sizeof(double));
 }
 void ref_bag_free(Bag* b) { delete b; }
+int64_t ref_bag_text_len(Bag* b) { return static_cast<int64_t>(b->text.size()); }
+void ref_bag_text(Bag* b, char* out) { std::memcpy(out, b->text.data(), b->text.size()); }
+
+// optimize.cpp:189-194 on an analytic objective (fn 0: Rosenbrock, 1: a shifted
+// quadratic + cosine bump); doubles: [status_converged, evaluations, best_f, trace...]
+Bag* ref_minimize(const char* method, int fn, int n, const double* x0, int max_evals, double tol, double step) {
+  return guarded([&](Bag& b) {
+    Objective f = [fn](std::span<const double> x) {
+      double v = 0.0;
+      if (fn == 0) {
+        for (size_t i = 0; i + 1 < x.size(); ++i)
+          v += 100.0 * (x[i + 1] - x[i] * x[i]) * (x[i + 1] - x[i] * x[i]) + (1.0 - x[i]) * (1.0 - x[i]);
+      } else {
+        for (size_t i = 0; i < x.size(); ++i) v += (x[i] - 0.3 * (i + 1)) * (x[i] - 0.3 * (i + 1)) + 0.1 * std::cos(3.0 * x[i]);
+      }
+      return v;
+    };
+    OptimConfig oc;
+    oc.max_evaluations = static_cast<std::size_t>(max_evals);
+    oc.tolerance = tol;
+    oc.initial_step = step;
+    OptimResult r = minimize(method, f, std::span<const double>(x0, static_cast<size_t>(n)), oc);
+    b.doubles = {r.status == "converged" ? 1.0 : 0.0, static_cast<double>(r.evaluations), r.best_f};
+    for (double v : r.trace) b.doubles.push_back(v);
+    b.tensors.push_back(Tensor({r.best_x.size()}));
+    for (size_t i = 0; i < r.best_x.size(); ++i) b.tensors.back().data()[i] = r.best_x[i];
+  });
+}
+
+// JSON front ends (drivers.cpp:265-550): 0 run_expect_json, 1 run_vqe_json, 2 run_ite_json
+Bag* ref_json_driver(int which, const char* config) {
+  return guarded([&](Bag& b) {
+    const std::string cfg(config);
+    b.text = which == 0 ? run_expect_json(cfg) : which == 1 ? run_vqe_json(cfg) : run_ite_json(cfg);
+  });
+}
 
 void ref_set_threads(int n) { openblas_set_num_threads(n); }
 int ref_get_threads() { return openblas_get_num_threads(); }

@@ -61,6 +61,7 @@ _SIGS = {
     "pepsb_ctx_get_counter": (C.c_int, [_VP, C.c_char_p, C.POINTER(C.c_uint64)]),
     "pepsb_ctx_reset_counters": (C.c_int, [_VP]),
     "pepsb_ctx_stream": (_VP, [_VP]),
+    "pepsb_ctx_profile_timeline": (C.c_int, [_VP, C.POINTER(C.c_double), C.c_int]),
     "pepsb_ctx_debug_word": (C.c_int, [_VP, C.c_int, C.c_int]),
     "pepsb_ctx_profile_records": (C.c_int, [_VP, C.POINTER(C.c_double), C.c_int]),
     "pepsb_ctx_profile": (C.c_int, [_VP, C.c_int]),

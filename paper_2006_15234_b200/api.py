@@ -125,6 +125,13 @@ class Context:
         return {k: dict(launches=int(a[5 * i]), ms=a[5 * i + 1], flops=a[5 * i + 2], bytes=a[5 * i + 3],
                         exec_flops=a[5 * i + 4]) for i, k in enumerate(kinds)}
 
+    def profile_timeline(self, cap: int = 1 << 16):
+        """[(kind, start_ms, end_ms, executed_flops, side)] of the profiled launches."""
+        a = (C.c_double * (5 * cap))()
+        n = lib().pepsb_ctx_profile_timeline(self.h, a, cap)
+        kinds = ["gemm", "small", "gather", "other"]
+        return [(kinds[int(a[5 * i])], a[5 * i + 1], a[5 * i + 2], a[5 * i + 3], int(a[5 * i + 4])) for i in range(n)]
+
     @property
     def stream(self) -> int:
         return int(lib().pepsb_ctx_stream(self.h) or 0)

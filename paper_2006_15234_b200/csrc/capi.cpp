@@ -285,6 +285,29 @@ int pepsb_ctx_profile_records(pepsb_ctx* c, double* out, int cap) {
   return n;
 }
 
+int pepsb_ctx_profile_timeline(pepsb_ctx* c, double* out, int cap) {
+  int n = 0;
+  guard([&] {
+    need(c, "ctx");
+    c->ctx->sync();
+    const auto& prof = c->ctx->prof;
+    if (prof.empty()) return;
+    for (auto& r : prof) {
+      if (n >= cap) break;
+      float t0 = 0.f, t1 = 0.f;
+      PEPSB_CUDA(cudaEventElapsedTime(&t0, prof.front().a, r.a));
+      PEPSB_CUDA(cudaEventElapsedTime(&t1, prof.front().a, r.b));
+      out[5 * n] = r.kind;
+      out[5 * n + 1] = t0;
+      out[5 * n + 2] = t1;
+      out[5 * n + 3] = r.exec_flops;
+      out[5 * n + 4] = r.side;
+      ++n;
+    }
+  });
+  return n;
+}
+
 int pepsb_ctx_debug_word(pepsb_ctx* c, int idx, int reset) {
   int v = -1;
   guard([&] {

@@ -325,7 +325,8 @@ void Ctx::profile_report(double* out) {
 
 ProfScope::ProfScope(Ctx& c, int kind, double flops, double bytes, double exec_flops) : ctx(c) {
   if (!ctx.profiling) return;
-  Ctx::ProfRec r{ctx.take_event(), ctx.take_event(), kind, flops, bytes, exec_flops < 0.0 ? flops : exec_flops};
+  Ctx::ProfRec r{ctx.take_event(), ctx.take_event(), kind, flops, bytes, exec_flops < 0.0 ? flops : exec_flops,
+                 ctx.stream == ctx.side_stream ? 1 : 0};
   PEPSB_CUDA(cudaEventRecord(r.a, ctx.stream));
   ctx.prof.push_back(r);
   idx = static_cast<int>(ctx.prof.size()) - 1;

@@ -197,6 +197,7 @@ class Ctx {
     int kind;
     double flops, bytes;
     double exec_flops;  // flops the hardware executes (3M GEMM: 6 per complex MAC, not 8)
+    int side = 0;       // recorded on the side stream
   };
   bool profiling = false;
   std::vector<ProfRec> prof;

@@ -133,32 +133,70 @@ def cfg4_states(refo):
     return plus, ref_state, ref_pert
 
 
-def test_config4_norm_energy_match_reference(A, cfg4_states):
-    """Config 4 (8x8 TFIM ITE, J=1, h=3, r=8, 100 steps) against the reference's
-    own evolution.  The compared quantities are gauge-invariant: norm, log-norm
-    and the TFIM energy of each final state, all evaluated by ONE contraction
-    (the device's two-layer BMPS at m=32 and m=48, identical options for every
-    state).  The m=32 and m=48 values agree to 1e-12, so the contraction is exact
-    at this precision and the differences are those of the states.  Bar: 1e-8,
-    or twice the reference's own spread under a 1e-14 perturbation of |+>."""
+def _bond_spectra(sites, rows, cols):
+    """Singular values of every bond's two-site block (gauge-invariant up to the
+    simple-update gauge on the bond itself): the spectrum of the bond matrix
+    obtained by contracting the two sites over the shared bond."""
+    out = []
+    for r in range(rows):
+        for c in range(cols):
+            a = sites[r * cols + c]
+            if c + 1 < cols:
+                b = sites[r * cols + c + 1]
+                m = np.einsum("puldr,qUrDR->puldqUDR", a, b).reshape(a.size // a.shape[4], -1)
+                out.append(np.linalg.svd(m, compute_uv=False)[:8])
+            if r + 1 < rows:
+                b = sites[(r + 1) * cols + c]
+                m = np.einsum("puldr,qdLDR->pulrqLDR", a, b).reshape(a.size // a.shape[3], -1)
+                out.append(np.linalg.svd(m, compute_uv=False)[:8])
+    return out
+
+
+def _spectra_err(x, y):
+    return max(float(np.abs(a[:len(b)] / a[0] - b[:len(a)] / b[0]).max()) for a, b in zip(x, y))
+
+
+def test_config4_matches_reference_within_its_own_spread(A, cfg4_states):
+    """Config 4 (8x8 TFIM ITE, J=1, h=3, r=8, 100 steps, 11 200 truncated bond
+    updates) against the reference's own evolution.
+
+    Shapes are bit-exact.  Gauge-invariant comparisons, each bounded by 1e-8 or
+    by twice the reference's OWN spread under a 1e-14 perturbation of |+>
+    (measured here, not assumed), whichever is larger:
+      - the normalised singular values of every bond's two-site block;
+      - the norm, log-norm and TFIM energy of each final state through ONE
+        identical contraction (device two-layer BMPS at m=32, same options for
+        every state).
+    The contraction itself is far from converged for this state (log-norm at
+    m = 16/32/64/96: 403.719/403.755/403.781/403.787,
+    profiles/r02_config4_contraction_convergence.log) and amplifies a 1e-14
+    input perturbation of the reference to ~1e-5 in the norm, so no
+    implementation can be compared with the reference to 1e-8 on these
+    quantities; the bound is the reference's own reproducibility."""
     plus, ref_state, ref_pert = cfg4_states
     dev = A.ite_tfim(A.PepsState(8, 8, 2, plus), 1.0, 3.0, 0.01, 100, 8)
     dev_sites = [s.numpy() for s in dev.sites]
     assert [s.shape for s in dev_sites] == [s.shape for s in ref_state]
+    assert [s.shape for s in ref_pert] == [s.shape for s in ref_state]
 
-    def measure(sites, m):
-        st = A.PepsState(8, 8, 2, sites)
-        opt = A.ContractOption.two_layer_opt(m, 7, 2, 8)
-        e = A.expectation(st, A.tfim_terms(8, 8, 1.0, 3.0), A.ExpectationOptions(opt, True, True, False))
-        return e.norm_sq, e.value
+    sp_ref = _bond_spectra(ref_state, 8, 8)
+    spread_sp = _spectra_err(_bond_spectra(ref_pert, 8, 8), sp_ref)
+    err_sp = _spectra_err(_bond_spectra(dev_sites, 8, 8), sp_ref)
+    assert err_sp <= max(1e-8, 2 * spread_sp), (err_sp, spread_sp)
 
-    n_dev, e_dev = measure(dev_sites, 48)
-    n_dev32, e_dev32 = measure(dev_sites, 32)
-    assert abs(n_dev32 - n_dev) <= 1e-12 * abs(n_dev) and abs(e_dev32 - e_dev) <= 1e-12 * abs(e_dev)
-    n_ref, e_ref = measure(ref_state, 48)
-    n_pert, e_pert = measure(ref_pert, 48)
-    spread_n = abs(n_pert - n_ref) / abs(n_ref)
+    def measure(sites):
+        mx = [float(np.abs(s).max()) for s in sites]
+        st = A.PepsState(8, 8, 2, [s / m for s, m in zip(sites, mx)])
+        opt = A.ContractOption.two_layer_opt(32, 7, 2, 8)
+        e = A.expectation(st, A.tfim_terms(8, 8, 1.0, 3.0), A.ExpectationOptions(opt, True, True, True))
+        return float(np.log(abs(e.norm_sq)) + 2 * np.log(mx).sum()), e.value
+
+    ln_ref, e_ref = measure(ref_state)
+    ln_pert, e_pert = measure(ref_pert)
+    ln_dev, e_dev = measure(dev_sites)
+    spread_n = abs(np.expm1(ln_pert - ln_ref))
+    spread_ln = abs(ln_pert - ln_ref) / abs(ln_ref)
     spread_e = abs(e_pert - e_ref) / abs(e_ref)
-    assert abs(n_dev - n_ref) <= max(1e-8, 2 * spread_n) * abs(n_ref)
-    assert abs(np.log(abs(n_dev)) - np.log(abs(n_ref))) <= max(1e-8, 2 * spread_n) * abs(np.log(abs(n_ref)))
-    assert abs(e_dev - e_ref) <= max(1e-8, 2 * spread_e) * abs(e_ref)
+    assert abs(np.expm1(ln_dev - ln_ref)) <= max(1e-8, 2 * spread_n), (ln_dev, ln_ref, ln_pert)
+    assert abs(ln_dev - ln_ref) / abs(ln_ref) <= max(1e-8, 2 * spread_ln)
+    assert abs(e_dev - e_ref) / abs(e_ref) <= max(1e-8, 2 * spread_e), (e_dev, e_ref, e_pert)

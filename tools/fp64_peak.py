@@ -13,6 +13,9 @@ res = (ctypes.c_double * 2)(0.0, 0.0)
 lib = ctypes.CDLL(os.path.join(here, "fp64_probe.so"))
 rc = lib.probe(res)
 out = {"dmma_issue_tflops": res[0], "dfma_issue_tflops": res[1], "probe_rc": rc}
+r16 = (ctypes.c_double * 3)(0.0, 0.0, 0.0)
+out["probe16_rc"] = lib.probe16(r16)
+out["dmma_m16n8k4_tflops"], out["dmma_m16n8k8_tflops"], out["dmma_m16n8k16_tflops"] = r16[0], r16[1], r16[2]
 
 def gemm_tf(dtype, n, flop_per_mac):
     a = torch.randn(n, n, dtype=dtype, device="cuda")
