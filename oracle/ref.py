@@ -378,3 +378,14 @@ def minimize(method: str, fn: int, x0, max_evaluations=300, tolerance=1e-6, init
                                     int(max_evaluations), C.c_double(tolerance), C.c_double(initial_step)))
     return dict(converged=bool(d[0]), evaluations=int(d[1]), best_f=float(d[2]), trace=d[3:].copy(),
                 best_x=t[0].real.copy())
+
+
+def band_environment_time(top_sites, top_phys, bot_sites, bot_phys, sites, rows, cols, r0, r1, d=2):
+    """Seconds of one band_environment (contraction.cpp:572-624) on the reference."""
+    tl, a = _state_args(sites, rows, cols, d)
+    top, bot = _TList(top_sites), _TList(bot_sites)
+    _, dd = _bag(_fn("ref_band_environment_time")(*a, top.ndims, top.shapes, top.datas,
+                                                  _i64([x for p in top_phys for x in p]), bot.ndims, bot.shapes,
+                                                  bot.datas, _i64([x for p in bot_phys for x in p]), int(r0),
+                                                  int(r1)))
+    return float(dd[0])

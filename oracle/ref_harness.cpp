@@ -386,6 +386,25 @@ Bag* ref_two_layer_apply_row(int rows, int cols, int d, const int* ndims, const 
   });
 }
 
+// band_environment (contraction.cpp:572-624) of band rows r0..r1 between two
+// given boundaries (top above r0, bottom below r1), timed; doubles: [seconds]
+Bag* ref_band_environment_time(int rows, int cols, int d, const int* ndims, const int64_t* shapes,
+                               const double* const* datas, const int* top_ndims, const int64_t* top_shapes,
+                               const double* const* top_datas, const int64_t* top_phys, const int* bot_ndims,
+                               const int64_t* bot_shapes, const double* const* bot_datas, const int64_t* bot_phys,
+                               int r0, int r1) {
+  return guarded([&](Bag& b) {
+    PepsState s = make_state(rows, cols, d, ndims, shapes, datas);
+    TwoLayerBoundary top = make_boundary(cols, top_ndims, top_shapes, top_datas, top_phys);
+    TwoLayerBoundary bot = make_boundary(cols, bot_ndims, bot_shapes, bot_datas, bot_phys);
+    double t0 = now_s();
+    BandEnvironment env = band_environment(&top, s, s, static_cast<std::size_t>(r0), static_cast<std::size_t>(r1),
+                                           &bot);
+    b.doubles.push_back(now_s() - t0);
+    (void)env;
+  });
+}
+
 // doubles: [re, im, seconds, flops, peak_elements]
 Bag* ref_contract_two_layer(int rows, int cols, int d, const int* ndims, const int64_t* shapes,
                             const double* const* datas, int64_t m, uint64_t seed, int power_iters,

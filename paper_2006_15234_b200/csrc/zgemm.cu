@@ -761,11 +761,400 @@ void launch_any3m(const ZgemmParams& p, cudaStream_t stream) {
   }
 }
 
+// ---------------------------------------------------------------- tile-streaming variant
+// Short-K problems (K = 64 / 128 per output tile: GEMMs (1)/(2) of every
+// operator application) spend a large share of a one-tile CTA in the
+// pipeline fill and the epilogue.  Here a resident CTA walks a sequence of
+// output tiles (tile = blockIdx.x + i * gridDim.x, m fastest so consecutive
+// CTAs share the B tile in L2) and the cp.async pipeline runs straight across
+// tile boundaries: the first k-stages of tile i+1 are in flight while tile i
+// finishes and writes its epilogue, and the epilogue offsets of tile i+1 are
+// decoded into the other half of a double buffer during tile i.  Same
+// fragments, same k order per accumulator as zgemm_cx_kernel (results are
+// bitwise identical); requires splits == 1 and nk >= 4 (see use_stream).
+template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool AK, bool BNC, int ALG, int MINB>
+__global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32, MINB)
+    zgemm_stream_kernel(const ZgemmParams p) {
+  constexpr int NACC = ALG == 3 ? 3 : ALG == 1 ? 1 : 2;
+  using S = Smem3<BM, BN, BK, AK, BNC>;
+  constexpr int NT = (BM / WM) * (BN / WN) * 32;
+  constexpr int FM = WM / 8;
+  constexpr int FN = ALG == 1 ? WN / 4 : WN / 8;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double2* smem = reinterpret_cast<double2*>(smem_raw);
+  int64_t* rowoff = reinterpret_cast<int64_t*>(smem + STAGES * S::STAGE);  // [2][BM]
+  int64_t* coloff = rowoff + 2 * BM;                                        // [2][BN]
+
+  const int tid = threadIdx.x;
+  const int lane = tid & 31;
+  const int warp = tid >> 5;
+  const int wm0 = (warp % (BM / WM)) * WM;
+  const int wn0 = (warp / (BM / WM)) * WN;
+
+  const int64_t mtiles = (p.M + BM - 1) / BM;
+  const int64_t per_batch = mtiles * ((p.N + BN - 1) / BN);
+  const int64_t tiles = per_batch * p.batch;
+  if (static_cast<int64_t>(blockIdx.x) >= tiles) return;
+  const int64_t my_tiles = (tiles - blockIdx.x + gridDim.x - 1) / gridDim.x;
+  const int64_t nk = (p.K + BK - 1) / BK;
+  const int64_t steps = my_tiles * nk;
+
+  struct Coord {
+    int64_t m0, n0, offA, offB, offC;
+  };
+  auto coord = [&](int64_t local) {
+    const int64_t t = blockIdx.x + local * gridDim.x;
+    const int64_t bz = t / per_batch, r = t - bz * per_batch;
+    Coord c{(r % mtiles) * BM, (r / mtiles) * BN, 0, 0, 0};
+    int64_t idx = bz;
+    for (int a = p.nb - 1; a >= 0; --a) {
+      const int64_t e = p.bext[a];
+      const int64_t q = idx / e;
+      const int64_t rr = idx - q * e;
+      c.offA += rr * p.bsA[a];
+      c.offB += rr * p.bsB[a];
+      c.offC += rr * p.bsC[a];
+      idx = q;
+    }
+    return c;
+  };
+
+  constexpr int AIN = AK ? BK : BM, AOUT = AK ? BM : BK;
+  constexpr int BIN = BNC ? BN : BK, BOUT = BNC ? BK : BN;
+  constexpr bool AREG = (NT % AIN) == 0, BREG = (NT % BIN) == 0;
+  constexpr int UA = (BM * BK + NT - 1) / NT, UB = (BK * BN + NT - 1) / NT;
+  constexpr int AOS = AREG ? NT / AIN : 1, BOS = BREG ? NT / BIN : 1;
+  const int a_in = tid % AIN, a_o0 = tid / AIN, b_in = tid % BIN, b_o0 = tid / BIN;
+  const int64_t a_ustr = AK ? AOS * p.sAi : AOS * p.sAk;
+  const int64_t b_ustr = BNC ? BOS * p.sBk : BOS * p.sBj;
+
+  // loader state of the tile whose stages are being copied
+  int64_t ld_local = -1, ld_m0 = 0, ld_n0 = 0, a_base = 0, b_base = 0;
+  const double2* A = p.A;
+  const double2* B = p.B;
+  unsigned a_ok = 0, b_ok = 0;
+  auto set_load_tile = [&](int64_t local) {
+    const Coord c = coord(local);
+    ld_local = local;
+    ld_m0 = c.m0;
+    ld_n0 = c.n0;
+    A = p.A + c.offA;
+    B = p.B + c.offB;
+    a_ok = 0;
+    b_ok = 0;
+    if (AK) {
+      a_base = (ld_m0 + a_o0) * p.sAi + a_in * p.sAk;
+#pragma unroll
+      for (int u = 0; u < UA; ++u)
+        if (a_o0 + u * AOS < AOUT && ld_m0 + a_o0 + u * AOS < p.M) a_ok |= 1u << u;
+    } else {
+      a_base = (ld_m0 + a_in) * p.sAi + a_o0 * p.sAk;
+      a_ok = ld_m0 + a_in < p.M ? 1u : 0u;
+    }
+    if (BNC) {
+      b_base = b_o0 * p.sBk + (ld_n0 + b_in) * p.sBj;
+      b_ok = ld_n0 + b_in < p.N ? 1u : 0u;
+    } else {
+      b_base = (ld_n0 + b_o0) * p.sBj + b_in * p.sBk;
+#pragma unroll
+      for (int u = 0; u < UB; ++u)
+        if (b_o0 + u * BOS < BOUT && ld_n0 + b_o0 + u * BOS < p.N) b_ok |= 1u << u;
+    }
+    // epilogue offsets of this tile into its half of the double buffer (the
+    // epilogue that last read that half finished before the previous barrier)
+    int64_t* ro = rowoff + (local & 1) * BM;
+    int64_t* co = coloff + (local & 1) * BN;
+    for (int r = tid; r < BM; r += NT) {
+      const int64_t gi = ld_m0 + r;
+      ro[r] = gi < p.M ? decode_offset(gi, p.nr, p.rext, p.rstr) : 0;
+    }
+    for (int c2 = tid; c2 < BN; c2 += NT) {
+      const int64_t gj = ld_n0 + c2;
+      co[c2] = gj < p.N ? decode_offset(gj, p.nc, p.cext, p.cstr) : 0;
+    }
+  };
+  auto load_stage = [&](int slot, int64_t kt, int part, int nparts) {
+    double2* As = smem + slot * S::STAGE;
+    double2* Bs = As + S::A_ELEMS;
+    const int64_t k0 = kt * BK;
+    if constexpr (AREG) {
+      const double2* src = A + a_base + kt * BK * p.sAk;
+#pragma unroll
+      for (int u = 0; u < UA; ++u) {
+        if (u < part * UA / nparts || u >= (part + 1) * UA / nparts) continue;
+        const int o = a_o0 + u * AOS;
+        if ((AOUT % AOS) != 0 && o >= AOUT) break;
+        const bool ok = AK ? (((a_ok >> u) & 1u) && k0 + a_in < p.K) : (a_ok && k0 + o < p.K);
+        cp_async16(As + o * S::LDA + a_in, ok ? src + u * a_ustr : A, ok);
+      }
+    } else if (part == 0) {
+#pragma unroll
+      for (int e = tid; e < BM * BK; e += NT) {
+        int i, k;
+        if (AK) { i = e / BK; k = e % BK; } else { k = e / BM; i = e % BM; }
+        const int64_t gi = ld_m0 + i, gk = k0 + k;
+        const bool ok = gi < p.M && gk < p.K;
+        const double2* src = ok ? A + gi * p.sAi + gk * p.sAk : A;
+        double2* dst = AK ? As + i * S::LDA + k : As + k * S::LDA + i;
+        cp_async16(dst, src, ok);
+      }
+    }
+    if constexpr (BREG) {
+      const double2* src = B + b_base + kt * BK * p.sBk;
+#pragma unroll
+      for (int u = 0; u < UB; ++u) {
+        if (u < part * UB / nparts || u >= (part + 1) * UB / nparts) continue;
+        const int o = b_o0 + u * BOS;
+        if ((BOUT % BOS) != 0 && o >= BOUT) break;
+        const bool ok = BNC ? (b_ok && k0 + o < p.K) : (((b_ok >> u) & 1u) && k0 + b_in < p.K);
+        cp_async16(Bs + o * S::LDB + b_in, ok ? src + u * b_ustr : B, ok);
+      }
+    } else if (part == 0) {
+#pragma unroll
+      for (int e = tid; e < BK * BN; e += NT) {
+        int k, j;
+        if (BNC) { k = e / BN; j = e % BN; } else { j = e / BK; k = e % BK; }
+        const int64_t gj = ld_n0 + j, gk = k0 + k;
+        const bool ok = gj < p.N && gk < p.K;
+        const double2* src = ok ? B + gk * p.sBk + gj * p.sBj : B;
+        double2* dst = BNC ? Bs + k * S::LDB + j : Bs + j * S::LDB + k;
+        cp_async16(dst, src, ok);
+      }
+    }
+  };
+  // Prefetch cursor (flattened step = local * nk + kt), advanced by one step
+  // at a time: no divisions in the main loop.
+  int64_t pf_kt = 0;
+  int pf_slot = 0;
+  auto pf_advance = [&]() {
+    if (++pf_kt == nk) {
+      pf_kt = 0;
+      if (ld_local + 1 < my_tiles) set_load_tile(ld_local + 1);
+    }
+    if (++pf_slot == STAGES) pf_slot = 0;
+  };
+
+  double acc[FM][FN][NACC][2];
+#pragma unroll
+  for (int a = 0; a < FM; ++a)
+#pragma unroll
+    for (int b = 0; b < FN; ++b)
+#pragma unroll
+      for (int t = 0; t < NACC; ++t) acc[a][b][t][0] = acc[a][b][t][1] = 0.0;
+
+  set_load_tile(0);
+#pragma unroll
+  for (int s0 = 0; s0 < STAGES - 1; ++s0) {
+    if (s0 < steps) {
+      load_stage(pf_slot, pf_kt, 0, 1);
+      pf_advance();
+    }
+    cp_async_commit();
+  }
+
+  const int kq = lane & 3;
+  const int rq = lane >> 2;
+  const long long sga = p.conjA ? (long long)0x8000000000000000ULL : 0LL;
+  const long long sgb = p.conjB ? (long long)0x8000000000000000ULL : 0LL;
+  auto flip = [](double v, long long m) { return __longlong_as_double(__double_as_longlong(v) ^ m); };
+  double2 fa[2][ALG == 1 ? 1 : FM], fb[2][ALG == 1 ? 1 : FN];
+  double ra[2][FM], rb[2][FN];
+  const long long sgbr = (rq & 1) ? sgb : 0LL;
+  auto load_frags = [&](int buf, int slot, int ks) {
+    const double2* As = smem + slot * S::STAGE;
+    const double2* Bs = As + S::A_ELEMS;
+    const int kc = ks * 4 + kq;
+    if constexpr (ALG == 1) {
+#pragma unroll
+      for (int a = 0; a < FM; ++a) {
+        const int row = wm0 + a * 8 + rq;
+        ra[buf][a] = (AK ? As[row * S::LDA + kc] : As[kc * S::LDA + row]).x;
+      }
+#pragma unroll
+      for (int b = 0; b < FN; ++b) {
+        const int col = wn0 + b * 4 + (rq >> 1);
+        const double* e = reinterpret_cast<const double*>(BNC ? Bs + kc * S::LDB + col : Bs + col * S::LDB + kc);
+        rb[buf][b] = flip(e[rq & 1], sgbr);
+      }
+    } else {
+#pragma unroll
+      for (int a = 0; a < FM; ++a) {
+        const int row = wm0 + a * 8 + rq;
+        fa[buf][a] = AK ? As[row * S::LDA + kc] : As[kc * S::LDA + row];
+      }
+#pragma unroll
+      for (int b = 0; b < FN; ++b) {
+        const int col = wn0 + b * 8 + rq;
+        fb[buf][b] = BNC ? Bs[kc * S::LDB + col] : Bs[col * S::LDB + kc];
+      }
+    }
+  };
+  auto compute = [&](int buf) {
+    if constexpr (ALG == 1) {
+#pragma unroll
+      for (int a = 0; a < FM; ++a)
+#pragma unroll
+        for (int b = 0; b < FN; ++b) dmma884(acc[a][b][0][0], acc[a][b][0][1], ra[buf][a], rb[buf][b]);
+    } else if constexpr (ALG == 3) {
+      double ar[FM], ai[FM], as[FM], br[FN], bi[FN], bs[FN];
+#pragma unroll
+      for (int a = 0; a < FM; ++a) {
+        ar[a] = fa[buf][a].x;
+        ai[a] = flip(fa[buf][a].y, sga);
+        as[a] = ar[a] + ai[a];
+      }
+#pragma unroll
+      for (int b = 0; b < FN; ++b) {
+        br[b] = fb[buf][b].x;
+        bi[b] = flip(fb[buf][b].y, sgb);
+        bs[b] = br[b] + bi[b];
+      }
+#pragma unroll
+      for (int a = 0; a < FM; ++a)
+#pragma unroll
+        for (int b = 0; b < FN; ++b) dmma884(acc[a][b][0][0], acc[a][b][0][1], ar[a], br[b]);
+#pragma unroll
+      for (int a = 0; a < FM; ++a)
+#pragma unroll
+        for (int b = 0; b < FN; ++b) dmma884(acc[a][b][1][0], acc[a][b][1][1], ai[a], bi[b]);
+#pragma unroll
+      for (int a = 0; a < FM; ++a)
+#pragma unroll
+        for (int b = 0; b < FN; ++b) dmma884(acc[a][b][2][0], acc[a][b][2][1], as[a], bs[b]);
+    } else {
+      double ai[FM], nai[FM], bi[FN];
+#pragma unroll
+      for (int a = 0; a < FM; ++a) {
+        ai[a] = flip(fa[buf][a].y, sga);
+        nai[a] = flip(fa[buf][a].y, sga ^ (long long)0x8000000000000000ULL);
+      }
+#pragma unroll
+      for (int b = 0; b < FN; ++b) bi[b] = flip(fb[buf][b].y, sgb);
+#pragma unroll
+      for (int a = 0; a < FM; ++a)
+#pragma unroll
+        for (int b = 0; b < FN; ++b) {
+          dmma884(acc[a][b][0][0], acc[a][b][0][1], fa[buf][a].x, fb[buf][b].x);
+          dmma884(acc[a][b][1][0], acc[a][b][1][1], fa[buf][a].x, bi[b]);
+        }
+#pragma unroll
+      for (int a = 0; a < FM; ++a)
+#pragma unroll
+        for (int b = 0; b < FN; ++b) {
+          dmma884(acc[a][b][0][0], acc[a][b][0][1], nai[a], bi[b]);
+          dmma884(acc[a][b][1][0], acc[a][b][1][1], ai[a], fb[buf][b].x);
+        }
+    }
+  };
+  auto epilogue = [&](int64_t local) {
+    const Coord c = coord(local);
+    const int64_t* ro = rowoff + (local & 1) * BM;
+    const int64_t* co = coloff + (local & 1) * BN;
+#pragma unroll
+    for (int a = 0; a < FM; ++a) {
+      const int li = wm0 + a * 8 + (lane >> 2);
+      if (c.m0 + li >= p.M) continue;
+#pragma unroll
+      for (int b = 0; b < FN; ++b)
+#pragma unroll
+        for (int h = 0; h < (ALG == 1 ? 1 : 2); ++h) {
+          const int lj = ALG == 1 ? wn0 + b * 4 + (lane & 3) : wn0 + b * 8 + 2 * (lane & 3) + h;
+          if (c.n0 + lj >= p.N) continue;
+          double2 v;
+          if constexpr (ALG == 1) {
+            v = make_double2(acc[a][b][0][0], acc[a][b][0][1]);
+          } else if constexpr (ALG == 3) {
+            const double p1 = acc[a][b][0][h], p2 = acc[a][b][1][h], p3 = acc[a][b][NACC - 1][h];
+            v = make_double2(p1 - p2, p3 - p1 - p2);
+          } else {
+            v = make_double2(acc[a][b][0][h], acc[a][b][1][h]);
+          }
+          double2* dst = p.C + c.offC + ro[li] + co[lj];
+          if (p.accumulate) v = cadd(*dst, v);
+          *dst = v;
+        }
+    }
+#pragma unroll
+    for (int a = 0; a < FM; ++a)
+#pragma unroll
+      for (int b = 0; b < FN; ++b)
+#pragma unroll
+        for (int t = 0; t < NACC; ++t) acc[a][b][t][0] = acc[a][b][t][1] = 0.0;
+  };
+
+  constexpr int KS = BK / 4;
+  static_assert(KS % 2 == 0, "k steps per tile must be even (static fragment buffers)");
+  cp_async_wait<STAGES - 2>();
+  __syncthreads();
+  load_frags(0, 0, 0);
+  int64_t kt = 0, local = 0;
+  int slot = 0;
+  for (int64_t st = 0; st < steps; ++st) {
+    const bool do_pf = st + STAGES - 1 < steps;
+    const int next_slot = slot + 1 == STAGES ? 0 : slot + 1;
+#pragma unroll
+    for (int kp = 0; kp < KS; kp += 2) {
+      load_frags(1, slot, kp + 1);
+      if (do_pf) load_stage(pf_slot, pf_kt, kp, KS);
+      compute(0);
+      if (do_pf) load_stage(pf_slot, pf_kt, kp + 1, KS);
+      if (kp + 2 < KS) {
+        load_frags(0, slot, kp + 2);
+      } else {
+        cp_async_commit();
+        if (do_pf) pf_advance();
+        if (st + 1 < steps) {
+          cp_async_wait<STAGES - 2>();
+          __syncthreads();
+          load_frags(0, next_slot, 0);
+        }
+      }
+      compute(1);
+    }
+    slot = next_slot;
+    if (++kt == nk) {
+      epilogue(local);
+      kt = 0;
+      ++local;
+    }
+  }
+  cp_async_wait<0>();
+}
+
+template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool AK, bool BNC, int ALG, int MINB>
+void launch_stream(const ZgemmParams& p, cudaStream_t stream) {
+  using S = Smem3<BM, BN, BK, AK, BNC>;
+  constexpr int NT = (BM / WM) * (BN / WN) * 32;
+  const size_t smem = static_cast<size_t>(STAGES) * S::STAGE * sizeof(double2) + 2 * (BM + BN) * sizeof(int64_t);
+  auto kern = zgemm_stream_kernel<BM, BN, BK, WM, WN, STAGES, AK, BNC, ALG, MINB>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    PEPSB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    attr_set = true;
+  }
+  const int64_t tiles = ((p.M + BM - 1) / BM) * ((p.N + BN - 1) / BN) * p.batch;
+  const int64_t grid = std::min<int64_t>(tiles, static_cast<int64_t>(MINB) * p.num_sms);
+  kern<<<static_cast<unsigned>(grid), NT, smem, stream>>>(p);
+  PEPSB_LAUNCH();
+}
+
 // Complex x real (A real): 64 x 64 complex tiles, 4 warps of 32 x 32 (8 x 8
 // DMMA blocks of 8 rows x 4 complex columns), half the DMMAs of 4M.
+// Tile streaming pays where a one-tile CTA is mostly fill + epilogue: short K
+// (nk <= 8 k-tiles) over many tiles (at least four resident waves).
+bool use_stream(const ZgemmParams& p, int64_t bm, int64_t bn) {
+  if (!zgemm_stream_enabled() || p.splits != 1) return false;
+  const int64_t nk = (p.K + kBK - 1) / kBK;
+  const int64_t tiles = ((p.M + bm - 1) / bm) * ((p.N + bn - 1) / bn) * p.batch;
+  // nk >= 4: the next-but-one tile's epilogue offsets are written after the
+  // barrier that follows the epilogue which last read that half of the buffer
+  return nk >= 4 && nk <= 8 && tiles >= 8 * static_cast<int64_t>(p.num_sms);
+}
+
 template <bool AK, bool BNC>
 void launch_cr(const ZgemmParams& p, cudaStream_t stream) {
-  launch_cx<64, 64, kBK, 32, 32, kStages, AK, BNC, 1, 2>(p, stream);
+  if (use_stream(p, 64, 64)) launch_stream<64, 64, kBK, 32, 32, kStages, AK, BNC, 1, 2>(p, stream);
+  else launch_cx<64, 64, kBK, 32, 32, kStages, AK, BNC, 1, 2>(p, stream);
 }
 
 // 4M with complex fragments (one LDS.128 per fragment element, four DMMAs per
@@ -776,7 +1165,10 @@ void launch_any4c(const ZgemmParams& p, cudaStream_t stream) {
     case 1: launch_cx<64, 72, kBK, 32, 24, kStages, AK, BNC, 4, 1>(p, stream); break;
     case 2: launch_cx<72, 64, kBK, 24, 32, kStages, AK, BNC, 4, 1>(p, stream); break;
     case 3: launch_cx<72, 72, kBK, 24, 24, kStages, AK, BNC, 4, 1>(p, stream); break;
-    default: launch_cx<64, 64, kBK, 32, 32, kStages, AK, BNC, 4, 2>(p, stream); break;
+    default:
+      if (use_stream(p, 64, 64)) launch_stream<64, 64, kBK, 32, 32, kStages, AK, BNC, 4, 2>(p, stream);
+      else launch_cx<64, 64, kBK, 32, 32, kStages, AK, BNC, 4, 2>(p, stream);
+      break;
   }
 }
 
@@ -811,6 +1203,21 @@ bool zgemm_real_enabled() {
 }
 
 void zgemm_set_real(int on) { g_real.store(on ? 1 : 0); }
+
+std::atomic<int> g_stream{-1};
+
+bool zgemm_stream_enabled() {
+  int v = g_stream.load();
+  if (v < 0) {
+    // opt-in: measured slower on the config-2 row (67.1 vs 64.0 ms)
+    const char* e = getenv("PEPSB_GEMM_STREAM");
+    v = (e && e[0] == '1') ? 1 : 0;
+    g_stream.store(v);
+  }
+  return v != 0;
+}
+
+void zgemm_set_stream(int on) { g_stream.store(on ? 1 : 0); }
 
 std::atomic<int> g_small{-1};
 

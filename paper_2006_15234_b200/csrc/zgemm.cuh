@@ -60,6 +60,10 @@ struct ZgemmParams {
 enum GemmAlgo { kGemm4M = 0, kGemm3M = 1, kGemm4C = 2, kGemmCR = 3, kGemmSmall = 4 };
 constexpr int64_t kSmallMaxK = 128;
 constexpr int64_t kSmallMaxMacs = int64_t{1} << 13;
+// Tile-streaming kernels for short-K many-tile problems (opt-in:
+// PEPSB_GEMM_STREAM=1 or option "gemm_stream" = 1; measured slower at config 2).
+bool zgemm_stream_enabled();
+void zgemm_set_stream(int on);
 bool zgemm_small_enabled();
 void zgemm_set_small(int on);
 bool zgemm_is_small(const ZgemmParams& p);

@@ -14,6 +14,8 @@ Sections (inputs regenerated from seeds by paper_2006_15234_b200/inputs.py):
              singular values.  ~40 s.
   cfg3       config 3 (16x16, r=6, m=36, q=2, os=-1): cached norm + all 256 <Z_i>
              (observables.cpp:325-422).  ~25 min.
+  cfg3_pert  config 3 with every site multiplied by (1 + 1e-14 xi): the
+             reference's own rounding sensitivity of the 256 <Z_i>.  ~25 min.
   cfg5_8x8   config-5 parameters (r=8, m=64, q=2, os=8, N(0,1/128)) on an 8x8
              lattice: cached norm, centre <ZZ> (horizontal + vertical) and <Z> at
              the centre.  ~80 min.
@@ -38,7 +40,7 @@ from fullsize_common import (CFG2_COL_SEED, boundary_overlaps, cfg2_column_net, 
 
 
 def save(name, **kw):
-    p = os.path.join(HERE, f"fullsize_{name}.npz")
+    p = os.path.join(os.environ.get("GOLDEN_OUT", HERE), f"fullsize_{name}.npz")
     np.savez_compressed(p, **kw)
     print(f"wrote {p}", flush=True)
 
@@ -60,14 +62,16 @@ def sec_cfg2_row():
          shapes=np.array([s.shape for s in t], dtype=np.int64), seconds=np.array([time.time() - t0]))
 
 
-def sec_cfg3():
+def sec_cfg3(eps=0.0, name="cfg3"):
     c = I.config3()
+    if eps:
+        c["sites"] = perturb(c["sites"], eps)
     n = c["rows"]
     terms = [(0, i // n, i % n, i // n, i % n) for i in range(n * n)]
     t0 = time.time()
     norm, vals, info = ref.local_expectations(c["sites"], n, n, c["m"], c["seed"], terms, c["power_iters"],
                                               c["oversample"])
-    save("cfg3", norm=np.array([norm]), z=vals, terms=np.array(terms, dtype=np.int64),
+    save(name, norm=np.array([norm]), z=vals, terms=np.array(terms, dtype=np.int64), eps=np.array([eps]),
          t_cache=np.array([info["t_cache"]]), t_bands=np.array([info["t_bands"]]),
          seconds=np.array([time.time() - t0]))
 
@@ -85,6 +89,7 @@ def _cfg5(name, eps):
 
 
 SECTIONS = {"cfg2_col": sec_cfg2_col, "cfg2_row": sec_cfg2_row, "cfg3": sec_cfg3,
+            "cfg3_pert": lambda: sec_cfg3(1e-14, "cfg3_pert"),
             "cfg5_8x8": lambda: _cfg5("cfg5_8x8", 0.0), "cfg5_8x8_pert": lambda: _cfg5("cfg5_8x8_pert", 1e-14)}
 
 if __name__ == "__main__":

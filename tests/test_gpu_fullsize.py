@@ -89,16 +89,21 @@ def test_config2_row_absorb_matches_reference(algo):
 def test_config3_norm_and_all_z_match_reference(algo):
     """BASELINE config 3 at full size (16x16, r=6, m=36, q=2, oversample default
     -> k=41): the cached norm and all 256 <Z_i> (observables.cpp:325-422 via the
-    cached environments and band splices) against the reference's own run."""
+    cached environments and band splices) against the reference's own run.
+    Norm: 1e-8.  <Z_i>: 1e-8, or twice the reference's own spread under a 1e-14
+    perturbation of the input sites when that is larger (fullsize_cfg3_pert,
+    measured on the reference: 30 truncated row absorbs amplify rounding to the
+    1e-8 level on the individual <Z_i>)."""
     A = algo
-    g = golden("cfg3")
+    g, gp = golden("cfg3"), golden("cfg3_pert")
     c = I.config3()
     st = A.PepsState(16, 16, 2, c["sites"])
     opt = A.ContractOption.two_layer_opt(c["m"], c["seed"], c["power_iters"], c["oversample"])
     norm, z = device_local_expectations(A, st, opt, [tuple(t) for t in g["terms"]])
     assert abs(norm - g["norm"][0]) <= 1e-8 * abs(g["norm"][0])
+    spread = float(np.max(np.abs(gp["z"] - g["z"])))
     err = np.abs(z - g["z"])
-    assert np.all(err <= 1e-8 * np.maximum(1.0, np.abs(g["z"]))), float(err.max())
+    assert float(err.max()) <= max(1e-8, 2 * spread), (float(err.max()), spread)
 
 
 def test_config5_parameters_8x8_match_reference(algo):
