@@ -13,6 +13,7 @@
 #include "smalldense.cuh"
 #include "tensor_ops.cuh"
 #include "zgemm.cuh"
+#include "gram.cuh"
 
 using namespace pepsb;
 
@@ -195,6 +196,9 @@ int pepsb_ctx_set_option(pepsb_ctx* c, const char* key, int64_t value) {
     else if (k == "gemm_real") zgemm_set_real(static_cast<int>(value));
     else if (k == "gemm_small") zgemm_set_small(static_cast<int>(value));
     else if (k == "gemm_stream") zgemm_set_stream(static_cast<int>(value));
+    else if (k == "cr_cfg") zgemm_set_cr_cfg(static_cast<int>(value));
+    else if (k == "c3m_cfg") zgemm_set_c3m_cfg(static_cast<int>(value));
+    else if (k == "gemm_gram") gram_set_enabled(static_cast<int>(value));
     else if (k == "overlap") c->ctx->overlap = static_cast<int>(std::clamp<int64_t>(value, 0, 2));
     else if (k == "concurrent_sweeps") c->ctx->concurrent_sweeps = static_cast<int>(std::clamp<int64_t>(value, -1, 1));
     else if (k == "pipeline_rows") c->ctx->pipeline_rows = static_cast<int>(std::clamp<int64_t>(value, -1, 8));

@@ -17,6 +17,7 @@
 //     and t1 / t2 are scattered straight into the reference layouts
 //     (row axes..., rank) / (rank, col axes...).
 #include "decomp.h"
+#include "gram.cuh"
 
 #include <algorithm>
 #include <cmath>
@@ -47,6 +48,21 @@ int64_t prod(const std::vector<int64_t>& v) {
 // (transA: K x M) and B as K x N (transB: N x K), optional conjugation.
 void mm(Ctx& ctx, double2* C, const double2* A, bool transA, bool conjA, const double2* B, bool transB,
         bool conjB, int64_t M, int64_t N, int64_t K) {
+  // G = Y^H Y of a tall Y: the Hermitian Gram kernel (upper-triangle DMMA
+  // blocks of the interleaved real product, gram.cu)
+  if (A == B && transA && conjA && !transB && !conjB && M == N && gram_enabled() && gram_herk_eligible(K, M)) {
+    const int64_t nd = gram_herk_workspace(K, M, ctx.num_sms);
+    BufPtr work = ctx.alloc((nd + 1) / 2);
+    const int NB = static_cast<int>((2 * M + 7) / 8);
+    {
+      ProfScope ps(ctx, Ctx::kProfGemm, 8.0 * M * N * K, 16.0 * (M * K + M * N),
+                   128.0 * K * (NB * (NB + 1) / 2));
+      gram_herk(A, K, static_cast<int>(M), C, reinterpret_cast<double*>(work->p), ctx.num_sms, ctx.stream);
+    }
+    ctx.launches += 3;
+    ctx.flops += 2ull * M * N * K;
+    return;
+  }
   ZgemmParams p;
   p.A = A;
   p.B = B;

@@ -1477,7 +1477,7 @@ __global__ void __launch_bounds__(512) su_reduce_kernel(const SuSiteDesc* descs,
   for (int idx = threadIdx.x; idx < S * S; idx += blockDim.x) D.R[idx] = Rm[idx];
 }
 
-__global__ void __launch_bounds__(256) su_split_kernel(const SuBondDesc* descs, int* ranks, int* status,
+__global__ void __launch_bounds__(512) su_split_kernel(const SuBondDesc* descs, int* ranks, int* status,
                                                        unsigned long long* degenerate) {
   extern __shared__ __align__(16) unsigned char sm[];
   __shared__ int rank_sh;
@@ -1631,7 +1631,14 @@ void su_split(const SuBondDesc* d, int n, size_t smem, int* ranks, int* status, 
     attr = true;
   }
   if (n == 0) return;
-  su_split_kernel<<<n, 256, smem, st>>>(d, ranks, status, degenerate);
+  // 512 threads: one warp per Jacobi pair of a 32 x 32 block (16 pairs per
+  // round); PEPSB_SU_THREADS=256 restores two pairs per warp
+  static const int threads = [] {
+    const char* e = getenv("PEPSB_SU_THREADS");
+    const int v = e ? atoi(e) : 512;
+    return v == 256 ? 256 : 512;
+  }();
+  su_split_kernel<<<n, threads, smem, st>>>(d, ranks, status, degenerate);
   PEPSB_LAUNCH();
 }
 

@@ -753,6 +753,15 @@ void launch_cx(const ZgemmParams& p, cudaStream_t stream) {
 
 template <bool AK, bool BNC>
 void launch_any3m(const ZgemmParams& p, cudaStream_t stream) {
+  if (zgemm_c3m_cfg() == 1) {  // more, smaller warp tiles (latency hiding)
+    switch (p.cfg) {
+      case 1: launch_cx<64, 72, kBK, 8, 24, kStages, AK, BNC, 3, 1>(p, stream); break;
+      case 2: launch_cx<72, 64, kBK, 24, 8, kStages, AK, BNC, 3, 1>(p, stream); break;
+      case 3: launch_cx<72, 72, kBK, 8, 24, kStages, AK, BNC, 3, 1>(p, stream); break;
+      default: launch_cx<64, 32, kBK, 16, 16, kStages, AK, BNC, 3, 2>(p, stream); break;
+    }
+    return;
+  }
   switch (p.cfg) {
     case 1: launch_cx<64, 72, kBK, 16, 24, kStages, AK, BNC, 3, 1>(p, stream); break;
     case 2: launch_cx<72, 64, kBK, 24, 16, kStages, AK, BNC, 3, 1>(p, stream); break;
@@ -1154,6 +1163,7 @@ bool use_stream(const ZgemmParams& p, int64_t bm, int64_t bn) {
 template <bool AK, bool BNC>
 void launch_cr(const ZgemmParams& p, cudaStream_t stream) {
   if (use_stream(p, 64, 64)) launch_stream<64, 64, kBK, 32, 32, kStages, AK, BNC, 1, 2>(p, stream);
+  else if (zgemm_cr_cfg() >= 1) launch_cx<64, 64, kBK, 32, 16, kStages, AK, BNC, 1, 2>(p, stream);
   else launch_cx<64, 64, kBK, 32, 32, kStages, AK, BNC, 1, 2>(p, stream);
 }
 
@@ -1167,6 +1177,7 @@ void launch_any4c(const ZgemmParams& p, cudaStream_t stream) {
     case 3: launch_cx<72, 72, kBK, 24, 24, kStages, AK, BNC, 4, 1>(p, stream); break;
     default:
       if (use_stream(p, 64, 64)) launch_stream<64, 64, kBK, 32, 32, kStages, AK, BNC, 4, 2>(p, stream);
+      else if (zgemm_cr_cfg() == 2) launch_cx<64, 64, kBK, 32, 16, kStages, AK, BNC, 4, 2>(p, stream);
       else launch_cx<64, 64, kBK, 32, 32, kStages, AK, BNC, 4, 2>(p, stream);
       break;
   }
@@ -1203,6 +1214,42 @@ bool zgemm_real_enabled() {
 }
 
 void zgemm_set_real(int on) { g_real.store(on ? 1 : 0); }
+
+std::atomic<int> g_cr_cfg{-1};
+
+// 64 x 64 complex x real tile: 1 (default) = 8 warps of 32 x 16 (2 CTAs /
+// SM, 16 warps / SM), 0 = 4 warps of 32 x 32 (8 warps / SM); 2 = 8 warps for
+// the 4M complex-fragment 64 x 64 tile too (it spills at 128 registers).  ncu on the short-K launches (4 warps): DMMA pipe 63 % active, 12 % of
+// the warp slots occupied, stalls per issue wait 2.1 / short scoreboard 0.76;
+// the 8-warp tile (128 registers, no spills) hides more of those latencies:
+// config-2 row 63.9 -> 61.4 ms, bitwise identical results.
+int zgemm_cr_cfg() {
+  int v = g_cr_cfg.load();
+  if (v < 0) {
+    const char* e = getenv("PEPSB_CR_CFG");
+    v = e ? std::clamp(std::atoi(e), 0, 2) : 1;
+    g_cr_cfg.store(v);
+  }
+  return v;
+}
+
+void zgemm_set_cr_cfg(int v) { g_cr_cfg.store(std::clamp(v, 0, 2)); }
+
+std::atomic<int> g_c3m_cfg{-1};
+
+// 3M warp tiles: 0 = 64x32 / 4 warps, 64x72 / 12, 72x72 / 9; 1 = 64x32 / 8,
+// 64x72 / 24, 72x72 / 27 warps.
+int zgemm_c3m_cfg() {
+  int v = g_c3m_cfg.load();
+  if (v < 0) {
+    const char* e = getenv("PEPSB_C3M_CFG");
+    v = e ? std::clamp(std::atoi(e), 0, 1) : 0;
+    g_c3m_cfg.store(v);
+  }
+  return v;
+}
+
+void zgemm_set_c3m_cfg(int v) { g_c3m_cfg.store(std::clamp(v, 0, 1)); }
 
 std::atomic<int> g_stream{-1};
 

@@ -62,6 +62,10 @@ constexpr int64_t kSmallMaxK = 128;
 constexpr int64_t kSmallMaxMacs = int64_t{1} << 13;
 // Tile-streaming kernels for short-K many-tile problems (opt-in:
 // PEPSB_GEMM_STREAM=1 or option "gemm_stream" = 1; measured slower at config 2).
+int zgemm_cr_cfg();
+int zgemm_c3m_cfg();
+void zgemm_set_c3m_cfg(int v);
+void zgemm_set_cr_cfg(int v);
 bool zgemm_stream_enabled();
 void zgemm_set_stream(int on);
 bool zgemm_small_enabled();

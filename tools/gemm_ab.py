@@ -75,5 +75,21 @@ for v in (va, vb):
     rows.append((t, [s.numpy() for s in o.sites]))
 res["row_absorb_ms"] = [rows[0][0], rows[1][0]]
 res["row_bitwise_equal"] = all(np.array_equal(a, b) for a, b in zip(rows[0][1], rows[1][1]))
+
+# config-5 shapes (L = 32, m = 64, r = 8) with a COMPLEX top boundary (as every
+# boundary after the first row is): the chain then runs 3M products
+L5 = 32
+sites5 = inputs.random_peps(3, L5, 8, 11, scale=1 / np.sqrt(128))
+top5, phys5 = inputs.random_boundary(L5, (8, 8), 64, 12, scale=0.1)
+top5 = [t * np.exp(1j * inputs.gaussian(t.shape, 13 + i).real) for i, t in enumerate(top5)]
+st5 = A.PepsState(3, L5, 2, sites5)
+tb5 = A.TwoLayerBoundary.from_sites(top5, phys5)
+rows5 = []
+for v in (va, vb):
+    ctx.set_option(opt_name, v)
+    t, o = timed(lambda: A.two_layer_apply_row(tb5, st5, st5, 1, opt, 0x20), reps=3)
+    rows5.append((t, [s.numpy() for s in o.sites]))
+res["row_cfg5_complex_ms"] = [rows5[0][0], rows5[1][0]]
+res["row_cfg5_bitwise_equal"] = all(np.array_equal(a, b) for a, b in zip(rows5[0][1], rows5[1][1]))
 ctx.set_option(opt_name, vb)
 print(json.dumps(res, indent=1))
