@@ -865,6 +865,44 @@ std::pair<DTensor, DTensor> gram_orthogonalize(Ctx& ctx, const DTensor& a, int s
 
 // ---------------------------------------------------------------------------- sharded-driver blocks
 
+DTensor orth_async(Ctx& ctx, const DTensor& y) {
+  std::string lab;
+  for (size_t i = 0; i < y.shape.size(); ++i) lab += static_cast<char>('a' + i);
+  LTensor q = orth(ctx, as_labelled(y, lab));
+  DTensor out;
+  out.buf = q.buf;
+  out.shape = q.ext;
+  return out;
+}
+
+GramFactorsAsync gram_factors_async(Ctx& ctx, const DTensor& g) {
+  if (g.shape.size() != 2 || g.shape[0] != g.shape[1]) throw Error(kShapeError, "gram_factors needs k x k");
+  const int64_t k = g.shape[0];
+  if (k < 1 || k > 256) throw Error(kShapeError, "gram_factors: 1 <= k <= 256");
+  GramFactorsAsync out;
+  out.P = ctx.empty({k, k});
+  BufPtr R = ctx.alloc(k * k), work;
+  out.flags = ctx.alloc(k / 4 + 2);
+  if (2 * k * (k + 1) * 16 > 176 * 1024) work = ctx.alloc(2 * k * (k + 1));
+  int* d_def = reinterpret_cast<int*>(out.flags->p);
+  {
+    ProfScope ps_(ctx, Ctx::kProfSmall);
+    gram_factors(g.data(), static_cast<int>(k), out.P.data(), R->p, d_def, d_def + k, ctx.d_status,
+                 work ? work->p : nullptr, ctx.stream);
+  }
+  ++ctx.launches;
+  out.any_deficient = d_def + k;
+  return out;
+}
+
+void read_status_bits(int status) { raise_status(status, true); }
+
+void read_status_now(Ctx& ctx, bool gram_stage) {
+  read_status(ctx);
+  ctx.sync();
+  raise_status(*ctx.h_status, gram_stage);
+}
+
 DTensor gram_matrix(Ctx& ctx, const DTensor& z) {
   if (z.shape.empty()) throw Error(kShapeError, "gram_matrix needs a tensor with a column axis");
   const int64_t k = z.shape.back();

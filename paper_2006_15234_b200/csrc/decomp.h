@@ -109,6 +109,21 @@ EinsumsvdResultD einsumsvd(Ctx& ctx, const ImplicitOp& op, const Trunc& policy, 
 DTensor gram_matrix(Ctx& ctx, const DTensor& z);
 GramFactorsD gram_factors_full(Ctx& ctx, const DTensor& g);
 std::pair<DTensor, std::vector<double>> projected_svd_full(Ctx& ctx, const DTensor& z, int64_t target);
+// Stream-ordered variants for the sharded driver (no host synchronisation):
+// the reference's Gram-eigh orthogonalisation with on-device completion
+// (status bits accumulate in ctx.d_status), and Gram factors whose
+// "any column deficient" flag stays on the device (checked later).
+DTensor orth_async(Ctx& ctx, const DTensor& y);
+struct GramFactorsAsync {
+  DTensor P;                 // k x k: X diag(l^-1/2)
+  BufPtr flags;              // deficient[k] followed by any_deficient
+  int* any_deficient = nullptr;
+};
+GramFactorsAsync gram_factors_async(Ctx& ctx, const DTensor& g);
+// Reads the status word (one sync) and raises the reference's errors.
+void read_status_now(Ctx& ctx, bool gram_stage);
+// Raises the reference's errors for a status word already read back.
+void read_status_bits(int status);
 // linalg.cpp:256-295 (Hermitian eigendecomposition of a square matrix, n <= 256)
 EighD eigh(Ctx& ctx, const DTensor& m);
 // linalg.cpp:193-207 (thin SVD of a matricised tensor; small matrices)

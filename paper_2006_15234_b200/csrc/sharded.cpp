@@ -244,9 +244,18 @@ struct ColumnOut {
   DTensor t2;  // (rank, b, c, t_r, e, f) local slice
 };
 
-// One column einsumsvd split along t (see the file comment).
-ColumnOut sharded_column(Ctx& ctx, const DTensor& v_r, const DTensor& S, const DTensor& bra, const DTensor& ket,
-                         std::pair<int64_t, int64_t> s_range, const Trunc& policy, int absorb, const Rsvd& cfg) {
+// Thrown by the stream-ordered column when a big-side Gram matrix turned out
+// deficient (its completed basis needs the global rows): the column is redone
+// on the robust path.  Every rank sees the same flags (the Gram matrices are
+// all-reduced, the factors replicated), so every rank redoes it.
+struct RedoColumn {};
+
+// One column einsumsvd split along t (see the file comment) -- the robust
+// form: every orthogonalisation checked on the host as it happens, deficient
+// big-side Gram matrices completed on the gathered rows.
+ColumnOut sharded_column_robust(Ctx& ctx, const DTensor& v_r, const DTensor& S, const DTensor& bra,
+                                const DTensor& ket, std::pair<int64_t, int64_t> s_range, const Trunc& policy,
+                                int absorb, const Rsvd& cfg, bool fast) {
   NcclComm& cm = need_comm(ctx);
   const auto& vs = v_r.shape;  // (a, p, q, s_r, m, n)
   const auto& bs = bra.shape;  // (d, u, m, b, e)
@@ -264,55 +273,117 @@ ColumnOut sharded_column(Ctx& ctx, const DTensor& v_r, const DTensor& S, const D
 
   const DTensor S_t = slice(ctx, S, 3, t0, t1);
 
-  auto apply = [&](const DTensor& x) {  // x (b, c, t_r, e, f, X) -> Y (a, p, q, X), replicated
-    DTensor w1 = contract(ctx, "dumbe,bctefX->dumctfX", {bra, x}, {true, false});
-    DTensor w2 = contract(ctx, "dvncf,dumctfX->vnumtX", {ket, w1}, {false, false});
-    DTensor w3 = contract(ctx, "uvst,vnumtX->snmX", {S_t, w2}, {false, false});
+  auto apply = [&](const DTensor& x) {  // x (b, e, c, t_r, f, X) -> Y (a, p, q, X), replicated
+    // intermediate orders chosen so that every contracted group is one
+    // uniform-stride block of both operands (no re-layout of the big tensors)
+    DTensor w1 = contract(ctx, "dumbe,bectfX->dcfumtX", {bra, x}, {true, false});
+    DTensor w2 = contract(ctx, "dvncf,dcfumtX->uvtnmX", {ket, w1}, {false, false});
+    DTensor w3 = contract(ctx, "uvst,uvtnmX->smnX", {S_t, w2}, {false, false});
     allreduce(ctx, w3);
     DTensor w3s = slice(ctx, w3, 0, s0, s1);
-    DTensor y = contract(ctx, "apqsmn,snmX->apqX", {v_r, w3s}, {false, false});
+    DTensor y = contract(ctx, "apqsmn,smnX->apqX", {v_r, w3s}, {false, false});
     allreduce(ctx, y);
     return y;
   };
-  auto adjoint = [&](const DTensor& p) {  // p (a, p, q, X) replicated -> Z_r (b, c, t_r, e, f, X)
-    DTensor r = contract(ctx, "apqsmn,apqX->snmX", {v_r, p}, {true, false});
+  auto adjoint_rest = [&](DTensor r) {  // r_r (s_r, m, n, X) -> Z_r (b, e, c, t_r, f, X)
     r = allgather_axis(ctx, r, 0, s_full);
-    DTensor w2 = contract(ctx, "uvst,snmX->vnumtX", {S_t, r}, {true, false});
+    DTensor w2 = contract(ctx, "uvst,smnX->vnumtX", {S_t, r}, {true, false});
     DTensor w1 = contract(ctx, "dvncf,vnumtX->dumctfX", {ket, w2}, {true, false});
-    return contract(ctx, "dumbe,dumctfX->bctefX", {bra, w1}, {false, false});
+    return contract(ctx, "dumbe,dumctfX->bectfX", {bra, w1}, {false, false});
   };
-  auto orth_small = [&](const DTensor& y) { return gram_orthogonalize(ctx, y, 3).first; };
+  auto adjoint = [&](const DTensor& p) {  // p (a, p, q, X) replicated -> Z_r (b, e, c, t_r, f, X)
+    return adjoint_rest(contract(ctx, "apqsmn,apqX->smnX", {v_r, p}, {true, false}));
+  };
+  // fast: stream-ordered orthogonalisations (one host sync per column, at the
+  // projected SVD); deficiency and status flags are checked there
+  std::vector<BufPtr> def_flags;
+  auto orth_small = [&](const DTensor& y) { return fast ? orth_async(ctx, y) : gram_orthogonalize(ctx, y, 3).first; };
   auto orth_big = [&](const DTensor& z) {
     DTensor g = gram_matrix(ctx, z);
     allreduce(ctx, g);
+    if (fast) {
+      GramFactorsAsync fa = gram_factors_async(ctx, g);
+      def_flags.push_back(fa.flags);
+      return contract(ctx, "bectfX,XY->bectfY", {z, fa.P}, {false, false});
+    }
     GramFactorsD f = gram_factors_full(ctx, g);
     if (std::any_of(f.deficient.begin(), f.deficient.end(), [](int d) { return d != 0; })) {
       // orthonormal completion needs the global rows: gather, complete, re-slice
-      DTensor q = gram_orthogonalize(ctx, allgather_axis(ctx, z, 2, T), 5).first;
-      return slice(ctx, q, 2, t0, t1);
+      DTensor q = gram_orthogonalize(ctx, allgather_axis(ctx, z, 3, T), 5).first;
+      return slice(ctx, q, 3, t0, t1);
     }
-    return contract(ctx, "bctefX,XY->bctefY", {z, f.P}, {false, false});
+    return contract(ctx, "bectfX,XY->bectfY", {z, f.P}, {false, false});
   };
 
-  DTensor omega = ctx.empty({bs[3], ks[3], t1 - t0, bs[4], ks[4], k});
+  // Omega_r stored in the (b, e, c, t_r, f, X) order GEMM (1) reads, each
+  // element the reference's random_tensor value at its logical (b,c,t,e,f,X)
+  // index (counter-based: bit-identical to the unsharded sketch's t-slice)
+  DTensor omega = ctx.empty({bs[3], bs[4], ks[3], t1 - t0, ks[4], k});
   {
     const std::vector<int64_t> full = {bs[3], ks[3], T, bs[4], ks[4], k};
-    const std::vector<int64_t> lstr = row_major_strides(full);
+    const std::vector<int64_t> fstr = row_major_strides(full);
+    const std::vector<int64_t> lstr = {fstr[0], fstr[3], fstr[1], fstr[2], fstr[4], fstr[5]};
     random_fill(omega.data(), 6, omega.shape.data(), lstr.data(), cfg.seed, 0, ctx.stream,
-                static_cast<uint64_t>(t0) * static_cast<uint64_t>(lstr[2]));
+                static_cast<uint64_t>(t0) * static_cast<uint64_t>(fstr[2]));
     ++ctx.launches;
   }
-  DTensor pm = orth_small(apply(omega));
-  for (int it = 0; it < cfg.power_iters; ++it) {
-    DTensor qm = orth_big(adjoint(pm));
-    pm = orth_small(apply(qm));
+  // fast: A orth(Z) = (A Z) P by linearity in the probe index -- the Gram
+  // matrix is all-reduced on the main stream, then its k x k eigensolver runs
+  // there while A Z (with its own collectives) runs on the side stream; the big
+  // Q_r = Z_r P product is never formed.  Deficient Gram matrices (completed
+  // bases are not of the form Z P) are caught at the column's end -> robust redo.
+  auto apply_orth = [&](const DTensor& z) {
+    if (!fast) return apply(orth_big(z));
+    DTensor g = gram_matrix(ctx, z);
+    allreduce(ctx, g);
+    ctx.fork();
+    GramFactorsAsync fa = gram_factors_async(ctx, g);
+    def_flags.push_back(fa.flags);
+    ctx.side();
+    DTensor az = apply(z);
+    ctx.join();
+    return contract(ctx, "apqX,XY->apqY", {az, fa.P}, {false, false});
+  };
+  // fast, small side: A^* orth(Y) = (A^* Y) P likewise -- Y's Gram and
+  // eigensolver on the main stream while the first adjoint step v_r^* Y runs on
+  // the side stream; the basis P_m = Y P itself is formed (cheap: rows_Y x k x k)
+  DTensor pm;
+  auto adjoint_orth = [&](const DTensor& y) {
+    if (!fast) {
+      pm = orth_small(y);
+      return adjoint(pm);
+    }
+    DTensor g = gram_matrix(ctx, y);
+    ctx.fork();
+    GramFactorsAsync fa = gram_factors_async(ctx, g);
+    def_flags.push_back(fa.flags);
+    ctx.side();
+    DTensor r0 = contract(ctx, "apqsmn,apqX->smnX", {v_r, y}, {true, false});
+    ctx.join();
+    pm = contract(ctx, "apqX,XY->apqY", {y, fa.P}, {false, false});
+    return adjoint_rest(contract(ctx, "smnX,XY->smnY", {r0, fa.P}, {false, false}));
+  };
+  DTensor z = adjoint_orth(apply(omega));
+  for (int it = 0; it < cfg.power_iters; ++it) z = adjoint_orth(apply_orth(z));
+  if (fast) {
+    // status bits of every orthogonalisation so far + the deficiency flags,
+    // read back with the projected SVD's synchronisation below
+    const int nf = static_cast<int>(def_flags.size());
+    PEPSB_CUDA(cudaMemcpyAsync(ctx.h_status + 20, ctx.d_status, sizeof(int), cudaMemcpyDeviceToHost, ctx.stream));
+    for (int i = 0; i < nf && i < 16; ++i)  // the "any" flag sits after the k per-column flags
+      PEPSB_CUDA(cudaMemcpyAsync(ctx.h_status + 21 + i, reinterpret_cast<int*>(def_flags[i]->p) + k, sizeof(int),
+                                 cudaMemcpyDeviceToHost, ctx.stream));
   }
-  DTensor z = adjoint(pm);
 
   // projected SVD of B = P^H A = Z^H (decomposition.cpp:293-306) by the Gram route
   DTensor g = gram_matrix(ctx, z);
   allreduce(ctx, g);
-  GramFactorsD f = gram_factors_full(ctx, g);
+  GramFactorsD f = gram_factors_full(ctx, g);  // synchronises
+  if (fast) {
+    read_status_bits(ctx.h_status[20]);
+    for (int i = 0; i < static_cast<int>(def_flags.size()) && i < 16; ++i)
+      if (ctx.h_status[21 + i]) throw RedoColumn{};
+  }
   std::vector<double> s(static_cast<size_t>(k));
   for (int64_t j = 0; j < k; ++j) s[j] = std::sqrt(std::max(f.lam[j], 0.0));
   std::vector<double2> ut(static_cast<size_t>(k * k));
@@ -320,7 +391,7 @@ ColumnOut sharded_column(Ctx& ctx, const DTensor& v_r, const DTensor& S, const D
   const int64_t tgt = std::max<int64_t>(1, std::min(target, k));
   if (!(s[0] > 0.0 && s[tgt - 1] >= 1e-4 * s[0])) {
     // ill-conditioned Gram route: the single-device projected SVD on the gathered Z
-    auto pr = projected_svd_full(ctx, allgather_axis(ctx, z, 2, T), target);
+    auto pr = projected_svd_full(ctx, allgather_axis(ctx, z, 3, T), target);
     utd = pr.first;
     s = pr.second;
   }
@@ -337,8 +408,22 @@ ColumnOut sharded_column(Ctx& ctx, const DTensor& v_r, const DTensor& S, const D
   }
   ColumnOut out;
   out.t1 = contract(ctx, "apqX,XR->pqaR", {pm, scaled_columns(ctx, ut, k, rank, wl, false)}, {false, false});
-  out.t2 = contract(ctx, "bctefX,XR->Rbctef", {z, scaled_columns(ctx, ut, k, rank, wv, true)}, {true, false});
+  out.t2 = contract(ctx, "bectfX,XR->Rbctef", {z, scaled_columns(ctx, ut, k, rank, wv, true)}, {true, false});
   return out;
+}
+
+ColumnOut sharded_column(Ctx& ctx, const DTensor& v_r, const DTensor& S, const DTensor& bra, const DTensor& ket,
+                         std::pair<int64_t, int64_t> s_range, const Trunc& policy, int absorb, const Rsvd& cfg) {
+  PEPSB_CUDA(cudaMemsetAsync(ctx.d_status, 0, 2 * sizeof(int), ctx.stream));
+  if (2 * cfg.power_iters + 1 > 16)  // more deficiency flags than the read-back slots
+    return sharded_column_robust(ctx, v_r, S, bra, ket, s_range, policy, absorb, cfg, false);
+  try {
+    return sharded_column_robust(ctx, v_r, S, bra, ket, s_range, policy, absorb, cfg, true);
+  } catch (const RedoColumn&) {
+    ++ctx.faithful_redos;  // counter "faithful_redos": columns redone on the robust path
+    PEPSB_CUDA(cudaMemsetAsync(ctx.d_status, 0, 2 * sizeof(int), ctx.stream));
+    return sharded_column_robust(ctx, v_r, S, bra, ket, s_range, policy, absorb, cfg, false);
+  }
 }
 
 uint64_t column_seed(const ContractOptD& opt, uint64_t tag, int row, int col) {

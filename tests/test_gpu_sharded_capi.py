@@ -71,3 +71,26 @@ def test_distributed_cached_environments_on_device(A, golden):
                                                    4, 4, 4, 13, 2, -1, terms)
     assert abs(norm - golden["bands_norm"][0]) <= 1e-8 * abs(golden["bands_norm"][0])
     assert np.abs(vals - golden["bands_values"]).max() <= 1e-8
+
+
+def test_sharded_deficient_grams_take_the_robust_path(A, refo, comm_ctx):
+    """Bond-2 sites carrying a rank-1 product state: the probe Grams are
+    deficient (the reference clamps and completes their columns,
+    decomposition.cpp:86-117).  The stream-ordered sharded column detects the
+    deficiency flags at its end and redoes the column on the robust path
+    (counter faithful_redos); the norm still matches the reference."""
+    rng = np.random.default_rng(5)
+    sites = []
+    for r in range(4):
+        for c in range(4):
+            shp = I.peps_site_shape(4, 4, r, c, 2)
+            t = np.zeros(shp, dtype=complex)
+            t[(slice(None),) + (0,) * 4] = rng.standard_normal(2)
+            t += 1e-3 * I.gaussian(shp, 100 + 4 * r + c)
+            sites.append(t)
+    st = A.PepsState(4, 4, 2, sites, ctx=comm_ctx)
+    opt = A.ContractOption.two_layer_opt(8, 3, 2, -1)
+    comm_ctx.reset_counters()
+    got = A.contract_two_layer_sharded(st, st, opt)
+    want, _ = refo.contract_two_layer(sites, 4, 4, 8, 3, 2, -1)
+    assert abs(got - want) <= 1e-8 * abs(want)

@@ -45,7 +45,9 @@ def timed(fn, reps=5):
 bra = A.to_device(inputs.gaussian((2, 8, 8, 8, 8), 3))
 omega = A.random_tensor((8, 8, 64, 8, 8, 72), 5)
 w1c = A.random_tensor((2, 8, 64, 8, 64, 8, 72), 6)  # (d,u,m,c,t,f,X) complex
+zbig = A.random_tensor((262144, 72), 21)
 cases = {
+    "Gram Z^H Z 262144 x 72": lambda: A.gram(zbig),
     "G1 bra*(dum|be).Omega(be|ctfX) 128x64x294912 cxr": lambda: A.contract("dumbe,bctefX->dumctfX", bra.conj(), omega),
     "G2 ket(vn|dcf).W1(dcf|umtX) 64x128x294912 cxr": lambda: A.contract("dvncf,dumctfX->vnumtX", bra,
                                                                           A.contract("dumbe,bctefX->dumctfX",
