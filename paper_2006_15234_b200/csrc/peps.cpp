@@ -334,13 +334,14 @@ std::vector<BoundaryD> pipelined_sweep(const std::vector<Ctx*>& ctxs, const Peps
 }
 
 // Rows in flight: option "pipeline_rows" (< 2 sequential), or automatic
-// (-1): 3 for small boundary bonds (m <= 48: latency-bound einsumsvds, the
-// one-block eigensolver dominates), 2 otherwise (GEMM-bound: more concurrent
-// rows only contend).  Measured: config 3 (m = 36) 0.43 / 0.37 / 0.36 s per
-// norm at K = 2 / 3 / 4; config 5 (m = 64) 9.2 / 9.5 / 10.0 s.
+// (-1): 4 for small boundary bonds (m <= 48: latency-bound einsumsvds, the
+// one-block eigensolver dominates), 3 otherwise.  Measured (round 2,
+// tools/pipeline_ab.py): config 3 (m = 36) 0.329 / 0.287 / 0.271 / 0.268 /
+// 0.267 s per norm at K = 2 / 3 / 4 / 6 / 8; config 5 (m = 64) 9.67 / 8.46 /
+// 8.38 s at K = 1 / 2 / 3.  Results are bitwise independent of K.
 int pipeline_depth(const Ctx& ctx, const ContractOptD& opt) {
   if (ctx.pipeline_rows >= 0) return ctx.pipeline_rows;
-  return (opt.trunc.max_rank != 0 && opt.trunc.max_rank <= 48) ? 3 : 2;
+  return (opt.trunc.max_rank != 0 && opt.trunc.max_rank <= 48) ? 4 : 3;
 }
 
 std::vector<Ctx*> pipeline_contexts(Ctx& ctx, int K) {
