@@ -80,10 +80,15 @@ __device__ void onesided_jacobi(double2* X, int m, int n, int ldx, double2* V, i
           gr += u.x * v.x + u.y * v.y;  // conj(u) * v
           gi += u.x * v.y - u.y * v.x;
         }
-        a = warp_sum(a);
-        b = warp_sum(b);
-        gr = warp_sum(gr);
-        gi = warp_sum(gi);
+        // the four reductions interleaved (independent shuffles in flight
+        // together); each variable sees the same add sequence as warp_sum
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          a += __shfl_xor_sync(0xffffffffu, a, o);
+          b += __shfl_xor_sync(0xffffffffu, b, o);
+          gr += __shfl_xor_sync(0xffffffffu, gr, o);
+          gi += __shfl_xor_sync(0xffffffffu, gi, o);
+        }
         const double ag = hypot(gr, gi);
         if (!(ag > tol * sqrt(a * b)) || !(ag > abs_skip)) continue;
         if (lane == 0) rotated = 1;
@@ -111,7 +116,10 @@ __device__ void onesided_jacobi(double2* X, int m, int n, int ldx, double2* V, i
     if (!any) break;
   }
   if (sweep == max_sweeps && threadIdx.x == 0) atomicOr(status, kSmallNoConverge);
-  if (threadIdx.x == 0) atomicAdd(status + 7, sweep + 1);  // diagnostics: total sweeps
+  if (threadIdx.x == 0) {  // diagnostics: total and largest sweep counts
+    atomicAdd(status + 7, sweep + 1);
+    atomicMax(status + 30, sweep + 1);
+  }
 }
 
 // Descending order of key[0..n) (ties by index) -> order[rank] = column.
