@@ -190,8 +190,10 @@ std::atomic<int> g_gram{-1};
 bool gram_enabled() {
   int v = g_gram.load();
   if (v < 0) {
+    // opt-in: measured slower in the row than the 3M split-K GEMM it replaces
+    // (config-2 row 60.4 vs 60.9 ms, config-5 row 318 vs 321 ms)
     const char* e = getenv("PEPSB_GEMM_GRAM");
-    v = (e && e[0] == '0') ? 0 : 1;
+    v = (e && e[0] == '1') ? 1 : 0;
     g_gram.store(v);
   }
   return v != 0;

@@ -13,7 +13,7 @@ constexpr int64_t kGramMaxK = 72;
 constexpr int64_t kGramMinRows = 2048;  // below: the generic GEMM path (few tiles, no split benefit)
 
 bool gram_herk_eligible(int64_t rows, int64_t k);
-// option "gemm_gram" / PEPSB_GEMM_GRAM (default on)
+// option "gemm_gram" / PEPSB_GEMM_GRAM (default off: measured slower in the row)
 bool gram_enabled();
 void gram_set_enabled(int on);
 // Workspace in doubles for gram_herk.

@@ -1,4 +1,4 @@
-"""The Hermitian Gram kernel (csrc/gram.cu): G = Z^H Z of a tall complex Z from
+"""The opt-in Hermitian Gram kernel (csrc/gram.cu, option gemm_gram): G = Z^H Z of a tall complex Z from
 the upper-triangle DMMA blocks of the interleaved real product, split over rows
 with a fixed-order reduction -- against numpy at 1e-13, exactly Hermitian,
 deterministic, and equal (to rounding) to the generic complex GEMM route it
@@ -13,7 +13,16 @@ pytestmark = pytest.mark.gpu
 
 @pytest.mark.parametrize("rows,k", [(2048, 1), (2048, 3), (5000, 8), (4096, 41), (10007, 64), (262144, 72),
                                     (2049, 72), (70000, 17)])
-def test_gram_kernel_matches_numpy(A, rows, k):
+@pytest.fixture
+def gram_on(A):
+    ctx = A.default_context()
+    ctx.set_option("gemm_gram", 1)
+    yield A
+    ctx.set_option("gemm_gram", 0)
+
+
+def test_gram_kernel_matches_numpy(gram_on, rows, k):
+    A = gram_on
     z = O.random_tensor((rows, k), rows + k)
     g = A.gram(z).numpy()
     want = z.conj().T @ z
@@ -23,13 +32,11 @@ def test_gram_kernel_matches_numpy(A, rows, k):
     assert np.array_equal(A.gram(z).numpy(), g)  # deterministic
 
 
-def test_gram_kernel_vs_generic_gemm_route(A):
+def test_gram_kernel_vs_generic_gemm_route(gram_on):
+    A = gram_on
     ctx = A.default_context()
     z = O.random_tensor((262144 // 4, 8, 72), 3)
     g1 = A.gram(z).numpy()
     ctx.set_option("gemm_gram", 0)
-    try:
-        g0 = A.gram(z).numpy()
-    finally:
-        ctx.set_option("gemm_gram", 1)
+    g0 = A.gram(z).numpy()
     assert np.linalg.norm(g1 - g0) <= 1e-14 * np.linalg.norm(g0)
