@@ -473,6 +473,23 @@ def norm_timings(A, ctx):
         out[name] = statistics.median(ts)
         out[name + "_all"] = ts
         del st
+    # config 3's full workload: the cached environments (both sweeps) plus all
+    # 256 <Z_i> (one expectation over 256 one-site terms with shared band
+    # environments, observables.cpp:335-422)
+    c3 = inputs.config3()
+    st = A.PepsState(16, 16, 2, c3["sites"], ctx=ctx)
+    z = np.diag([1.0, -1.0]).astype(np.complex128)
+    terms = [A.LocalTerm(1.0, [(r, c)], z) for r in range(16) for c in range(16)]
+    eo = A.ExpectationOptions(A.ContractOption.two_layer_opt(36, c3["seed"], 2, -1), True, True, False)
+    A.expectation(st, terms, eo)
+    ts = []
+    for _ in range(3):
+        ctx.sync()
+        t0 = time.perf_counter()
+        A.expectation(st, terms, eo)
+        ts.append(time.perf_counter() - t0)
+    out["config3_cache_plus_256_z"] = statistics.median(ts)
+    del st
     plus = [np.array([1, 1], dtype=complex).reshape(2, 1, 1, 1, 1) / np.sqrt(2) for _ in range(64)]
     st = A.PepsState(8, 8, 2, plus, ctx=ctx)
     A.ite_tfim(st, 1.0, 3.0, 0.01, 2, 8)
@@ -481,7 +498,8 @@ def norm_timings(A, ctx):
     A.ite_tfim(st, 1.0, 3.0, 0.01, 20, 8)
     ctx.sync()
     out["config4_ite_8x8_r8_s_per_step"] = (time.perf_counter() - t0) / 20
-    out["note"] = "seconds per norm (config 4: per Trotter step); wall clock, synchronised, one B200"
+    out["note"] = ("seconds per norm (config 4: per Trotter step; config3_cache_plus_256_z: both cached sweeps + "
+                   "all 256 <Z_i>); wall clock, synchronised, one B200")
     return out
 
 
