@@ -11,8 +11,6 @@ from oracle import peps_oracle as O
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("rows,k", [(2048, 1), (2048, 3), (5000, 8), (4096, 41), (10007, 64), (262144, 72),
-                                    (2049, 72), (70000, 17)])
 @pytest.fixture
 def gram_on(A):
     ctx = A.default_context()
@@ -21,6 +19,8 @@ def gram_on(A):
     ctx.set_option("gemm_gram", 0)
 
 
+@pytest.mark.parametrize("rows,k", [(2048, 1), (2048, 3), (5000, 8), (4096, 41), (10007, 64), (262144, 72),
+                                    (2049, 72), (70000, 17)])
 def test_gram_kernel_matches_numpy(gram_on, rows, k):
     A = gram_on
     z = O.random_tensor((rows, k), rows + k)
