@@ -118,6 +118,11 @@ def test_flip_vertical_and_bottom_sweep(A, refo):
     v = A.chain_scalar(b)
     w, _ = refo.contract_two_layer(want_sites, 4, 3, 4, 2, 2, -1)  # tag 0x20 there: compare loosely
     assert abs(v - w) / abs(w) < 1e-2
+    # the same bottom sweep (tag 0x21, observables.cpp:325-333) in the numpy
+    # restatement pinned to the reference: 1e-8
+    bots = O.sweep_boundaries(want_sites, 4, 3, 4, 2, 2, -1, 0x21)
+    wb = O.chain_scalar(bots[-1][0])
+    assert abs(v - wb) <= 1e-8 * abs(wb)
 
 
 def test_row_cache_scheduling_is_bitwise_invariant(A):
