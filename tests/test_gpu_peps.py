@@ -241,6 +241,18 @@ def test_apply_two_site_matches_reference(A, refo):
                 assert rel(s.numpy(), w) < 1e-9, (bond, cap, i)
 
 
+def test_apply_two_site_oversized_site_is_a_shape_error(A):
+    """An interior r = 9 site needs (2 r^4 + 20 r^2 + 4 r) * 16 B ~ 236 KB of
+    shared memory in the batched reduction, above its 176 KB attribute: the
+    library raises ShapeError up front (the guard's throw had been
+    swallowed by a comment, so the launch failed with a generic CUDA error)."""
+    sites = I.random_peps(3, 3, 9, 57, scale=0.1)
+    st = A.PepsState(3, 3, 2, sites)
+    g = O.random_tensor((2, 2, 2, 2), 58)
+    with pytest.raises(A.PepsError, match="ShapeError: simple update: site too large"):
+        A.apply_two_site(st, g, [(1, 1, 1, 2)], A.TruncationPolicy(9, 1e-14))
+
+
 def test_ite_tfim_matches_reference(A, refo):
     """TFIM ITE (J=1, h=3, tau=0.01) from |+> on 3x3, r=3, 8 Trotter steps; bonds
     batched per colour.  Shapes bit-exact, state fidelity and norm to 1e-8."""
