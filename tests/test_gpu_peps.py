@@ -444,6 +444,24 @@ def test_peps_container_interchange_with_reference(A, refo, tmp_path):
     (tmp_path / "short.peps").write_bytes((tmp_path / "ref.peps").read_bytes()[:200])
     with pytest.raises(A.PepsError, match="truncated"):
         A.load_peps(tmp_path / "short.peps")
+    # untrusted counts are bounded by the file size before any allocation
+    import struct
+    good = (tmp_path / "ref.peps").read_bytes()
+    hdr = b"PEPS2D01" + struct.pack("<QQQQ", 1 << 40, 1 << 40, 2, 5) + b"pudlr"
+    (tmp_path / "huge.peps").write_bytes(hdr + good[8 + 32 + 5:])
+    with pytest.raises(A.PepsError, match="ValidationError: corrupt PEPS container header"):
+        A.load_peps(tmp_path / "huge.peps")
+    body = bytearray(good)
+    off = 8 + 32 + 5  # first site: u64 order, then extents
+    body[off:off + 8] = struct.pack("<Q", 4)
+    (tmp_path / "order.peps").write_bytes(bytes(body))
+    with pytest.raises(A.PepsError, match="corrupt PEPS site order"):
+        A.load_peps(tmp_path / "order.peps")
+    body = bytearray(good)
+    body[off + 8:off + 16] = struct.pack("<Q", (1 << 63) + 5)
+    (tmp_path / "ext.peps").write_bytes(bytes(body))
+    with pytest.raises(A.PepsError, match="corrupt PEPS site extent"):
+        A.load_peps(tmp_path / "ext.peps")
 
 
 @pytest.mark.parametrize("initial", ["neel", "zeros"])
