@@ -339,6 +339,12 @@ def run_b200(args, rank, world, local_rank):
     ctx.profile(False)
     ctx.set_option("overlap", 1)
     del out
+    # ---- stream timeline of one row as timed (overlap on): where the row waits
+    ctx.profile(True)
+    out = A.two_layer_apply_row(top, st, st, 1, opt, 0x20)
+    timeline = _timeline_summary(ctx.profile_timeline())
+    ctx.profile(False)
+    del out
 
     if dist:
         t = torch.tensor([dt, dt_e2e], dtype=torch.float64, device="cuda")
@@ -385,6 +391,7 @@ def run_b200(args, rank, world, local_rank):
             "e2e": {"value": world * flops / dt_e2e / 1e12, "unit": UNIT, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "s_per_step": dt_e2e},
             "roofline": roof}
+    line["timeline"] = timeline
     if extra_roofs:
         line["roofline_configs"] = extra_roofs
     if world == 1 and not args.no_norms:
@@ -405,6 +412,40 @@ def run_b200(args, rank, world, local_rank):
                                     "sample": f"unavailable: {e}"}
     print(json.dumps(line), flush=True)
     return 0
+
+
+def _union_ms(iv):
+    tot, cs, ce = 0.0, None, None
+    for a, b in sorted(iv):
+        if cs is None or a > ce:
+            if cs is not None:
+                tot += ce - cs
+            cs, ce = a, b
+        else:
+            ce = max(ce, b)
+    return tot + (ce - cs if cs is not None else 0.0)
+
+
+def _timeline_summary(tl):
+    """Per-launch events on both streams of one row (tools/timeline.py): span,
+    busy time per stream, time with no kernel running, and the main stream's
+    (latency chain's) work that ran while the side stream was idle, by kind."""
+    if not tl:
+        return None
+    main = [(s, e) for k, s, e, f, sd in tl if sd == 0]
+    side = sorted((s, e) for k, s, e, f, sd in tl if sd == 1)
+    span = max(e for _, _, e, _, _ in tl) - min(s for _, s, _, _, _ in tl)
+    exposed = {}
+    for k, s, e, f, sd in tl:
+        if sd:
+            continue
+        ov = sum(max(0.0, min(e, b) - max(s, a)) for a, b in side if b > s and a < e)
+        exposed[k] = round(exposed.get(k, 0.0) + (e - s) - ov, 3)
+    return {"span_ms": round(span, 3), "busy_main_ms": round(_union_ms(main), 3),
+            "busy_side_ms": round(_union_ms(side), 3), "idle_ms": round(span - _union_ms(main + side), 3),
+            "main_exposed_ms_by_kind": exposed,
+            "note": "per-launch CUDA events on the main / side stream of one row absorb, overlap on "
+                    "(event overhead included)"}
 
 
 def config_rooflines(A, ctx):
