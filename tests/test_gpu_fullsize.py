@@ -113,6 +113,8 @@ def test_config5_parameters_8x8_match_reference(algo):
     or the reference's own spread under a 1e-14 input perturbation when that is
     larger (fullsize_cfg5_8x8_pert: measured, not assumed)."""
     A = algo
+    if not all(os.path.exists(os.path.join(GOLDEN, f"fullsize_{n}.npz")) for n in ("cfg5_8x8", "cfg5_8x8_pert")):
+        pytest.skip("config-5 8x8 reference golden not generated yet (make_golden_fullsize.py cfg5_8x8 cfg5_8x8_pert)")
     g, gp = golden("cfg5_8x8"), golden("cfg5_8x8_pert")
     c = cfg5_small()
     st = A.PepsState(8, 8, 2, c["sites"])
