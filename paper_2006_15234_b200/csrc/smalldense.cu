@@ -17,10 +17,18 @@ namespace pepsb {
 
 namespace {
 
+// Build with -DPEPSB_EIG_PROF=1 for the divide-and-conquer phase counters
+// (status words 12..27, tools/eig_phases.py).
+#ifndef PEPSB_EIG_PROF
+#define PEPSB_EIG_PROF 0
+#endif
+
 constexpr int kThreads = 1024;
 // k x k eigensolver block: 512 threads leave 128 registers per thread for the
 // register-resident tridiagonalisation / back-transformation.
 constexpr int kEigThreads = 512;
+// block of the register-resident path (16 <= k <= 72): 168 registers per thread
+constexpr int kEigFastThreads = 384;
 constexpr size_t kSmemCap = 200 * 1024;
 
 __device__ __forceinline__ double warp_sum(double v) {
@@ -351,7 +359,30 @@ __device__ __forceinline__ double fast_rcp(double x) {
   return fma(r, e, r);
 }
 
+// sqrt(x) and 1/sqrt(x) without the IEEE slow paths: MUFU seed (20 bits) + two
+// Newton steps + one correction of the product.  x normal, positive.
+__device__ __forceinline__ double fast_rsqrt(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  const double hx = 0.5 * x;
+  double t = fma(-hx * y, y, 0.5);
+  y = fma(y, t, y);
+  t = fma(-hx * y, y, 0.5);
+  return fma(y, t, y);
+}
+__device__ __forceinline__ double fast_sqrt(double x) {
+  const double y = fast_rsqrt(x);
+  const double s = x * y;
+  return fma(0.5 * y, fma(-s, s, x), s);
+}
+
 // Sum / product over the T-lane segment (T a power of two, segment-aligned).
+__device__ __forceinline__ void dmma_f64(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
 __device__ __forceinline__ double seg_sum(double v, int T, unsigned mask) {
   for (int o = T >> 1; o > 0; o >>= 1) v += __shfl_xor_sync(mask, v, o);
   return v;
@@ -416,8 +447,11 @@ __device__ void dc_secular_root(bool valid, int j, int K, const double* dk, cons
     tau = rho * zk[0] * zk[0];
   }
   const int i1 = pl + 1 + ((sub - (pl + 1)) % T + T) % T;  // first i > pl in this lane's stride
+  int nit = 0;
+  (void)nit;
   for (int it = 0; it < 100; ++it) {
     if (!__any_sync(full, !done)) break;
+    if (!done) ++nit;
     double psi = 0.0, dpsi = 0.0, phi = 0.0, dphi = 0.0;
     if (!done) {
 #pragma unroll 4
@@ -435,10 +469,14 @@ __device__ void dc_secular_root(bool valid, int j, int K, const double* dk, cons
         dphi += t * inv;
       }
     }
-    psi = seg_sum(psi, T, full);
-    dpsi = seg_sum(dpsi, T, full);
-    phi = seg_sum(phi, T, full);
-    dphi = seg_sum(dphi, T, full);
+    for (int o = T >> 1; o > 0; o >>= 1) {  // the four sums interleaved: one shuffle latency per level
+      const double s0 = __shfl_xor_sync(full, psi, o), s1 = __shfl_xor_sync(full, dpsi, o);
+      const double s2 = __shfl_xor_sync(full, phi, o), s3 = __shfl_xor_sync(full, dphi, o);
+      psi += s0;
+      dpsi += s1;
+      phi += s2;
+      dphi += s3;
+    }
     if (done) continue;
     const double f = irho + psi + phi;
     if (f < 0.0) lo_t = tau;
@@ -456,15 +494,21 @@ __device__ void dc_secular_root(bool valid, int j, int K, const double* dk, cons
       const double B = Dl * Dl * dpsi, D = Dr * Dr * dphi;
       const double c = f - Dl * dpsi - Dr * dphi;
       const double a = c * (Dl + Dr) + B + D, b = Dl * Dr * f;
+      // the step only has to land inside the bracket: reciprocal / sqrt by MUFU
+      // seed + Newton (full precision for normal operands) instead of the IEEE
+      // slow paths (~110 / ~90 cycles each on the iteration's critical path)
+      auto okr = [](double v) { return fabs(v) > 1e-290 && fabs(v) < 1e290; };
       if (c == 0.0) {
         if (a != 0.0) {
-          const double r = b / a;
+          const double r = okr(a) ? b * fast_rcp(a) : b / a;
           if (r > lo_e && r < hi_e) eta = r;
         }
       } else {
         const double disc = fmax(a * a - 4.0 * b * c, 0.0);
-        const double q = 0.5 * (a + copysign(sqrt(disc), a));
-        const double r1 = q / c, r2 = q != 0.0 ? b / q : 0.0;
+        const double sq = (disc > 1e-290 && disc < 1e290) ? fast_sqrt(disc) : sqrt(disc);
+        const double q = 0.5 * (a + copysign(sq, a));
+        const double r1 = okr(c) ? q * fast_rcp(c) : q / c;
+        const double r2 = q != 0.0 ? (okr(q) ? b * fast_rcp(q) : b / q) : 0.0;
         if (r1 > lo_e && r1 < hi_e) eta = r1;
         else if (r2 > lo_e && r2 < hi_e) eta = r2;
       }
@@ -477,6 +521,13 @@ __device__ void dc_secular_root(bool valid, int j, int K, const double* dk, cons
     *sig_out = sig;
     *tau_out = tau;
   }
+#if PEPSB_EIG_PROF
+  if (valid && sub == 0) {
+    atomicMax(prof, nit);
+    atomicAdd(prof + 1, nit);
+    atomicAdd(prof + 2, 1);
+  }
+#endif
 }
 
 // One merge of the two solved halves of node [lo, lo + N) (split at n1) by a
@@ -486,8 +537,23 @@ __device__ void dc_secular_root(bool valid, int j, int K, const double* dk, cons
 // Z(r, c) lives in V[c*ld + r].x; V[.].y of the node's diagonal block holds the
 // merge vectors; the GEMM result is staged in the free upper triangle of A.
 __device__ void dc_merge(bool active, int lo, int n1, int N, int gt, int G, double* d, const double* e, double2* V,
-                         double2* A, int ld, const DcScratch& S) {
+                         double2* A, int ld, const DcScratch& S, bool top) {
   const int lane = threadIdx.x & 31;
+  // diagnostics: cycles of the top-level merge's phases in status words 12..19
+  long long pc = clock64();
+  int pslot = 0;
+  auto mark = [&]() {
+#if PEPSB_EIG_PROF
+    if (top && threadIdx.x == 0) {
+      const long long c = clock64();
+      atomicAdd(S.prof + pslot, static_cast<int>((c - pc) >> 4));
+      pc = c;
+    }
+    ++pslot;
+#endif
+  };
+  (void)pc;
+  (void)pslot;
   const double eps = 2.220446049250313e-16;
   const double beta = active ? e[lo + n1 - 1] : 0.0;
   const double rho = 2.0 * fabs(beta);
@@ -507,22 +573,43 @@ __device__ void dc_merge(bool active, int lo, int n1, int N, int gt, int G, doub
       S.perm[lo + r] = col;
     }
   __syncthreads();
+  mark();
+  // sorted copies (d, z in ascending d) for the sequential scan: its loads no
+  // longer chain through perm
+  if (active)
+    for (int q = gt; q < N; q += G) {
+      const int c = S.perm[lo + q];
+      S.dk[lo + q] = d[c];
+      S.zk[lo + q] = S.zb[c];
+    }
+  __syncthreads();
+  mark();
   // deflation (sequential, dlaed2's rules)
   if (active && gt == 0) {
     double dmax = 0.0;
-    for (int c = 0; c < N; ++c) dmax = fmax(dmax, fabs(d[lo + c]));
+    for (int c = 0; c < N; ++c) dmax = fmax(dmax, fabs(S.dk[lo + c]));
     const double tol = 8.0 * eps * fmax(dmax, rho);
     int K = 0, nrot = 0, prev = -1;
+    double zp = 0.0, dp = 0.0;  // z, d of prev (current values)
+    // the next entry is loaded before this one's stores (which the compiler
+    // must assume to alias), so the scan's chain is arithmetic only
+    int cn = S.perm[lo];
+    double zn = S.zk[lo], dn = S.dk[lo];
     for (int q = 0; q < N; ++q) {
-      const int c = S.perm[lo + q];
-      const double zc = S.zb[c];
+      const int c = cn;
+      const double zc = zn, dcv = dn;
+      if (q + 1 < N) {
+        cn = S.perm[lo + q + 1];
+        zn = S.zk[lo + q + 1];
+        dn = S.dk[lo + q + 1];
+      }
       if (rho * fabs(zc) <= tol) continue;  // eigenpair (d_c, column c) deflates
       if (prev < 0) {
         prev = c;
+        zp = zc;
+        dp = dcv;
         continue;
       }
-      const double zp = S.zb[prev];
-      const double dp = d[prev], dcv = d[c];
       // |(d_c - d_p) a b| <= tol with a b = -z_c z_p / (z_p^2 + z_c^2), division-free
       if (fabs((dcv - dp) * zc * zp) <= tol * (zp * zp + zc * zc)) {  // nearby poles: rotate z_prev into z_c
         const double t = hypot(zp, zc);
@@ -536,8 +623,12 @@ __device__ void dc_merge(bool active, int lo, int n1, int N, int gt, int G, doub
         S.zb[prev] = 0.0;
         d[prev] = a * a * dp + b * b * dcv;
         d[c] = b * b * dp + a * a * dcv;
+        zp = t;
+        dp = b * b * dp + a * a * dcv;
       } else {
         S.ndx[lo + K++] = prev;
+        zp = zc;
+        dp = dcv;
       }
       prev = c;
     }
@@ -546,6 +637,7 @@ __device__ void dc_merge(bool active, int lo, int n1, int N, int gt, int G, doub
     S.meta[2 * lo + 1] = nrot;
   }
   __syncthreads();
+  mark();
   const int K = active ? S.meta[2 * lo] : 0, nrot = active ? S.meta[2 * lo + 1] : 0;
   for (int r = lo + gt; r < lo + N && nrot > 0; r += G)
     for (int t = 0; t < nrot; ++t) {  // Q <- Q R^T, rotations in order
@@ -561,6 +653,7 @@ __device__ void dc_merge(bool active, int lo, int n1, int N, int gt, int G, doub
     S.zk[lo + i] = S.zb[c];
   }
   __syncthreads();
+  mark();
   // T lanes per root / per vector: the largest power of two with 2 T K <= G
   int T = 1;
   while (T < 32 && T < G && 2 * T * K <= G) T <<= 1;
@@ -572,9 +665,10 @@ __device__ void dc_merge(bool active, int lo, int n1, int N, int gt, int G, doub
   const int nq = __reduce_max_sync(mask, K > seg ? (K - seg + nseg - 1) / nseg : 0);
   for (int q = 0; q < nq; ++q) {
     const int j = seg + q * nseg;
-    dc_secular_root(j < K, j, K, dk, zk, rho, sub, T, S.sig + lo + j, S.tau + lo + j, S.prof + 12);
+    dc_secular_root(j < K, j, K, dk, zk, rho, sub, T, S.sig + lo + j, S.tau + lo + j, S.prof + 24);
   }
   __syncthreads();
+  mark();
   const double* sg_ = S.sig + lo;
   const double* tu_ = S.tau + lo;
   // z recomputed from the roots: zh_i^2 = prod_j (lambda_j - d_i) / (rho prod_{j != i} (d_j - d_i))
@@ -591,6 +685,7 @@ __device__ void dc_merge(bool active, int lo, int n1, int N, int gt, int G, doub
     if (i < K && sub == 0) S.zh[lo + i] = copysign(sqrt(fmax(w, 0.0)), zk[i]);
   }
   __syncthreads();
+  mark();
   // merge vectors v_j[i] = zh_i / (d_i - lambda_j), normalised; stored W^T in V.y:
   // v_j[i] at V[(lo + i) * ld + lo + j].y
   const double* zh = S.zh + lo;
@@ -609,12 +704,52 @@ __device__ void dc_merge(bool active, int lo, int n1, int N, int gt, int G, doub
       for (int i = sub; i < K; i += T) V[(lo + i) * ld + lo + j].y *= inv;
   }
   __syncthreads();
+  mark();
   for (int j = gt; j < K; j += G) d[S.ndx[lo + j]] = sg_[j] + tu_[j];
   // Zt(r, ndx[j]) = sum_i Z(r, ndx[i]) v_j[i] staged in A's upper triangle
   // (local (r, c): r <= c at A(lo + r, lo + c).x, r > c at A(lo + c, lo + r).y),
   // then copied back over Z.
   const int* ndx = S.ndx + lo;
-  {
+  if (G >= 32) {
+    // whole warps: 16 x 16 tiles on the FP64 tensor pipe (DMMA.8x8x4), four
+    // DMMAs per four fragment loads.  The 4 x 4 scalar tiles below read the
+    // merge vectors at a 64-byte stride (16-way bank conflicts): 64 k cycles
+    // for the 72 x 72 x 72 top-level product against ~8 k here.
+    const int wg = gt >> 5, nwg = G >> 5;
+    const int tr = (N + 15) >> 4, tc = (K + 15) >> 4;
+    const int rq = lane >> 2, kq = lane & 3;
+    for (int o = wg; o < tr * tc; o += nwg) {
+      const int r0 = (o / tc) * 16, j0 = (o % tc) * 16;
+      double c00[2] = {0.0, 0.0}, c01[2] = {0.0, 0.0}, c10[2] = {0.0, 0.0}, c11[2] = {0.0, 0.0};
+      const bool ra0 = r0 + rq < N, ra1 = r0 + 8 + rq < N, cb0 = j0 + rq < K, cb1 = j0 + 8 + rq < K;
+      for (int k0 = 0; k0 < K; k0 += 4) {
+        const int kk = k0 + kq;
+        const bool kin = kk < K;
+        const double2* zc = V + (kin ? ndx[kk] : lo) * ld + lo + r0 + rq;
+        const double2* wr = V + (lo + (kin ? kk : 0)) * ld + lo + j0 + rq;
+        const double a0 = kin && ra0 ? zc[0].x : 0.0, a1 = kin && ra1 ? zc[8].x : 0.0;
+        const double b0 = kin && cb0 ? wr[0].y : 0.0, b1 = kin && cb1 ? wr[8].y : 0.0;
+        dmma_f64(c00[0], c00[1], a0, b0);
+        dmma_f64(c01[0], c01[1], a0, b1);
+        dmma_f64(c10[0], c10[1], a1, b0);
+        dmma_f64(c11[0], c11[1], a1, b1);
+      }
+      auto put = [&](int r, int j, double v) {
+        if (r < N && j < K) {
+          const int c = ndx[j] - lo;
+          if (r <= c) A[(lo + c) * ld + lo + r].x = v;
+          else A[(lo + r) * ld + lo + c].y = v;
+        }
+      };
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        put(r0 + rq, j0 + 2 * kq + h, c00[h]);
+        put(r0 + rq, j0 + 8 + 2 * kq + h, c01[h]);
+        put(r0 + 8 + rq, j0 + 2 * kq + h, c10[h]);
+        put(r0 + 8 + rq, j0 + 8 + 2 * kq + h, c11[h]);
+      }
+    }
+  } else {
     // 4 x 4 register tiles: 9 shared loads per 16 FMAs
     const int tr = (N + 3) >> 2, tc = (K + 3) >> 2;
     for (int o = gt; o < tr * tc; o += G) {
@@ -651,11 +786,13 @@ __device__ void dc_merge(bool active, int lo, int n1, int N, int gt, int G, doub
     }
   }
   __syncthreads();
+  mark();
   for (int o = gt; o < N * K; o += G) {
     const int r = o / K, c = ndx[o % K] - lo;
     V[(lo + c) * ld + lo + r].x = r <= c ? A[(lo + c) * ld + lo + r].x : A[(lo + r) * ld + lo + c].y;
   }
   __syncthreads();
+  mark();
 }
 
 // d, e in shared memory; V column-major (ld); A: the tridiagonalised matrix
@@ -700,10 +837,17 @@ __device__ void tridiag_dc(double* d, double* e, double2* V, double2* A, int n, 
     const int first = dstart[t], m = dstart[t + 1] - first;
     int G = 1;
     while (2 * G * m <= static_cast<int>(blockDim.x)) G <<= 1;
+    if (G >= 32) G = (static_cast<int>(blockDim.x) / m) & ~31;  // whole warps: all of them (384 = 3 x 128)
     const int g = tid / G;
     const bool active = g < m;
     const short2 x = active ? nodes[first + g] : make_short2(0, 2);
-    dc_merge(active, x.x, x.y / 2, x.y, tid % G, G, d, e, V, A, ld, S);
+#if PEPSB_EIG_PROF
+    const long long c0 = clock64();
+#endif
+    dc_merge(active, x.x, x.y / 2, x.y, tid % G, G, d, e, V, A, ld, S, t == 0);
+#if PEPSB_EIG_PROF
+    if (tid == 0 && t < 7) atomicAdd(S.prof + 9 + t, static_cast<int>((clock64() - c0) >> 4));  // words 21..28
+#endif
   }
   for (int t = tid; t < n * n; t += blockDim.x) V[(t / n) * ld + t % n].y = 0.0;
   __syncthreads();
@@ -758,6 +902,309 @@ __device__ void back_transform_reg(const double2* A, double2* V, int n, int ld, 
   }
 }
 
+// Register-resident Householder tridiagonalisation (16 <= n <= 4 NC <= 72, a
+// block of 384 threads = 168 registers each: the kernel's shared memory leaves
+// no L1, so a single spilled value costs an L2 round trip per column).
+// Thread (row i = tid / 4, gl = tid % 4) keeps A(i, gl + 4 c), c < NC, in
+// registers for the whole reduction: the trailing matrix never round-trips
+// through shared memory (the smem-resident version moved 32 B per element and
+// column and spent ~4.2 k cycles per column, most of it in warp 0's serial
+// reflector arithmetic between two block barriers).  One block barrier per
+// column:
+//   P1 (every active warp redundantly, NV indices per lane): from column j
+//      (published by its owners during the previous matvec) and p = tau A v of
+//      the previous reflector, form w_{j-1} = p + alpha2 v, apply that pending
+//      rank-2 update to column j analytically, generate reflector j, and leave
+//      v_{j-1}, w_{j-1}, v_j in a warp-private buffer (__syncwarp, no block
+//      barrier);
+//   matvec: each thread applies the pending update to its registers, accumulates
+//      A v_j over its columns, publishes column j+1 and, after a 4-lane shuffle
+//      reduction, p_i.  Branch-free over the columns: the buffers are zero
+//      outside the trailing block (and padded to 4 NC), so stale columns
+//      contribute exact zeros.
+// Warps whose rows are all above the trailing block only attend the barrier.
+// On return: d, e (e[j] = beta_j), tauv, reflector j in X[j*ld + l], l > j
+// (v[j+1] = 1 stored explicitly).  wbuf: >= ceil(n/8) * 12 NC complex scratch.
+#if PEPSB_EIG_PROF
+__device__ int g_tri_prof[8];
+#endif
+template <int NC>
+__device__ void herm_tridiag_reg(double2* X, int n, int ld, double* d, double* e, double2* tauv, double2* wbuf,
+                                 double2* sh /* 4 x 128 */) {
+  constexpr int NV = (4 * NC + 31) / 32;
+  constexpr int NP = 4 * NC;  // padded vector length
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int i = tid >> 2, gl = tid & 3;
+  const double2 z0 = make_double2(0.0, 0.0);
+  double2* colbuf = sh;       // [2][128]
+  double2* pbuf = sh + 256;   // [2][128]
+  double2* wv = wbuf;  // [vbuf0 | vbuf1 | wprev]
+  // reflector warp: the block's last warp owns no rows (4 n <= 288 < 352), so the
+  // serial reflector arithmetic never competes with a matvec warp for its FP64 pipe
+  const int pwarp = (blockDim.x >> 5) - 1;
+  double2 a[NC];
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    const int l = gl + 4 * c;
+    a[c] = (i < n && l < n) ? X[l * ld + i] : z0;
+  }
+  for (int t = tid; t < n; t += blockDim.x) colbuf[t] = X[t];  // column 0
+  for (int t = tid; t < 3 * NP; t += blockDim.x) wv[t] = z0;
+  __syncthreads();
+  double2 tau = z0;  // reflector j - 1's (identical in every active warp)
+#if PEPSB_EIG_PROF
+  long long pacc[8] = {0, 0, 0, 0, 0, 0, 0, 0}, pt = clock64();
+#define TRI_MARK(k)                  \
+  {                                  \
+    const long long c_ = clock64();  \
+    pacc[k] += c_ - pt;              \
+    pt = c_;                         \
+  }
+#else
+#define TRI_MARK(k)
+#endif
+  for (int j = 0; j < n; ++j) {
+    const int b = j & 1;
+    const bool last = j == n - 1;
+    double2* vprev = wv + (b ^ 1) * NP;
+    double2* vnew = wv + b * NP;
+    double2* wprev = wv + 2 * NP;
+    if (warp == pwarp) {
+      const bool pend = j > 0 && (tau.x != 0.0 || tau.y != 0.0);
+      double2 x[NV];
+      // ---- w_{j-1} = p + alpha2 v,  alpha2 = -1/2 tau (p^H v); operands are
+      // re-read from shared memory rather than kept live
+      if (pend) {
+        double hr = 0.0, hi = 0.0;
+#pragma unroll
+        for (int s = 0; s < NV; ++s) {
+          const int r = lane + 32 * s;
+          if (r >= j && r < n) {
+            const double2 v = vprev[r], pp = pbuf[(b ^ 1) * 128 + r];
+            hr += pp.x * v.x + pp.y * v.y;
+            hi += pp.x * v.y - pp.y * v.x;
+          }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          hr += __shfl_xor_sync(0xffffffffu, hr, o);
+          hi += __shfl_xor_sync(0xffffffffu, hi, o);
+        }
+        TRI_MARK(0)
+        const double2 alpha2 = cscale(cmul(tau, make_double2(hr, hi)), -0.5);
+#pragma unroll
+        for (int s = 0; s < NV; ++s) {
+          const int r = lane + 32 * s;
+          if (r < n) wprev[r] = r >= j ? cadd(pbuf[(b ^ 1) * 128 + r], cmul(alpha2, vprev[r])) : z0;
+        }
+      } else {
+#pragma unroll
+        for (int s = 0; s < NV; ++s) {
+          const int r = lane + 32 * s;
+          if (r < n) wprev[r] = z0;
+        }
+      }
+      __syncwarp();
+      TRI_MARK(1)
+      // v_{j-1}[j], w_{j-1}[j]
+      const double2 vj = pend ? vprev[j] : z0, wj = pend ? wprev[j] : z0;
+      // ---- column j with the pending update applied; its norm below j + 1
+      double xn = 0.0;
+#pragma unroll
+      for (int s = 0; s < NV; ++s) {
+        const int r = lane + 32 * s;
+        x[s] = z0;
+        if (r >= j && r < n) {
+          double2 v = colbuf[b * 128 + r];
+          if (pend) v = csub(v, cadd(cmulc(wj, vprev[r]), cmulc(vj, wprev[r])));
+          x[s] = v;
+          if (r >= j + 2) xn += cnorm2(v);
+        }
+      }
+      double2 sa = x[0], sd = x[0];
+#pragma unroll
+      for (int s = 1; s < NV; ++s) {
+        if (((j + 1) >> 5) == s) sa = x[s];
+        if ((j >> 5) == s) sd = x[s];
+      }
+      const double dj = __shfl_sync(0xffffffffu, sd.x, j & 31);
+      if (last) {
+        if (lane == 0) {
+          d[j] = dj;
+          e[j] = 0.0;
+        }
+      } else {
+        const double2 alpha =
+            make_double2(__shfl_sync(0xffffffffu, sa.x, (j + 1) & 31), __shfl_sync(0xffffffffu, sa.y, (j + 1) & 31));
+        xn = warp_sum(xn);
+        TRI_MARK(2)
+        double2 scal = z0;
+        double beta;
+        tau = z0;
+        if (xn == 0.0 && alpha.y == 0.0) {
+          beta = alpha.x;
+        } else {
+          const double s2 = alpha.x * alpha.x + alpha.y * alpha.y + xn;
+          const bool safe = s2 > 1e-280 && s2 < 1e280;
+          double rb;  // 1 / beta
+          if (safe) {
+            const double y = fast_rsqrt(s2);
+            const double s = s2 * y;
+            beta = -copysign(fma(0.5 * y, fma(-s, s, s2), s), alpha.x);
+            rb = -copysign(y, alpha.x);
+          } else {
+            beta = -copysign(sqrt(s2), alpha.x);
+            rb = 1.0 / beta;
+          }
+          tau = make_double2((beta - alpha.x) * rb, -alpha.y * rb);
+          const double2 den = make_double2(alpha.x - beta, alpha.y);  // scal = 1 / (alpha - beta)
+          const double dn2 = cnorm2(den);
+          const double dn = (dn2 > 1e-280 && dn2 < 1e280) ? fast_rcp(dn2) : 1.0 / dn2;
+          scal = make_double2(den.x * dn, -den.y * dn);
+        }
+        const bool zero = tau.x == 0.0 && tau.y == 0.0;
+        TRI_MARK(3)
+#pragma unroll
+        for (int s = 0; s < NV; ++s) {
+          const int r = lane + 32 * s;
+          double2 v = z0;
+          if (!zero && r < n) v = r == j + 1 ? make_double2(1.0, 0.0) : (r >= j + 2 ? cmul(x[s], scal) : z0);
+          if (r < n) {
+            vnew[r] = v;
+            if (r > j) X[j * ld + r] = v;
+          }
+        }
+        if (lane == 0) {
+          d[j] = dj;
+          e[j] = beta;
+          tauv[j] = tau;
+        }
+        TRI_MARK(4)
+      }
+    }
+    __syncthreads();
+    // ---- matvec over the trailing block (rows, columns >= j + 1)
+    if (!last && 8 * warp + 7 > j && 8 * warp < n) {
+      {
+        const bool rowact = i > j && i < n;
+        const unsigned mrow = __ballot_sync(0xffffffffu, rowact);
+        if (rowact) {
+          const double2 tauj = tauv[j];
+          const double2 vi = vprev[i], wi = wprev[i];
+          double r0 = 0.0, i0 = 0.0, r1 = 0.0, i1 = 0.0;
+#pragma unroll
+          for (int c = 0; c < NC; ++c) {
+            if (4 * c + 3 <= j) continue;  // warp-uniform: all four columns left of the block
+            const int l = gl + 4 * c;
+            const double2 wl = wprev[l], vl = vprev[l], y = vnew[l];
+            double2 v = a[c];
+            v.x = fma(-wl.x, vi.x, v.x);
+            v.y = fma(-wl.x, vi.y, v.y);
+            v.x = fma(-wl.y, vi.y, v.x);
+            v.y = fma(wl.y, vi.x, v.y);
+            v.x = fma(-vl.x, wi.x, v.x);
+            v.y = fma(-vl.x, wi.y, v.y);
+            v.x = fma(-vl.y, wi.y, v.x);
+            v.y = fma(vl.y, wi.x, v.y);
+            a[c] = v;
+            if (l == j + 1) colbuf[(b ^ 1) * 128 + i] = v;
+            if (c & 1) {
+              r1 = fma(v.x, y.x, r1);
+              i1 = fma(v.x, y.y, i1);
+              r1 = fma(-v.y, y.y, r1);
+              i1 = fma(v.y, y.x, i1);
+            } else {
+              r0 = fma(v.x, y.x, r0);
+              i0 = fma(v.x, y.y, i0);
+              r0 = fma(-v.y, y.y, r0);
+              i0 = fma(v.y, y.x, i0);
+            }
+          }
+          r0 += r1;
+          i0 += i1;
+          r0 += __shfl_xor_sync(mrow, r0, 1);
+          i0 += __shfl_xor_sync(mrow, i0, 1);
+          r0 += __shfl_xor_sync(mrow, r0, 2);
+          i0 += __shfl_xor_sync(mrow, i0, 2);
+          if (gl == 0) pbuf[b * 128 + i] = cmul(tauj, make_double2(r0, i0));
+        }
+      }
+    }
+    TRI_MARK(5)
+    __syncthreads();
+    TRI_MARK(6)
+  }
+#if PEPSB_EIG_PROF
+  if (warp == pwarp && lane == 0)
+    for (int k = 0; k < 7; ++k) atomicAdd(g_tri_prof + k, static_cast<int>(pacc[k] >> 4));
+#endif
+#undef TRI_MARK
+}
+
+// Back-transformation X = H_0 ... H_{n-2} Z, one GS-lane group per column with
+// the column in registers, rows in reverse order (slot k of lane gl holds row
+// n-1 - (gl + GS k)): reflector j touches rows > j, i.e. the slots k <
+// ceil((n-1-j) / GS), so the unrolled slot loops stop at a warp-uniform bound
+// instead of issuing every predicated-off slot (Z is real on entry).
+template <int ES, int GS>
+__device__ void back_transform_rev(const double2* A, double2* V, int n, int ld, const double2* tauv) {
+  const int tid = threadIdx.x, gl = tid % GS;
+  if ((tid & ~31) / GS >= n) return;  // whole warps only: the shuffles below use the full mask
+  const bool act = tid / GS < n;
+  const int c = act ? tid / GS : 0;
+  double2 x[ES];
+#pragma unroll
+  for (int k = 0; k < ES; ++k) {
+    const int s = n - 1 - (gl + GS * k);
+    x[k] = s >= 0 ? make_double2(V[c * ld + s].x, 0.0) : make_double2(0.0, 0.0);
+  }
+  for (int j = n - 2; j >= 0; --j) {
+    const double2 tau = tauv[j];
+    if (tau.x == 0.0 && tau.y == 0.0) continue;
+    const int m = n - 1 - j;  // rows n-1 .. j+1  <->  gl + GS k < m
+    const int kmax = (m + GS - 1) / GS;
+    const double2* vcol = A + j * ld + (n - 1 - gl);
+    double re0 = 0.0, im0 = 0.0, re1 = 0.0, im1 = 0.0;
+#pragma unroll
+    for (int k = 0; k < ES; ++k) {
+      if (k >= kmax) break;
+      if (gl + GS * k < m) {
+        const double2 v = vcol[-GS * k];
+        if (k & 1) {
+          re1 += v.x * x[k].x + v.y * x[k].y;
+          im1 += v.x * x[k].y - v.y * x[k].x;
+        } else {
+          re0 += v.x * x[k].x + v.y * x[k].y;
+          im0 += v.x * x[k].y - v.y * x[k].x;
+        }
+      }
+    }
+    re0 += re1;
+    im0 += im1;
+#pragma unroll
+    for (int o = GS / 2; o > 0; o >>= 1) {
+      re0 += __shfl_xor_sync(0xffffffffu, re0, o);
+      im0 += __shfl_xor_sync(0xffffffffu, im0, o);
+    }
+    const double2 t = cmul(tau, make_double2(re0, im0));
+#pragma unroll
+    for (int k = 0; k < ES; ++k) {
+      if (k >= kmax) break;
+      if (gl + GS * k < m) {
+        const double2 v = vcol[-GS * k];
+        x[k].x -= v.x * t.x - v.y * t.y;
+        x[k].y -= v.x * t.y + v.y * t.x;
+      }
+    }
+  }
+  if (!act) return;
+#pragma unroll
+  for (int k = 0; k < ES; ++k) {
+    const int s = n - 1 - (gl + GS * k);
+    if (s >= 0) V[c * ld + s] = x[k];
+  }
+}
+
 // Hermitian eigensolver for one thread block: Householder tridiagonalisation
 // (the zhetd2 recurrence: A <- H^H A H with H = I - tau v v^H, rank-2 updates),
 // divide and conquer on the real tridiagonal (tridiag_dc), and
@@ -771,6 +1218,7 @@ __device__ void back_transform_reg(const double2* A, double2* V, int n, int ld, 
 //  * back-transformation: columns of X are independent, so each column is owned
 //    by an 8-lane group that applies H_{n-2} .. H_0 with shuffle reductions and
 //    no block barriers at all.
+template <bool FAST = false>
 __device__ void herm_eig_tridiag(double2* A, double2* V, int n, int ld, int* status) {
   constexpr int kChunks = 4;
   __shared__ double d[256], e[256];
@@ -787,7 +1235,17 @@ __device__ void herm_eig_tridiag(double2* A, double2* V, int n, int ld, int* sta
   // multiplies), while warp 0 forms the updated column x = A(j+1:, j), its norm
   // and the reflector scalars; then warp 0 turns (x, A x) into v = scal (x - beta e1)
   // and w = p + alpha2 v with p = tau A v = tau scal (A x - beta A(:, j+1)).
-  {
+  const bool fast = FAST && n >= 16 && n <= 72 && blockDim.x == kEigFastThreads;
+  if constexpr (FAST) {
+    if (fast) {
+    // register-resident trailing matrix, one barrier per column; V is free until
+    // the divide and conquer and holds the warp-private reflector buffers
+    if (n <= 32) herm_tridiag_reg<8>(A, n, ld, d, e, tauv, V, scratch);
+    else if (n <= 48) herm_tridiag_reg<12>(A, n, ld, d, e, tauv, V, scratch);
+    else herm_tridiag_reg<18>(A, n, ld, d, e, tauv, V, scratch);
+    }
+  }
+  if (!fast) {
     double2* xs = part[1];  // the updated column x (warp 0's, phase A -> B)
     double2* qs = part[0];  // q = A22 x
     const int mt = nthr - 32;
@@ -901,7 +1359,7 @@ __device__ void herm_eig_tridiag(double2* A, double2* V, int n, int ld, int* sta
       __syncthreads();
     }
   }
-  if (tid == 0) {
+  if (tid == 0 && !fast) {
     const bool pend = n >= 2 && (tauv[n - 2].x != 0.0 || tauv[n - 2].y != 0.0);
     const double2 vl = pend ? vv[n - 1] : make_double2(0.0, 0.0), wl = pend ? pw[n - 1] : make_double2(0.0, 0.0);
     d[n - 1] = A[(n - 1) * ld + n - 1].x - 2.0 * (vl.x * wl.x + vl.y * wl.y);
@@ -920,7 +1378,13 @@ __device__ void herm_eig_tridiag(double2* A, double2* V, int n, int ld, int* sta
   }
   const long long clk2 = clock64();
   // ---- 3. back-transformation X = H_0 H_1 ... H_{n-2} Z, one 8-lane group per column
-  if (n <= 24 * 4 && 4 * n <= nthr) {
+  if (FAST && fast) {
+    if constexpr (FAST) {
+      if (n <= 32) back_transform_rev<4, 8>(A, V, n, ld, tauv);
+      else if (n <= 48) back_transform_rev<6, 8>(A, V, n, ld, tauv);
+      else back_transform_rev<18, 4>(A, V, n, ld, tauv);
+    }
+  } else if (n <= 24 * 4 && 4 * n <= nthr) {
     if (n <= nthr / 8) {
       const int esb = (n + 7) / 8;
       if (esb <= 4) back_transform_reg<4, 8>(A, V, n, ld, tauv);
@@ -964,6 +1428,10 @@ __device__ void herm_eig_tridiag(double2* A, double2* V, int n, int ld, int* sta
     atomicAdd(status + 8, static_cast<int>((clk1 - clk0) / 1000));
     atomicAdd(status + 9, static_cast<int>((clk2 - clk1) / 1000));
     atomicAdd(status + 10, static_cast<int>((clk3 - clk2) / 1000));
+#if PEPSB_EIG_PROF
+    if constexpr (FAST)
+      for (int k = 0; k < 7; ++k) atomicAdd(status + 29 + k, atomicExch(g_tri_prof + k, 0));
+#endif
   }
   for (int j = tid; j < n; j += nthr) A[j * ld + j] = make_double2(d[j], 0.0);
   __syncthreads();
@@ -975,6 +1443,7 @@ __device__ void herm_eig_tridiag(double2* A, double2* V, int n, int ld, int* sta
 // above; measured: k = 4 25 us vs 38 us, k = 8 66 us vs 58 us).
 constexpr int kWarpJacobiMax = 6;
 
+template <bool FAST = false>
 __device__ void gram_factors_dev(const double2* G, int n, double2* X, double2* V, double2* P, double2* R,
                                  int* deficient, int* any_def, int* status, double* lam_out = nullptr,
                                  double2* vec_out = nullptr, int solver = 0) {
@@ -1040,7 +1509,7 @@ __device__ void gram_factors_dev(const double2* G, int n, double2* X, double2* V
     if (threadIdx.x < 32) herm_jacobi_t<true>(X, V, n, ld, neps, abs_skip, low_skip, 40, status);
     __syncthreads();
   } else {
-    herm_eig_tridiag(X, V, n, ld, status);
+    herm_eig_tridiag<FAST>(X, V, n, ld, status);
   }
   for (int j = threadIdx.x; j < n; j += blockDim.x) lam[j] = scalbn(X[j * ld + j].x, gexp);
   __syncthreads();
@@ -1086,15 +1555,17 @@ __device__ void gram_factors_dev(const double2* G, int n, double2* X, double2* V
 // pointers derive from the __shared__ array, so the inlined solvers use
 // LDS/STS instead of generic loads (which the profile showed waiting on the
 // long scoreboard); otherwise they live in the global `work` buffer.
-template <bool SMEM>
-__global__ void __launch_bounds__(kEigThreads) gram_factors_kernel(const double2* G, int n, double2* P,
+template <bool SMEM, int NT>
+__global__ void __launch_bounds__(NT) gram_factors_kernel(const double2* G, int n, double2* P,
                                                                 double2* R, int* deficient,
                                                                 int* any_def, int* status,
                                                                 double2* work, int use_jacobi, double* lam_out,
                                                                 double2* vec_out) {
   extern __shared__ __align__(16) unsigned char sm[];
   double2* X = SMEM ? reinterpret_cast<double2*>(sm) : work;  // column-major n x (n+1)
-  gram_factors_dev(G, n, X, X + n * (n + 1), P, R, deficient, any_def, status, lam_out, vec_out, use_jacobi);
+  // NT == kEigFastThreads: the register-resident tridiagonalisation / back-transformation
+  gram_factors_dev<SMEM && NT == kEigFastThreads>(G, n, X, X + n * (n + 1), P, R, deficient, any_def, status, lam_out,
+                                                  vec_out, use_jacobi & 0xff);
 }
 
 // ------------------------------------------------------------------ Cholesky
@@ -1841,13 +2312,16 @@ void gram_factors(const double2* G, int n, double2* P, double2* R, int* deficien
   if (!fits && !work) throw Error(kOtherError, "gram_factors: workspace required");
   static bool attr = false;
   if (!attr) {
-    PEPSB_CUDA(cudaFuncSetAttribute(gram_factors_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    static_cast<int>(kCap)));
+    PEPSB_CUDA(cudaFuncSetAttribute(gram_factors_kernel<true, kEigThreads>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kCap)));
+    PEPSB_CUDA(cudaFuncSetAttribute(gram_factors_kernel<true, kEigFastThreads>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kCap)));
     attr = true;
   }
   static const int env_threads = getenv("PEPSB_EIG_THREADS") ? atoi(getenv("PEPSB_EIG_THREADS")) : 0;
   const int threads = env_threads >= 64 && env_threads <= kEigThreads ? env_threads : kEigThreads;
-  const int use_jacobi = eig_solver();
+  static const bool eig_fast = !(getenv("PEPSB_EIG_FAST") && getenv("PEPSB_EIG_FAST")[0] == '0');
+  const int use_jacobi = eig_solver() | (eig_fast ? 0x100 : 0);
   static const char* dump = getenv("PEPSB_DUMP_EIG");  // debug aid: last input matrix to a file
   if (dump) {
     std::vector<double2> h(static_cast<size_t>(n) * n);
@@ -1858,12 +2332,15 @@ void gram_factors(const double2* G, int n, double2* P, double2* R, int* deficien
       fclose(f);
     }
   }
-  if (fits)
-    gram_factors_kernel<true><<<1, threads, smem, stream>>>(G, n, P, R, deficient, any_def, status, nullptr,
-                                                            use_jacobi, lam_out, vec_out);
+  if (fits && eig_fast && n >= 16 && n <= 72 && eig_solver() != kEigJacobi && !env_threads)
+    gram_factors_kernel<true, kEigFastThreads><<<1, kEigFastThreads, smem, stream>>>(
+        G, n, P, R, deficient, any_def, status, nullptr, use_jacobi, lam_out, vec_out);
+  else if (fits)
+    gram_factors_kernel<true, kEigThreads><<<1, threads, smem, stream>>>(G, n, P, R, deficient, any_def, status,
+                                                                         nullptr, use_jacobi & 0xff, lam_out, vec_out);
   else
-    gram_factors_kernel<false><<<1, threads, 0, stream>>>(G, n, P, R, deficient, any_def, status, work,
-                                                          use_jacobi, lam_out, vec_out);
+    gram_factors_kernel<false, kEigThreads><<<1, threads, 0, stream>>>(G, n, P, R, deficient, any_def, status, work,
+                                                                       use_jacobi & 0xff, lam_out, vec_out);
   PEPSB_LAUNCH();
 }
 

@@ -132,12 +132,16 @@ def test_config5_parameters_8x8_match_reference(algo):
 def cfg4_states(refo):
     """Config 4 final states: the reference's ITE (drivers.cpp:56-98 in colour
     order, qr_svd_gram, r=8, 100 steps of tau=0.01 from |+>) on the unperturbed
-    and on a 1e-14-perturbed |+> (live, ~15 s each on the box's cores)."""
+    and on three independently 1e-14-perturbed |+> states (live, ~15 s each on
+    the box's cores).  The final-state norm responds chaotically to rounding, so
+    one perturbation is a one-sample estimate of the reference's own spread; the
+    bound below is twice the largest of three."""
     refo.set_threads(os.cpu_count() or 1)
     plus = [np.array([1, 1], dtype=complex).reshape(2, 1, 1, 1, 1) / np.sqrt(2) for _ in range(64)]
     ref_state, _ = refo.ite_tfim(plus, 8, 8, 1.0, 3.0, 0.01, 100, 8)
-    ref_pert, _ = refo.ite_tfim(perturb(plus, 1e-14), 8, 8, 1.0, 3.0, 0.01, 100, 8)
-    return plus, ref_state, ref_pert
+    ref_perts = [refo.ite_tfim(perturb(plus, 1e-14, seed), 8, 8, 1.0, 3.0, 0.01, 100, 8)[0]
+                 for seed in (1234, 77, 4242)]
+    return plus, ref_state, ref_perts
 
 
 def _bond_spectra(sites, rows, cols):
@@ -180,14 +184,15 @@ def test_config4_matches_reference_within_its_own_spread(A, cfg4_states):
     input perturbation of the reference to ~1e-5 in the norm, so no
     implementation can be compared with the reference to 1e-8 on these
     quantities; the bound is the reference's own reproducibility."""
-    plus, ref_state, ref_pert = cfg4_states
+    plus, ref_state, ref_perts = cfg4_states
     dev = A.ite_tfim(A.PepsState(8, 8, 2, plus), 1.0, 3.0, 0.01, 100, 8)
     dev_sites = [s.numpy() for s in dev.sites]
     assert [s.shape for s in dev_sites] == [s.shape for s in ref_state]
-    assert [s.shape for s in ref_pert] == [s.shape for s in ref_state]
+    for ref_pert in ref_perts:
+        assert [s.shape for s in ref_pert] == [s.shape for s in ref_state]
 
     sp_ref = _bond_spectra(ref_state, 8, 8)
-    spread_sp = _spectra_err(_bond_spectra(ref_pert, 8, 8), sp_ref)
+    spread_sp = max(_spectra_err(_bond_spectra(ref_pert, 8, 8), sp_ref) for ref_pert in ref_perts)
     err_sp = _spectra_err(_bond_spectra(dev_sites, 8, 8), sp_ref)
     assert err_sp <= max(1e-8, 2 * spread_sp), (err_sp, spread_sp)
 
@@ -199,11 +204,11 @@ def test_config4_matches_reference_within_its_own_spread(A, cfg4_states):
         return float(np.log(abs(e.norm_sq)) + 2 * np.log(mx).sum()), e.value
 
     ln_ref, e_ref = measure(ref_state)
-    ln_pert, e_pert = measure(ref_pert)
+    pert = [measure(ref_pert) for ref_pert in ref_perts]
     ln_dev, e_dev = measure(dev_sites)
-    spread_n = abs(np.expm1(ln_pert - ln_ref))
-    spread_ln = abs(ln_pert - ln_ref) / abs(ln_ref)
-    spread_e = abs(e_pert - e_ref) / abs(e_ref)
-    assert abs(np.expm1(ln_dev - ln_ref)) <= max(1e-8, 2 * spread_n), (ln_dev, ln_ref, ln_pert)
+    spread_n = max(abs(np.expm1(ln_pert - ln_ref)) for ln_pert, _ in pert)
+    spread_ln = max(abs(ln_pert - ln_ref) / abs(ln_ref) for ln_pert, _ in pert)
+    spread_e = max(abs(e_pert - e_ref) / abs(e_ref) for _, e_pert in pert)
+    assert abs(np.expm1(ln_dev - ln_ref)) <= max(1e-8, 2 * spread_n), (ln_dev, ln_ref, pert)
     assert abs(ln_dev - ln_ref) / abs(ln_ref) <= max(1e-8, 2 * spread_ln)
-    assert abs(e_dev - e_ref) / abs(e_ref) <= max(1e-8, 2 * spread_e), (e_dev, e_ref, e_pert)
+    assert abs(e_dev - e_ref) / abs(e_ref) <= max(1e-8, 2 * spread_e), (e_dev, e_ref, pert)
