@@ -5,15 +5,21 @@
 // With Zh = Z viewed as a real rows x 2k matrix (interleaved re, im), the real
 // symmetric C = Zh^T Zh holds every product the complex Gram needs:
 //   G_ij = C(2i,2j) + C(2i+1,2j+1) + i (C(2i,2j+1) - C(2i+1,2j)).
-// Only the upper triangle of 8 x 8 blocks of C is computed: NB (NB+1) / 2
-// blocks for NB = ceil(2k / 8), i.e. 171 DMMAs per 4 rows at k = 72 against
-// 3 x 81 = 243 for the 3M complex GEMM (0.70x the executed flops), and the
+// C is symmetric, so block row I only needs the NJ = NB/2 + 1 blocks (I, (I + j)
+// mod NB), j = 0 .. NB/2, NB = ceil(2k / 8): every unordered pair of block
+// indices is covered (for even NB the pairs at distance NB/2 twice), 180 DMMAs
+// per 4 rows at k = 72 against 3 x 81 = 243 for the 3M complex GEMM, and the
 // DMMA A and B fragments of Zh^T and Zh are the same shared-memory element
-// (row lane&3, column 8 b + lane>>2), so one fragment load serves both roles.
-// Warp w owns block rows w and NB-1-w (NB+1 blocks), so the triangle splits
-// evenly over ceil(NB/2) warps.  Split-K over rows: each CTA writes its
-// partial triangle, a second kernel sums the partials in a fixed order (the
-// result is deterministic) and assembles the complex Hermitian G.
+// (row lane&3, column 8 b + lane>>2).  One warp per block row, and EVERY warp
+// runs the same instruction stream on its own rotated column list: no
+// predicated DMMAs (a predicated-off DMMA still occupies the FP64 pipe: the
+// triangular version issued 18 per warp and k-step for 9.5 useful, ncu pipe 69 %
+// active at 36 % of the flop rate), no per-row code specialisation (18 code
+// paths in flight ran at a third of the speed on instruction fetch), equal DMMA
+// counts on the four SM sub-partitions, 20 accumulator registers per thread.
+// Split-K over rows: each CTA writes its partial blocks, a second kernel sums
+// the partials in a fixed order (the result is deterministic) and a third
+// assembles the complex Hermitian G.
 #include "gram.cuh"
 
 #include <algorithm>
@@ -24,8 +30,9 @@ namespace pepsb {
 
 namespace {
 
-constexpr int kGramBK = 16;       // rows per pipeline stage
+constexpr int kGramBK = 32;       // rows per pipeline stage
 constexpr int kGramStages = 3;
+constexpr int kGramCtasPerSm = 1;  // resident CTAs per SM the split over rows is sized for
 constexpr int kGramLd = 152;      // doubles per smem row (144 + pad: rows alternate bank halves)
 
 __device__ __forceinline__ void cp_async16g(void* smem, const void* gmem, bool pred) {
@@ -44,15 +51,13 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
                : "d"(a), "d"(b));
 }
 
-// Block (I, J), I <= J, of the NB x NB triangle -> its index in the packed list.
-__host__ __device__ __forceinline__ int tri_index(int I, int J, int NB) { return I * NB - I * (I - 1) / 2 + (J - I); }
+__host__ __device__ __forceinline__ int gram_nj(int NB) { return NB / 2 + 1; }
 
-template <int NB>
-__global__ void __launch_bounds__(((NB + 1) / 2) * 32) gram_partial_kernel(const double2* __restrict__ Z, int64_t rows,
-                                                                        int k, int64_t chunk, double* __restrict__ work) {
-  constexpr int NW = (NB + 1) / 2;
-  constexpr int NT = NW * 32;
-  constexpr int NTRI = NB * (NB + 1) / 2;
+template <int NB, int MINB>
+__global__ void __launch_bounds__(NB * 32, MINB) gram_partial_kernel(const double2* __restrict__ Z, int64_t rows, int k,
+                                                                    int64_t chunk, double* __restrict__ work) {
+  constexpr int NT = NB * 32;
+  constexpr int NJ = NB / 2 + 1;
   extern __shared__ __align__(16) double gsm[];  // [stages][kGramBK][kGramLd]
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int64_t r0 = static_cast<int64_t>(blockIdx.x) * chunk;
@@ -79,10 +84,13 @@ __global__ void __launch_bounds__(((NB + 1) / 2) * 32) gram_partial_kernel(const
     cp_commit();
   }
 
-  const int I0 = w, I1 = NB - 1 - w;  // this warp's two block rows (I0 == I1 for the middle row of odd NB)
-  double acc0[NB][2], acc1[NB][2];
+  // block row w: blocks (w, (w + j) mod NB); fragment column offsets in registers
+  int coff[NJ];
 #pragma unroll
-  for (int j = 0; j < NB; ++j) acc0[j][0] = acc0[j][1] = acc1[j][0] = acc1[j][1] = 0.0;
+  for (int j = 0; j < NJ; ++j) coff[j] = 8 * ((w + j) % NB);
+  double acc[NJ][2];
+#pragma unroll
+  for (int j = 0; j < NJ; ++j) acc[j][0] = acc[j][1] = 0.0;
   const int frow = lane & 3, fcol = lane >> 2;
 
   for (int64_t kt = 0; kt < nk; ++kt) {
@@ -93,37 +101,26 @@ __global__ void __launch_bounds__(((NB + 1) / 2) * 32) gram_partial_kernel(const
       if (pf < nk) load_stage(static_cast<int>(pf % kGramStages), pf);
       cp_commit();
     }
-    const double* S = gsm + static_cast<int>(kt % kGramStages) * kGramBK * kGramLd;
+    const double* S = gsm + static_cast<int>(kt % kGramStages) * kGramBK * kGramLd + frow * kGramLd + fcol;
 #pragma unroll
     for (int ks = 0; ks < kGramBK / 4; ++ks) {
-      const double* Sr = S + (ks * 4 + frow) * kGramLd + fcol;
-      const double a0 = Sr[8 * I0], a1 = Sr[8 * I1];
+      const double* Sr = S + ks * 4 * kGramLd;
+      const double a0 = Sr[coff[0]];
+      dmma(acc[0][0], acc[0][1], a0, a0);
 #pragma unroll
-      for (int J = 0; J < NB; ++J) {
-        if (J < I0) continue;  // warp-uniform
-        const double b = Sr[8 * J];
-        dmma(acc0[J][0], acc0[J][1], a0, b);
-        if (I1 != I0 && J >= I1) dmma(acc1[J][0], acc1[J][1], a1, b);
-      }
+      for (int j = 1; j < NJ; ++j) dmma(acc[j][0], acc[j][1], a0, Sr[coff[j]]);
     }
   }
   cp_wait<0>();
-  // partial triangle of this CTA: block (I, J) as 8 x 8 row-major doubles;
+  // partial blocks of this CTA: block (w, j) as 8 x 8 row-major doubles;
   // lane owns C[lane>>2][2 (lane&3) + {0,1}] of every block
-  double* out = work + static_cast<int64_t>(blockIdx.x) * NTRI * 64;
+  double* out = work + (static_cast<int64_t>(blockIdx.x) * NB + w) * NJ * 64;
   const int cr = lane >> 2, cc = 2 * (lane & 3);
 #pragma unroll
-  for (int J = 0; J < NB; ++J) {
-    if (J >= I0) {
-      double* blk = out + tri_index(I0, J, NB) * 64 + cr * 8 + cc;
-      blk[0] = acc0[J][0];
-      blk[1] = acc0[J][1];
-    }
-    if (I1 != I0 && J >= I1) {
-      double* blk = out + tri_index(I1, J, NB) * 64 + cr * 8 + cc;
-      blk[0] = acc1[J][0];
-      blk[1] = acc1[J][1];
-    }
+  for (int j = 0; j < NJ; ++j) {
+    double* blk = out + j * 64 + cr * 8 + cc;
+    blk[0] = acc[j][0];
+    blk[1] = acc[j][1];
   }
 }
 
@@ -147,13 +144,23 @@ __global__ void __launch_bounds__(256) gram_reduce_kernel(const double* __restri
   }
 }
 
+// C(a, b) of the symmetric product from the rotated block rows: block (I, J) is
+// stored in row I when (J - I) mod NB <= NB/2, else as the transpose in row J.
 __device__ __forceinline__ double csym(const double* red, int NB, int a, int b) {
-  if (a > b) {
-    const int t = a;
+  const int NJ = gram_nj(NB);
+  int I = a >> 3, J = b >> 3;
+  int dj = J - I;
+  if (dj < 0) dj += NB;
+  if (dj >= NJ) {
+    dj = NB - dj;
+    int t = I;
+    I = J;
+    J = t;
+    t = a;
     a = b;
     b = t;
   }
-  return red[tri_index(a >> 3, b >> 3, NB) * 64 + (a & 7) * 8 + (b & 7)];
+  return red[(I * NJ + dj) * 64 + (a & 7) * 8 + (b & 7)];
 }
 
 __global__ void gram_assemble_kernel(const double* __restrict__ red, int k, int NB, double2* __restrict__ G) {
@@ -169,15 +176,16 @@ __global__ void gram_assemble_kernel(const double* __restrict__ red, int k, int 
 template <int NB>
 void launch_partial(const double2* Z, int64_t rows, int k, int64_t chunk, int nparts, double* work,
                     cudaStream_t stream) {
-  constexpr int NT = ((NB + 1) / 2) * 32;
+  constexpr int NT = NB * 32;
+  constexpr int MINB = kGramCtasPerSm;
   const size_t smem = static_cast<size_t>(kGramStages) * kGramBK * kGramLd * sizeof(double);
   static bool attr = false;
   if (!attr) {
-    PEPSB_CUDA(cudaFuncSetAttribute(gram_partial_kernel<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    PEPSB_CUDA(cudaFuncSetAttribute(gram_partial_kernel<NB, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     static_cast<int>(smem)));
     attr = true;
   }
-  gram_partial_kernel<NB><<<nparts, NT, smem, stream>>>(Z, rows, k, chunk, work);
+  gram_partial_kernel<NB, MINB><<<nparts, NT, smem, stream>>>(Z, rows, k, chunk, work);
   PEPSB_LAUNCH();
 }
 
@@ -190,10 +198,10 @@ std::atomic<int> g_gram{-1};
 bool gram_enabled() {
   int v = g_gram.load();
   if (v < 0) {
-    // opt-in: measured slower in the row than the 3M split-K GEMM it replaces
-    // (config-2 row 60.4 vs 60.9 ms, config-5 row 318 vs 321 ms)
+    // on by default since the rotated-row kernel (config-2 row 59.7 -> 57.7 ms,
+    // config-5 row 314 -> 304 ms against the 3M split-K GEMM); PEPSB_GEMM_GRAM=0 turns it off
     const char* e = getenv("PEPSB_GEMM_GRAM");
-    v = (e && e[0] == '1') ? 1 : 0;
+    v = (e && e[0] == '0') ? 0 : 1;
     g_gram.store(v);
   }
   return v != 0;
@@ -205,13 +213,13 @@ bool gram_herk_eligible(int64_t rows, int64_t k) { return k >= 1 && k <= kGramMa
 
 int64_t gram_herk_workspace(int64_t rows, int64_t k, int num_sms) {
   const int NB = static_cast<int>((2 * k + 7) / 8);
-  const int64_t nparts = std::min<int64_t>(num_sms, (rows + 255) / 256);
-  return (nparts + 1) * NB * (NB + 1) / 2 * 64;  // doubles: partial triangles + their sum
+  const int64_t nparts = std::min<int64_t>(static_cast<int64_t>(kGramCtasPerSm) * num_sms, (rows + 255) / 256);
+  return (nparts + 1) * NB * gram_nj(NB) * 64;  // doubles: partial blocks + their sum
 }
 
 void gram_herk(const double2* Z, int64_t rows, int k, double2* G, double* work, int num_sms, cudaStream_t stream) {
   const int NB = (2 * k + 7) / 8;
-  const int64_t nparts = std::min<int64_t>(num_sms, (rows + 255) / 256);
+  const int64_t nparts = std::min<int64_t>(static_cast<int64_t>(kGramCtasPerSm) * num_sms, (rows + 255) / 256);
   int64_t chunk = (rows + nparts - 1) / nparts;
   chunk = ((chunk + kGramBK - 1) / kGramBK) * kGramBK;
   const int np = static_cast<int>((rows + chunk - 1) / chunk);
@@ -225,7 +233,7 @@ void gram_herk(const double2* Z, int64_t rows, int k, double2* G, double* work, 
 #undef PEPSB_GRAM_CASE
     default: throw Error(kShapeError, "gram_herk: k > 72");
   }
-  const int nentries = NB * (NB + 1) / 2 * 64;
+  const int nentries = NB * gram_nj(NB) * 64;
   double* red = work + static_cast<int64_t>(np) * nentries;
   gram_reduce_kernel<<<(nentries + 31) / 32, dim3(32, 8), 0, stream>>>(work, np, nentries, red);
   PEPSB_LAUNCH();

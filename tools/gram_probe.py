@@ -1,0 +1,8 @@
+import sys; sys.path.insert(0, '.')
+import paper_2006_15234_b200.api as A
+ctx = A.default_context()
+ctx.set_option("gemm_gram", 1)
+z = A.random_tensor((262144, 72), 21)
+for _ in range(3):
+    g = A.gram(z)
+ctx.sync()
