@@ -82,7 +82,7 @@ int pepsb_ctx_sync(pepsb_ctx* ctx);
 /* keys: "orth_mode" (0 reference Gram-eigh, 1 CholeskyQR2),
  * "eig_solver" (0 auto, 1 Jacobi, 2 divide and conquer; process-wide),
  * "gemm_algo" (0 4M real embedding, 1 3M, 2 4M complex fragments), "gemm_real",
- * "gemm_small", "gemm_stream", "gemm_ws" (process-wide GEMM kernel choices), "overlap" (0..2),
+ * "gemm_small", "gemm_stream", "gemm_ws", "gemm_gram" (process-wide GEMM kernel choices), "overlap" (0..2),
  * "pipeline_rows" (-1 auto, 0..8), "concurrent_sweeps" (-1 auto, 0, 1).
  * Unknown keys fail with ConfigError. */
 int pepsb_ctx_set_option(pepsb_ctx* ctx, const char* key, int64_t value);

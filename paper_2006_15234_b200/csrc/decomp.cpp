@@ -48,15 +48,17 @@ int64_t prod(const std::vector<int64_t>& v) {
 // (transA: K x M) and B as K x N (transB: N x K), optional conjugation.
 void mm(Ctx& ctx, double2* C, const double2* A, bool transA, bool conjA, const double2* B, bool transB,
         bool conjB, int64_t M, int64_t N, int64_t K) {
-  // G = Y^H Y of a tall Y: the Hermitian Gram kernel (upper-triangle DMMA
-  // blocks of the interleaved real product, gram.cu)
+  // G = Y^H Y of a tall Y: the Hermitian Gram kernel (NB (NB/2 + 1) DMMA
+  // blocks of the symmetric interleaved real product, gram.cu)
   if (A == B && transA && conjA && !transB && !conjB && M == N && gram_enabled() && gram_herk_eligible(K, M)) {
     const int64_t nd = gram_herk_workspace(K, M, ctx.num_sms);
     BufPtr work = ctx.alloc((nd + 1) / 2);
     const int NB = static_cast<int>((2 * M + 7) / 8);
+    static const bool trace = getenv("PEPSB_TRACE_GEMM") != nullptr;  // one line per profiled GEMM-class record
+    if (trace) fprintf(stderr, "[zgemm] gram_herk M=%ld N=%ld K=%ld NB=%d\n", (long)M, (long)N, (long)K, NB);
     {
       ProfScope ps(ctx, Ctx::kProfGemm, 8.0 * M * N * K, 16.0 * (M * K + M * N),
-                   128.0 * K * (NB * (NB + 1) / 2));
+                   128.0 * K * (NB * (NB / 2 + 1)));
       gram_herk(A, K, static_cast<int>(M), C, reinterpret_cast<double*>(work->p), ctx.num_sms, ctx.stream);
     }
     ctx.launches += 3;

@@ -17,8 +17,9 @@ Sections (inputs regenerated from seeds by paper_2006_15234_b200/inputs.py):
   cfg3_pert  config 3 with every site multiplied by (1 + 1e-14 xi): the
              reference's own rounding sensitivity of the 256 <Z_i>.  ~25 min.
   cfg5_8x8   config-5 parameters (r=8, m=64, q=2, os=8, N(0,1/128)) on an 8x8
-             lattice: cached norm, centre <ZZ> (horizontal + vertical) and <Z> at
-             the centre.  ~80 min.
+             lattice: cached norm, <ZZ> on all 56 horizontal bonds and <Z> at
+             the centre (one-row bands only: the reference's two-row band zipper
+             for a vertical bond exceeds 62 GB here).  ~80 min.
   cfg5_8x8_pert  the same lattice with every site multiplied by (1 + 1e-14 xi):
              the reference's own rounding sensitivity at this size.  ~80 min.
 """
