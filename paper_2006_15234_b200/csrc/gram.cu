@@ -213,13 +213,13 @@ bool gram_herk_eligible(int64_t rows, int64_t k) { return k >= 1 && k <= kGramMa
 
 int64_t gram_herk_workspace(int64_t rows, int64_t k, int num_sms) {
   const int NB = static_cast<int>((2 * k + 7) / 8);
-  const int64_t nparts = std::min<int64_t>(static_cast<int64_t>(kGramCtasPerSm) * num_sms, (rows + 255) / 256);
+  const int64_t nparts = std::min<int64_t>(static_cast<int64_t>(kGramCtasPerSm) * num_sms, (rows + 63) / 64);
   return (nparts + 1) * NB * gram_nj(NB) * 64;  // doubles: partial blocks + their sum
 }
 
 void gram_herk(const double2* Z, int64_t rows, int k, double2* G, double* work, int num_sms, cudaStream_t stream) {
   const int NB = (2 * k + 7) / 8;
-  const int64_t nparts = std::min<int64_t>(static_cast<int64_t>(kGramCtasPerSm) * num_sms, (rows + 255) / 256);
+  const int64_t nparts = std::min<int64_t>(static_cast<int64_t>(kGramCtasPerSm) * num_sms, (rows + 63) / 64);
   int64_t chunk = (rows + nparts - 1) / nparts;
   chunk = ((chunk + kGramBK - 1) / kGramBK) * kGramBK;
   const int np = static_cast<int>((rows + chunk - 1) / chunk);
