@@ -108,22 +108,28 @@ def test_config3_norm_and_all_z_match_reference(algo):
 
 def test_config5_parameters_8x8_match_reference(algo):
     """BASELINE config-5 parameters (r=8, m=64, q=2, oversample 8, N(0,1/128))
-    on an 8x8 lattice: cached norm, <Z> at the centre, <ZZ> on all 56 horizontal
-    bonds and the centre vertical bond against the reference.  The bar is 1e-8,
-    or the reference's own spread under a 1e-14 input perturbation when that is
-    larger (fullsize_cfg5_8x8_pert: measured, not assumed)."""
+    on an 8x8 lattice: cached norm, <Z> at the centre and <ZZ> on all 56
+    horizontal bonds against the reference (golden generated by the reference
+    itself, 62 min on 8 cores; one-row bands only -- the reference's two-row band
+    zipper for a vertical bond needs more than 62 GB at these parameters).  The
+    bar is 1e-8 (observed: 3e-12 on the norm and on the values, 3M and 4M alike);
+    where the reference's own spread under a 1e-14 input perturbation has been
+    generated (fullsize_cfg5_8x8_pert) twice that spread is admitted if larger."""
     A = algo
-    if not all(os.path.exists(os.path.join(GOLDEN, f"fullsize_{n}.npz")) for n in ("cfg5_8x8", "cfg5_8x8_pert")):
-        pytest.skip("config-5 8x8 reference golden not generated yet (make_golden_fullsize.py cfg5_8x8 cfg5_8x8_pert)")
-    g, gp = golden("cfg5_8x8"), golden("cfg5_8x8_pert")
+    if not os.path.exists(os.path.join(GOLDEN, "fullsize_cfg5_8x8.npz")):
+        pytest.skip("config-5 8x8 reference golden not generated (make_golden_fullsize.py cfg5_8x8)")
+    g = golden("cfg5_8x8")
     c = cfg5_small()
     st = A.PepsState(8, 8, 2, c["sites"])
     opt = A.ContractOption.two_layer_opt(c["m"], c["seed"], c["power_iters"], c["oversample"])
     terms = [tuple(t) for t in g["terms"]]
     assert terms == cfg5_terms(8)
     norm, vals = device_local_expectations(A, st, opt, terms)
-    spread_norm = abs(gp["norm"][0] - g["norm"][0]) / abs(g["norm"][0])
-    spread_vals = float(np.max(np.abs(gp["values"] - g["values"])))
+    spread_norm = spread_vals = 0.0
+    if os.path.exists(os.path.join(GOLDEN, "fullsize_cfg5_8x8_pert.npz")):
+        gp = golden("cfg5_8x8_pert")
+        spread_norm = abs(gp["norm"][0] - g["norm"][0]) / abs(g["norm"][0])
+        spread_vals = float(np.max(np.abs(gp["values"] - g["values"])))
     assert abs(norm - g["norm"][0]) <= max(1e-8, 2 * spread_norm) * abs(g["norm"][0])
     assert np.max(np.abs(vals - g["values"])) <= max(1e-8, 2 * spread_vals)
 
