@@ -1,3 +1,5 @@
+"""Developer tool: the metrics quoted in profiles/*ncu*summary.txt from `ncu -i X.ncu-rep --page raw --csv > X.csv`:
+    python tools/ncu_extract.py X.csv"""
 import csv,sys
 rows=list(csv.reader(open(sys.argv[1])))
 hdr=rows[0]
