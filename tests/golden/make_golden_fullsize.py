@@ -20,6 +20,7 @@ Sections (inputs regenerated from seeds by paper_2006_15234_b200/inputs.py):
              lattice: cached norm, <ZZ> on all 56 horizontal bonds and <Z> at
              the centre (one-row bands only: the reference's two-row band zipper
              for a vertical bond exceeds 62 GB here).  ~80 min.
+  cfg5_12x12_norm  config-5 parameters on a 12x12 lattice: the norm by contract_two_layer.  ~65 min.
   cfg5_8x8_pert  the same lattice with every site multiplied by (1 + 1e-14 xi):
              the reference's own rounding sensitivity at this size.  ~80 min.
 """
@@ -89,9 +90,20 @@ def _cfg5(name, eps):
          t_cache=np.array([info["t_cache"]]), seconds=np.array([time.time() - t0]), eps=np.array([eps]))
 
 
+def sec_cfg5_12x12_norm():
+    """<psi|psi> of a 12x12 lattice with the config-5 parameters by contract_two_layer
+    (contraction.cpp:313-338): 11 row absorbs of 12 columns at m = 64, r = 8.  ~65 min."""
+    c = cfg5_small(12)
+    t0 = time.time()
+    val = ref.contract_two_layer(c["sites"], 12, 12, c["m"], c["seed"], c["power_iters"], c["oversample"])
+    save("cfg5_12x12_norm", norm=np.array([val[0] if isinstance(val, tuple) else val]),
+         seconds=np.array([time.time() - t0]))
+
+
 SECTIONS = {"cfg2_col": sec_cfg2_col, "cfg2_row": sec_cfg2_row, "cfg3": sec_cfg3,
             "cfg3_pert": lambda: sec_cfg3(1e-14, "cfg3_pert"),
-            "cfg5_8x8": lambda: _cfg5("cfg5_8x8", 0.0), "cfg5_8x8_pert": lambda: _cfg5("cfg5_8x8_pert", 1e-14)}
+            "cfg5_8x8": lambda: _cfg5("cfg5_8x8", 0.0), "cfg5_8x8_pert": lambda: _cfg5("cfg5_8x8_pert", 1e-14),
+            "cfg5_12x12_norm": sec_cfg5_12x12_norm}
 
 if __name__ == "__main__":
     args = [a for a in sys.argv[1:] if not a.startswith("--")]

@@ -134,6 +134,23 @@ def test_config5_parameters_8x8_match_reference(algo):
     assert np.max(np.abs(vals - g["values"])) <= max(1e-8, 2 * spread_vals)
 
 
+def test_config5_parameters_12x12_norm_matches_reference(algo):
+    """<psi|psi> of a 12x12 lattice with the BASELINE config-5 parameters (r=8,
+    m=64, q=2, oversample 8, N(0,1/128)) by `contract_two_layer`
+    (contraction.cpp:313-338: 11 row absorbs of 12 columns, 132 truncating
+    einsumsvd calls at k = 72) against the reference's own value (golden, ~65 min
+    of the reference on 8 cores).  Bar: 1e-8 relative."""
+    A = algo
+    if not os.path.exists(os.path.join(GOLDEN, "fullsize_cfg5_12x12_norm.npz")):
+        pytest.skip("12x12 config-5 norm golden not generated (make_golden_fullsize.py cfg5_12x12_norm)")
+    g = golden("cfg5_12x12_norm")
+    c = cfg5_small(12)
+    st = A.PepsState(12, 12, 2, c["sites"])
+    opt = A.ContractOption.two_layer_opt(c["m"], c["seed"], c["power_iters"], c["oversample"])
+    norm = A.contract_two_layer(st, st, opt)
+    assert abs(norm - g["norm"][0]) <= 1e-8 * abs(g["norm"][0]), (norm, g["norm"][0])
+
+
 @pytest.fixture(scope="module")
 def cfg4_states(refo):
     """Config 4 final states: the reference's ITE (drivers.cpp:56-98 in colour
