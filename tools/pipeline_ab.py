@@ -6,7 +6,7 @@ from paper_2006_15234_b200 import inputs
 ctx = A.default_context()
 res = {}
 for name, cfg, m, q, os_, depths in (("config3", inputs.config3(), 36, 2, -1, [2, 3, 4, 6, 8]),
-                                     ("config5", inputs.config5(), 64, 2, 8, [1, 2, 3])):
+                                     ("config5", inputs.config5(), 64, 2, 8, [2, 3, 4, 5])):
     n = cfg["rows"]
     st = A.PepsState(n, n, 2, cfg["sites"], ctx=ctx)
     opt = A.ContractOption.two_layer_opt(m, cfg["seed"], q, os_)
