@@ -31,7 +31,7 @@ namespace pepsb {
 namespace {
 
 constexpr int kGramBK = 32;       // rows per pipeline stage
-constexpr int kGramStages = 3;
+constexpr int kGramStages = 4;
 constexpr int kGramCtasPerSm = 1;  // resident CTAs per SM the split over rows is sized for
 constexpr int kGramLd = 152;      // doubles per smem row (144 + pad: rows alternate bank halves)
 
