@@ -127,3 +127,23 @@ def test_reference_vqe_ansatz_known_answers(refo):
     sites, e1 = refo.vqe_ansatz(rows, cols, 1, [np.pi] * (rows * cols), 2, J, h, 8, 1, 3)
     assert len(sites) == rows * cols
     assert abs(e1 - _classical_tfim_energy(bits, rows, cols, J)) < 1e-12
+
+
+def test_fullsize_goldens_are_packaged():
+    """The reference-generated full-size goldens the GPU parity tests read
+    (tests/golden/make_golden_fullsize.py; hours of reference CPU time) are in the
+    tree with the fields those tests use."""
+    import os
+
+    import numpy as np
+
+    gdir = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+    want = {"cfg2_col": ["s"], "cfg2_row": ["bb", "xb", "shapes"], "cfg3": ["norm", "z", "terms"],
+            "cfg3_pert": ["norm", "z"], "cfg5_8x8": ["norm", "values", "terms"],
+            "cfg5_8x8_pert": ["norm", "values"], "cfg5_12x12_norm": ["norm"]}
+    for name, keys in want.items():
+        g = np.load(os.path.join(gdir, f"fullsize_{name}.npz"))
+        for k in keys:
+            assert k in g.files, (name, k)
+    g5 = np.load(os.path.join(gdir, "fullsize_cfg5_8x8.npz"))
+    assert g5["values"].shape == (57,) and g5["terms"].shape == (57, 5)
