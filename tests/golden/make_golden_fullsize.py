@@ -90,6 +90,17 @@ def _cfg5(name, eps):
          t_cache=np.array([info["t_cache"]]), seconds=np.array([time.time() - t0]), eps=np.array([eps]))
 
 
+def sec_cfg5_12x12_norm_pert():
+    """The same 12x12 norm with every site multiplied by (1 + 1e-14 xi): the reference's own
+    rounding sensitivity at this size.  ~65 min."""
+    c = cfg5_small(12)
+    t0 = time.time()
+    val = ref.contract_two_layer(perturb(c["sites"], 1e-14), 12, 12, c["m"], c["seed"], c["power_iters"],
+                                 c["oversample"])
+    save("cfg5_12x12_norm_pert", norm=np.array([val[0] if isinstance(val, tuple) else val]),
+         seconds=np.array([time.time() - t0]), eps=np.array([1e-14]))
+
+
 def sec_cfg5_12x12_norm():
     """<psi|psi> of a 12x12 lattice with the config-5 parameters by contract_two_layer
     (contraction.cpp:313-338): 11 row absorbs of 12 columns at m = 64, r = 8.  ~65 min."""
@@ -103,7 +114,7 @@ def sec_cfg5_12x12_norm():
 SECTIONS = {"cfg2_col": sec_cfg2_col, "cfg2_row": sec_cfg2_row, "cfg3": sec_cfg3,
             "cfg3_pert": lambda: sec_cfg3(1e-14, "cfg3_pert"),
             "cfg5_8x8": lambda: _cfg5("cfg5_8x8", 0.0), "cfg5_8x8_pert": lambda: _cfg5("cfg5_8x8_pert", 1e-14),
-            "cfg5_12x12_norm": sec_cfg5_12x12_norm}
+            "cfg5_12x12_norm": sec_cfg5_12x12_norm, "cfg5_12x12_norm_pert": sec_cfg5_12x12_norm_pert}
 
 if __name__ == "__main__":
     args = [a for a in sys.argv[1:] if not a.startswith("--")]
