@@ -140,7 +140,7 @@ def test_fullsize_goldens_are_packaged():
     gdir = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
     want = {"cfg2_col": ["s"], "cfg2_row": ["bb", "xb", "shapes"], "cfg3": ["norm", "z", "terms"],
             "cfg3_pert": ["norm", "z"], "cfg5_8x8": ["norm", "values", "terms"],
-            "cfg5_8x8_pert": ["norm", "values"], "cfg5_12x12_norm": ["norm"]}
+            "cfg5_8x8_pert": ["norm", "values"], "cfg5_12x12_norm": ["norm"], "cfg5_12x12_norm_pert": ["norm"]}
     for name, keys in want.items():
         g = np.load(os.path.join(gdir, f"fullsize_{name}.npz"))
         for k in keys:
